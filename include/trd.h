@@ -1,0 +1,179 @@
+/*
+ * trd.h -- C ABI of libtrd: the B200 (sm_100a) hot path of AWRTRD / SAWRTRD
+ * (auto-weighted robust tensor-ring decomposition with FGMC and RStS, arXiv 2305.09044).
+ *
+ * Citations "P:L" are PAPER.md line numbers (section / equation in brackets).
+ *
+ * The method (Alg. 1): for a partially observed N-way tensor X with mask P,
+ * find TR cores Z_k in R^{r_k x I_k x r_{k+1}} (Def. 1) maximising the
+ * correntropy objective (Eq. 4) by a half-quadratic, cyclic, scaled steepest
+ * descent: per block k, weights (Eq. 7), gradient on a randomized subtensor
+ * sketch (Eq. 14-15), FGMC Gram (Eq. 13), scaled gradient
+ * (Eq. 16), exact line search (Eq. 18), update (Eq. 17).
+ * Readings of silent/garbled passages (R1..R18) are listed in DESIGN.md section 3.
+ *
+ * Conventions (0-based):
+ *   - linear index of X: lin = i_0 + I_0*(i_1 + I_1*(i_2 + ...))   (Def. 2 multi-index)
+ *   - core k on the host: float[r_k][I_k][r_{k+1}], C order (paper index order)
+ *   - mask: bit (lin % 32) of uint32 word (lin / 32); 1 = observed
+ *   - Zk2 column a + r_k*b (classical mode-2 unfolding, Thm 1); d and h use it too.
+ *
+ * Errors: every call returns trd_status and never throws across the ABI.  Arguments are
+ * validated before anything is enqueued.  A CUDA or NCCL failure puts the context into a
+ * sticky error state in which only trd_get_cores / trd_last_error / trd_destroy are valid.
+ *
+ * Threading: a context is used by one host thread at a time.  All device work is enqueued
+ * on the stream given to trd_init.  No call keeps pointers to caller host memory.
+ */
+#ifndef TRD_H
+#define TRD_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TRD_MAX_ORDER 8
+#define TRD_MAX_RANK 16
+
+typedef struct trd_ctx trd_ctx;
+
+typedef enum {
+  TRD_OK = 0,
+  TRD_ERR_INVALID_ARG = 1,  /* bad pointer / value (sigma <= 0, lambda_rel < 0, ...)   */
+  TRD_ERR_SHAPE = 2,        /* N, dims, ranks, sketch sizes or shard range inconsistent */
+  TRD_ERR_OOM = 3,          /* device allocation failed                                 */
+  TRD_ERR_CUDA = 4,         /* CUDA runtime error (sticky)                              */
+  TRD_ERR_NCCL = 5,         /* NCCL error or NCCL unavailable for world > 1 (sticky)    */
+  TRD_ERR_NOT_SPD = 6,      /* G + lambda I not positive definite after 3 retries       */
+  TRD_ERR_NONFINITE = 7,    /* non-finite value in d, h, eta or the cores               */
+  TRD_ERR_STATE = 8         /* call not valid in the current state                      */
+} trd_status;
+
+typedef enum {
+  TRD_SIGMA_FIXED = 0,  /* Alg. 1 input sigma, kept fixed                        */
+  TRD_SIGMA_INF = 1,    /* sigma -> inf: W == 1, the masked LS problem Eq. 2     */
+  TRD_SIGMA_RMS = 2     /* reading R9: sigma_{t+1} = max(sigma_min, theta * RMS(e))      */
+} trd_sigma_mode;
+
+typedef struct {
+  int32_t order;                    /* N, 3..TRD_MAX_ORDER                                  */
+  int64_t dims[TRD_MAX_ORDER];      /* global I_0..I_{N-1}                                  */
+  int32_t ranks[TRD_MAX_ORDER];     /* r_0..r_{N-1}, 1..TRD_MAX_RANK, ring r_N = r_0   */
+  int32_t sigma_mode;               /* trd_sigma_mode                                       */
+  double sigma;                     /* FIXED: the kernel width; RMS: ignored (sigma_0 from
+                                       an initial residual pass); INF: ignored              */
+  double sigma_theta;               /* RMS multiplier theta (default 1.0)                   */
+  double sigma_min;                 /* RMS floor (default 1e-3)                             */
+  double lambda_rel;                /* R5: lambda = lambda_rel * tr(G) / R_k^2 (default 1e-6) */
+  double step;                      /* 0: exact line search Eq. 12/18; > 0: fixed eta        */
+  int64_t sketch[TRD_MAX_ORDER];    /* s_m used when m != k; 0 or >= I_m means the full mode
+                                       (AWRTRD); s_k = I_k always (Alg. 1 line 4)     */
+  uint64_t seed;                    /* RStS sampler seed (reading R11)                      */
+  int32_t shard_mode;               /* X is sharded along this mode (0 when world == 1)     */
+  int32_t world, rank;              /* data-parallel group; world == 1: no NCCL             */
+  const void* nccl_unique_id;       /* 128 bytes from trd_nccl_unique_id() on rank 0,
+                                       broadcast by the caller; NULL when world == 1         */
+} trd_config;
+
+/* Local shard of X and P.  Local tensor = global X restricted to
+ * i_{shard_mode} in [shard_begin, shard_end), stored in its own linear order (same formula
+ * with the local extent of the shard mode).  Device pointers, caller owned, read only,
+ * must stay valid and unmodified until trd_destroy (or until trd_upload replaces them when
+ * the shard is library-owned). */
+typedef struct {
+  int64_t shard_begin, shard_end;   /* [0, I_shard) when world == 1                          */
+  const float* values;              /* dense: value of local entry lin at values[lin];
+                                       packed: value of the n-th observed entry (in local
+                                       linear order) at values[n]                            */
+  const uint32_t* mask_bits;        /* 1 bit per local entry                                */
+  int32_t packed;                   /* 0 dense, 1 packed (values of observed entries only)   */
+  int32_t host;                     /* 0: pointers are device memory (zero copy).
+                                       1: pointers are host memory; the library allocates
+                                       device buffers and copies them (trd_upload re-copies) */
+} trd_shard;
+
+/* One record per sweep.  ms is the device time of the sweep (CUDA events). */
+typedef struct {
+  double sigma;                     /* kernel width used in this sweep                      */
+  double sum_e2;                    /* sum of squared pass-1 residuals over all blocks       */
+  double welsch_loss;               /* sum over blocks of sum_WS sigma^2 (1 - w)  (R3)       */
+  double stop_e;                    /* Alg. 1 line 13 relative change of D^t; NaN at t = 0    */
+  double ms;                        /* device milliseconds of this sweep                     */
+  int64_t n_obs;                    /* observed entries processed (sum over blocks)          */
+  double eta[TRD_MAX_ORDER];        /* step size per block (0 if skipped)                    */
+  double num[TRD_MAX_ORDER];        /* <d, h> per block                                      */
+  double den[TRD_MAX_ORDER];        /* ||sqrt(W) o P o (h S^T)||^2 per block                  */
+  int64_t nnz[TRD_MAX_ORDER];       /* observed entries in block k's working set             */
+  uint32_t skipped_mask;            /* bit k set: block k skipped (num <= 0 or den == 0, R14) */
+} trd_sweep_stats;
+
+typedef struct {
+  double rel_err_all;               /* ||X_hat - X_ref|| / ||X_ref|| over evaluated entries  */
+  double rel_err_observed;          /* same, restricted to observed entries                  */
+  double psnr;                      /* 10 log10(peak^2 / MSE), peak = max |X_ref|    */
+  int64_t n_eval;                   /* entries evaluated                                      */
+} trd_error_stats;
+
+/* Create a context.  init_cores: host pointers, N arrays float[r_k][I_k][r_{k+1}] (Alg. 1
+ * line 1).  stream: a cudaStream_t (NULL = legacy default stream).  Builds the FGMC
+ * cache Q_k and, for TRD_SIGMA_RMS, sigma_0 from all local observed residuals
+ * (allreduced).  Synchronises the stream once.  *out is NULL on failure. */
+trd_status trd_init(const trd_config* cfg, const trd_shard* shard,
+                    const float* const* init_cores, void* stream, trd_ctx** out);
+
+/* Re-copy host-resident X / P into the context's device buffers (shard.host == 1 only):
+ * the host->device leg of an end-to-end step.  Asynchronous on the context stream;
+ * host memory should be pinned for overlap.  Same layout and sizes as at trd_init. */
+trd_status trd_upload(trd_ctx* ctx, const float* values_host, const uint32_t* mask_host);
+
+/* Write the RStS index sets of sweep `sweep`, block k (Alg. 1 line 4; reading R11)
+ * to idx_dev (device, int32, sum_m sizes[m] entries, mode-major, each set ascending) and
+ * their sizes to sizes_host[N] (host).  Mode k gets 0..I_k-1.  Synchronises the stream. */
+trd_status trd_sketch(trd_ctx* ctx, int32_t sweep, int32_t k, int32_t* idx_dev,
+                      int64_t* sizes_host);
+
+/* Run n_sweeps iterations of Alg. 1 (lines 3-13).  stats: host array of n_sweeps records
+ * or NULL.  With stats == NULL the call only enqueues work (no host synchronisation).
+ * Returns TRD_ERR_NONFINITE if a non-finite value appeared (checked when stats != NULL
+ * and at trd_get_cores). */
+trd_status trd_sweep(trd_ctx* ctx, int32_t n_sweeps, trd_sweep_stats* stats);
+
+/* Evaluate the TR model (Def. 1) at n global linear indices (device int64) into
+ * out_dev (device float).  Enqueued on the context stream; no synchronisation. */
+trd_status trd_reconstruct(trd_ctx* ctx, const int64_t* lin_idx_dev, int64_t n, float* out_dev);
+
+/* Relative error of the model against ref_dev (device float, dense local shard layout),
+ * over all local entries, or over those whose bit is set in eval_bits (device, may be
+ * NULL).  Partial sums are allreduced when world > 1.  Synchronises the stream. */
+trd_status trd_error(trd_ctx* ctx, const float* ref_dev, const uint32_t* eval_bits,
+                     trd_error_stats* out);
+
+/* Copy cores to / from the host (layout as init_cores).  Synchronises the stream.
+ * trd_set_cores rebuilds the FGMC cache. */
+trd_status trd_get_cores(trd_ctx* ctx, float* const* cores_host);
+trd_status trd_set_cores(trd_ctx* ctx, const float* const* cores_host);
+
+/* Diagnostic probe of block k at the current cores without updating them (parity tests):
+ * runs a1-a10 of the block exactly as trd_sweep would at sweep index `sweep` and copies
+ * d (I_k x R_k^2, row-major, column a + r_k b), G (R_k^2 x R_k^2), h (like d) and
+ * stats5 = {sum_e2, n_obs, welsch, num, den} to the host.  Any output pointer may be NULL. */
+trd_status trd_block_probe(trd_ctx* ctx, int32_t sweep, int32_t k, double* d_host,
+                           double* G_host, double* h_host, double* stats5_host);
+
+/* Number of kernels the library launched since the context was created (a counter the
+ * host increments at every launch; bench.py reports it as gpu_launches). */
+int64_t trd_launch_count(const trd_ctx* ctx);
+
+/* 128-byte NCCL unique id for world > 1 (call on rank 0; caller broadcasts it). */
+trd_status trd_nccl_unique_id(void* out128);
+
+void trd_destroy(trd_ctx* ctx);
+const char* trd_last_error(const trd_ctx* ctx);
+const char* trd_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TRD_H */
