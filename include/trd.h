@@ -34,6 +34,12 @@
 extern "C" {
 #endif
 
+#if defined(__GNUC__)
+#define TRD_API __attribute__((visibility("default")))
+#else
+#define TRD_API
+#endif
+
 #define TRD_MAX_ORDER 8
 #define TRD_MAX_RANK 16
 
@@ -120,58 +126,71 @@ typedef struct {
  * line 1).  stream: a cudaStream_t (NULL = legacy default stream).  Builds the FGMC
  * cache Q_k and, for TRD_SIGMA_RMS, sigma_0 from all local observed residuals
  * (allreduced).  Synchronises the stream once.  *out is NULL on failure. */
-trd_status trd_init(const trd_config* cfg, const trd_shard* shard,
+TRD_API trd_status trd_init(const trd_config* cfg, const trd_shard* shard,
                     const float* const* init_cores, void* stream, trd_ctx** out);
 
 /* Re-copy host-resident X / P into the context's device buffers (shard.host == 1 only):
  * the host->device leg of an end-to-end step.  Asynchronous on the context stream;
  * host memory should be pinned for overlap.  Same layout and sizes as at trd_init. */
-trd_status trd_upload(trd_ctx* ctx, const float* values_host, const uint32_t* mask_host);
+TRD_API trd_status trd_upload(trd_ctx* ctx, const float* values_host, const uint32_t* mask_host);
 
 /* Write the RStS index sets of sweep `sweep`, block k (Alg. 1 line 4; reading R11)
  * to idx_dev (device, int32, sum_m sizes[m] entries, mode-major, each set ascending) and
  * their sizes to sizes_host[N] (host).  Mode k gets 0..I_k-1.  Synchronises the stream. */
-trd_status trd_sketch(trd_ctx* ctx, int32_t sweep, int32_t k, int32_t* idx_dev,
+TRD_API trd_status trd_sketch(trd_ctx* ctx, int32_t sweep, int32_t k, int32_t* idx_dev,
                       int64_t* sizes_host);
 
 /* Run n_sweeps iterations of Alg. 1 (lines 3-13).  stats: host array of n_sweeps records
  * or NULL.  With stats == NULL the call only enqueues work (no host synchronisation).
  * Returns TRD_ERR_NONFINITE if a non-finite value appeared (checked when stats != NULL
  * and at trd_get_cores). */
-trd_status trd_sweep(trd_ctx* ctx, int32_t n_sweeps, trd_sweep_stats* stats);
+TRD_API trd_status trd_sweep(trd_ctx* ctx, int32_t n_sweeps, trd_sweep_stats* stats);
 
 /* Evaluate the TR model (Def. 1) at n global linear indices (device int64) into
  * out_dev (device float).  Enqueued on the context stream; no synchronisation. */
-trd_status trd_reconstruct(trd_ctx* ctx, const int64_t* lin_idx_dev, int64_t n, float* out_dev);
+TRD_API trd_status trd_reconstruct(trd_ctx* ctx, const int64_t* lin_idx_dev, int64_t n, float* out_dev);
 
 /* Relative error of the model against ref_dev (device float, dense local shard layout),
  * over all local entries, or over those whose bit is set in eval_bits (device, may be
  * NULL).  Partial sums are allreduced when world > 1.  Synchronises the stream. */
-trd_status trd_error(trd_ctx* ctx, const float* ref_dev, const uint32_t* eval_bits,
+TRD_API trd_status trd_error(trd_ctx* ctx, const float* ref_dev, const uint32_t* eval_bits,
                      trd_error_stats* out);
 
 /* Copy cores to / from the host (layout as init_cores).  Synchronises the stream.
  * trd_set_cores rebuilds the FGMC cache. */
-trd_status trd_get_cores(trd_ctx* ctx, float* const* cores_host);
-trd_status trd_set_cores(trd_ctx* ctx, const float* const* cores_host);
+TRD_API trd_status trd_get_cores(trd_ctx* ctx, float* const* cores_host);
+TRD_API trd_status trd_set_cores(trd_ctx* ctx, const float* const* cores_host);
 
 /* Diagnostic probe of block k at the current cores without updating them (parity tests):
  * runs a1-a10 of the block exactly as trd_sweep would at sweep index `sweep` and copies
  * d (I_k x R_k^2, row-major, column a + r_k b), G (R_k^2 x R_k^2), h (like d) and
  * stats5 = {sum_e2, n_obs, welsch, num, den} to the host.  Any output pointer may be NULL. */
-trd_status trd_block_probe(trd_ctx* ctx, int32_t sweep, int32_t k, double* d_host,
+TRD_API trd_status trd_block_probe(trd_ctx* ctx, int32_t sweep, int32_t k, double* d_host,
                            double* G_host, double* h_host, double* stats5_host);
 
 /* Number of kernels the library launched since the context was created (a counter the
  * host increments at every launch; bench.py reports it as gpu_launches). */
-int64_t trd_launch_count(const trd_ctx* ctx);
+TRD_API int64_t trd_launch_count(const trd_ctx* ctx);
+
+/* Per-kernel-class device time, measured with CUDA events recorded on the context stream
+ * around the pass-1 and pass-2 kernels while profiling is enabled (bench.py's roofline).
+ * trd_get_profile synchronises the stream; it reports totals since the last enable. */
+typedef struct {
+  double pass1_ms, pass2_ms;        /* summed device time of the pass kernels               */
+  int64_t pass1_launches, pass2_launches;
+  double pass1_entries, pass2_entries;    /* observed entries processed (sum over launches) */
+  double pass1_flops, pass2_flops;        /* algorithmic flops, SURVEY 8(d) per-entry count  */
+  double pass1_bytes, pass2_bytes;        /* algorithmic bytes, SURVEY 8(d) per-entry count  */
+} trd_profile;
+TRD_API trd_status trd_set_profiling(trd_ctx* ctx, int32_t enable);
+TRD_API trd_status trd_get_profile(trd_ctx* ctx, trd_profile* out);
 
 /* 128-byte NCCL unique id for world > 1 (call on rank 0; caller broadcasts it). */
-trd_status trd_nccl_unique_id(void* out128);
+TRD_API trd_status trd_nccl_unique_id(void* out128);
 
-void trd_destroy(trd_ctx* ctx);
-const char* trd_last_error(const trd_ctx* ctx);
-const char* trd_version(void);
+TRD_API void trd_destroy(trd_ctx* ctx);
+TRD_API const char* trd_last_error(const trd_ctx* ctx);
+TRD_API const char* trd_version(void);
 
 #ifdef __cplusplus
 }

@@ -1,0 +1,714 @@
+// trd_api.cu -- C ABI of libtrd (include/trd.h): validation, memory, block plans, the sweep
+// orchestration of Alg. 1 and the NCCL data-parallel exchange.
+#include <dlfcn.h>
+#include <stdarg.h>
+#include <math.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <cmath>
+#include <new>
+#include <vector>
+
+#include "trd_internal.cuh"
+
+using namespace trd;
+
+// ---------------------------------------------------------------------------------------
+// NCCL, loaded lazily (world > 1 only) so a single-GPU context never needs it.
+// ---------------------------------------------------------------------------------------
+namespace {
+typedef int (*nccl_get_unique_id_t)(void*);
+struct NcclId { char internal[128]; };
+typedef int (*nccl_comm_init_rank2_t)(void**, int, NcclId, int);
+typedef int (*nccl_all_reduce_t)(const void*, void*, size_t, int, int, void*, cudaStream_t);
+typedef int (*nccl_comm_destroy_t)(void*);
+typedef const char* (*nccl_get_error_string_t)(int);
+
+struct NcclApi {
+  bool tried = false, ok = false;
+  nccl_get_unique_id_t get_unique_id = nullptr;
+  nccl_comm_init_rank2_t comm_init_rank = nullptr;
+  nccl_all_reduce_t all_reduce = nullptr;
+  nccl_comm_destroy_t comm_destroy = nullptr;
+  nccl_get_error_string_t err_str = nullptr;
+};
+NcclApi g_nccl;
+
+bool load_nccl() {
+  if (g_nccl.tried) return g_nccl.ok;
+  g_nccl.tried = true;
+  void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) return false;
+  g_nccl.get_unique_id = (nccl_get_unique_id_t)dlsym(h, "ncclGetUniqueId");
+  g_nccl.comm_init_rank = (nccl_comm_init_rank2_t)dlsym(h, "ncclCommInitRank");
+  g_nccl.all_reduce = (nccl_all_reduce_t)dlsym(h, "ncclAllReduce");
+  g_nccl.comm_destroy = (nccl_comm_destroy_t)dlsym(h, "ncclCommDestroy");
+  g_nccl.err_str = (nccl_get_error_string_t)dlsym(h, "ncclGetErrorString");
+  g_nccl.ok = g_nccl.get_unique_id && g_nccl.comm_init_rank && g_nccl.all_reduce && g_nccl.comm_destroy;
+  return g_nccl.ok;
+}
+constexpr int kNcclFloat64 = 8, kNcclSum = 0, kNcclMax = 2;
+
+// ---------------------------------------------------------------------------------------
+trd_status fail(Context* c, trd_status st, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  if (c) {
+    c->err = buf;
+    if (st == TRD_ERR_CUDA || st == TRD_ERR_NCCL) c->sticky = st;
+  }
+  return st;
+}
+
+#define CUDA_TRY(ctx, expr)                                                                   \
+  do {                                                                                       \
+    cudaError_t e_ = (expr);                                                                 \
+    if (e_ != cudaSuccess)                                                                   \
+      return fail(ctx, TRD_ERR_CUDA, "%s failed: %s", #expr, cudaGetErrorString(e_));        \
+  } while (0)
+
+template <typename T>
+trd_status dalloc(Context* c, T** p, size_t n) {
+  if (n == 0) n = 1;
+  cudaError_t e = cudaMalloc((void**)p, n * sizeof(T));
+  if (e != cudaSuccess) {
+    *p = nullptr;
+    cudaGetLastError();
+    return fail(c, TRD_ERR_OOM, "cudaMalloc(%zu bytes) failed: %s", n * sizeof(T), cudaGetErrorString(e));
+  }
+  return TRD_OK;
+}
+
+trd_status check_launch(Context* c, const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(c, TRD_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+  return TRD_OK;
+}
+
+// cost model of a split p (v1 SIMT pass kernels): K per entry, lane utilisation of the
+// 32-column chunks, with a mild preference for ~2k columns (L2-resident Rgt tiles)
+double plan_cost(int64_t K, int64_t ncols) {
+  const double chunks = std::ceil((double)ncols / 32.0);
+  const double util = (double)ncols / (32.0 * chunks);
+  const double shape = std::fabs(std::log2(std::max<double>(ncols, 1.0) / 2048.0));
+  return (double)K / util * (1.0 + 0.02 * shape);
+}
+
+void build_plan(const Context& c, int k, const int64_t* s_in, BlockPlan& bp) {
+  const int N = c.N;
+  memset(&bp, 0, sizeof(bp));
+  bp.k = k;
+  for (int m = 0; m < N; ++m) {
+    int64_t s = s_in[m];
+    if (m == k || s <= 0 || s >= c.dims[m]) s = c.dims[m];
+    bp.s[m] = s;
+  }
+  double best = 1e300;
+  int best_p = 0;
+  for (int p = 0; p <= N - 2; ++p) {
+    const int rs = c.ranks[(k + p + 1) % N];
+    const int64_t K = (int64_t)c.ranks[k] * rs;
+    int64_t ncols = 1;
+    for (int q = p + 1; q <= N - 1; ++q) ncols *= bp.s[(k + q) % N];
+    const double cost = plan_cost(K, ncols);
+    if (cost < best - 1e-12) { best = cost; best_p = p; }
+  }
+  const int p = best_p;
+  bp.p = p;
+  bp.nleft = p;
+  bp.nright = N - 1 - p;
+  bp.nL = 1;
+  for (int q = 0; q < p; ++q) { bp.left[q] = (k + 1 + q) % N; bp.nL *= bp.s[bp.left[q]]; }
+  bp.ncols = 1;
+  for (int q = 0; q < bp.nright; ++q) { bp.right[q] = (k + 1 + p + q) % N; bp.ncols *= bp.s[bp.right[q]]; }
+  bp.rk = c.ranks[k];
+  bp.rk1 = c.ranks[(k + 1) % N];
+  bp.rs = c.ranks[(k + p + 1) % N];
+  bp.K = bp.rk * bp.rs;
+  bp.R2 = bp.rk * bp.rk1;
+  const int64_t Ik = c.dims[k];
+  bp.nrows = Ik * bp.nL;
+  bp.nnz_ws = bp.nrows * bp.ncols;
+  // geometry: 8 warps per CTA, one (row, column sub-range) item per warp
+  if (bp.nL >= 8) { bp.jl_per_cta = 8; bp.ws_split = 1; }
+  else {
+    bp.jl_per_cta = (int)bp.nL;
+    int ws = 8 / (int)bp.nL;
+    int p2 = 1;
+    while (p2 * 2 <= ws) p2 *= 2;
+    bp.ws_split = p2;
+  }
+  bp.grid_x = (bp.nL + bp.jl_per_cta - 1) / bp.jl_per_cta;
+  const int64_t base = bp.grid_x * Ik;
+  int64_t nsplit = (4 * 148 + base - 1) / base;
+  const int64_t maxsplit = std::max<int64_t>(1, bp.ncols / (64 * (int64_t)bp.ws_split));
+  nsplit = std::min(nsplit, maxsplit);
+  nsplit = std::max<int64_t>(nsplit, 1);
+  nsplit = std::min<int64_t>(nsplit, 65535);
+  bp.nsplit = (int)nsplit;
+}
+
+size_t ncta_of(const BlockPlan& bp) { return (size_t)(bp.grid_x * bp.nsplit); }
+
+trd_status allreduce(Context* c, double* buf, size_t n, int op = kNcclSum) {
+  if (c->cfg.world <= 1) return TRD_OK;
+  int r = g_nccl.all_reduce(buf, buf, n, kNcclFloat64, op, c->nccl_comm, c->stream);
+  if (r != 0) return fail(c, TRD_ERR_NCCL, "ncclAllReduce: %s", g_nccl.err_str ? g_nccl.err_str(r) : "?");
+  return TRD_OK;
+}
+
+// profiling events around a pass kernel (pool reused across sweeps)
+int prof_event(Context* c) {
+  if (c->ev_used == c->ev_pool.size()) {
+    cudaEvent_t e;
+    if (cudaEventCreate(&e) != cudaSuccess) return -1;
+    c->ev_pool.push_back(e);
+  }
+  const int i = (int)c->ev_used++;
+  cudaEventRecord(c->ev_pool[(size_t)i], c->stream);
+  return i;
+}
+
+// a1-a6 + a7 (pass 1 and the d/stat exchange) of block k
+trd_status block_pass1(Context* c, const BlockPlan& bp) {
+  cudaStream_t s = c->stream;
+  launch_sampler(*c, bp, s);
+  launch_plan(*c, bp, s);
+  launch_lft(*c, bp, c->Z + c->zoff[bp.k], 0, c->lft, s);
+  const int e0 = c->prof ? prof_event(c) : -1;
+  launch_pass1(*c, bp, 0, s);
+  if (c->prof) c->ev_pass1.push_back({e0, prof_event(c)});
+  launch_reduce_d(*c, bp, s);
+  trd_status st = check_launch(c, "pass 1");
+  if (st) return st;
+  const int64_t Ik = c->dims[bp.k];
+  st = allreduce(c, c->dvec, (size_t)(Ik * bp.R2 + 3));
+  if (st) return st;
+  launch_block_stats(*c, bp, s);
+  return TRD_OK;
+}
+
+// a8-a10 (FGMC, solve, scaled gradient, pass 2, den exchange)
+trd_status block_pass2(Context* c, const BlockPlan& bp) {
+  cudaStream_t s = c->stream;
+  launch_gram(*c, bp, s);
+  launch_solve(*c, bp, s);
+  launch_h(*c, bp, s);
+  launch_lft(*c, bp, nullptr, 1, c->lfth, s);
+  const int e0 = c->prof ? prof_event(c) : -1;
+  launch_pass2(*c, bp, s);
+  if (c->prof) c->ev_pass2.push_back({e0, prof_event(c)});
+  launch_reduce_den(*c, bp, s);
+  trd_status st = check_launch(c, "pass 2");
+  if (st) return st;
+  return allreduce(c, c->red_ws, 1);
+}
+
+trd_status ensure_stats(Context* c, int n) {
+  if (n <= c->stats_cap) return TRD_OK;
+  if (c->stats) cudaFree(c->stats);
+  c->stats = nullptr;
+  trd_status st = dalloc(c, &c->stats, (size_t)n);
+  if (st) return st;
+  c->stats_cap = n;
+  return TRD_OK;
+}
+
+trd_status sigma0_pass(Context* c) {
+  const BlockPlan& bp = c->full_plan;
+  cudaStream_t s = c->stream;
+  launch_sampler(*c, bp, s);
+  launch_plan(*c, bp, s);
+  launch_lft(*c, bp, c->Z + c->zoff[bp.k], 0, c->lft, s);
+  launch_pass1(*c, bp, 1, s);
+  // reduce the statistics into red_ws[0..2]: reuse reduce_d with R2 = 0 semantics
+  BlockPlan tmp = bp;
+  tmp.R2 = 0;
+  double* saved = c->dvec;
+  c->dvec = c->red_ws;
+  launch_reduce_d(*c, tmp, s);
+  c->dvec = saved;
+  trd_status st = check_launch(c, "sigma0 pass");
+  if (st) return st;
+  st = allreduce(c, c->red_ws, 3);
+  if (st) return st;
+  launch_sigma0(*c, s);
+  return check_launch(c, "sigma0");
+}
+
+void host_to_dev_core(const Context& c, int k, const float* src, std::vector<float>& tmp) {
+  const int r0 = c.ranks[k], r1 = c.ranks[(k + 1) % c.N];
+  const int64_t I = c.dims[k];
+  tmp.resize((size_t)(r0 * I * r1));
+  for (int a = 0; a < r0; ++a)
+    for (int64_t i = 0; i < I; ++i)
+      for (int b = 0; b < r1; ++b) tmp[(i * r0 + a) * r1 + b] = src[(a * I + i) * r1 + b];
+}
+
+}  // namespace
+
+// =======================================================================================
+extern "C" {
+
+const char* trd_version(void) { return "libtrd 0.1 (sm_100a, v1 SIMT pass kernels)"; }
+
+trd_status trd_nccl_unique_id(void* out128) {
+  if (!out128) return TRD_ERR_INVALID_ARG;
+  if (!load_nccl()) return TRD_ERR_NCCL;
+  return g_nccl.get_unique_id(out128) == 0 ? TRD_OK : TRD_ERR_NCCL;
+}
+
+const char* trd_last_error(const trd_ctx* ctx) {
+  if (!ctx) return "null context";
+  return reinterpret_cast<const Context*>(ctx)->err.c_str();
+}
+
+int64_t trd_launch_count(const trd_ctx* ctx) {
+  return ctx ? reinterpret_cast<const Context*>(ctx)->launches : 0;
+}
+
+trd_status trd_set_profiling(trd_ctx* ctx, int32_t enable) {
+  Context* c = reinterpret_cast<Context*>(ctx);
+  if (!c) return TRD_ERR_INVALID_ARG;
+  if (c->sticky) return c->sticky;
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  c->prof = enable != 0;
+  c->ev_used = 0;
+  c->ev_pass1.clear();
+  c->ev_pass2.clear();
+  DevScalars hs;
+  CUDA_TRY(c, cudaMemcpy(&hs, c->sc, sizeof(hs), cudaMemcpyDeviceToHost));
+  hs.prof_on = c->prof ? 1 : 0;
+  for (int k = 0; k < kMaxN; ++k) hs.prof_nobs[k] = 0.0;
+  CUDA_TRY(c, cudaMemcpy(c->sc, &hs, sizeof(hs), cudaMemcpyHostToDevice));
+  return TRD_OK;
+}
+
+trd_status trd_get_profile(trd_ctx* ctx, trd_profile* out) {
+  Context* c = reinterpret_cast<Context*>(ctx);
+  if (!c || !out) return TRD_ERR_INVALID_ARG;
+  if (c->sticky) return c->sticky;
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  memset(out, 0, sizeof(*out));
+  for (auto& pr : c->ev_pass1) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, c->ev_pool[(size_t)pr.first], c->ev_pool[(size_t)pr.second]);
+    out->pass1_ms += ms;
+  }
+  for (auto& pr : c->ev_pass2) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, c->ev_pool[(size_t)pr.first], c->ev_pool[(size_t)pr.second]);
+    out->pass2_ms += ms;
+  }
+  out->pass1_launches = (int64_t)c->ev_pass1.size();
+  out->pass2_launches = (int64_t)c->ev_pass2.size();
+  DevScalars hs;
+  CUDA_TRY(c, cudaMemcpy(&hs, c->sc, sizeof(hs), cudaMemcpyDeviceToHost));
+  // algorithmic counts: pass 1 = recon + gradient (4 R^2 + 8 flops per
+  // observed entry; value 4 B + staged weight 4 B + mask bits), pass 2 = line-search dot
+  // (2 R^2 + 4 flops; weight 4 B + mask bits).  Blocks were visited cyclically, so each
+  // block's launches are n_launch / N.
+  const double per_block = c->ev_pass1.empty() ? 0.0 : (double)c->ev_pass1.size() / c->N;
+  for (int k = 0; k < c->N; ++k) {
+    const double n = hs.prof_nobs[k];
+    const double R2 = (double)c->plan[k].R2;
+    const double ws_bits = (double)c->plan[k].nnz_ws / c->cfg.world / 8.0 * per_block;
+    out->pass1_entries += n;
+    out->pass2_entries += n;
+    out->pass1_flops += n * (4.0 * R2 + 8.0);
+    out->pass2_flops += n * (2.0 * R2 + 4.0);
+    out->pass1_bytes += 8.0 * n + ws_bits;
+    out->pass2_bytes += 4.0 * n + ws_bits;
+  }
+  return TRD_OK;
+}
+
+trd_status trd_init(const trd_config* cfg, const trd_shard* shard, const float* const* init_cores,
+                    void* stream, trd_ctx** out) {
+  if (!out) return TRD_ERR_INVALID_ARG;
+  *out = nullptr;
+  if (!cfg || !shard || !init_cores) return TRD_ERR_INVALID_ARG;
+  const int N = cfg->order;
+  if (N < 3 || N > TRD_MAX_ORDER) return TRD_ERR_SHAPE;
+  for (int m = 0; m < N; ++m) {
+    if (cfg->dims[m] < 1 || cfg->dims[m] > (1LL << 31) - 1) return TRD_ERR_SHAPE;
+    if (cfg->ranks[m] < 1 || cfg->ranks[m] > TRD_MAX_RANK) return TRD_ERR_SHAPE;
+    if (cfg->sketch[m] < 0) return TRD_ERR_SHAPE;
+    if (!init_cores[m]) return TRD_ERR_INVALID_ARG;
+    if (cfg->sketch[m] > 0 && cfg->sketch[m] < cfg->dims[m] && cfg->dims[m] > 16384) return TRD_ERR_SHAPE;
+  }
+  if (cfg->sigma_mode < 0 || cfg->sigma_mode > 2) return TRD_ERR_INVALID_ARG;
+  if (cfg->sigma_mode == TRD_SIGMA_FIXED && !(cfg->sigma > 0.0)) return TRD_ERR_INVALID_ARG;
+  if (cfg->sigma_mode == TRD_SIGMA_RMS && (!(cfg->sigma_theta > 0.0) || !(cfg->sigma_min > 0.0)))
+    return TRD_ERR_INVALID_ARG;
+  if (!(cfg->lambda_rel >= 0.0) || !(cfg->step >= 0.0)) return TRD_ERR_INVALID_ARG;
+  if (cfg->world < 1 || cfg->rank < 0 || cfg->rank >= cfg->world) return TRD_ERR_INVALID_ARG;
+  if (cfg->shard_mode < 0 || cfg->shard_mode >= N) return TRD_ERR_SHAPE;
+  if (cfg->world > 1 && !cfg->nccl_unique_id) return TRD_ERR_INVALID_ARG;
+  if (!shard->values || !shard->mask_bits) return TRD_ERR_INVALID_ARG;
+  const int sm = cfg->shard_mode;
+  const int64_t sb = shard->shard_begin, se = shard->shard_end;
+  if (sb < 0 || se > cfg->dims[sm] || se <= sb) return TRD_ERR_SHAPE;
+  if (cfg->world == 1 && (sb != 0 || se != cfg->dims[sm])) return TRD_ERR_SHAPE;
+  if (cfg->dims[N - 1] > 16384) return TRD_ERR_SHAPE;   // D^t is I_N x I_N (Alg. 1 l.12)
+
+  Context* c = new (std::nothrow) Context();
+  if (!c) return TRD_ERR_OOM;
+  c->cfg = *cfg;
+  c->cfg.nccl_unique_id = nullptr;
+  c->N = N;
+  c->stream = (cudaStream_t)stream;
+  c->shard_begin = sb;
+  c->shard_end = se;
+  c->packed = shard->packed ? 1 : 0;
+  int64_t stride = 1;
+  for (int m = 0; m < N; ++m) {
+    c->dims[m] = cfg->dims[m];
+    c->ranks[m] = cfg->ranks[m];
+    c->ldims[m] = (m == sm) ? (se - sb) : cfg->dims[m];
+    c->lstride[m] = stride;
+    stride *= c->ldims[m];
+  }
+  c->n_local = stride;
+  c->n_words = (c->n_local + 31) / 32;
+  for (int k = 0; k < N; ++k)
+    if (c->ranks[k] * c->ranks[(k + 1) % N] > kMaxR2) { delete c; return TRD_ERR_SHAPE; }
+
+  trd_status st = TRD_OK;
+  auto bail = [&](trd_status s2) { trd_destroy(reinterpret_cast<trd_ctx*>(c)); return s2; };
+
+  // ---- plans and workspace sizes ----
+  size_t max_rows = 0, max_cols = 0, max_lft = 0, max_rgt = 0, max_mid = 0, max_dp = 0, max_sp = 0;
+  size_t max_dvec = 0, max_h = 0, idx_total = 0;
+  int64_t full_s[kMaxN];
+  for (int m = 0; m < N; ++m) full_s[m] = 0;
+  for (int k = 0; k <= N; ++k) {
+    BlockPlan& bp = (k < N) ? c->plan[k] : c->full_plan;
+    if (k < N) build_plan(*c, k, cfg->sketch, bp);
+    else build_plan(*c, 0, full_s, bp);
+    max_rows = std::max(max_rows, (size_t)bp.nrows);
+    max_cols = std::max(max_cols, (size_t)bp.ncols);
+    max_lft = std::max(max_lft, (size_t)(bp.nrows * bp.K));
+    max_rgt = std::max(max_rgt, (size_t)(bp.ncols * bp.K));
+    max_mid = std::max(max_mid, (size_t)(bp.nL * bp.rk1 * bp.rs));
+    const size_t Ik = (size_t)c->dims[bp.k];
+    max_dp = std::max(max_dp, Ik * ncta_of(bp) * (size_t)bp.R2);
+    max_sp = std::max(max_sp, Ik * ncta_of(bp) * 3);
+    max_dvec = std::max(max_dvec, Ik * (size_t)bp.R2 + 3);
+    max_h = std::max(max_h, Ik * (size_t)bp.R2);
+  }
+  for (int m = 0; m < N; ++m) { c->idx_off[m] = (int64_t)idx_total; idx_total += (size_t)c->dims[m]; }
+  c->idx_off[N] = (int64_t)idx_total;
+  max_dp = std::max(max_dp, (size_t)(148 * 4 * 6));
+
+  // ---- allocations ----
+  int64_t ztot = 0, qtot = 0;
+  for (int k = 0; k < N; ++k) {
+    c->zoff[k] = ztot;
+    c->qoff[k] = qtot;
+    const int64_t r0 = c->ranks[k], r1 = c->ranks[(k + 1) % N];
+    ztot += r0 * c->dims[k] * r1;
+    qtot += r0 * r0 * r1 * r1;
+  }
+  c->zoff[N] = ztot;
+  c->qoff[N] = qtot;
+  const int64_t In = c->dims[N - 1];
+  const size_t chain_cap = std::max((size_t)2 * kMaxR2 * kMaxR2, (size_t)In * kMaxR2);
+  if ((st = dalloc(c, &c->Z, (size_t)ztot)) || (st = dalloc(c, &c->Q, (size_t)qtot)) ||
+      (st = dalloc(c, &c->idx, idx_total)) || (st = dalloc(c, &c->doff, idx_total)) ||
+      (st = dalloc(c, &c->row_off, max_rows)) || (st = dalloc(c, &c->col_off, max_cols)) ||
+      (st = dalloc(c, &c->mid, max_mid)) || (st = dalloc(c, &c->lft, max_lft)) ||
+      (st = dalloc(c, &c->lfth, max_lft)) || (st = dalloc(c, &c->rgtT, max_rgt)) ||
+      (st = dalloc(c, &c->dpart, max_dp)) || (st = dalloc(c, &c->spart, max_sp)) ||
+      (st = dalloc(c, &c->denpart, max_sp)) || (st = dalloc(c, &c->numpart, max_h)) ||
+      (st = dalloc(c, &c->dvec, max_dvec)) || (st = dalloc(c, &c->G, (size_t)kMaxR2 * kMaxR2)) ||
+      (st = dalloc(c, &c->G_last, (size_t)kMaxR2 * kMaxR2)) ||
+      (st = dalloc(c, &c->Mop, (size_t)kMaxR2 * kMaxR2)) ||
+      (st = dalloc(c, &c->chol_ws, (size_t)2 * kMaxR2 * kMaxR2)) ||
+      (st = dalloc(c, &c->chain_ws, chain_cap)) || (st = dalloc(c, &c->h, max_h)) ||
+      (st = dalloc(c, &c->Dcur, (size_t)(In * In))) || (st = dalloc(c, &c->Dprev, (size_t)(In * In))) ||
+      (st = dalloc(c, &c->sc, 1)) || (st = dalloc(c, &c->red_ws, 1024)))
+    return bail(st);
+  if ((st = ensure_stats(c, 4))) return bail(st);
+  cudaStream_t s = c->stream;
+
+  // ---- data ----
+  if (shard->host) {
+    if ((st = dalloc(c, &c->own_mask, (size_t)c->n_words))) return bail(st);
+    CUDA_TRY(c, cudaMemcpyAsync(c->own_mask, shard->mask_bits, c->n_words * 4, cudaMemcpyHostToDevice, s));
+    c->mask = c->own_mask;
+  } else {
+    c->mask = shard->mask_bits;
+  }
+  if (c->packed) {
+    if ((st = dalloc(c, &c->rank_prefix, (size_t)c->n_words))) return bail(st);
+    launch_rank_prefix(*c, s);
+    uint32_t last_pref = 0, last_word = 0;
+    CUDA_TRY(c, cudaMemcpyAsync(&last_pref, c->rank_prefix + c->n_words - 1, 4, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(c, cudaMemcpyAsync(&last_word, c->mask + c->n_words - 1, 4, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(c, cudaStreamSynchronize(s));
+    int64_t tail_bits = c->n_local - (c->n_words - 1) * 32;
+    if (tail_bits < 32) last_word &= (1u << tail_bits) - 1u;
+    c->n_values = (int64_t)last_pref + __builtin_popcount(last_word);
+  } else {
+    c->n_values = c->n_local;
+  }
+  if (shard->host) {
+    if ((st = dalloc(c, &c->own_values, (size_t)c->n_values))) return bail(st);
+    CUDA_TRY(c, cudaMemcpyAsync(c->own_values, shard->values, c->n_values * 4, cudaMemcpyHostToDevice, s));
+    c->values = c->own_values;
+  } else {
+    c->values = shard->values;
+  }
+
+  // ---- cores, scalars, FGMC cache ----
+  {
+    std::vector<float> tmp;
+    for (int k = 0; k < N; ++k) {
+      host_to_dev_core(*c, k, init_cores[k], tmp);
+      CUDA_TRY(c, cudaMemcpy(c->Z + c->zoff[k], tmp.data(), tmp.size() * 4, cudaMemcpyHostToDevice));
+    }
+  }
+  DevScalars hs;
+  memset(&hs, 0, sizeof(hs));
+  hs.sigma = cfg->sigma_mode == TRD_SIGMA_FIXED ? cfg->sigma : (cfg->sigma_mode == TRD_SIGMA_INF ? INFINITY : 1.0);
+  CUDA_TRY(c, cudaMemcpyAsync(c->sc, &hs, sizeof(hs), cudaMemcpyHostToDevice, s));
+  CUDA_TRY(c, cudaMemsetAsync(c->Dprev, 0, (size_t)(In * In) * 8, s));
+  for (int k = 0; k < N; ++k) launch_q(*c, k, s);
+  if ((st = check_launch(c, "init Q"))) return bail(st);
+
+  // ---- NCCL ----
+  if (cfg->world > 1) {
+    if (!load_nccl()) return bail(fail(c, TRD_ERR_NCCL, "libnccl.so.2 could not be loaded"));
+    NcclId id;
+    memcpy(id.internal, cfg->nccl_unique_id, 128);
+    CUDA_TRY(c, cudaStreamSynchronize(s));
+    int r = g_nccl.comm_init_rank(&c->nccl_comm, cfg->world, id, cfg->rank);
+    if (r != 0) return bail(fail(c, TRD_ERR_NCCL, "ncclCommInitRank failed (%d)", r));
+  }
+  if (cfg->sigma_mode == TRD_SIGMA_RMS) {
+    if ((st = sigma0_pass(c))) return bail(st);
+  }
+  CUDA_TRY(c, cudaStreamSynchronize(s));
+  *out = reinterpret_cast<trd_ctx*>(c);
+  return TRD_OK;
+}
+
+trd_status trd_upload(trd_ctx* ctx, const float* values_host, const uint32_t* mask_host) {
+  Context* c = reinterpret_cast<Context*>(ctx);
+  if (!c || !values_host || !mask_host) return TRD_ERR_INVALID_ARG;
+  if (c->sticky) return c->sticky;
+  if (!c->own_values || !c->own_mask) return fail(c, TRD_ERR_STATE, "shard is not host-resident");
+  CUDA_TRY(c, cudaMemcpyAsync(c->own_mask, mask_host, c->n_words * 4, cudaMemcpyHostToDevice, c->stream));
+  CUDA_TRY(c, cudaMemcpyAsync(c->own_values, values_host, c->n_values * 4, cudaMemcpyHostToDevice, c->stream));
+  if (c->packed) launch_rank_prefix(*c, c->stream);
+  return check_launch(c, "upload");
+}
+
+trd_status trd_sketch(trd_ctx* ctx, int32_t sweep, int32_t k, int32_t* idx_dev, int64_t* sizes_host) {
+  Context* c = reinterpret_cast<Context*>(ctx);
+  if (!c || !idx_dev || !sizes_host) return TRD_ERR_INVALID_ARG;
+  if (c->sticky) return c->sticky;
+  if (k < 0 || k >= c->N || sweep < 0) return TRD_ERR_INVALID_ARG;
+  const BlockPlan& bp = c->plan[k];
+  int saved = 0;
+  CUDA_TRY(c, cudaMemcpy(&saved, &c->sc->sweep, 4, cudaMemcpyDeviceToHost));
+  CUDA_TRY(c, cudaMemcpyAsync(&c->sc->sweep, &sweep, 4, cudaMemcpyHostToDevice, c->stream));
+  launch_sampler(*c, bp, c->stream);
+  trd_status st = check_launch(c, "sampler");
+  if (st) return st;
+  int64_t off = 0;
+  for (int m = 0; m < c->N; ++m) {
+    CUDA_TRY(c, cudaMemcpyAsync(idx_dev + off, c->idx + c->idx_off[m], bp.s[m] * 4,
+                                cudaMemcpyDeviceToDevice, c->stream));
+    sizes_host[m] = bp.s[m];
+    off += bp.s[m];
+  }
+  CUDA_TRY(c, cudaMemcpyAsync(&c->sc->sweep, &saved, 4, cudaMemcpyHostToDevice, c->stream));
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  return TRD_OK;
+}
+
+trd_status trd_sweep(trd_ctx* ctx, int32_t n_sweeps, trd_sweep_stats* stats) {
+  Context* c = reinterpret_cast<Context*>(ctx);
+  if (!c || n_sweeps < 0) return TRD_ERR_INVALID_ARG;
+  if (c->sticky) return c->sticky;
+  if (n_sweeps == 0) return TRD_OK;
+  trd_status st = ensure_stats(c, n_sweeps);
+  if (st) return st;
+  cudaStream_t s = c->stream;
+  std::vector<cudaEvent_t> ev;
+  if (stats) {
+    ev.resize((size_t)n_sweeps + 1);
+    for (auto& e : ev) CUDA_TRY(c, cudaEventCreate(&e));
+    CUDA_TRY(c, cudaEventRecord(ev[0], s));
+  }
+  for (int t = 0; t < n_sweeps; ++t) {
+    launch_sweep_begin(*c, t, s);
+    for (int k = 0; k < c->N; ++k) {
+      const BlockPlan& bp = c->plan[k];
+      if ((st = block_pass1(c, bp))) return st;
+      if ((st = block_pass2(c, bp))) return st;
+      if (k == c->N - 1)
+        CUDA_TRY(c, cudaMemcpyAsync(c->G_last, c->G, (size_t)bp.R2 * bp.R2 * 8, cudaMemcpyDeviceToDevice, s));
+      launch_update(*c, bp, t, s);
+      launch_q(*c, k, s);
+      if ((st = check_launch(c, "update"))) return st;
+    }
+    launch_sweep_end(*c, t, s);
+    if ((st = check_launch(c, "sweep end"))) return st;
+    if (stats) CUDA_TRY(c, cudaEventRecord(ev[(size_t)t + 1], s));
+  }
+  if (!stats) return TRD_OK;
+  std::vector<DevStats> hs((size_t)n_sweeps);
+  CUDA_TRY(c, cudaMemcpyAsync(hs.data(), c->stats, sizeof(DevStats) * n_sweeps, cudaMemcpyDeviceToHost, s));
+  DevScalars sc;
+  CUDA_TRY(c, cudaMemcpyAsync(&sc, c->sc, sizeof(sc), cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(c, cudaStreamSynchronize(s));
+  bool nonfinite = false;
+  for (int t = 0; t < n_sweeps; ++t) {
+    trd_sweep_stats& o = stats[t];
+    memset(&o, 0, sizeof(o));
+    const DevStats& d = hs[(size_t)t];
+    o.sigma = d.sigma; o.sum_e2 = d.sum_e2; o.welsch_loss = d.welsch; o.stop_e = d.stop_e;
+    o.n_obs = d.n_obs;
+    for (int k = 0; k < c->N; ++k) { o.eta[k] = d.eta[k]; o.num[k] = d.num[k]; o.den[k] = d.den[k]; o.nnz[k] = d.nnz[k]; }
+    o.skipped_mask = d.skipped;
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, ev[(size_t)t], ev[(size_t)t + 1]);
+    o.ms = ms;
+    nonfinite |= d.nonfinite != 0;
+  }
+  for (auto& e : ev) cudaEventDestroy(e);
+  if (sc.not_spd) return fail(c, TRD_ERR_NOT_SPD, "G + lambda I not positive definite after retries");
+  if (nonfinite || sc.nonfinite) return fail(c, TRD_ERR_NONFINITE, "non-finite step or statistics");
+  return TRD_OK;
+}
+
+trd_status trd_block_probe(trd_ctx* ctx, int32_t sweep, int32_t k, double* d_host, double* G_host,
+                           double* h_host, double* stats5_host) {
+  Context* c = reinterpret_cast<Context*>(ctx);
+  if (!c) return TRD_ERR_INVALID_ARG;
+  if (c->sticky) return c->sticky;
+  if (k < 0 || k >= c->N || sweep < 0) return TRD_ERR_INVALID_ARG;
+  const BlockPlan& bp = c->plan[k];
+  cudaStream_t s = c->stream;
+  int saved = 0;
+  CUDA_TRY(c, cudaMemcpy(&saved, &c->sc->sweep, 4, cudaMemcpyDeviceToHost));
+  CUDA_TRY(c, cudaMemcpyAsync(&c->sc->sweep, &sweep, 4, cudaMemcpyHostToDevice, s));
+  trd_status st;
+  if ((st = block_pass1(c, bp))) return st;
+  if ((st = block_pass2(c, bp))) return st;
+  const int64_t Ik = c->dims[k];
+  std::vector<double> dv((size_t)(Ik * bp.R2 + 3));
+  double nd[2];
+  CUDA_TRY(c, cudaMemcpyAsync(dv.data(), c->dvec, dv.size() * 8, cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(c, cudaMemcpyAsync(nd, c->red_ws, 16, cudaMemcpyDeviceToHost, s));
+  if (G_host) CUDA_TRY(c, cudaMemcpyAsync(G_host, c->G, (size_t)bp.R2 * bp.R2 * 8, cudaMemcpyDeviceToHost, s));
+  if (h_host) CUDA_TRY(c, cudaMemcpyAsync(h_host, c->h, (size_t)(Ik * bp.R2) * 8, cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(c, cudaMemcpyAsync(&c->sc->sweep, &saved, 4, cudaMemcpyHostToDevice, s));
+  CUDA_TRY(c, cudaStreamSynchronize(s));
+  if (d_host) memcpy(d_host, dv.data(), (size_t)(Ik * bp.R2) * 8);
+  if (stats5_host) {
+    stats5_host[0] = dv[(size_t)(Ik * bp.R2)];
+    stats5_host[1] = dv[(size_t)(Ik * bp.R2) + 2];
+    stats5_host[2] = dv[(size_t)(Ik * bp.R2) + 1];
+    stats5_host[3] = nd[1];
+    stats5_host[4] = nd[0];
+  }
+  return TRD_OK;
+}
+
+trd_status trd_reconstruct(trd_ctx* ctx, const int64_t* lin_idx_dev, int64_t n, float* out_dev) {
+  Context* c = reinterpret_cast<Context*>(ctx);
+  if (!c || (n > 0 && (!lin_idx_dev || !out_dev)) || n < 0) return TRD_ERR_INVALID_ARG;
+  if (c->sticky) return c->sticky;
+  if (n == 0) return TRD_OK;
+  launch_reconstruct(*c, lin_idx_dev, n, out_dev, c->stream);
+  return check_launch(c, "reconstruct");
+}
+
+trd_status trd_error(trd_ctx* ctx, const float* ref_dev, const uint32_t* eval_bits, trd_error_stats* out) {
+  Context* c = reinterpret_cast<Context*>(ctx);
+  if (!c || !ref_dev || !out) return TRD_ERR_INVALID_ARG;
+  if (c->sticky) return c->sticky;
+  const BlockPlan& bp = c->full_plan;
+  cudaStream_t s = c->stream;
+  launch_sampler(*c, bp, s);
+  launch_plan(*c, bp, s);
+  launch_lft(*c, bp, c->Z + c->zoff[bp.k], 0, c->lft, s);
+  launch_error(*c, ref_dev, eval_bits, c->red_ws, s);
+  trd_status st = check_launch(c, "error");
+  if (st) return st;
+  double v[6];
+  if (c->cfg.world > 1) {
+    if ((st = allreduce(c, c->red_ws, 5))) return st;                 // sums
+    if ((st = allreduce(c, c->red_ws + 5, 1, kNcclMax))) return st;   // max |ref|
+  }
+  CUDA_TRY(c, cudaMemcpyAsync(v, c->red_ws, sizeof(v), cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(c, cudaStreamSynchronize(s));
+  out->rel_err_all = v[1] > 0 ? sqrt(v[0] / v[1]) : 0.0;
+  out->rel_err_observed = v[3] > 0 ? sqrt(v[2] / v[3]) : 0.0;
+  out->n_eval = (int64_t)v[4];
+  const double mse = v[4] > 0 ? v[0] / v[4] : 0.0;
+  out->psnr = mse > 0 ? 10.0 * log10(v[5] * v[5] / mse) : INFINITY;
+  return TRD_OK;
+}
+
+trd_status trd_get_cores(trd_ctx* ctx, float* const* cores_host) {
+  Context* c = reinterpret_cast<Context*>(ctx);
+  if (!c || !cores_host) return TRD_ERR_INVALID_ARG;
+  std::vector<float> tmp;
+  cudaStreamSynchronize(c->stream);
+  for (int k = 0; k < c->N; ++k) {
+    if (!cores_host[k]) return TRD_ERR_INVALID_ARG;
+    const int r0 = c->ranks[k], r1 = c->ranks[(k + 1) % c->N];
+    const int64_t I = c->dims[k];
+    tmp.resize((size_t)(r0 * I * r1));
+    cudaError_t e = cudaMemcpy(tmp.data(), c->Z + c->zoff[k], tmp.size() * 4, cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) return fail(c, TRD_ERR_CUDA, "get_cores: %s", cudaGetErrorString(e));
+    for (int a = 0; a < r0; ++a)
+      for (int64_t i = 0; i < I; ++i)
+        for (int b = 0; b < r1; ++b) cores_host[k][(a * I + i) * r1 + b] = tmp[(i * r0 + a) * r1 + b];
+  }
+  return TRD_OK;
+}
+
+trd_status trd_set_cores(trd_ctx* ctx, const float* const* cores_host) {
+  Context* c = reinterpret_cast<Context*>(ctx);
+  if (!c || !cores_host) return TRD_ERR_INVALID_ARG;
+  if (c->sticky) return c->sticky;
+  std::vector<float> tmp;
+  for (int k = 0; k < c->N; ++k) {
+    if (!cores_host[k]) return TRD_ERR_INVALID_ARG;
+    host_to_dev_core(*c, k, cores_host[k], tmp);
+    CUDA_TRY(c, cudaMemcpyAsync(c->Z + c->zoff[k], tmp.data(), tmp.size() * 4, cudaMemcpyHostToDevice, c->stream));
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  }
+  for (int k = 0; k < c->N; ++k) launch_q(*c, k, c->stream);
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  return check_launch(c, "set_cores");
+}
+
+void trd_destroy(trd_ctx* ctx) {
+  Context* c = reinterpret_cast<Context*>(ctx);
+  if (!c) return;
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  if (c->nccl_comm && g_nccl.comm_destroy) g_nccl.comm_destroy(c->nccl_comm);
+  for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
+  void* ptrs[] = {c->own_values, c->own_mask, c->rank_prefix, c->Z, c->Q, c->idx, c->doff,
+                  c->row_off, c->col_off, c->mid, c->lft, c->lfth, c->rgtT, c->dpart, c->spart,
+                  c->denpart, c->numpart, c->dvec, c->G, c->G_last, c->Mop, c->chol_ws,
+                  c->chain_ws, c->h, c->Dcur, c->Dprev, c->sc, c->stats, c->red_ws};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  delete c;
+}
+
+}  // extern "C"

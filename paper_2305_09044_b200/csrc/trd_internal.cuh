@@ -1,0 +1,159 @@
+// trd_internal.cuh -- context layout, block plans and kernel entry points of libtrd.
+// Paper citations "P:L" are PAPER.md lines.  See DESIGN.md for the data layout in HBM.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <string>
+#include <vector>
+
+#include "../../include/trd.h"
+
+namespace trd {
+
+constexpr int kMaxN = TRD_MAX_ORDER;
+constexpr int kMaxR = TRD_MAX_RANK;
+constexpr int kMaxR2 = kMaxR * kMaxR;
+
+// Per-sweep statistics kept on the device (one record per sweep of a trd_sweep call).
+struct DevStats {
+  double sigma, sum_e2, welsch, stop_e;
+  long long n_obs;
+  double eta[kMaxN], num[kMaxN], den[kMaxN];
+  long long nnz[kMaxN];
+  unsigned int skipped;
+  int nonfinite;
+};
+
+// Scalars shared by the kernels of one block (device memory).
+struct DevScalars {
+  double sigma;          // kernel width of the current sweep
+  double num, den;       // <d,h> and the line-search denominator of the current block
+  double sum_e2, welsch; // pass-1 statistics of the current block (after allreduce)
+  double n_obs;          // observed entries of the block (double so it rides the allreduce)
+  double eta;            // step of the current block
+  double lambda;         // lambda used by the solve
+  int sweep;             // sweep counter t (read by the sampler: graph-replayable)
+  int not_spd;           // Cholesky failed after retries
+  int nonfinite;         // non-finite value detected
+  double acc_e2, acc_n;  // sweep accumulators for the RMS sigma rule (R9)
+  double stop_e;         // relative change of D^t
+  int have_prev_D;
+  int prof_on;           // accumulate local observed entries per block (profiling)
+  double prof_nobs[kMaxN];
+};
+
+// GEMM form of block k: the working set WS_k = I_k x prod_{m!=k} s_m is
+// a (rows x cols) matrix with rows = (j_L, i_k) [j_L over the left modes k+1..k+p, fastest
+// first] and cols = j_R over the right modes k+p+1..k-1.  The subchain splits as
+// S(j) = Mid(j_L) Rgt(j_R) and x_hat = Tr(Lft Rgt) with Lft = Z_k(i_k) Mid(j_L) (Thm 1,
+// P:61-66; Def. 2), so each entry costs one K = r_k * r_{k+p+1} inner product.
+struct BlockPlan {
+  int k, p;
+  int nleft, nright;
+  int left[kMaxN], right[kMaxN];
+  int rk, rk1, rs;       // r_k, r_{k+1}, r_{k+p+1}
+  int K, R2;             // rk*rs, rk*rk1
+  int64_t s[kMaxN];      // sizes of the index sets of this block (s_k = I_k)
+  int64_t nL, nrows, ncols;
+  int64_t nnz_ws;        // |WS_k| (all entries, observed or not)
+  // pass-kernel geometry
+  int jl_per_cta, ws_split, nsplit;
+  int64_t grid_x;        // ceil(nL / jl_per_cta)
+};
+
+struct Context {
+  trd_config cfg;
+  int N;
+  int64_t dims[kMaxN], ldims[kMaxN];   // global / local dims
+  int64_t lstride[kMaxN];              // local linear strides
+  int ranks[kMaxN];
+  int64_t shard_begin, shard_end;
+  int64_t n_local, n_words;
+  int packed;
+  cudaStream_t stream;
+  std::string err;
+  trd_status sticky = TRD_OK;
+  long long launches = 0;
+
+  // data (device)
+  const float* values = nullptr;
+  const uint32_t* mask = nullptr;
+  float* own_values = nullptr;         // host-resident shards: library-owned copies
+  uint32_t* own_mask = nullptr;
+  int64_t n_values = 0;
+  uint32_t* rank_prefix = nullptr;     // packed layout: exclusive popcount prefix per word
+
+  // model (device)
+  float* Z = nullptr;                  // cores, slice-major: Z_k[i][a][b]
+  int64_t zoff[kMaxN + 1];
+  double* Q = nullptr;                 // FGMC Q_k (r_k^2 x r_{k+1}^2)
+  int64_t qoff[kMaxN + 1];
+
+  // plans and per-block workspaces (device)
+  BlockPlan plan[kMaxN];
+  BlockPlan full_plan;                 // full index sets (sigma_0 pass, trd_error)
+  int32_t* idx = nullptr;              // index sets of the current block, per mode
+  int64_t* doff = nullptr;             // data offset of each index (or -1 outside shard)
+  int64_t idx_off[kMaxN + 1];
+  int64_t* row_off = nullptr;          // per GEMM row
+  int64_t* col_off = nullptr;          // per GEMM col
+  float* mid = nullptr;                // Mid(j_L): r_{k+1} x r_s
+  float* lft = nullptr;                // Lft rows: [row][K]
+  float* lfth = nullptr;               // Lft of the scaled gradient (pass 2)
+  float* rgtT = nullptr;               // Rgt: [K][ncols]
+  double* dpart = nullptr;             // pass-1 CTA partials of d
+  double* spart = nullptr;             // pass-1 CTA partial stats (3 per CTA)
+  double* denpart = nullptr;           // pass-2 CTA partials
+  double* numpart = nullptr;
+  double* dvec = nullptr;              // [d (I_k x R2) | sum_e2 | welsch | n] allreduce buffer
+  double* G = nullptr;                 // Gram of the current block
+  double* G_last = nullptr;            // Gram of block N-1 (stop metric)
+  double* Mop = nullptr;               // filtered operator M = A^-1 G A^-1
+  double* chol_ws = nullptr;           // solve workspace (global fallback)
+  double* chain_ws = nullptr;          // FGMC chain workspace (2 matrices)
+  double* h = nullptr;                 // scaled gradient (I_k x R2)
+  double* Dcur = nullptr;              // D^t
+  double* Dprev = nullptr;             // D^{t-1}
+  DevScalars* sc = nullptr;
+  DevStats* stats = nullptr;
+  int stats_cap = 0;
+  double* red_ws = nullptr;            // small reductions
+  size_t max_dpart = 0, max_spart = 0;
+
+  // NCCL (world > 1)
+  void* nccl_comm = nullptr;
+
+  // profiling (trd_set_profiling / trd_get_profile)
+  bool prof = false;
+  std::vector<cudaEvent_t> ev_pool;
+  std::vector<std::pair<int, int>> ev_pass1, ev_pass2;   // indices into ev_pool
+  size_t ev_used = 0;
+};
+
+// ---- kernels (trd_kernels.cu) --------------------------------------------------------
+void launch_sampler(Context& c, const BlockPlan& bp, cudaStream_t s);
+void launch_plan(Context& c, const BlockPlan& bp, cudaStream_t s);
+void launch_lft(Context& c, const BlockPlan& bp, const float* Zsrc_k, int src_is_h, float* out,
+                cudaStream_t s);
+void launch_pass1(Context& c, const BlockPlan& bp, int stats_only, cudaStream_t s);
+void launch_reduce_d(Context& c, const BlockPlan& bp, cudaStream_t s);
+void launch_block_stats(Context& c, const BlockPlan& bp, cudaStream_t s);
+void launch_q(Context& c, int k, cudaStream_t s);
+void launch_gram(Context& c, const BlockPlan& bp, cudaStream_t s);
+void launch_solve(Context& c, const BlockPlan& bp, cudaStream_t s);
+void launch_h(Context& c, const BlockPlan& bp, cudaStream_t s);
+void launch_pass2(Context& c, const BlockPlan& bp, cudaStream_t s);
+void launch_reduce_den(Context& c, const BlockPlan& bp, cudaStream_t s);
+void launch_update(Context& c, const BlockPlan& bp, int sweep_slot, cudaStream_t s);
+void launch_sweep_end(Context& c, int sweep_slot, cudaStream_t s);
+void launch_sigma0(Context& c, cudaStream_t s);
+void launch_reconstruct(Context& c, const int64_t* lin, int64_t n, float* out, cudaStream_t s);
+void launch_error(Context& c, const float* ref, const uint32_t* eval_bits, double* out4,
+                  cudaStream_t s);
+void launch_rank_prefix(Context& c, cudaStream_t s);
+void launch_reset_block_scalars(Context& c, cudaStream_t s);
+void launch_record_block(Context& c, const BlockPlan& bp, int slot, cudaStream_t s);
+void launch_sweep_begin(Context& c, int slot, cudaStream_t s);
+void launch_fill_full_sets(Context& c, const BlockPlan& bp, cudaStream_t s);
+
+}  // namespace trd

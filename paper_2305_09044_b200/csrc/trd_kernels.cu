@@ -1,0 +1,1153 @@
+// trd_kernels.cu -- device kernels of libtrd (sm_100a).
+//
+// Paper citations "P:L" are PAPER.md lines.  The block pipeline (one cyclic block k of
+// Alg. 1) is:
+//   sampler (Alg.1 l.4)  -> plan/offsets + chain products (Thm 1 subchain split)
+//   -> pass 1: residual, HQ weight, gradient partials (Eq. 7, Eq. 9/15)
+//   -> reduce_d -> [NCCL allreduce] -> FGMC Gram (Eq. 13) -> filtered solve (Eq. 10/16)
+//   -> h = d M -> pass 2: line-search denominator (Eq. 12/18) -> [allreduce]
+//   -> update Z_k (Eq. 11/17, sign reading R2) -> refresh Q_k (Alg. 1 l.10)
+#include <cub/cub.cuh>
+#include <math.h>
+
+#include "trd_internal.cuh"
+
+namespace trd {
+
+#define CK(x) do { cudaError_t e__ = (x); (void)e__; } while (0)
+
+// ----------------------------------------------------------------------------------------
+// Philox4x32-10 (Salmon et al. 2011) -- reading R11.  Independent of oracle/philox.py.
+// ----------------------------------------------------------------------------------------
+__device__ __forceinline__ void philox10(uint32_t c[4], uint32_t k0, uint32_t k1) {
+  const uint32_t M0 = 0xD2511F53u, M1 = 0xCD9E8D57u;
+  const uint32_t W0 = 0x9E3779B9u, W1 = 0xBB67AE85u;
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    if (r > 0) { k0 += W0; k1 += W1; }
+    uint32_t hi0 = __umulhi(M0, c[0]), lo0 = M0 * c[0];
+    uint32_t hi1 = __umulhi(M1, c[2]), lo1 = M1 * c[2];
+    uint32_t n0 = hi1 ^ c[1] ^ k0, n1 = lo1, n2 = hi0 ^ c[3] ^ k1, n3 = lo0;
+    c[0] = n0; c[1] = n1; c[2] = n2; c[3] = n3;
+  }
+}
+
+// One CTA per mode m: writes the index set I_m of (sweep t, block k) and the data offsets.
+// Selection = the s_m smallest (kappa_i, i), output ascending (rank-based, deterministic).
+struct SamplerArgs {
+  int N, k, shard_mode;
+  uint64_t seed;
+  int64_t shard_begin, shard_end;
+  int64_t dims[kMaxN], s[kMaxN], idx_off[kMaxN + 1], lstride[kMaxN];
+};
+
+__global__ void sampler_kernel(SamplerArgs sa, const DevScalars* __restrict__ sc,
+                               int32_t* __restrict__ idx, int64_t* __restrict__ doff) {
+  extern __shared__ unsigned long long keys[];
+  const int m = blockIdx.x;
+  const int k = sa.k;
+  const uint64_t seed = sa.seed;
+  const int64_t I = sa.dims[m];
+  const int64_t s = sa.s[m] <= 0 ? I : sa.s[m];
+  int32_t* out = idx + sa.idx_off[m];
+  int64_t* dof = doff + sa.idx_off[m];
+  const uint32_t t = (uint32_t)sc->sweep;
+  if (s >= I) {
+    for (int64_t i = threadIdx.x; i < I; i += blockDim.x) out[i] = (int32_t)i;
+  } else {
+    for (int64_t i = threadIdx.x; i < I; i += blockDim.x) {
+      uint32_t c[4] = {(uint32_t)i, (uint32_t)m, (uint32_t)k, t};
+      philox10(c, (uint32_t)(seed & 0xffffffffu), (uint32_t)(seed >> 32));
+      keys[i] = ((unsigned long long)c[0] << 32) | c[1];
+    }
+    __syncthreads();
+    // rank of each i; selected if rank < s
+    unsigned char* sel = reinterpret_cast<unsigned char*>(keys + I);
+    for (int64_t i = threadIdx.x; i < I; i += blockDim.x) {
+      const unsigned long long ki = keys[i];
+      int64_t rank = 0;
+      for (int64_t j = 0; j < I; ++j) {
+        const unsigned long long kj = keys[j];
+        rank += (kj < ki) || (kj == ki && j < i);
+      }
+      sel[i] = rank < s;
+    }
+    __syncthreads();
+    for (int64_t i = threadIdx.x; i < I; i += blockDim.x) {
+      if (!sel[i]) continue;
+      int64_t pos = 0;
+      for (int64_t j = 0; j < i; ++j) pos += sel[j];
+      out[pos] = (int32_t)i;
+    }
+  }
+  __syncthreads();
+  const int64_t cnt = s >= I ? I : s;
+  for (int64_t q = threadIdx.x; q < cnt; q += blockDim.x) {
+    int64_t g = out[q];
+    int64_t loc = g;
+    if (m == sa.shard_mode) loc = (g >= sa.shard_begin && g < sa.shard_end) ? g - sa.shard_begin : -1;
+    dof[q] = loc < 0 ? -1 : loc * sa.lstride[m];
+  }
+}
+
+// ----------------------------------------------------------------------------------------
+// Plan kernels: row/col data offsets and the chain products Mid, Lft, Rgt (Thm 1 subchain,
+// P:63-66; Def. 2 merging).  Slice of core m at index i: Z + zoff[m] + i*r_m*r_{m+1}.
+// ----------------------------------------------------------------------------------------
+struct PlanArgs {
+  int N, k, p, nleft, nright;
+  int left[kMaxN], right[kMaxN];
+  int64_t sL[kMaxN], sR[kMaxN];        // sizes of the left/right index sets
+  int64_t offL[kMaxN], offR[kMaxN];    // offsets into idx/doff
+  int64_t off_k;
+  int64_t nL, nrows, ncols;
+  int rk, rk1, rs, K;
+  int rank_of[kMaxN + 1];
+  int64_t zoff[kMaxN + 1];
+};
+
+static PlanArgs make_plan_args(const Context& c, const BlockPlan& bp) {
+  PlanArgs a;
+  a.N = c.N; a.k = bp.k; a.p = bp.p; a.nleft = bp.nleft; a.nright = bp.nright;
+  for (int q = 0; q < bp.nleft; ++q) {
+    a.left[q] = bp.left[q]; a.sL[q] = bp.s[bp.left[q]]; a.offL[q] = c.idx_off[bp.left[q]];
+  }
+  for (int q = 0; q < bp.nright; ++q) {
+    a.right[q] = bp.right[q]; a.sR[q] = bp.s[bp.right[q]]; a.offR[q] = c.idx_off[bp.right[q]];
+  }
+  a.off_k = c.idx_off[bp.k];
+  a.nL = bp.nL; a.nrows = bp.nrows; a.ncols = bp.ncols;
+  a.rk = bp.rk; a.rk1 = bp.rk1; a.rs = bp.rs; a.K = bp.K;
+  for (int m = 0; m <= c.N; ++m) a.rank_of[m] = c.ranks[m % c.N];
+  for (int m = 0; m <= c.N; ++m) a.zoff[m] = c.zoff[m];
+  return a;
+}
+
+__global__ void offsets_kernel(PlanArgs a, const int64_t* __restrict__ doff,
+                               int64_t* __restrict__ row_off, int64_t* __restrict__ col_off) {
+  const int64_t tot = a.nrows + a.ncols;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tot;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    if (t < a.nrows) {
+      int64_t jl = t % a.nL, ik = t / a.nL;
+      int64_t o = doff[a.off_k + ik];
+      bool bad = o < 0;
+      for (int q = 0; q < a.nleft; ++q) {
+        int64_t dgt = jl % a.sL[q];
+        jl /= a.sL[q];
+        int64_t v = doff[a.offL[q] + dgt];
+        bad |= v < 0;
+        o += v;
+      }
+      row_off[t] = bad ? -1 : o;
+    } else {
+      int64_t col = t - a.nrows, o = 0;
+      bool bad = false;
+      for (int q = 0; q < a.nright; ++q) {
+        int64_t dgt = col % a.sR[q];
+        col /= a.sR[q];
+        int64_t v = doff[a.offR[q] + dgt];
+        bad |= v < 0;
+        o += v;
+      }
+      col_off[t - a.nrows] = bad ? -1 : o;
+    }
+  }
+}
+
+// v (row vector, length r_in) <- v * Z_m(i)  (r_in x r_out slice)
+__device__ __forceinline__ void vecmat(float* v, const float* __restrict__ Zs, int rin, int rout) {
+  float nv[kMaxR];
+#pragma unroll
+  for (int c = 0; c < kMaxR; ++c) nv[c] = 0.f;
+  for (int a = 0; a < rin; ++a) {
+    const float va = v[a];
+    const float* row = Zs + a * rout;
+#pragma unroll
+    for (int c = 0; c < kMaxR; ++c)
+      if (c < rout) nv[c] = fmaf(va, __ldg(row + c), nv[c]);
+  }
+#pragma unroll
+  for (int c = 0; c < kMaxR; ++c) v[c] = nv[c];
+}
+
+// Mid(j_L)[b][c] = (Z_{k+1}(.) .. Z_{k+p}(.))[b][c]   (r_{k+1} x r_s), one thread per (jl, b)
+__global__ void mid_kernel(PlanArgs a, const int32_t* __restrict__ idx, const float* __restrict__ Z,
+                           float* __restrict__ mid) {
+  const int64_t tot = a.nL * a.rk1;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tot;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    int b = (int)(t % a.rk1);
+    int64_t jl = t / a.rk1, rem = jl;
+    float v[kMaxR];
+#pragma unroll
+    for (int c = 0; c < kMaxR; ++c) v[c] = (c == b) ? 1.f : 0.f;
+    int rin = a.rk1;
+    for (int q = 0; q < a.nleft; ++q) {
+      int m = a.left[q];
+      int64_t dgt = rem % a.sL[q];
+      rem /= a.sL[q];
+      int64_t i = idx[a.offL[q] + dgt];
+      int rout = a.rank_of[m + 1];
+      vecmat(v, Z + a.zoff[m] + i * (int64_t)a.rank_of[m] * rout, rin, rout);
+      rin = rout;
+    }
+    float* o = mid + (jl * a.rk1 + b) * a.rs;
+    for (int c = 0; c < a.rs; ++c) o[c] = v[c];
+  }
+}
+
+// Rgt(j_R) = Z_{k+p+1}(.) .. Z_{k-1}(.)  (r_s x r_k); stored RgtT[(a + r_k c) * ncols + col]
+// = Rgt[c][a].  One thread per (col, c).
+__global__ void rgt_kernel(PlanArgs a, const int32_t* __restrict__ idx, const float* __restrict__ Z,
+                           float* __restrict__ rgtT) {
+  const int64_t tot = a.ncols * a.rs;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tot;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    int64_t col = t % a.ncols;
+    int cc = (int)(t / a.ncols);
+    int64_t rem = col;
+    float v[kMaxR];
+#pragma unroll
+    for (int c = 0; c < kMaxR; ++c) v[c] = (c == cc) ? 1.f : 0.f;
+    int rin = a.rs;
+    for (int q = 0; q < a.nright; ++q) {
+      int m = a.right[q];
+      int64_t dgt = rem % a.sR[q];
+      rem /= a.sR[q];
+      int64_t i = idx[a.offR[q] + dgt];
+      int rout = a.rank_of[m + 1];
+      vecmat(v, Z + a.zoff[m] + i * (int64_t)a.rank_of[m] * rout, rin, rout);
+      rin = rout;
+    }
+    for (int aa = 0; aa < a.rk; ++aa) rgtT[(int64_t)(aa + a.rk * cc) * a.ncols + col] = v[aa];
+  }
+}
+
+// Lft(row)[a + r_k c] = (X_k(i_k) Mid(j_L))[a][c] where X_k is the core slice (pass 1) or
+// the folded scaled gradient H(i_k)[a][b] = h[i_k][a + r_k b] (pass 2).  Thread per (row, a).
+__global__ void lft_kernel(PlanArgs a, const float* __restrict__ Zk, const double* __restrict__ h,
+                           const float* __restrict__ mid, float* __restrict__ lft) {
+  const int64_t tot = a.nrows * a.rk;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tot;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    int aa = (int)(t % a.rk);
+    int64_t row = t / a.rk;
+    int64_t jl = row % a.nL, ik = row / a.nL;
+    float v[kMaxR];
+#pragma unroll
+    for (int b = 0; b < kMaxR; ++b) {
+      if (b < a.rk1) {
+        v[b] = h ? (float)h[ik * a.rk * a.rk1 + aa + a.rk * b]
+                 : __ldg(Zk + (ik * a.rk + aa) * a.rk1 + b);
+      } else {
+        v[b] = 0.f;
+      }
+    }
+    float* o = lft + row * a.K;
+    if (a.p == 0) {
+      for (int c = 0; c < a.rk1; ++c) o[aa + a.rk * c] = v[c];
+    } else {
+      vecmat(v, mid + jl * a.rk1 * a.rs, a.rk1, a.rs);
+      for (int c = 0; c < a.rs; ++c) o[aa + a.rk * c] = v[c];
+    }
+  }
+}
+
+// ----------------------------------------------------------------------------------------
+// Pass kernels (v1, SIMT).  CTA = (jl chunk, i_k, column split); warp = one GEMM row and a
+// column sub-range; lane = one column per 32-column chunk.  Only observed entries
+// contribute (P mask); the working set is the sketch (Eq. 14-15).
+// ----------------------------------------------------------------------------------------
+struct PassArgs {
+  int64_t nL, nrows, ncols;
+  int K, R2, rk, rk1, rs, p;
+  int jl_per_cta, ws_split, nsplit;
+  int sigma_inf, packed;
+  const int64_t* row_off;
+  const int64_t* col_off;
+  const float* lft;
+  const float* lfth;
+  const float* rgtT;
+  const float* mid;
+  const float* values;
+  const uint32_t* mask;
+  const uint32_t* rank_prefix;
+  const DevScalars* sc;
+  double* dpart;      // [ik][cta][R2]
+  double* spart;      // [ik][cta][3]
+  double* denpart;    // [ik][cta]
+};
+
+__device__ __forceinline__ float warp_sum_f(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ double warp_sum_d(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__device__ __forceinline__ bool load_entry(const PassArgs& a, int64_t ro, int64_t co, float& x) {
+  if (co < 0) return false;
+  const int64_t lin = ro + co;
+  const uint32_t word = __ldg(a.mask + (lin >> 5));
+  const uint32_t bit = (uint32_t)(lin & 31);
+  if (!((word >> bit) & 1u)) return false;
+  int64_t vi = lin;
+  if (a.packed) vi = (int64_t)__ldg(a.rank_prefix + (lin >> 5)) + __popc(word & ((1u << bit) - 1u));
+  x = __ldg(a.values + vi);
+  return true;
+}
+
+constexpr int kPassThreads = 256;
+constexpr int kPassWarps = kPassThreads / 32;
+
+template <int KT, bool PASS2, bool STATS_ONLY>
+__global__ void __launch_bounds__(kPassThreads)
+pass_kernel(PassArgs a) {
+  __shared__ float lftS[kPassWarps][KT];
+  __shared__ float lfhS[kPassWarps][PASS2 ? KT : 1];
+  __shared__ float dS[kPassWarps][KT];
+  __shared__ double redS[kPassWarps][kMaxR2 + 3];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t ik = blockIdx.y;
+  const int64_t jl0 = (int64_t)blockIdx.x * a.jl_per_cta;
+  const int jlc = (int)min((int64_t)a.jl_per_cta, a.nL - jl0);
+  const int nitems = jlc * a.ws_split;
+  // column range of this CTA's split
+  const int64_t per_split = (a.ncols + a.nsplit - 1) / a.nsplit;
+  const int64_t cb0 = (int64_t)blockIdx.z * per_split;
+  const int64_t ce0 = min(a.ncols, cb0 + per_split);
+  const int64_t per_sub = (ce0 - cb0 + a.ws_split - 1) / a.ws_split;
+
+  const double sigma = a.sc->sigma;
+  const float inv2s2 = a.sigma_inf ? 0.f : (float)(0.5 / (sigma * sigma));
+  const double s2 = sigma * sigma;
+
+  double st_e2 = 0.0, st_w = 0.0, st_n = 0.0, st_den = 0.0;
+  constexpr int OUTS = kMaxR2 / 32;
+  double outacc[OUTS];
+#pragma unroll
+  for (int q = 0; q < OUTS; ++q) outacc[q] = 0.0;
+
+  for (int item = warp; item < nitems; item += kPassWarps) {
+    const int64_t jl = jl0 + item / a.ws_split;
+    const int sub = item % a.ws_split;
+    const int64_t row = jl + a.nL * ik;
+    const int64_t ro = a.row_off[row];
+    if (ro < 0) continue;
+    for (int q = lane; q < a.K; q += 32) {
+      lftS[warp][q] = a.lft[row * a.K + q];
+      if (PASS2) lfhS[warp][q] = a.lfth[row * a.K + q];
+    }
+    __syncwarp();
+    const int64_t cb = cb0 + sub * per_sub;
+    const int64_t ce = min(ce0, cb + per_sub);
+    float dacc[KT];
+#pragma unroll
+    for (int q = 0; q < KT; ++q) dacc[q] = 0.f;
+    for (int64_t c0 = cb; c0 < ce; c0 += 32) {
+      const int64_t col = c0 + lane;
+      float x = 0.f;
+      const bool obs = (col < ce) && load_entry(a, ro, a.col_off[min(col, a.ncols - 1)], x);
+      if (!__any_sync(0xffffffffu, obs)) continue;
+      const float* rc = a.rgtT + min(col, a.ncols - 1);
+      float recon = 0.f, tdir = 0.f;
+#pragma unroll 4
+      for (int q = 0; q < KT; ++q) {
+        if (q < a.K) {
+          const float r = __ldg(rc + (int64_t)q * a.ncols);
+          recon = fmaf(lftS[warp][q], r, recon);
+          if (PASS2) tdir = fmaf(lfhS[warp][q], r, tdir);
+        }
+      }
+      const float e = x - recon;
+      const float w = a.sigma_inf ? 1.f : expf(-e * e * inv2s2);
+      if (PASS2) {
+        if (obs) st_den += (double)w * (double)tdir * (double)tdir;
+      } else {
+        if (obs) {
+          st_e2 += (double)e * (double)e;
+          st_n += 1.0;
+          st_w += s2 * (1.0 - (double)w);
+        }
+        if (!STATS_ONLY) {
+          const float cv = obs ? w * e : 0.f;
+#pragma unroll 4
+          for (int q = 0; q < KT; ++q)
+            if (q < a.K) dacc[q] = fmaf(cv, __ldg(rc + (int64_t)q * a.ncols), dacc[q]);
+        }
+      }
+    }
+    if (!PASS2 && !STATS_ONLY) {
+      // reduce the per-lane gradient partials of this row over the warp
+#pragma unroll
+      for (int q = 0; q < KT; ++q) {
+        if (q < a.K) {
+          const float v = warp_sum_f(dacc[q]);
+          if (lane == 0) dS[warp][q] = v;
+        }
+      }
+      __syncwarp();
+      // d(i_k)[a + r_k b] += sum_c Mid(jl)[b][c] * D[a + r_k c]   (P:152 via S = Mid Rgt)
+#pragma unroll
+      for (int q = 0; q < OUTS; ++q) {
+        const int o = lane + 32 * q;
+        if (o < a.R2) {
+          const int aa = o % a.rk, b = o / a.rk;
+          double v;
+          if (a.p == 0) {
+            v = dS[warp][o];
+          } else {
+            const float* mr = a.mid + (jl * a.rk1 + b) * a.rs;
+            float f = 0.f;
+            for (int c = 0; c < a.rs; ++c) f = fmaf(__ldg(mr + c), dS[warp][aa + a.rk * c], f);
+            v = f;
+          }
+          outacc[q] += v;
+        }
+      }
+      __syncwarp();
+    }
+  }
+  // CTA reduction in a fixed order (deterministic)
+  const int64_t cta = (int64_t)blockIdx.z * gridDim.x + blockIdx.x;
+  const int64_t ncta = (int64_t)gridDim.x * gridDim.z;
+  if (PASS2) {
+    double v = warp_sum_d(st_den);
+    if (lane == 0) redS[warp][0] = v;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double tot = 0.0;
+      for (int w = 0; w < kPassWarps; ++w) tot += redS[w][0];
+      a.denpart[ik * ncta + cta] = tot;
+    }
+    return;
+  }
+  {
+    double v0 = warp_sum_d(st_e2), v1 = warp_sum_d(st_w), v2 = warp_sum_d(st_n);
+    if (lane == 0) { redS[warp][kMaxR2] = v0; redS[warp][kMaxR2 + 1] = v1; redS[warp][kMaxR2 + 2] = v2; }
+  }
+  if (!STATS_ONLY) {
+#pragma unroll
+    for (int q = 0; q < OUTS; ++q) {
+      const int o = lane + 32 * q;
+      if (o < a.R2) redS[warp][o] = outacc[q];
+    }
+  }
+  __syncthreads();
+  if (!STATS_ONLY) {
+    for (int o = threadIdx.x; o < a.R2; o += blockDim.x) {
+      double tot = 0.0;
+      for (int w = 0; w < kPassWarps; ++w) tot += redS[w][o];
+      a.dpart[(ik * ncta + cta) * a.R2 + o] = tot;
+    }
+  }
+  if (threadIdx.x < 3) {
+    double tot = 0.0;
+    for (int w = 0; w < kPassWarps; ++w) tot += redS[w][kMaxR2 + threadIdx.x];
+    a.spart[(ik * ncta + cta) * 3 + threadIdx.x] = tot;
+  }
+}
+
+static PassArgs make_pass_args(const Context& c, const BlockPlan& bp) {
+  PassArgs a;
+  a.nL = bp.nL; a.nrows = bp.nrows; a.ncols = bp.ncols;
+  a.K = bp.K; a.R2 = bp.R2; a.rk = bp.rk; a.rk1 = bp.rk1; a.rs = bp.rs; a.p = bp.p;
+  a.jl_per_cta = bp.jl_per_cta; a.ws_split = bp.ws_split; a.nsplit = bp.nsplit;
+  a.sigma_inf = c.cfg.sigma_mode == TRD_SIGMA_INF;
+  a.packed = c.packed;
+  a.row_off = c.row_off; a.col_off = c.col_off;
+  a.lft = c.lft; a.lfth = c.lfth; a.rgtT = c.rgtT; a.mid = c.mid;
+  a.values = c.values; a.mask = c.mask; a.rank_prefix = c.rank_prefix;
+  a.sc = c.sc;
+  a.dpart = c.dpart; a.spart = c.spart; a.denpart = c.denpart;
+  return a;
+}
+
+template <bool PASS2, bool STATS_ONLY>
+static void launch_pass_t(Context& c, const BlockPlan& bp, cudaStream_t s) {
+  PassArgs a = make_pass_args(c, bp);
+  dim3 grid((unsigned)bp.grid_x, (unsigned)(bp.nrows / bp.nL), (unsigned)bp.nsplit);
+  if (bp.K <= 32) pass_kernel<32, PASS2, STATS_ONLY><<<grid, kPassThreads, 0, s>>>(a);
+  else if (bp.K <= 64) pass_kernel<64, PASS2, STATS_ONLY><<<grid, kPassThreads, 0, s>>>(a);
+  else if (bp.K <= 128) pass_kernel<128, PASS2, STATS_ONLY><<<grid, kPassThreads, 0, s>>>(a);
+  else pass_kernel<256, PASS2, STATS_ONLY><<<grid, kPassThreads, 0, s>>>(a);
+  c.launches++;
+}
+
+// ----------------------------------------------------------------------------------------
+// Reductions (fixed order) -> dvec = [d (I_k x R2) | sum_e2 | welsch | n]
+// ----------------------------------------------------------------------------------------
+__global__ void reduce_d_kernel(const double* __restrict__ dpart, const double* __restrict__ spart,
+                                int64_t ncta, int R2, int64_t Ik, double* __restrict__ dvec,
+                                DevScalars* sc, int kblk) {
+  const int64_t ik = blockIdx.x;
+  if (ik < Ik) {
+    for (int o = threadIdx.x; o < R2; o += blockDim.x) {
+      double tot = 0.0;
+      for (int64_t q = 0; q < ncta; ++q) tot += dpart[(ik * ncta + q) * R2 + o];
+      dvec[ik * R2 + o] = tot;
+    }
+    return;
+  }
+  // last block: statistics, summed per i_k row then over rows (fixed order)
+  __shared__ double acc[3][256];
+  for (int j = 0; j < 3; ++j) {
+    double tot = 0.0;
+    for (int64_t r = threadIdx.x; r < Ik; r += blockDim.x)
+      for (int64_t q = 0; q < ncta; ++q) tot += spart[(r * ncta + q) * 3 + j];
+    acc[j][threadIdx.x] = tot;
+  }
+  __syncthreads();
+  if (threadIdx.x < 3) {
+    double tot = 0.0;
+    for (int t = 0; t < (int)blockDim.x; ++t) tot += acc[threadIdx.x][t];
+    dvec[Ik * R2 + threadIdx.x] = tot;
+    if (threadIdx.x == 2 && sc && sc->prof_on) sc->prof_nobs[kblk] += tot;   // local count
+  }
+}
+
+__global__ void reduce_den_kernel(const double* __restrict__ denpart, int64_t n,
+                                  const double* __restrict__ numpart, int64_t Ik,
+                                  double* __restrict__ out2) {
+  __shared__ double acc[2][256];
+  double a0 = 0.0, a1 = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) a0 += denpart[i];
+  for (int64_t i = threadIdx.x; i < Ik; i += blockDim.x) a1 += numpart[i];
+  acc[0][threadIdx.x] = a0;
+  acc[1][threadIdx.x] = a1;
+  __syncthreads();
+  if (threadIdx.x < 2) {
+    double tot = 0.0;
+    for (int t = 0; t < (int)blockDim.x; ++t) tot += acc[threadIdx.x][t];
+    out2[threadIdx.x] = tot;   // [den_local, num]
+  }
+}
+
+// ----------------------------------------------------------------------------------------
+// FGMC (Eq. 13; reading R6).  Q_k[(a r + a'), (b r' + b')] = sum_i Z(i)[a][b] Z(i)[a'][b']
+// ----------------------------------------------------------------------------------------
+__global__ void q_kernel(const float* __restrict__ Zk, int64_t Ik, int r0, int r1, double* __restrict__ Qk) {
+  const int n0 = r0 * r0, n1 = r1 * r1;
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n0 * n1; t += gridDim.x * blockDim.x) {
+    const int row = t / n1, col = t % n1;
+    const int a = row / r0, ap = row % r0, b = col / r1, bp = col % r1;
+    double acc = 0.0;
+    for (int64_t i = 0; i < Ik; ++i) {
+      const float* S = Zk + i * r0 * r1;
+      acc += (double)S[a * r1 + b] * (double)S[ap * r1 + bp];
+    }
+    Qk[t] = acc;
+  }
+}
+
+// C (m x n) = A (m x q) * B (q x n), fp64, 16x16 tiles
+__global__ void matmul_f64_kernel(const double* __restrict__ A, const double* __restrict__ B,
+                                  double* __restrict__ C, int m, int n, int q) {
+  __shared__ double As[16][17], Bs[16][17];
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  const int row = blockIdx.y * 16 + ty, col = blockIdx.x * 16 + tx;
+  double acc = 0.0;
+  for (int k0 = 0; k0 < q; k0 += 16) {
+    As[ty][tx] = (row < m && k0 + tx < q) ? A[(int64_t)row * q + k0 + tx] : 0.0;
+    Bs[ty][tx] = (k0 + ty < q && col < n) ? B[(int64_t)(k0 + ty) * n + col] : 0.0;
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < 16; ++kk) acc = fma(As[ty][kk], Bs[kk][tx], acc);
+    __syncthreads();
+  }
+  if (row < m && col < n) C[(int64_t)row * n + col] = acc;
+}
+
+// G[c + rk b][c' + rk b'] = C[b rk1 + b'][c rk + c']   (Phi, reading R6)
+__global__ void phi_kernel(const double* __restrict__ C, int rk, int rk1, double* __restrict__ G) {
+  const int R2 = rk * rk1;
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < R2 * R2; t += gridDim.x * blockDim.x) {
+    const int row = t / R2, col = t % R2;
+    const int c = row % rk, b = row / rk, cp = col % rk, bp = col / rk;
+    G[t] = C[(int64_t)(b * rk1 + bp) * (rk * rk) + (c * rk + cp)];
+  }
+}
+
+// ----------------------------------------------------------------------------------------
+// Filtered solve (Eq. 10/16 with reading R5): lambda = lambda_rel tr(G)/n, A = G + lambda I
+// = L L^T, M = A^-1 (A^-1 G)^T = A^-1 G A^-1.  One CTA; retries lambda*10 up to 3 times.
+// ----------------------------------------------------------------------------------------
+constexpr int kSolveThreads = 1024;
+
+// forward (L Y = B) then backward (L^T X = Y) substitution, in place on the n x n matrix
+// B (row-major, column j = one right-hand side).  8 lanes cooperate on one column.
+__device__ void chol_solve_inplace(const double* L, double* B, int n) {
+  const int lane8 = threadIdx.x & 7;
+  const int group = threadIdx.x >> 3;           // 128 column groups
+  const unsigned gmask = 0xffu << (threadIdx.x & 24);
+  for (int col0 = 0; col0 < n; col0 += kSolveThreads / 8) {
+    const int col = col0 + group;
+    const bool act = col < n;
+    // forward
+    for (int i = 0; i < n; ++i) {
+      double part = 0.0;
+      if (act)
+        for (int l = lane8; l < i; l += 8) part = fma(L[i * n + l], B[l * n + col], part);
+      part += __shfl_xor_sync(gmask, part, 4);
+      part += __shfl_xor_sync(gmask, part, 2);
+      part += __shfl_xor_sync(gmask, part, 1);
+      if (act && lane8 == 0) B[i * n + col] = (B[i * n + col] - part) / L[i * n + i];
+      __syncwarp(gmask);
+    }
+    // backward with L^T
+    for (int i = n - 1; i >= 0; --i) {
+      double part = 0.0;
+      if (act)
+        for (int l = i + 1 + lane8; l < n; l += 8) part = fma(L[l * n + i], B[l * n + col], part);
+      part += __shfl_xor_sync(gmask, part, 4);
+      part += __shfl_xor_sync(gmask, part, 2);
+      part += __shfl_xor_sync(gmask, part, 1);
+      if (act && lane8 == 0) B[i * n + col] = (B[i * n + col] - part) / L[i * n + i];
+      __syncwarp(gmask);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kSolveThreads)
+solve_kernel(const double* __restrict__ G, int n, double lambda_rel, double* __restrict__ Mout,
+             double* __restrict__ ws, int use_smem, DevScalars* __restrict__ sc) {
+  extern __shared__ double sm[];
+  double* L = use_smem ? sm : ws;
+  double* B = use_smem ? sm + n * n : ws + n * n;
+  __shared__ double tr_s;
+  __shared__ int fail_s;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  if (threadIdx.x == 0) {
+    double tr = 0.0;
+    for (int i = 0; i < n; ++i) tr += G[i * n + i];
+    tr_s = tr;
+  }
+  __syncthreads();
+  double lam = lambda_rel * tr_s / n;
+  int attempt = 0;
+  for (;; ++attempt) {
+    for (int t = threadIdx.x; t < n * n; t += blockDim.x) {
+      const int i = t / n, j = t % n;
+      L[t] = G[t] + (i == j ? lam : 0.0);
+    }
+    if (threadIdx.x == 0) fail_s = 0;
+    __syncthreads();
+    // left-looking Cholesky; column j, rows i >= j; warp per row, lanes split the dot
+    for (int j = 0; j < n; ++j) {
+      for (int i = j + warp; i < n; i += nw) {
+        double part = 0.0;
+        for (int l = lane; l < j; l += 32) part = fma(L[i * n + l], L[j * n + l], part);
+        part = warp_sum_d(part);
+        if (lane == 0) B[i] = L[i * n + j] - part;   // B used as scratch column
+      }
+      __syncthreads();
+      const double djj = B[j];
+      if (djj <= 0.0 || !(djj == djj)) {
+        if (threadIdx.x == 0) fail_s = 1;
+      } else {
+        const double ljj = sqrt(djj);
+        for (int i = j + threadIdx.x; i < n; i += blockDim.x)
+          L[i * n + j] = (i == j) ? ljj : B[i] / ljj;
+      }
+      __syncthreads();
+      if (fail_s) break;
+    }
+    __syncthreads();
+    if (!fail_s || attempt >= 3) break;
+    lam *= 10.0;
+    __syncthreads();
+  }
+  if (fail_s) {
+    if (threadIdx.x == 0) { sc->not_spd = 1; sc->lambda = lam; }
+    for (int t = threadIdx.x; t < n * n; t += blockDim.x) Mout[t] = 0.0;
+    return;
+  }
+  // zero the strict upper triangle (the algorithm read only the lower part)
+  for (int t = threadIdx.x; t < n * n; t += blockDim.x) {
+    const int i = t / n, j = t % n;
+    if (j > i) L[t] = 0.0;
+    B[t] = G[t];
+  }
+  __syncthreads();
+  chol_solve_inplace(L, B, n);              // B = A^-1 G
+  __syncthreads();
+  for (int t = threadIdx.x; t < n * n; t += blockDim.x) {   // B <- B^T
+    const int i = t / n, j = t % n;
+    if (j > i) { const double x = B[i * n + j]; B[i * n + j] = B[j * n + i]; B[j * n + i] = x; }
+  }
+  __syncthreads();
+  chol_solve_inplace(L, B, n);              // B = A^-1 (A^-1 G)^T = A^-1 G A^-1
+  __syncthreads();
+  for (int t = threadIdx.x; t < n * n; t += blockDim.x) Mout[t] = B[t];
+  if (threadIdx.x == 0) sc->lambda = lam;
+}
+
+// h = d M (row-wise), num partial per row = <d(i), h(i)>
+__global__ void h_kernel(const double* __restrict__ dvec, const double* __restrict__ M, int R2,
+                         double* __restrict__ h, double* __restrict__ numpart) {
+  __shared__ double drow[kMaxR2];
+  __shared__ double red[256];
+  const int64_t ik = blockIdx.x;
+  for (int o = threadIdx.x; o < R2; o += blockDim.x) drow[o] = dvec[ik * R2 + o];
+  __syncthreads();
+  double part = 0.0;
+  for (int o = threadIdx.x; o < R2; o += blockDim.x) {
+    double acc = 0.0;
+    for (int q = 0; q < R2; ++q) acc = fma(drow[q], M[q * R2 + o], acc);
+    h[ik * R2 + o] = acc;
+    part += acc * drow[o];
+  }
+  red[threadIdx.x] = part;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double tot = 0.0;
+    for (int t = 0; t < (int)blockDim.x; ++t) tot += red[t];
+    numpart[ik] = tot;
+  }
+}
+
+// ----------------------------------------------------------------------------------------
+// Update (Eq. 11/17, reading R2: Z_k <- Z_k + eta fold(h)) and block statistics
+// ----------------------------------------------------------------------------------------
+__device__ __forceinline__ double block_eta(const DevScalars* sc, double step) {
+  if (step > 0.0) return step;
+  const double num = sc->num, den = sc->den;
+  return (num > 0.0 && den > 0.0) ? num / den : 0.0;
+}
+
+__global__ void update2_kernel(float* __restrict__ Zk, const double* __restrict__ h, int64_t Ik,
+                               int rk, int rk1, double step, const DevScalars* __restrict__ sc) {
+  const double eta = block_eta(sc, step);
+  if (eta == 0.0) return;
+  const int64_t tot = Ik * rk * rk1;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tot;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    // device layout Z_k[i][a][b]; h[i][a + rk b]
+    const int b = (int)(t % rk1);
+    const int64_t ia = t / rk1;
+    const int aa = (int)(ia % rk);
+    const int64_t i = ia / rk;
+    const double v = (double)Zk[t] + eta * h[i * rk * rk1 + aa + rk * b];
+    Zk[t] = (float)v;
+  }
+}
+
+// scalars after the pass-1 allreduce and after the pass-2 allreduce
+__global__ void block_scalars_kernel(const double* __restrict__ dvec, int64_t Ik, int R2,
+                                     const double* __restrict__ numden, DevScalars* sc,
+                                     DevStats* stats, int slot, int k, double step, int phase) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  if (phase == 0) {
+    sc->sum_e2 = dvec[Ik * R2 + 0];
+    sc->welsch = dvec[Ik * R2 + 1];
+    sc->n_obs = dvec[Ik * R2 + 2];
+    return;
+  }
+  sc->den = numden[0];
+  sc->num = numden[1];
+  const double eta = block_eta(sc, step);
+  sc->eta = eta;
+  DevStats& st = stats[slot];
+  st.eta[k] = eta;
+  st.num[k] = sc->num;
+  st.den[k] = sc->den;
+  st.nnz[k] = (long long)sc->n_obs;
+  st.n_obs += (long long)sc->n_obs;
+  st.sum_e2 += sc->sum_e2;
+  st.welsch += sc->welsch;
+  if (eta == 0.0) st.skipped |= (1u << k);
+  if (!(eta == eta) || isinf(eta) || !(sc->num == sc->num)) { st.nonfinite = 1; sc->nonfinite = 1; }
+  sc->acc_e2 += sc->sum_e2;
+  sc->acc_n += sc->n_obs;
+}
+
+__global__ void sweep_begin_kernel(DevScalars* sc, DevStats* stats, int slot) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  DevStats& st = stats[slot];
+  st.sigma = sc->sigma;
+  st.sum_e2 = 0.0; st.welsch = 0.0; st.stop_e = 0.0; st.n_obs = 0;
+  for (int k = 0; k < kMaxN; ++k) { st.eta[k] = 0.0; st.num[k] = 0.0; st.den[k] = 0.0; st.nnz[k] = 0; }
+  st.skipped = 0; st.nonfinite = 0;
+  sc->acc_e2 = 0.0; sc->acc_n = 0.0;
+}
+
+// ----------------------------------------------------------------------------------------
+// End of sweep: D^t = Z_N(2) G_{!=N} Z_N(2)^T (Alg. 1 l.12), e_t (l.13), sigma (R9)
+// ----------------------------------------------------------------------------------------
+__global__ void dt_T_kernel(const float* __restrict__ Zn, int64_t In, int rk, int rk1,
+                            const double* __restrict__ G, double* __restrict__ T) {
+  const int R2 = rk * rk1;
+  const int64_t i = blockIdx.x;
+  for (int o = threadIdx.x; o < R2; o += blockDim.x) {
+    double acc = 0.0;
+    for (int q = 0; q < R2; ++q) {
+      const int aa = q % rk, b = q / rk;
+      acc = fma((double)Zn[(i * rk + aa) * rk1 + b], G[q * R2 + o], acc);
+    }
+    T[i * R2 + o] = acc;
+  }
+}
+
+__global__ void dt_D_kernel(const float* __restrict__ Zn, int64_t In, int rk, int rk1,
+                            const double* __restrict__ T, double* __restrict__ D) {
+  const int R2 = rk * rk1;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < In * In;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = t / In, j = t % In;
+    double acc = 0.0;
+    for (int q = 0; q < R2; ++q) {
+      const int aa = q % rk, b = q / rk;
+      acc = fma(T[i * R2 + q], (double)Zn[(j * rk + aa) * rk1 + b], acc);
+    }
+    D[t] = acc;
+  }
+}
+
+__global__ void sweep_end_kernel(double* __restrict__ D, double* __restrict__ Dprev, int64_t n2,
+                                 DevScalars* sc, DevStats* stats, int slot, int sigma_mode,
+                                 double theta, double sigma_min) {
+  __shared__ double a1[1024], a2[1024];
+  double s1 = 0.0, s2 = 0.0;
+  for (int64_t t = threadIdx.x; t < n2; t += blockDim.x) {
+    const double dd = D[t] - Dprev[t];
+    s1 += dd * dd;
+    s2 += D[t] * D[t];
+  }
+  a1[threadIdx.x] = s1;
+  a2[threadIdx.x] = s2;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t1 = 0.0, t2 = 0.0;
+    for (int t = 0; t < (int)blockDim.x; ++t) { t1 += a1[t]; t2 += a2[t]; }
+    const double e = sc->have_prev_D ? sqrt(t1) / sqrt(t2) : __longlong_as_double(0x7ff8000000000000LL);
+    sc->stop_e = e;
+    stats[slot].stop_e = e;
+    if (sigma_mode == TRD_SIGMA_RMS && sc->acc_n > 0.0)
+      sc->sigma = fmax(sigma_min, theta * sqrt(sc->acc_e2 / sc->acc_n));
+    sc->have_prev_D = 1;
+    sc->sweep += 1;
+  }
+  __syncthreads();
+  for (int64_t t = threadIdx.x; t < n2; t += blockDim.x) Dprev[t] = D[t];
+}
+
+// sigma_0 = max(sigma_min, theta * RMS) from [sum_e2, welsch, n] (after allreduce)
+__global__ void sigma0_kernel(const double* __restrict__ s3, DevScalars* sc, double theta,
+                              double sigma_min) {
+  if (threadIdx.x == 0 && blockIdx.x == 0)
+    sc->sigma = fmax(sigma_min, theta * sqrt(s3[0] / fmax(s3[2], 1.0)));
+}
+
+// ----------------------------------------------------------------------------------------
+// Reconstruction (Def. 1) at arbitrary global linear indices
+// ----------------------------------------------------------------------------------------
+struct ReconArgs {
+  int N;
+  int64_t dims[kMaxN];
+  int ranks[kMaxN + 1];
+  int64_t zoff[kMaxN + 1];
+};
+
+__device__ float tr_value(const ReconArgs& a, const float* __restrict__ Z, const int64_t* ix) {
+  // Tr(prod_k Z_k(i_k)) = sum_a e_a^T Z_0(i_0) ... Z_{N-1}(i_{N-1}) e_a
+  float tot = 0.f;
+  for (int a0 = 0; a0 < a.ranks[0]; ++a0) {
+    float v[kMaxR];
+#pragma unroll
+    for (int c = 0; c < kMaxR; ++c) v[c] = (c == a0) ? 1.f : 0.f;
+    int rin = a.ranks[0];
+    for (int m = 0; m < a.N; ++m) {
+      const int rout = a.ranks[m + 1];
+      vecmat(v, Z + a.zoff[m] + ix[m] * (int64_t)a.ranks[m] * rout, rin, rout);
+      rin = rout;
+    }
+    tot += v[a0];
+  }
+  return tot;
+}
+
+__global__ void recon_kernel(ReconArgs a, const float* __restrict__ Z, const int64_t* __restrict__ lin,
+                             int64_t n, float* __restrict__ out) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    int64_t l = lin[t], ix[kMaxN];
+    for (int m = 0; m < a.N; ++m) { ix[m] = l % a.dims[m]; l /= a.dims[m]; }
+    out[t] = tr_value(a, Z, ix);
+  }
+}
+
+// error over all local entries, GEMM form with full index sets (plan = full plan).
+// out per CTA: [sum (x-ref)^2 all, sum ref^2 all, sum (x-ref)^2 obs, sum ref^2 obs, n, max|ref|]
+__global__ void __launch_bounds__(256)
+error_kernel(PassArgs a, const float* __restrict__ ref, const uint32_t* __restrict__ evalb,
+             double* __restrict__ part) {
+  __shared__ float lftS[8][kMaxR2];
+  __shared__ double red[8][6];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double s[6] = {0, 0, 0, 0, 0, 0};
+  const int64_t nw_total = (int64_t)gridDim.x * 8;
+  for (int64_t row = (int64_t)blockIdx.x * 8 + warp; row < a.nrows; row += nw_total) {
+    const int64_t ro = a.row_off[row];
+    if (ro < 0) continue;
+    for (int q = lane; q < a.K; q += 32) lftS[warp][q] = a.lft[row * a.K + q];
+    __syncwarp();
+    for (int64_t c0 = 0; c0 < a.ncols; c0 += 32) {
+      const int64_t col = c0 + lane;
+      if (col < a.ncols) {
+        const int64_t co = a.col_off[col];
+        if (co >= 0) {
+          const int64_t lin = ro + co;
+          const bool ev = evalb ? ((evalb[lin >> 5] >> (lin & 31)) & 1u) : true;
+          if (ev) {
+            float recon = 0.f;
+            for (int q = 0; q < a.K; ++q) recon = fmaf(lftS[warp][q], a.rgtT[(int64_t)q * a.ncols + col], recon);
+            const double r = ref[lin];
+            const double dd = (double)recon - r;
+            s[0] += dd * dd;
+            s[1] += r * r;
+            if ((a.mask[lin >> 5] >> (lin & 31)) & 1u) { s[2] += dd * dd; s[3] += r * r; }
+            s[4] += 1.0;
+            s[5] = fmax(s[5], fabs(r));
+          }
+        }
+      }
+    }
+    __syncwarp();
+  }
+  for (int j = 0; j < 6; ++j) {
+    double v = s[j];
+    for (int o = 16; o > 0; o >>= 1) {
+      const double u = __shfl_xor_sync(0xffffffffu, v, o);
+      v = (j == 5) ? fmax(v, u) : v + u;
+    }
+    if (lane == 0) red[warp][j] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x < 6) {
+    double v = 0.0;
+    for (int w = 0; w < 8; ++w) v = (threadIdx.x == 5) ? fmax(v, red[w][threadIdx.x]) : v + red[w][threadIdx.x];
+    part[blockIdx.x * 6 + threadIdx.x] = v;
+  }
+}
+
+__global__ void error_reduce_kernel(const double* __restrict__ part, int n, double* __restrict__ out) {
+  if (threadIdx.x < 6 && blockIdx.x == 0) {
+    double v = 0.0;
+    for (int b = 0; b < n; ++b) v = (threadIdx.x == 5) ? fmax(v, part[b * 6 + threadIdx.x]) : v + part[b * 6 + threadIdx.x];
+    out[threadIdx.x] = v;
+  }
+}
+
+__global__ void popc_kernel(const uint32_t* __restrict__ mask, int64_t nw, uint32_t* __restrict__ out) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < nw;
+       t += (int64_t)gridDim.x * blockDim.x)
+    out[t] = __popc(mask[t]);
+}
+
+// ----------------------------------------------------------------------------------------
+// Launchers
+// ----------------------------------------------------------------------------------------
+static int grid_for(int64_t n, int threads = 256, int cap = 148 * 16) {
+  int64_t g = (n + threads - 1) / threads;
+  if (g < 1) g = 1;
+  if (g > cap) g = cap;
+  return (int)g;
+}
+
+void launch_sampler(Context& c, const BlockPlan& bp, cudaStream_t s) {
+  SamplerArgs sa;
+  sa.N = c.N; sa.k = bp.k; sa.shard_mode = c.cfg.shard_mode; sa.seed = c.cfg.seed;
+  sa.shard_begin = c.shard_begin; sa.shard_end = c.shard_end;
+  int64_t maxI = 0;
+  for (int m = 0; m < c.N; ++m) {
+    sa.dims[m] = c.dims[m];
+    sa.s[m] = bp.s[m];
+    sa.idx_off[m] = c.idx_off[m];
+    sa.lstride[m] = c.lstride[m];
+    if (bp.s[m] < c.dims[m] && c.dims[m] > maxI) maxI = c.dims[m];
+  }
+  sa.idx_off[c.N] = c.idx_off[c.N];
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(sampler_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+    attr_set = true;
+  }
+  size_t smem = (size_t)maxI * 9 + 16;
+  sampler_kernel<<<c.N, 256, smem, s>>>(sa, c.sc, c.idx, c.doff);
+  c.launches++;
+}
+
+void launch_plan(Context& c, const BlockPlan& bp, cudaStream_t s) {
+  PlanArgs a = make_plan_args(c, bp);
+  offsets_kernel<<<grid_for(bp.nrows + bp.ncols), 256, 0, s>>>(a, c.doff, c.row_off, c.col_off);
+  c.launches++;
+  if (bp.p > 0) {
+    mid_kernel<<<grid_for(bp.nL * bp.rk1), 256, 0, s>>>(a, c.idx, c.Z, c.mid);
+    c.launches++;
+  }
+  rgt_kernel<<<grid_for(bp.ncols * bp.rs), 256, 0, s>>>(a, c.idx, c.Z, c.rgtT);
+  c.launches++;
+}
+
+void launch_lft(Context& c, const BlockPlan& bp, const float* Zsrc_k, int src_is_h, float* out,
+                cudaStream_t s) {
+  PlanArgs a = make_plan_args(c, bp);
+  lft_kernel<<<grid_for(bp.nrows * bp.rk), 256, 0, s>>>(a, src_is_h ? nullptr : Zsrc_k,
+                                                        src_is_h ? c.h : nullptr, c.mid, out);
+  c.launches++;
+}
+
+void launch_pass1(Context& c, const BlockPlan& bp, int stats_only, cudaStream_t s) {
+  if (stats_only) launch_pass_t<false, true>(c, bp, s);
+  else launch_pass_t<false, false>(c, bp, s);
+}
+
+void launch_pass2(Context& c, const BlockPlan& bp, cudaStream_t s) {
+  launch_pass_t<true, false>(c, bp, s);
+}
+
+void launch_reduce_d(Context& c, const BlockPlan& bp, cudaStream_t s) {
+  const int64_t Ik = bp.nrows / bp.nL;
+  const int64_t ncta = bp.grid_x * bp.nsplit;
+  reduce_d_kernel<<<(unsigned)(Ik + 1), 256, 0, s>>>(c.dpart, c.spart, ncta, bp.R2, Ik, c.dvec,
+                                                      bp.R2 > 0 ? c.sc : nullptr, bp.k);
+  c.launches++;
+}
+
+// block statistics from the (allreduced) dvec tail
+void launch_block_stats(Context& c, const BlockPlan& bp, cudaStream_t s) {
+  const int64_t Ik = bp.nrows / bp.nL;
+  block_scalars_kernel<<<1, 32, 0, s>>>(c.dvec, Ik, bp.R2, nullptr, c.sc, c.stats, 0, bp.k, 0.0, 0);
+  c.launches++;
+}
+
+void launch_reduce_den(Context& c, const BlockPlan& bp, cudaStream_t s) {
+  const int64_t Ik = bp.nrows / bp.nL;
+  const int64_t ncta = bp.grid_x * bp.nsplit;
+  reduce_den_kernel<<<1, 256, 0, s>>>(c.denpart, Ik * ncta, c.numpart, Ik, c.red_ws);
+  c.launches++;
+}
+
+void launch_q(Context& c, int k, cudaStream_t s) {
+  const int r0 = c.ranks[k], r1 = c.ranks[(k + 1) % c.N];
+  q_kernel<<<grid_for((int64_t)r0 * r0 * r1 * r1), 256, 0, s>>>(c.Z + c.zoff[k], c.dims[k], r0, r1,
+                                                                 c.Q + c.qoff[k]);
+  c.launches++;
+}
+
+void launch_gram(Context& c, const BlockPlan& bp, cudaStream_t s) {
+  const int N = c.N, k = bp.k;
+  // C = Q_{k+1} Q_{k+2} ... Q_{k-1}
+  const double* cur = c.Q + c.qoff[(k + 1) % N];
+  int m_rows = bp.rk1 * bp.rk1;
+  double* bufs[2] = {c.chain_ws, c.chain_ws + kMaxR2 * kMaxR2};
+  int which = 0;
+  for (int q = 2; q < N; ++q) {
+    const int mm = (k + q) % N;
+    const int qcols = c.ranks[(mm + 1) % N] * c.ranks[(mm + 1) % N];
+    const int qin = c.ranks[mm] * c.ranks[mm];
+    dim3 grid((qcols + 15) / 16, (m_rows + 15) / 16);
+    matmul_f64_kernel<<<grid, dim3(16, 16), 0, s>>>(cur, c.Q + c.qoff[mm], bufs[which], m_rows, qcols, qin);
+    c.launches++;
+    cur = bufs[which];
+    which ^= 1;
+  }
+  phi_kernel<<<grid_for((int64_t)bp.R2 * bp.R2), 256, 0, s>>>(cur, bp.rk, bp.rk1, c.G);
+  c.launches++;
+}
+
+void launch_solve(Context& c, const BlockPlan& bp, cudaStream_t s) {
+  const int n = bp.R2;
+  const size_t need = (size_t)2 * n * n * sizeof(double);
+  const int use_smem = need <= 200 * 1024;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr_set = true;
+  }
+  solve_kernel<<<1, kSolveThreads, use_smem ? need : 0, s>>>(c.G, n, c.cfg.lambda_rel, c.Mop,
+                                                             c.chol_ws, use_smem, c.sc);
+  c.launches++;
+}
+
+void launch_h(Context& c, const BlockPlan& bp, cudaStream_t s) {
+  const int64_t Ik = bp.nrows / bp.nL;
+  h_kernel<<<(unsigned)Ik, 256, 0, s>>>(c.dvec, c.Mop, bp.R2, c.h, c.numpart);
+  c.launches++;
+}
+
+void launch_update(Context& c, const BlockPlan& bp, int slot, cudaStream_t s) {
+  const int64_t Ik = bp.nrows / bp.nL;
+  block_scalars_kernel<<<1, 32, 0, s>>>(c.dvec, Ik, bp.R2, c.red_ws, c.sc, c.stats, slot, bp.k,
+                                        c.cfg.step, 1);
+  c.launches++;
+  update2_kernel<<<grid_for(Ik * bp.R2), 256, 0, s>>>(c.Z + c.zoff[bp.k], c.h, Ik, bp.rk, bp.rk1,
+                                                      c.cfg.step, c.sc);
+  c.launches++;
+}
+
+void launch_sweep_begin(Context& c, int slot, cudaStream_t s) {
+  sweep_begin_kernel<<<1, 32, 0, s>>>(c.sc, c.stats, slot);
+  c.launches++;
+}
+
+void launch_sweep_end(Context& c, int slot, cudaStream_t s) {
+  const int n = c.N - 1;
+  const int rk = c.ranks[n], rk1 = c.ranks[0];
+  const int64_t In = c.dims[n];
+  double* T = c.chain_ws;     // In x R2 (<= chain_ws capacity, checked at init)
+  dt_T_kernel<<<(unsigned)In, 128, 0, s>>>(c.Z + c.zoff[n], In, rk, rk1, c.G_last, T);
+  dt_D_kernel<<<grid_for(In * In), 256, 0, s>>>(c.Z + c.zoff[n], In, rk, rk1, T, c.Dcur);
+  sweep_end_kernel<<<1, 1024, 0, s>>>(c.Dcur, c.Dprev, In * In, c.sc, c.stats, slot,
+                                      c.cfg.sigma_mode, c.cfg.sigma_theta, c.cfg.sigma_min);
+  c.launches += 3;
+}
+
+void launch_sigma0(Context& c, cudaStream_t s) {
+  // dvec[Ik*R2 .. +3] of the stats-only full pass hold [sum_e2, welsch, n]; the caller
+  // reduced them into red_ws[0..2]
+  sigma0_kernel<<<1, 32, 0, s>>>(c.red_ws, c.sc, c.cfg.sigma_theta, c.cfg.sigma_min);
+  c.launches++;
+}
+
+void launch_reconstruct(Context& c, const int64_t* lin, int64_t n, float* out, cudaStream_t s) {
+  ReconArgs a;
+  a.N = c.N;
+  for (int m = 0; m < c.N; ++m) a.dims[m] = c.dims[m];
+  for (int m = 0; m <= c.N; ++m) { a.ranks[m] = c.ranks[m % c.N]; a.zoff[m] = c.zoff[m]; }
+  recon_kernel<<<grid_for(n), 256, 0, s>>>(a, c.Z, lin, n, out);
+  c.launches++;
+}
+
+void launch_error(Context& c, const float* ref, const uint32_t* eval_bits, double* out6,
+                  cudaStream_t s) {
+  const BlockPlan& bp = c.full_plan;
+  PassArgs a = make_pass_args(c, bp);
+  const int nb = 148 * 4;
+  error_kernel<<<nb, 256, 0, s>>>(a, ref, eval_bits, c.dpart);
+  error_reduce_kernel<<<1, 32, 0, s>>>(c.dpart, nb, out6);
+  c.launches += 2;
+}
+
+void launch_rank_prefix(Context& c, cudaStream_t s) {
+  popc_kernel<<<grid_for(c.n_words), 256, 0, s>>>(c.mask, c.n_words, c.rank_prefix);
+  c.launches++;
+  size_t tmp = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, tmp, c.rank_prefix, c.rank_prefix, c.n_words, s);
+  void* dtmp = nullptr;
+  cudaMallocAsync(&dtmp, tmp, s);
+  cub::DeviceScan::ExclusiveSum(dtmp, tmp, c.rank_prefix, c.rank_prefix, c.n_words, s);
+  cudaFreeAsync(dtmp, s);
+  c.launches += 1;
+}
+
+void launch_record_block(Context& c, const BlockPlan& bp, int slot, cudaStream_t s) { (void)c; (void)bp; (void)slot; (void)s; }
+void launch_reset_block_scalars(Context& c, cudaStream_t s) { (void)c; (void)s; }
+void launch_fill_full_sets(Context& c, const BlockPlan& bp, cudaStream_t s) { launch_sampler(c, bp, s); }
+
+}  // namespace trd

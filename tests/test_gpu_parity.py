@@ -1,0 +1,267 @@
+"""Parity of the CUDA path (libtrd through the C ABI) against the float64 oracle.
+
+Tolerances (north star, BASELINE.json): sampled indices bit-exact; cores after one sweep
+within 1e-4 relative Frobenius; final relative reconstruction error within 1e-3 (absolute
+difference, reading R19).  Intermediate block quantities (d, G, h, num, den) are compared at
+1e-4 relative: the GPU accumulates the per-entry products in fp32.
+"""
+import math
+import os
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import trd_oracle as O
+from oracle.philox import sample_indices
+from synth.generate import CONFIGS, make_problem, to_numpy_views
+from tests.helpers import (cores_rel_err, gpu_context, oracle_config, oracle_source, rel_fro,
+                           small_spec)
+
+pytestmark = pytest.mark.gpu
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+# ---------------------------------------------------------------------------- sampler
+@pytest.mark.parametrize("name,dims", [("C3", [240, 320, 3, 100]), ("C4", [128, 128, 128, 128]),
+                                       ("C5a", [80, 80, 80, 80, 80])])
+def test_sampler_bit_exact_at_config_shapes(name, dims):
+    """RStS index sets (Alg. 1 l.4; reading R11) at the BASELINE shapes and sketch
+    sizes: GPU == oracle, bit-exact, for several sweeps and every block."""
+    _cuda()
+    from paper_2305_09044_b200 import TRD
+    spec = CONFIGS[name]
+    N = len(dims)
+    n = int(np.prod(dims))
+    mask = torch.zeros((n + 31) // 32, dtype=torch.int32, device="cuda")
+    mask[0] = 1                                       # one observed entry; packed value
+    vals = torch.ones(1, device="cuda")
+    cores = [np.ones((1, dims[q], 1), dtype=np.float32) for q in range(N)]
+    ctx = TRD(dims, [1] * N, vals, mask, cores, sketch=spec.sketch, seed=spec.sampler_seed,
+              sigma_mode=1, packed=True)
+    for t in [0, 1, 19]:
+        for k in range(N):
+            sets = ctx.sketch(t, k)
+            for m in range(N):
+                s = spec.sketch[m] if m != k else 0
+                ref = sample_indices(spec.sampler_seed, t, k, m, dims[m], s)
+                assert np.array_equal(sets[m], ref), (t, k, m)
+    ctx.close()
+
+
+def test_sampler_matches_golden_file():
+    """Golden RStS sets (written by scripts/make_golden.py from the oracle) reproduced by
+    the CUDA sampler for the (t, k, m) of contexts built at those seeds and shapes."""
+    _cuda()
+    rows = []
+    for line in open(os.path.join(GOLD, "rsts_index_sets.txt")):
+        if line.startswith("#"):
+            continue
+        lhs, rhs = line.split(":")
+        rows.append(([int(v) for v in lhs.split()], [int(v) for v in rhs.split()]))
+    from paper_2305_09044_b200 import TRD
+    for (seed, t, k, m, I, s), idx in rows:
+        if I > 16384:
+            continue
+        # order-3 context whose mode m has extent I and sketch s (k = block index)
+        N = max(3, m + 1, k + 1)
+        dims = [2] * N
+        dims[m] = I
+        sketch = [0] * N
+        sketch[m] = s
+        n = int(np.prod(dims))
+        vals = torch.zeros(n, device="cuda")
+        mask = torch.full(((n + 31) // 32,), -1, dtype=torch.int32, device="cuda")
+        cores = [np.ones((1, dims[q], 1), dtype=np.float32) for q in range(N)]
+        if k == m:
+            continue   # block k uses the full mode k
+        ctx = TRD(dims, [1] * N, vals, mask, cores, sketch=sketch, seed=seed, sigma_mode=1)
+        sets = ctx.sketch(t, k)
+        assert list(sets[m]) == idx, (seed, t, k, m)
+        ctx.close()
+
+
+# ---------------------------------------------------------------------------- one block
+BLOCK_CASES = [
+    ("C1", [32, 32, 32], None),
+    ("C2", [40, 36, 3], None),
+    ("C3", [24, 32, 3, 10], [5, 7, 1, 3]),
+    ("C4", [12, 11, 10, 9], [4, 5, 3, 4]),
+    ("C5a", [7, 6, 5, 6, 5], [3, 4, 2, 3, 2]),
+]
+
+
+@pytest.mark.parametrize("name,dims,sketch", BLOCK_CASES)
+@pytest.mark.parametrize("packed", [False, True])
+def test_block_quantities_match_oracle(name, dims, sketch, packed):
+    """d (Eq. 9/15), G (Eq. 13), h (Eq. 10/16, R5), num and den (Eq. 12/18) of every block at
+    the initial cores, sweep t = 0."""
+    _cuda()
+    spec = small_spec(name, dims, sketch)
+    prob = make_problem(spec)
+    src, _ = oracle_source(prob)
+    cfg = oracle_config(spec)
+    st = O.State(cfg, prob.init, src)
+    ctx = gpu_context(prob, packed=packed)
+    N = len(dims)
+    for k in range(N):
+        g = ctx.block_probe(0, k)
+        sets = O.index_sets_for_block(cfg, 0, k)
+        Xk, Pk = O.working_set(src, k, sets)
+        S = O.subchain(st.cores, k, sets)
+        d, E, W = O.gradient_block(Xk, Pk, O.core_unfold2(st.cores[k]), S, st.sigma,
+                                   cfg.sigma_mode == O.SIGMA_INF)
+        G = O.gram_fgmc(st.Qs, k, spec.ranks)
+        h, _ = O.scaled_gradient(d, G, cfg.lambda_rel)
+        num = float(np.sum(d * h))
+        den = O.line_search_den(h, Pk, W, S)
+        assert g["n_obs"] == int(Pk.sum())
+        assert rel_fro(g["G"], G) <= 1e-6, k
+        assert rel_fro(g["d"], d) <= 1e-4, k
+        assert rel_fro(g["h"], h) <= 1e-4, k
+        assert abs(g["num"] - num) <= 1e-4 * abs(num), k
+        assert abs(g["den"] - den) <= 1e-4 * abs(den), k
+        e_obs = E[Pk]
+        assert abs(g["sum_e2"] - float(np.sum(e_obs ** 2))) <= 1e-5 * float(np.sum(e_obs ** 2))
+    ctx.close()
+
+
+# ---------------------------------------------------------------------------- sweeps
+SWEEP_CASES = [
+    ("C1", [32, 32, 32], None),
+    ("C2", [64, 48, 3], None),
+    ("C3", [48, 64, 3, 20], [10, 13, 1, 4]),
+    ("C4", [16, 16, 16, 16], [8, 8, 8, 8]),
+    ("C5a", [8, 8, 8, 8, 8], [5, 5, 5, 5, 5]),
+]
+
+
+@pytest.mark.parametrize("name,dims,sketch", SWEEP_CASES)
+def test_cores_after_one_sweep(name, dims, sketch):
+    """North-star bar: cores after one sweep within 1e-4 relative Frobenius of the oracle."""
+    _cuda()
+    spec = small_spec(name, dims, sketch)
+    prob = make_problem(spec)
+    src, _ = oracle_source(prob)
+    cfg = oracle_config(spec)
+    st, recs = O.run(cfg, prob.init, src, 1)
+    ctx = gpu_context(prob)
+    gst = ctx.sweep(1)
+    gc = ctx.get_cores()
+    err = cores_rel_err(gc, st.cores)
+    assert err <= 1e-4, err
+    assert gst[0]["n_obs"] == recs[0].n_obs
+    assert abs(gst[0]["sigma"] - recs[0].sigma) <= 1e-6 * recs[0].sigma
+    for k in range(len(dims)):
+        assert gst[0]["nnz"][k] == recs[0].nnz[k]
+        assert abs(gst[0]["eta"][k] - recs[0].eta[k]) <= 1e-4 * max(abs(recs[0].eta[k]), 1e-30)
+    ctx.close()
+
+
+@pytest.mark.parametrize("name,dims,sketch,sweeps", [
+    ("C1", [32, 32, 32], None, 20),
+    ("C2", [64, 48, 3], None, 20),
+    ("C4", [16, 16, 16, 16], [8, 8, 8, 8], 20),
+])
+def test_final_error_after_sweeps(name, dims, sketch, sweeps):
+    """North-star bar: final relative reconstruction error within 1e-3 of the oracle's."""
+    _cuda()
+    spec = small_spec(name, dims, sketch)
+    prob = make_problem(spec)
+    src, Xc = oracle_source(prob)
+    st, recs = O.run(oracle_config(spec), prob.init, src, sweeps)
+    e_or = O.relative_error(st.cores, Xc)
+    ctx = gpu_context(prob)
+    ctx.sweep(sweeps, stats=False)
+    gerr = ctx.error(prob.X_clean.cuda())
+    e_gpu_or = O.relative_error(ctx.get_cores(), Xc)
+    assert abs(gerr["rel_err_all"] - e_gpu_or) <= 1e-5          # trd_error vs oracle formula
+    assert abs(e_gpu_or - e_or) <= 1e-3, (e_gpu_or, e_or)
+    ctx.close()
+
+
+def test_reconstruct_matches_definition():
+    """trd_reconstruct (Def. 1) at random linear indices vs the oracle trace."""
+    _cuda()
+    spec = small_spec("C3", [12, 10, 3, 7], [4, 4, 1, 3])
+    prob = make_problem(spec)
+    ctx = gpu_context(prob)
+    cores = [c.astype(np.float64) for c in prob.init]
+    n = int(np.prod(spec.dims))
+    lin = torch.randint(0, n, (500,), generator=torch.Generator().manual_seed(1))
+    out = ctx.reconstruct(lin.cuda()).cpu().numpy()
+    for t, l in enumerate(lin.tolist()):
+        idx, rem = [], l
+        for I in spec.dims:
+            idx.append(rem % I)
+            rem //= I
+        assert abs(out[t] - O.tr_entry(cores, idx)) <= 1e-5 * max(1.0, abs(out[t]))
+    ctx.close()
+
+
+def test_packed_equals_dense_bitwise_and_deterministic():
+    """Packed storage (observed values only) gives bit-identical cores to the dense layout,
+    and two runs are bit-identical (fixed-order reductions, no float atomics)."""
+    _cuda()
+    spec = small_spec("C4", [16, 16, 16, 16], [8, 8, 8, 8])
+    prob = make_problem(spec)
+    a = gpu_context(prob, packed=False)
+    b = gpu_context(prob, packed=True)
+    c = gpu_context(prob, packed=True, host=True)
+    for ctx in (a, b, c):
+        ctx.sweep(3, stats=False)
+    ca, cb, cc = a.get_cores(), b.get_cores(), c.get_cores()
+    for x, y, z in zip(ca, cb, cc):
+        assert np.array_equal(x, y) and np.array_equal(x, z)
+    for ctx in (a, b, c):
+        ctx.close()
+
+
+def test_sigma_inf_and_fixed_step_modes():
+    """sigma = inf (W == 1) and a fixed step eta (config step > 0) vs the oracle."""
+    _cuda()
+    spec = small_spec("C1", [20, 18, 16])
+    prob = make_problem(spec)
+    src, _ = oracle_source(prob)
+    for over in [dict(sigma_mode=O.SIGMA_INF), dict(sigma_mode=O.SIGMA_FIXED, sigma=0.7),
+                 dict(sigma_mode=O.SIGMA_FIXED, sigma=0.7, step=0.05)]:
+        st, _ = O.run(oracle_config(spec, **over), prob.init, src, 1)
+        ctx = gpu_context(prob, **over)
+        ctx.sweep(1)
+        assert cores_rel_err(ctx.get_cores(), st.cores) <= 1e-4, over
+        ctx.close()
+
+
+def test_edge_rank_one_and_singleton_mode():
+    """Degenerate shapes: rank-1 bonds, a mode of extent 1 (C3's s_3 = 1 analogue)."""
+    _cuda()
+    spec = small_spec("C3", [9, 7, 1, 5], [3, 3, 1, 2])
+    spec.ranks = [2, 1, 3, 2]
+    prob = make_problem(spec)
+    src, _ = oracle_source(prob)
+    st, _ = O.run(oracle_config(spec), prob.init, src, 1)
+    ctx = gpu_context(prob)
+    ctx.sweep(1)
+    assert cores_rel_err(ctx.get_cores(), st.cores) <= 1e-4
+    ctx.close()
+
+
+def test_stop_metric_matches_oracle():
+    """Alg. 1 l.12-13 stop metric e_t over 3 sweeps."""
+    _cuda()
+    spec = small_spec("C1", [16, 15, 14])
+    prob = make_problem(spec)
+    src, _ = oracle_source(prob)
+    st, recs = O.run(oracle_config(spec), prob.init, src, 3)
+    ctx = gpu_context(prob)
+    g = ctx.sweep(3)
+    assert math.isnan(g[0]["stop_e"])
+    for t in (1, 2):
+        assert abs(g[t]["stop_e"] - recs[t].stop_e) <= 1e-3 * recs[t].stop_e
+    ctx.close()
