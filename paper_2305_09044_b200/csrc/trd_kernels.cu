@@ -356,7 +356,7 @@ pass_kernel(PassArgs a) {
       if (!__any_sync(0xffffffffu, obs)) continue;
       const float* rc = a.rgtT + min(col, a.ncols - 1);
       float recon = 0.f, tdir = 0.f;
-#pragma unroll 4
+#pragma unroll
       for (int q = 0; q < KT; ++q) {
         if (q < a.K) {
           const float r = __ldg(rc + (int64_t)q * a.ncols);
@@ -376,7 +376,7 @@ pass_kernel(PassArgs a) {
         }
         if (!STATS_ONLY) {
           const float cv = obs ? w * e : 0.f;
-#pragma unroll 4
+#pragma unroll
           for (int q = 0; q < KT; ++q)
             if (q < a.K) dacc[q] = fmaf(cv, __ldg(rc + (int64_t)q * a.ncols), dacc[q]);
         }

@@ -176,12 +176,13 @@ class Problem:
     mask: torch.Tensor
     init: list
     n_obs: int
+    mask_bool: Optional[torch.Tensor] = None
 
     def packed_values(self):
         return self.X[unpack_bits(self.mask, self.spec.numel)]
 
 
-def make_problem(spec: ProblemSpec, device="cpu", chunk=1 << 24) -> Problem:
+def make_problem(spec: ProblemSpec, device="cpu", chunk=1 << 24, keep_mask_bool=False) -> Problem:
     """Build X = outliers(mask, X* + noise) with the seeded recipe of `spec`.
 
     Random draws come from one torch.Generator on `device` seeded with data_seed + 1, in a
@@ -222,7 +223,8 @@ def make_problem(spec: ProblemSpec, device="cpu", chunk=1 << 24) -> Problem:
         mask_bool[0] = True
     words = pack_bits(mask_bool)
     n_obs = int(mask_bool.sum().item())
-    return Problem(spec, X, Xc, words, init_cores(spec), n_obs)
+    return Problem(spec, X, Xc, words, init_cores(spec), n_obs,
+                   mask_bool if keep_mask_bool else None)
 
 
 def to_numpy_views(prob: Problem):
