@@ -100,7 +100,16 @@ double plan_cost(int64_t K, int64_t ncols) {
   return (double)K / util * (1.0 + 0.02 * shape);
 }
 
-void build_plan(const Context& c, int k, const int64_t* s_in, BlockPlan& bp) {
+// cost model of a split p for the tensor-core pass kernels: dense MMA work scales with the
+// padded inner dimension KP; narrow column sets (< one 64-column tile) waste the tile
+double plan_cost_tc(int64_t K, int64_t ncols) {
+  const double KP = (double)((K + 15) / 16 * 16);
+  const double waste = ncols >= 64 ? std::ceil(ncols / 64.0) * 64.0 / ncols : 64.0 / ncols;
+  const double shape = std::fabs(std::log2(std::max<double>(ncols, 1.0) / 4096.0));
+  return KP * waste * (1.0 + 0.02 * shape);
+}
+
+void build_plan(const Context& c, int k, const int64_t* s_in, BlockPlan& bp, bool want_tc) {
   const int N = c.N;
   memset(&bp, 0, sizeof(bp));
   bp.k = k;
@@ -116,7 +125,7 @@ void build_plan(const Context& c, int k, const int64_t* s_in, BlockPlan& bp) {
     const int64_t K = (int64_t)c.ranks[k] * rs;
     int64_t ncols = 1;
     for (int q = p + 1; q <= N - 1; ++q) ncols *= bp.s[(k + q) % N];
-    const double cost = plan_cost(K, ncols);
+    const double cost = want_tc ? plan_cost_tc(K, ncols) : plan_cost(K, ncols);
     if (cost < best - 1e-12) { best = cost; best_p = p; }
   }
   const int p = best_p;
@@ -127,6 +136,19 @@ void build_plan(const Context& c, int k, const int64_t* s_in, BlockPlan& bp) {
   for (int q = 0; q < p; ++q) { bp.left[q] = (k + 1 + q) % N; bp.nL *= bp.s[bp.left[q]]; }
   bp.ncols = 1;
   for (int q = 0; q < bp.nright; ++q) { bp.right[q] = (k + 1 + p + q) % N; bp.ncols *= bp.s[bp.right[q]]; }
+  // digit orders: mode 0 (unit stride in memory) becomes the fastest digit of its group, and
+  // for k == 0 the rows enumerate i_0 fastest, so that the bitmask / packed values of
+  // consecutive rows or columns are contiguous (coalesced in the pass kernels)
+  auto order = [](const int* modes, int n, int* dig) {
+    int q0 = -1;
+    for (int q = 0; q < n; ++q) if (modes[q] == 0) q0 = q;
+    int d = 0;
+    if (q0 >= 0) dig[d++] = q0;
+    for (int q = 0; q < n; ++q) if (q != q0) dig[d++] = q;
+  };
+  order(bp.left, bp.nleft, bp.ldig);
+  order(bp.right, bp.nright, bp.rdig);
+  bp.rowmode = (k == 0) ? 1 : 0;
   bp.rk = c.ranks[k];
   bp.rk1 = c.ranks[(k + 1) % N];
   bp.rs = c.ranks[(k + p + 1) % N];
@@ -135,6 +157,16 @@ void build_plan(const Context& c, int k, const int64_t* s_in, BlockPlan& bp) {
   const int64_t Ik = c.dims[k];
   bp.nrows = Ik * bp.nL;
   bp.nnz_ws = bp.nrows * bp.ncols;
+  bp.KP = (bp.K + 15) / 16 * 16;
+  bp.use_tc = want_tc && bp.KP <= 256;
+  bp.n_row_tiles = (bp.nrows + 127) / 128;
+  bp.n_col_tiles = (bp.ncols + 63) / 64;
+  {
+    int64_t ns = (2 * 148 + bp.n_row_tiles - 1) / bp.n_row_tiles;
+    ns = std::min<int64_t>(ns, bp.n_col_tiles);
+    ns = std::max<int64_t>(ns, 1);
+    bp.tc_nsplit = (int)std::min<int64_t>(ns, 65535);
+  }
   // geometry: 8 warps per CTA, one (row, column sub-range) item per warp
   if (bp.nL >= 8) { bp.jl_per_cta = 8; bp.ws_split = 1; }
   else {
@@ -181,10 +213,21 @@ trd_status block_pass1(Context* c, const BlockPlan& bp) {
   launch_sampler(*c, bp, s);
   launch_plan(*c, bp, s);
   launch_lft(*c, bp, c->Z + c->zoff[bp.k], 0, c->lft, s);
+  TcStage& stg = c->stage[bp.k];
+  if (bp.use_tc) {
+    launch_tc_pack_rows(*c, bp, c->lft, c->lftHL, s);
+    launch_tc_pack_cols(*c, bp, s);
+    if (!stg.valid) {                       // a2: stage the sketch in tile order
+      launch_tc_stage(*c, bp, stg, s);
+      stg.valid = stg.invariant;
+    }
+  }
   const int e0 = c->prof ? prof_event(c) : -1;
-  launch_pass1(*c, bp, 0, s);
+  if (bp.use_tc) launch_tc_pass(*c, bp, stg, false, s);
+  else launch_pass1(*c, bp, 0, s);
   if (c->prof) c->ev_pass1.push_back({e0, prof_event(c)});
-  launch_reduce_d(*c, bp, s);
+  if (bp.use_tc) launch_tc_reduce_d(*c, bp, s);
+  else launch_reduce_d(*c, bp, s);
   trd_status st = check_launch(c, "pass 1");
   if (st) return st;
   const int64_t Ik = c->dims[bp.k];
@@ -201,8 +244,10 @@ trd_status block_pass2(Context* c, const BlockPlan& bp) {
   launch_solve(*c, bp, s);
   launch_h(*c, bp, s);
   launch_lft(*c, bp, nullptr, 1, c->lfth, s);
+  if (bp.use_tc) launch_tc_pack_rows(*c, bp, c->lfth, c->lfthHL, s);
   const int e0 = c->prof ? prof_event(c) : -1;
-  launch_pass2(*c, bp, s);
+  if (bp.use_tc) launch_tc_pass(*c, bp, c->stage[bp.k], true, s);
+  else launch_pass2(*c, bp, s);
   if (c->prof) c->ev_pass2.push_back({e0, prof_event(c)});
   launch_reduce_den(*c, bp, s);
   trd_status st = check_launch(c, "pass 2");
@@ -386,12 +431,30 @@ trd_status trd_init(const trd_config* cfg, const trd_shard* shard, const float* 
   // ---- plans and workspace sizes ----
   size_t max_rows = 0, max_cols = 0, max_lft = 0, max_rgt = 0, max_mid = 0, max_dp = 0, max_sp = 0;
   size_t max_dvec = 0, max_h = 0, idx_total = 0;
+  size_t max_lhl = 0, max_rhl = 0, max_contrib = 0;
   int64_t full_s[kMaxN];
   for (int m = 0; m < N; ++m) full_s[m] = 0;
+  {
+    const char* pe = getenv("TRD_PASS");
+    c->want_tc = !(pe && strcmp(pe, "simt") == 0);
+  }
   for (int k = 0; k <= N; ++k) {
     BlockPlan& bp = (k < N) ? c->plan[k] : c->full_plan;
-    if (k < N) build_plan(*c, k, cfg->sketch, bp);
-    else build_plan(*c, 0, full_s, bp);
+    if (k < N) build_plan(*c, k, cfg->sketch, bp, c->want_tc != 0);
+    else build_plan(*c, 0, full_s, bp, false);
+    if (bp.use_tc && !tc_supported_kp(bp.KP)) bp.use_tc = 0;
+    if (bp.use_tc) {
+      TcStage& st = c->stage[k];
+      st.n_tiles = bp.n_row_tiles * bp.n_col_tiles;
+      st.invariant = true;
+      for (int m = 0; m < N; ++m)
+        if (m != k && bp.s[m] < c->dims[m]) st.invariant = false;
+      st.vcap = bp.n_row_tiles * 128 * bp.n_col_tiles * 64;   // refined after the data is known
+      max_lhl = std::max(max_lhl, (size_t)(bp.n_row_tiles * 2 * 128 * bp.KP));
+      max_rhl = std::max(max_rhl, (size_t)(bp.n_col_tiles * 2 * 64 * bp.KP));
+      max_contrib = std::max(max_contrib, (size_t)bp.tc_nsplit * bp.n_row_tiles * 128 * bp.R2);
+      max_sp = std::max(max_sp, (size_t)(bp.n_row_tiles * bp.tc_nsplit * 3));
+    }
     max_rows = std::max(max_rows, (size_t)bp.nrows);
     max_cols = std::max(max_cols, (size_t)bp.ncols);
     max_lft = std::max(max_lft, (size_t)(bp.nrows * bp.K));
@@ -435,6 +498,11 @@ trd_status trd_init(const trd_config* cfg, const trd_shard* shard, const float* 
       (st = dalloc(c, &c->Dcur, (size_t)(In * In))) || (st = dalloc(c, &c->Dprev, (size_t)(In * In))) ||
       (st = dalloc(c, &c->sc, 1)) || (st = dalloc(c, &c->red_ws, 1024)))
     return bail(st);
+  if (max_lhl > 0) {
+    if ((st = dalloc(c, &c->lftHL, max_lhl)) || (st = dalloc(c, &c->lfthHL, max_lhl)) ||
+        (st = dalloc(c, &c->rgtHL, max_rhl)) || (st = dalloc(c, &c->contrib, max_contrib)))
+      return bail(st);
+  }
   if ((st = ensure_stats(c, 4))) return bail(st);
   cudaStream_t s = c->stream;
 
@@ -458,6 +526,25 @@ trd_status trd_init(const trd_config* cfg, const trd_shard* shard, const float* 
     c->n_values = (int64_t)last_pref + __builtin_popcount(last_word);
   } else {
     c->n_values = c->n_local;
+  }
+  // ---- staged working sets of the tensor-core blocks (a2) ----
+  {
+    int64_t max_v = 0;
+    for (int k = 0; k < N; ++k) {
+      if (!c->plan[k].use_tc) continue;
+      TcStage& sg = c->stage[k];
+      const int64_t obs_cap = c->packed ? c->n_values : c->n_local;
+      sg.vcap = std::max<int64_t>(1, std::min(sg.vcap, obs_cap));
+      sg.scan_tmp_bytes = tc_scan_tmp_bytes(sg.n_tiles);
+      if ((st = dalloc(c, &sg.tbits, (size_t)sg.n_tiles * 128)) ||
+          (st = dalloc(c, &sg.troff, (size_t)sg.n_tiles * 128)) ||
+          (st = dalloc(c, &sg.tbase, (size_t)sg.n_tiles + 1)) ||
+          (st = dalloc(c, &sg.tvals, (size_t)sg.vcap)) ||
+          (st = dalloc(c, reinterpret_cast<char**>(&sg.scan_tmp), sg.scan_tmp_bytes + 16)))
+        return bail(st);
+      max_v = std::max(max_v, sg.vcap);
+    }
+    if (max_v > 0 && (st = dalloc(c, &c->tw, (size_t)max_v))) return bail(st);
   }
   if (shard->host) {
     if ((st = dalloc(c, &c->own_values, (size_t)c->n_values))) return bail(st);
@@ -508,6 +595,7 @@ trd_status trd_upload(trd_ctx* ctx, const float* values_host, const uint32_t* ma
   CUDA_TRY(c, cudaMemcpyAsync(c->own_mask, mask_host, c->n_words * 4, cudaMemcpyHostToDevice, c->stream));
   CUDA_TRY(c, cudaMemcpyAsync(c->own_values, values_host, c->n_values * 4, cudaMemcpyHostToDevice, c->stream));
   if (c->packed) launch_rank_prefix(*c, c->stream);
+  for (int k = 0; k < c->N; ++k) c->stage[k].valid = false;   // staged sketches are stale
   return check_launch(c, "upload");
 }
 
@@ -705,9 +793,17 @@ void trd_destroy(trd_ctx* ctx) {
   void* ptrs[] = {c->own_values, c->own_mask, c->rank_prefix, c->Z, c->Q, c->idx, c->doff,
                   c->row_off, c->col_off, c->mid, c->lft, c->lfth, c->rgtT, c->dpart, c->spart,
                   c->denpart, c->numpart, c->dvec, c->G, c->G_last, c->Mop, c->chol_ws,
-                  c->chain_ws, c->h, c->Dcur, c->Dprev, c->sc, c->stats, c->red_ws};
+                  c->chain_ws, c->h, c->Dcur, c->Dprev, c->sc, c->stats, c->red_ws,
+                  c->lftHL, c->lfthHL, c->rgtHL, c->contrib};
   for (void* p : ptrs)
     if (p) cudaFree(p);
+  if (c->tw) cudaFree(c->tw);
+  for (int k = 0; k < kMaxN; ++k) {
+    TcStage& sg = c->stage[k];
+    void* sp[] = {sg.tbits, sg.troff, sg.tbase, sg.tvals, sg.scan_tmp};
+    for (void* p : sp)
+      if (p) cudaFree(p);
+  }
   delete c;
 }
 

@@ -1,6 +1,7 @@
 // trd_internal.cuh -- context layout, block plans and kernel entry points of libtrd.
 // Paper citations "P:L" are PAPER.md lines.  See DESIGN.md for the data layout in HBM.
 #pragma once
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <string>
@@ -56,9 +57,32 @@ struct BlockPlan {
   int64_t s[kMaxN];      // sizes of the index sets of this block (s_k = I_k)
   int64_t nL, nrows, ncols;
   int64_t nnz_ws;        // |WS_k| (all entries, observed or not)
-  // pass-kernel geometry
+  // digit orders: rows = (i_k, j_L) with rowmode 0: row = jl + nL*ik, 1: row = ik + I_k*jl;
+  // j_L / j_R mixed radix with ldig / rdig (indices into left / right, fastest first), chosen
+  // so that mode 0 (contiguous in memory) is the fastest digit of rows or columns
+  int rowmode;
+  int ldig[kMaxN], rdig[kMaxN];
+  // pass-kernel geometry (v1 SIMT)
   int jl_per_cta, ws_split, nsplit;
   int64_t grid_x;        // ceil(nL / jl_per_cta)
+  // tensor-core pass kernels (trd_tc.cu)
+  int use_tc;            // 1: tcgen05 pass kernels
+  int KP;                // K padded to a multiple of 16
+  int64_t n_row_tiles, n_col_tiles;
+  int tc_nsplit;         // column splits per row tile
+};
+
+// Staged working set of one block in tile order (trd_tc.cu "stage sketch", row a2)
+struct TcStage {
+  uint64_t* tbits = nullptr;     // [tile][128] observation mask of (row, 64 columns)
+  uint16_t* troff = nullptr;     // [tile][128] row offset into the tile's compacted values
+  uint64_t* tbase = nullptr;     // [tile] exclusive prefix of the tile counts
+  float* tvals = nullptr;        // compacted observed values, tile-major, row-major in a tile
+  void* scan_tmp = nullptr;
+  size_t scan_tmp_bytes = 0;
+  int64_t n_tiles = 0, vcap = 0;
+  bool invariant = false;        // working set identical every sweep (full index sets)
+  bool valid = false;            // staged data current
 };
 
 struct Context {
@@ -101,6 +125,14 @@ struct Context {
   float* lft = nullptr;                // Lft rows: [row][K]
   float* lfth = nullptr;               // Lft of the scaled gradient (pass 2)
   float* rgtT = nullptr;               // Rgt: [K][ncols]
+  // tensor-core operands: fp16 hi/lo core-matrix tiles, and per-row gradient contributions
+  int want_tc = 1;                     // TRD_PASS=simt disables the tcgen05 pass kernels
+  __half* lftHL = nullptr;             // [row][hi KP | lo KP] (A operand, loaded into TMEM)
+  __half* lfthHL = nullptr;            // same for the scaled gradient (pass 2)
+  __half* rgtHL = nullptr;             // [col tile][hi | lo][64 x KP] core-matrix layout
+  float* contrib = nullptr;            // [split][row][R2]
+  float* tw = nullptr;                 // staged HQ weights of the current block (pass 1 -> 2)
+  TcStage stage[kMaxN];
   double* dpart = nullptr;             // pass-1 CTA partials of d
   double* spart = nullptr;             // pass-1 CTA partial stats (3 per CTA)
   double* denpart = nullptr;           // pass-2 CTA partials
@@ -155,5 +187,14 @@ void launch_reset_block_scalars(Context& c, cudaStream_t s);
 void launch_record_block(Context& c, const BlockPlan& bp, int slot, cudaStream_t s);
 void launch_sweep_begin(Context& c, int slot, cudaStream_t s);
 void launch_fill_full_sets(Context& c, const BlockPlan& bp, cudaStream_t s);
+
+// ---- tensor-core pass kernels (trd_tc.cu) ---------------------------------------------
+bool tc_supported_kp(int KP);
+void launch_tc_pack_rows(Context& c, const BlockPlan& bp, const float* src, __half* dst, cudaStream_t s);
+void launch_tc_pack_cols(Context& c, const BlockPlan& bp, cudaStream_t s);
+void launch_tc_pass(Context& c, const BlockPlan& bp, const TcStage& st, bool pass2, cudaStream_t s);
+void launch_tc_reduce_d(Context& c, const BlockPlan& bp, cudaStream_t s);
+void launch_tc_stage(Context& c, const BlockPlan& bp, TcStage& st, cudaStream_t s);
+size_t tc_scan_tmp_bytes(int64_t n_tiles);
 
 }  // namespace trd

@@ -97,10 +97,12 @@ __global__ void sampler_kernel(SamplerArgs sa, const DevScalars* __restrict__ sc
 struct PlanArgs {
   int N, k, p, nleft, nright;
   int left[kMaxN], right[kMaxN];
+  int ldig[kMaxN], rdig[kMaxN];        // digit order (fastest first) as indices into left/right
+  int rowmode;                         // 0: row = jl + nL*ik ; 1: row = ik + Ik*jl
   int64_t sL[kMaxN], sR[kMaxN];        // sizes of the left/right index sets
   int64_t offL[kMaxN], offR[kMaxN];    // offsets into idx/doff
   int64_t off_k;
-  int64_t nL, nrows, ncols;
+  int64_t nL, nrows, ncols, Ik;
   int rk, rk1, rs, K;
   int rank_of[kMaxN + 1];
   int64_t zoff[kMaxN + 1];
@@ -111,16 +113,39 @@ static PlanArgs make_plan_args(const Context& c, const BlockPlan& bp) {
   a.N = c.N; a.k = bp.k; a.p = bp.p; a.nleft = bp.nleft; a.nright = bp.nright;
   for (int q = 0; q < bp.nleft; ++q) {
     a.left[q] = bp.left[q]; a.sL[q] = bp.s[bp.left[q]]; a.offL[q] = c.idx_off[bp.left[q]];
+    a.ldig[q] = bp.ldig[q];
   }
   for (int q = 0; q < bp.nright; ++q) {
     a.right[q] = bp.right[q]; a.sR[q] = bp.s[bp.right[q]]; a.offR[q] = c.idx_off[bp.right[q]];
+    a.rdig[q] = bp.rdig[q];
   }
+  a.rowmode = bp.rowmode;
   a.off_k = c.idx_off[bp.k];
-  a.nL = bp.nL; a.nrows = bp.nrows; a.ncols = bp.ncols;
+  a.nL = bp.nL; a.nrows = bp.nrows; a.ncols = bp.ncols; a.Ik = bp.nrows / bp.nL;
   a.rk = bp.rk; a.rk1 = bp.rk1; a.rs = bp.rs; a.K = bp.K;
   for (int m = 0; m <= c.N; ++m) a.rank_of[m] = c.ranks[m % c.N];
   for (int m = 0; m <= c.N; ++m) a.zoff[m] = c.zoff[m];
   return a;
+}
+
+// row <-> (ik, jl) and mixed-radix digits of jl / col (per ring position q)
+__device__ __forceinline__ void row_split(const PlanArgs& a, int64_t row, int64_t& ik, int64_t& jl) {
+  if (a.rowmode == 0) { jl = row % a.nL; ik = row / a.nL; }
+  else { ik = row % a.Ik; jl = row / a.Ik; }
+}
+__device__ __forceinline__ void left_digits(const PlanArgs& a, int64_t jl, int64_t* dq) {
+  for (int d = 0; d < a.nleft; ++d) {
+    const int q = a.ldig[d];
+    dq[q] = jl % a.sL[q];
+    jl /= a.sL[q];
+  }
+}
+__device__ __forceinline__ void right_digits(const PlanArgs& a, int64_t col, int64_t* dq) {
+  for (int d = 0; d < a.nright; ++d) {
+    const int q = a.rdig[d];
+    dq[q] = col % a.sR[q];
+    col /= a.sR[q];
+  }
 }
 
 __global__ void offsets_kernel(PlanArgs a, const int64_t* __restrict__ doff,
@@ -128,29 +153,30 @@ __global__ void offsets_kernel(PlanArgs a, const int64_t* __restrict__ doff,
   const int64_t tot = a.nrows + a.ncols;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tot;
        t += (int64_t)gridDim.x * blockDim.x) {
+    int64_t dq[kMaxN];
     if (t < a.nrows) {
-      int64_t jl = t % a.nL, ik = t / a.nL;
+      int64_t ik, jl;
+      row_split(a, t, ik, jl);
+      left_digits(a, jl, dq);
       int64_t o = doff[a.off_k + ik];
       bool bad = o < 0;
       for (int q = 0; q < a.nleft; ++q) {
-        int64_t dgt = jl % a.sL[q];
-        jl /= a.sL[q];
-        int64_t v = doff[a.offL[q] + dgt];
+        int64_t v = doff[a.offL[q] + dq[q]];
         bad |= v < 0;
         o += v;
       }
       row_off[t] = bad ? -1 : o;
     } else {
-      int64_t col = t - a.nrows, o = 0;
+      const int64_t col = t - a.nrows;
+      right_digits(a, col, dq);
+      int64_t o = 0;
       bool bad = false;
       for (int q = 0; q < a.nright; ++q) {
-        int64_t dgt = col % a.sR[q];
-        col /= a.sR[q];
-        int64_t v = doff[a.offR[q] + dgt];
+        int64_t v = doff[a.offR[q] + dq[q]];
         bad |= v < 0;
         o += v;
       }
-      col_off[t - a.nrows] = bad ? -1 : o;
+      col_off[col] = bad ? -1 : o;
     }
   }
 }
@@ -178,16 +204,16 @@ __global__ void mid_kernel(PlanArgs a, const int32_t* __restrict__ idx, const fl
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tot;
        t += (int64_t)gridDim.x * blockDim.x) {
     int b = (int)(t % a.rk1);
-    int64_t jl = t / a.rk1, rem = jl;
+    int64_t jl = t / a.rk1;
+    int64_t dq[kMaxN];
+    left_digits(a, jl, dq);
     float v[kMaxR];
 #pragma unroll
     for (int c = 0; c < kMaxR; ++c) v[c] = (c == b) ? 1.f : 0.f;
     int rin = a.rk1;
     for (int q = 0; q < a.nleft; ++q) {
       int m = a.left[q];
-      int64_t dgt = rem % a.sL[q];
-      rem /= a.sL[q];
-      int64_t i = idx[a.offL[q] + dgt];
+      int64_t i = idx[a.offL[q] + dq[q]];
       int rout = a.rank_of[m + 1];
       vecmat(v, Z + a.zoff[m] + i * (int64_t)a.rank_of[m] * rout, rin, rout);
       rin = rout;
@@ -206,16 +232,15 @@ __global__ void rgt_kernel(PlanArgs a, const int32_t* __restrict__ idx, const fl
        t += (int64_t)gridDim.x * blockDim.x) {
     int64_t col = t % a.ncols;
     int cc = (int)(t / a.ncols);
-    int64_t rem = col;
+    int64_t dq[kMaxN];
+    right_digits(a, col, dq);
     float v[kMaxR];
 #pragma unroll
     for (int c = 0; c < kMaxR; ++c) v[c] = (c == cc) ? 1.f : 0.f;
     int rin = a.rs;
     for (int q = 0; q < a.nright; ++q) {
       int m = a.right[q];
-      int64_t dgt = rem % a.sR[q];
-      rem /= a.sR[q];
-      int64_t i = idx[a.offR[q] + dgt];
+      int64_t i = idx[a.offR[q] + dq[q]];
       int rout = a.rank_of[m + 1];
       vecmat(v, Z + a.zoff[m] + i * (int64_t)a.rank_of[m] * rout, rin, rout);
       rin = rout;
@@ -233,7 +258,8 @@ __global__ void lft_kernel(PlanArgs a, const float* __restrict__ Zk, const doubl
        t += (int64_t)gridDim.x * blockDim.x) {
     int aa = (int)(t % a.rk);
     int64_t row = t / a.rk;
-    int64_t jl = row % a.nL, ik = row / a.nL;
+    int64_t jl, ik;
+    row_split(a, row, ik, jl);
     float v[kMaxR];
 #pragma unroll
     for (int b = 0; b < kMaxR; ++b) {
@@ -264,6 +290,8 @@ struct PassArgs {
   int K, R2, rk, rk1, rs, p;
   int jl_per_cta, ws_split, nsplit;
   int sigma_inf, packed;
+  int rowmode;
+  int64_t Ik;
   const int64_t* row_off;
   const int64_t* col_off;
   const float* lft;
@@ -336,7 +364,7 @@ pass_kernel(PassArgs a) {
   for (int item = warp; item < nitems; item += kPassWarps) {
     const int64_t jl = jl0 + item / a.ws_split;
     const int sub = item % a.ws_split;
-    const int64_t row = jl + a.nL * ik;
+    const int64_t row = a.rowmode == 0 ? jl + a.nL * ik : ik + a.Ik * jl;
     const int64_t ro = a.row_off[row];
     if (ro < 0) continue;
     for (int q = lane; q < a.K; q += 32) {
@@ -458,6 +486,7 @@ static PassArgs make_pass_args(const Context& c, const BlockPlan& bp) {
   a.nL = bp.nL; a.nrows = bp.nrows; a.ncols = bp.ncols;
   a.K = bp.K; a.R2 = bp.R2; a.rk = bp.rk; a.rk1 = bp.rk1; a.rs = bp.rs; a.p = bp.p;
   a.jl_per_cta = bp.jl_per_cta; a.ws_split = bp.ws_split; a.nsplit = bp.nsplit;
+  a.rowmode = bp.rowmode; a.Ik = bp.nrows / bp.nL;
   a.sigma_inf = c.cfg.sigma_mode == TRD_SIGMA_INF;
   a.packed = c.packed;
   a.row_off = c.row_off; a.col_off = c.col_off;
@@ -1029,7 +1058,8 @@ void launch_block_stats(Context& c, const BlockPlan& bp, cudaStream_t s) {
 void launch_reduce_den(Context& c, const BlockPlan& bp, cudaStream_t s) {
   const int64_t Ik = bp.nrows / bp.nL;
   const int64_t ncta = bp.grid_x * bp.nsplit;
-  reduce_den_kernel<<<1, 256, 0, s>>>(c.denpart, Ik * ncta, c.numpart, Ik, c.red_ws);
+  const int64_t nden = bp.use_tc ? bp.n_row_tiles * bp.tc_nsplit : Ik * ncta;
+  reduce_den_kernel<<<1, 256, 0, s>>>(c.denpart, nden, c.numpart, Ik, c.red_ws);
   c.launches++;
 }
 

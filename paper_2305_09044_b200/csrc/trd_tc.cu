@@ -1,0 +1,817 @@
+// trd_tc.cu -- tcgen05 (5th-gen tensor core) pass kernels of the AWRTRD / SAWRTRD block.
+//
+// The working set of block k in GEMM form: rows = (i_k, j_L), cols = j_R,
+// x_hat(row, col) = <Lft(row), Rgt(col)> over K = r_k r_s (Thm 1 P:61 with S = Mid Rgt).
+// Pass 1 (Eq. 7 + Eq. 9/15):
+//     S   = Lft . Rgt^T                       (tcgen05.mma, A = Lft in TMEM, B = Rgt in smem)
+//     c   = P o W o (X - S),  W = exp(-E^2/2s^2)   (epilogue warps; only observed entries)
+//     D  += c . Rgt                           (tcgen05.mma, A = c in TMEM)
+//     d(i_k) += Mid(j_L) D(row)                (per-row contraction, fixed-order reduce)
+// Pass 2 (Eq. 12/18):  T = Lft_h . Rgt^T, den += W T^2 (W staged by pass 1).
+//
+// Precision (R18): every fp32 operand a is split into fp16 a_hi + a_lo with
+// a_lo = fp16(a - a_hi); products use hi.hi + hi.lo + lo.hi accumulated in fp32 in TMEM,
+// which keeps the per-entry dot products at fp32-level accuracy.
+//
+// Stage sketch: per block, the working set is staged in tile order --
+// for every (128-row, 64-column) tile the 64-bit observation mask of each row, the row's
+// offset into the tile's compacted values, and the observed values themselves.  The pass
+// kernels then read 8 B of mask and 4 B per observed entry, coalesced, and their epilogue
+// visits only the set bits.  Sweep-invariant working sets (full index sets, e.g. C5b) are
+// staged once and cached.
+//
+// Tiles: M = 128 rows (one TMEM lane and one epilogue thread per row), NT = 64 columns, K
+// padded to KP (multiple of 16).  The B operand uses the canonical SWIZZLE_NONE core-matrix
+// layout (8 rows x 16 B per 128-byte core matrix, core matrix (g, h) at (g*HK + h)*128 B,
+// HK = KP/8); the same tile is the K-major B of S = A.B^T and the MN-major B of D += c.B.
+#include <cub/cub.cuh>
+#include <cuda_fp16.h>
+
+#include "trd_internal.cuh"
+
+namespace trd {
+
+constexpr int TC_M = 128;
+constexpr int TC_NT = 64;
+constexpr int TC_PREF = 12;          // observed entries per (row, tile) prefetched into registers
+constexpr int TC_DUMP_STRIDE = 68;   // floats per row of the S/T dump buffer (16-B aligned rows)
+
+// ---------------------------------------------------------------------------------------
+// PTX wrappers (tcgen05, mbarrier, proxy fences, cp.async)
+// ---------------------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void tmem_alloc(uint32_t* slot, uint32_t ncols) {
+  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(slot)),
+               "r"(ncols));
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+}
+__device__ __forceinline__ void tmem_dealloc(uint32_t taddr, uint32_t ncols) {
+  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols));
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  const uint32_t addr = smem_u32(bar);
+  uint32_t ok = 0;
+  do {
+    asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+                 "selp.u32 %0, 1, 0, p;\n\t}" : "=r"(ok) : "r"(addr), "r"(phase) : "memory");
+  } while (!ok);
+}
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+// D[tmem] (+)= A[tmem] . B[smem]
+__device__ __forceinline__ void mma_ts(uint32_t d, uint32_t ta, uint64_t db, uint32_t idesc, uint32_t acc) {
+  asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+               "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}"
+               ::"r"(d), "r"(ta), "l"(db), "r"(idesc), "r"(acc));
+}
+// 32 lanes x 16 / 8 consecutive 32-bit columns
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t* v) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+                 "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+               : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t* v) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};"
+               ::"r"(taddr), "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]),
+                 "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]));
+}
+__device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t* v) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};"
+               ::"r"(taddr), "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]));
+}
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem_dst)), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
+// SWIZZLE_NONE shared-memory matrix descriptor (sm_100 version bit 46 = 1)
+__device__ __forceinline__ uint64_t make_sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
+  d |= (uint64_t)1 << 46;
+  return d;
+}
+// kind::f16 instruction descriptor: F32 accumulate, F16 A/B, A K-major, B K- or MN-major
+__host__ __device__ constexpr uint32_t make_idesc(int M, int N, int b_mn_major) {
+  return (1u << 4) | ((uint32_t)b_mn_major << 16) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+__device__ __forceinline__ uint32_t pack_half2(__half lo, __half hi) {
+  return (uint32_t)__half_as_ushort(lo) | ((uint32_t)__half_as_ushort(hi) << 16);
+}
+
+// ---------------------------------------------------------------------------------------
+// Operand packing
+// ---------------------------------------------------------------------------------------
+// A (Lft or Lft_h) row-major: [row][hi KP | lo KP] halves, rows padded to the tile count
+__global__ void tc_pack_rows_kernel(const float* __restrict__ src, int64_t nrows, int K, int KP,
+                                    int64_t nrows_pad, __half* __restrict__ dst) {
+  const int64_t tot = nrows_pad * KP;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tot;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int kap = (int)(t % KP);
+    const int64_t row = t / KP;
+    const float v = (row < nrows && kap < K) ? src[row * K + kap] : 0.f;
+    const __half hi = __float2half_rn(v);
+    const __half lo = __float2half_rn(v - __half2float(hi));
+    dst[row * 2 * KP + kap] = hi;
+    dst[row * 2 * KP + KP + kap] = lo;
+  }
+}
+
+__device__ __forceinline__ int64_t cm_offset(int r, int kap, int HK) {
+  return ((int64_t)((r >> 3) * HK + (kap >> 3)) * 8 + (r & 7)) * 8 + (kap & 7);
+}
+
+// B (Rgt) core-matrix tiles: [col tile][hi | lo][64 x KP]
+__global__ void tc_pack_cols_kernel(const float* __restrict__ rgtT, int64_t ncols, int K, int KP,
+                                    int64_t ntiles, __half* __restrict__ dst) {
+  const int HK = KP / 8;
+  const int64_t tot = ntiles * TC_NT * KP;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tot;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t col = t % (ntiles * TC_NT);
+    const int kap = (int)(t / (ntiles * TC_NT));
+    const float v = (col < ncols && kap < K) ? rgtT[(int64_t)kap * ncols + col] : 0.f;
+    const __half hi = __float2half_rn(v);
+    const __half lo = __float2half_rn(v - __half2float(hi));
+    const int64_t tile = col / TC_NT;
+    const int64_t off = cm_offset((int)(col % TC_NT), kap, HK);
+    __half* base = dst + tile * (2LL * TC_NT * KP);
+    base[off] = hi;
+    base[(int64_t)TC_NT * KP + off] = lo;
+  }
+}
+
+// ---------------------------------------------------------------------------------------
+// Stage sketch: tile-ordered mask bits, row offsets and compacted observed values
+// ---------------------------------------------------------------------------------------
+struct StageArgs {
+  int64_t nrows, ncols, n_col_tiles, n_tiles;
+  int packed;
+  const int64_t* row_off;
+  const int64_t* col_off;
+  const uint32_t* mask;
+  const uint32_t* rank_prefix;
+  const float* values;
+  uint64_t* tbits;        // [tile][128]
+  uint16_t* troff;        // [tile][128]
+  uint64_t* tcount;       // [tile]  (counts, then exclusive prefix)
+  float* tvals;           // compacted values
+};
+
+__global__ void __launch_bounds__(128) stage_bits_kernel(StageArgs s) {
+  __shared__ int64_t sco[TC_NT];
+  __shared__ int wsum[4];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int64_t tile = blockIdx.x; tile < s.n_tiles; tile += gridDim.x) {
+    const int64_t rt = tile / s.n_col_tiles, ct = tile % s.n_col_tiles;
+    if (tid < TC_NT) {
+      const int64_t col = ct * TC_NT + tid;
+      sco[tid] = col < s.ncols ? s.col_off[col] : -1;
+    }
+    __syncthreads();
+    const int64_t row = rt * TC_M + tid;
+    const int64_t ro = row < s.nrows ? s.row_off[row] : -1;
+    uint64_t bits = 0;
+    int64_t cwi = -1;
+    uint32_t cw = 0;
+    if (ro >= 0) {
+      for (int j = 0; j < TC_NT; ++j) {
+        const int64_t co = sco[j];
+        if (co < 0) continue;
+        const int64_t lin = ro + co;
+        const int64_t wi = lin >> 5;
+        if (wi != cwi) { cw = __ldg(s.mask + wi); cwi = wi; }
+        if ((cw >> (lin & 31)) & 1u) bits |= 1ull << j;
+      }
+    }
+    const int cnt = __popcll(bits);
+    int inc = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += v;
+    }
+    if (lane == 31) wsum[warp] = inc;
+    __syncthreads();
+    int base = 0;
+    for (int w = 0; w < warp; ++w) base += wsum[w];
+    const int excl = base + inc - cnt;
+    s.tbits[tile * TC_M + tid] = bits;
+    s.troff[tile * TC_M + tid] = (uint16_t)excl;
+    if (tid == TC_M - 1) s.tcount[tile] = (uint64_t)(excl + cnt);
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(128) stage_vals_kernel(StageArgs s) {
+  __shared__ int64_t sco[TC_NT];
+  const int tid = threadIdx.x;
+  for (int64_t tile = blockIdx.x; tile < s.n_tiles; tile += gridDim.x) {
+    const int64_t rt = tile / s.n_col_tiles, ct = tile % s.n_col_tiles;
+    if (tid < TC_NT) {
+      const int64_t col = ct * TC_NT + tid;
+      sco[tid] = col < s.ncols ? s.col_off[col] : -1;
+    }
+    __syncthreads();
+    const int64_t row = rt * TC_M + tid;
+    uint64_t bits = s.tbits[tile * TC_M + tid];
+    if (bits) {
+      const int64_t ro = s.row_off[row];
+      float* out = s.tvals + s.tcount[tile] + s.troff[tile * TC_M + tid];
+      int q = 0;
+      int64_t cwi = -1;
+      uint32_t cw = 0, cp = 0;
+      while (bits) {
+        const int j = __ffsll((long long)bits) - 1;
+        bits &= bits - 1;
+        const int64_t lin = ro + sco[j];
+        int64_t vi = lin;
+        if (s.packed) {
+          const int64_t wi = lin >> 5;
+          if (wi != cwi) { cw = __ldg(s.mask + wi); cp = __ldg(s.rank_prefix + wi); cwi = wi; }
+          vi = (int64_t)cp + __popc(cw & ((1u << (lin & 31)) - 1u));
+        }
+        out[q++] = __ldg(s.values + vi);
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------------------
+struct TcArgs {
+  int64_t nrows, ncols, nL, Ik, n_col_tiles, nrows_pad;
+  int rowmode, K, R2, rk, rk1, rs, p, nsplit;
+  int sigma_inf;
+  const __half* arow;      // Lft (pass 1) or Lft_h (pass 2), row-major hi | lo
+  const __half* rgtHL;
+  const float* mid;
+  const uint64_t* tbits;
+  const uint16_t* troff;
+  const uint64_t* tbase;
+  const float* tvals;
+  float* tw;               // staged weights (pass 1 writes, pass 2 reads)
+  const DevScalars* sc;
+  float* contrib;          // [split][nrows_pad][R2]
+  double* spart;           // [row_tile][split][3]
+  double* denpart;         // [row_tile][split]
+};
+
+template <int KP>
+struct TcLayout {
+  static constexpr int HK = KP / 8;
+  static constexpr int B_HALVES = 2 * TC_NT * KP;    // hi block then lo block
+  static constexpr uint32_t B_LO_BYTES = TC_NT * KP * 2;
+  static constexpr uint32_t IDESC_S = make_idesc(TC_M, TC_NT, 0);   // S = A . B^T
+  static constexpr uint32_t IDESC_D = make_idesc(TC_M, KP, 1);      // D += P . B (B MN-major)
+};
+
+// S[tmem] = A_hi.B_hi + A_hi.B_lo + A_lo.B_hi with A in TMEM (hi at acol, lo at acol + KP/2)
+template <int KP>
+__device__ __forceinline__ void issue_split_gemm_ts(uint32_t dtmem, uint32_t acol, uint32_t bH) {
+  using L = TcLayout<KP>;
+  uint32_t acc = 0;
+#pragma unroll
+  for (int term = 0; term < 3; ++term) {
+    const uint32_t aa = acol + (term == 2 ? KP / 2 : 0);
+    const uint32_t bb = bH + (term == 1 ? L::B_LO_BYTES : 0u);
+#pragma unroll
+    for (int ks = 0; ks < KP / 16; ++ks) {
+      const uint64_t db = make_sdesc(bb + ks * 256, 128, L::HK * 128);
+      mma_ts(dtmem, aa + ks * 8, db, L::IDESC_S, acc);
+      acc = 1;
+    }
+  }
+}
+
+template <int KP>
+__device__ __forceinline__ void stage_b_async(const TcArgs& a, int64_t ct, __half* sBbuf, int tid) {
+  using L = TcLayout<KP>;
+  const char* g = reinterpret_cast<const char*>(a.rgtHL + ct * L::B_HALVES);
+  char* s = reinterpret_cast<char*>(sBbuf);
+  for (int i = tid; i < L::B_HALVES / 8; i += TC_M) cp_async16(s + i * 16, g + i * 16);
+}
+
+// this thread's row of A (hi | lo) -> TMEM columns [acol, acol + KP)
+template <int KP>
+__device__ __forceinline__ void load_a_to_tmem(const TcArgs& a, int64_t row, uint32_t lane_base, uint32_t acol) {
+  const uint4* g = reinterpret_cast<const uint4*>(a.arow + row * 2 * KP);
+#pragma unroll
+  for (int c = 0; c < KP / 16; ++c) {          // 16 words = 32 halves per chunk
+    uint32_t v[16];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const uint4 q = g[c * 4 + u];
+      v[u * 4 + 0] = q.x; v[u * 4 + 1] = q.y; v[u * 4 + 2] = q.z; v[u * 4 + 3] = q.w;
+    }
+    tmem_st16(lane_base + acol + c * 16, v);
+  }
+}
+
+// ---------------------------------------------------------------------------------------
+// Pass 1: gradient partials, residual statistics, staged weights
+// ---------------------------------------------------------------------------------------
+template <int KP>
+__global__ void __launch_bounds__(128, 1) tc_pass1_kernel(TcArgs a) {
+  using L = TcLayout<KP>;
+  constexpr uint32_t TMEM_COLS = (2 * TC_NT + 2 * KP <= 256) ? 256 : 512;
+  constexpr uint32_t COL_S = 0, COL_P = TC_NT, COL_D = 2 * TC_NT, COL_A = 2 * TC_NT + KP;
+  extern __shared__ __align__(1024) unsigned char smem[];
+  __half* sB = reinterpret_cast<__half*>(smem);                          // [2][B_HALVES]
+  float* dump = reinterpret_cast<float*>(sB + 2 * L::B_HALVES);          // [128][DUMP_STRIDE]
+  float* dbuf = reinterpret_cast<float*>(smem);                          // aliases sB at the end
+  __shared__ uint64_t mbar;
+  __shared__ uint32_t tmem_slot;
+  __shared__ double red[4][3];
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t rt = blockIdx.x;
+  const int split = blockIdx.y;
+  const int64_t row = rt * TC_M + tid;
+  const bool row_ok = row < a.nrows;
+  float* mydump = dump + tid * TC_DUMP_STRIDE;
+
+  const int64_t per = (a.n_col_tiles + a.nsplit - 1) / a.nsplit;
+  const int64_t t0 = (int64_t)split * per;
+  const int64_t t1 = min(a.n_col_tiles, t0 + per);
+
+  if (warp == 0) tmem_alloc(&tmem_slot, TMEM_COLS);
+  if (tid == 0) mbar_init(&mbar, 1);
+  if (t0 < t1) stage_b_async<KP>(a, t0, sB, tid);
+  cp_async_commit();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = tmem_slot;
+  const uint32_t lane_base = tbase + ((uint32_t)(warp * 32) << 16);
+  load_a_to_tmem<KP>(a, row, lane_base, COL_A);
+  tmem_wait_st();
+  cp_async_wait_all();
+  fence_proxy_async();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+
+  const double sigma = a.sc->sigma;
+  const float inv2s2 = a.sigma_inf ? 0.f : (float)(0.5 / (sigma * sigma));
+  const double s2 = sigma * sigma;
+  double st_e2 = 0.0, st_w = 0.0, st_n = 0.0;
+  uint32_t phase = 0;
+  bool d_acc = false;
+
+  for (int64_t t = t0; t < t1; ++t) {
+    const int buf = (int)((t - t0) & 1);
+    const __half* sBc = sB + buf * L::B_HALVES;
+    if (tid == 0) {
+      tc_fence_after();
+      issue_split_gemm_ts<KP>(tbase + COL_S, tbase + COL_A, smem_u32(sBc));
+      mma_commit(&mbar);
+    }
+    // staged tile data of this row (independent of S: overlaps the MMA)
+    const int64_t tile = rt * a.n_col_tiles + t;
+    const uint64_t bits = a.tbits[tile * TC_M + tid];
+    const int64_t vbase = (int64_t)a.tbase[tile] + a.troff[tile * TC_M + tid];
+    const int cnt = __popcll(bits);
+    float xr[TC_PREF];
+#pragma unroll
+    for (int q = 0; q < TC_PREF; ++q) xr[q] = q < cnt ? __ldg(a.tvals + vbase + q) : 0.f;
+    mbar_wait(&mbar, phase);       // S(t) ready; GEMM2(t-1) finished (in-order execution)
+    phase ^= 1;
+    tc_fence_after();
+    const bool has_next = t + 1 < t1;
+    if (has_next) stage_b_async<KP>(a, t + 1, sB + (buf ^ 1) * L::B_HALVES, tid);
+    cp_async_commit();
+    // S row -> dump (only 16-column chunks holding observed entries)
+    {
+      uint32_t sv[TC_NT];
+#pragma unroll
+      for (int q = 0; q < TC_NT / 16; ++q) tmem_ld16(lane_base + COL_S + q * 16, sv + q * 16);
+      tmem_wait_ld();
+#pragma unroll
+      for (int q = 0; q < TC_NT / 16; ++q) {
+        if ((bits >> (16 * q)) & 0xffffull) {
+          float4* d4 = reinterpret_cast<float4*>(mydump + 16 * q);
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            d4[u] = make_float4(__uint_as_float(sv[q * 16 + 4 * u]), __uint_as_float(sv[q * 16 + 4 * u + 1]),
+                                __uint_as_float(sv[q * 16 + 4 * u + 2]), __uint_as_float(sv[q * 16 + 4 * u + 3]));
+        }
+      }
+    }
+    // observed entries: e = x - s, w, c = w e (in place of s), staged w
+    uint64_t b = bits;
+#pragma unroll
+    for (int q = 0; q < TC_PREF; ++q) {
+      if (b) {
+        const int j = __ffsll((long long)b) - 1;
+        b &= b - 1;
+        const float e = xr[q] - mydump[j];
+        const float w = a.sigma_inf ? 1.f : expf(-e * e * inv2s2);
+        mydump[j] = w * e;
+        a.tw[vbase + q] = w;
+        st_e2 += (double)e * (double)e;
+        st_n += 1.0;
+        st_w += s2 * (1.0 - (double)w);
+      }
+    }
+    for (int q = TC_PREF; b; ++q) {          // rare: more than TC_PREF entries in this row tile
+      const int j = __ffsll((long long)b) - 1;
+      b &= b - 1;
+      const float e = __ldg(a.tvals + vbase + q) - mydump[j];
+      const float w = a.sigma_inf ? 1.f : expf(-e * e * inv2s2);
+      mydump[j] = w * e;
+      a.tw[vbase + q] = w;
+      st_e2 += (double)e * (double)e;
+      st_n += 1.0;
+      st_w += s2 * (1.0 - (double)w);
+    }
+    // P = c_hi | c_lo (zero where unobserved) -> TMEM
+#pragma unroll
+    for (int q = 0; q < TC_NT / 16; ++q) {
+      const uint32_t chunk = (uint32_t)((bits >> (16 * q)) & 0xffffull);
+      uint32_t ph[8], pl[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) { ph[u] = 0u; pl[u] = 0u; }
+      if (chunk) {
+        const float4* d4 = reinterpret_cast<const float4*>(mydump + 16 * q);
+        float cv[16];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const float4 v = d4[u];
+          cv[4 * u] = v.x; cv[4 * u + 1] = v.y; cv[4 * u + 2] = v.z; cv[4 * u + 3] = v.w;
+        }
+#pragma unroll
+        for (int u = 0; u < 16; u += 2) {
+          const float c0 = ((chunk >> u) & 1u) ? cv[u] : 0.f;
+          const float c1 = ((chunk >> (u + 1)) & 1u) ? cv[u + 1] : 0.f;
+          const __half h0 = __float2half_rn(c0), h1 = __float2half_rn(c1);
+          ph[u / 2] = pack_half2(h0, h1);
+          pl[u / 2] = pack_half2(__float2half_rn(c0 - __half2float(h0)), __float2half_rn(c1 - __half2float(h1)));
+        }
+      }
+      tmem_st8(lane_base + COL_P + q * 8, ph);
+      tmem_st8(lane_base + COL_P + TC_NT / 2 + q * 8, pl);
+    }
+    tmem_wait_st();
+    cp_async_wait_all();           // B(t+1) has landed
+    fence_proxy_async();
+    tc_fence_before();
+    __syncthreads();
+    if (tid == 0) {
+      tc_fence_after();
+      const uint32_t bH = smem_u32(sBc);
+#pragma unroll
+      for (int term = 0; term < 3; ++term) {
+        const uint32_t pa = COL_P + (term == 2 ? TC_NT / 2 : 0);
+        const uint32_t bb = bH + (term == 1 ? L::B_LO_BYTES : 0u);
+#pragma unroll
+        for (int ks = 0; ks < TC_NT / 16; ++ks) {
+          // B as MN-major (N = kappa, K = columns): LBO = K-group stride, SBO = N-group stride
+          const uint64_t db = make_sdesc(bb + ks * 2 * L::HK * 128, L::HK * 128, 128);
+          mma_ts(tbase + COL_D, tbase + pa + ks * 8, db, L::IDESC_D, d_acc ? 1u : 0u);
+          d_acc = true;
+        }
+      }
+      if (!has_next) mma_commit(&mbar);
+    }
+  }
+  if (t1 > t0) {
+    mbar_wait(&mbar, phase);       // last GEMM2 done
+    tc_fence_after();
+  }
+  // ---- D(row) -> d contribution of this row: d[a + rk b] = sum_c Mid[b][c] D[a + rk c] ----
+  __syncthreads();
+  const bool have_d = t1 > t0;
+  float* drow = dbuf + (size_t)tid * (KP + 1);
+#pragma unroll
+  for (int q = 0; q < KP / 16; ++q) {
+    uint32_t v[16];
+    if (have_d) {
+      tmem_ld16(lane_base + COL_D + q * 16, v);
+      tmem_wait_ld();
+    }
+#pragma unroll
+    for (int u = 0; u < 16; ++u) drow[q * 16 + u] = have_d ? __uint_as_float(v[u]) : 0.f;
+  }
+  if (row_ok) {
+    const int64_t jl = a.rowmode == 0 ? row % a.nL : row / a.Ik;
+    float* out = a.contrib + ((int64_t)split * a.nrows_pad + row) * a.R2;
+    for (int o = 0; o < a.R2; ++o) {
+      const int aa = o % a.rk, bq = o / a.rk;
+      float v;
+      if (a.p == 0) {
+        v = drow[o];
+      } else {
+        const float* mr = a.mid + (jl * a.rk1 + bq) * a.rs;
+        v = 0.f;
+        for (int c = 0; c < a.rs; ++c) v = fmaf(__ldg(mr + c), drow[aa + a.rk * c], v);
+      }
+      out[o] = v;
+    }
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    st_e2 += __shfl_xor_sync(0xffffffffu, st_e2, off);
+    st_w += __shfl_xor_sync(0xffffffffu, st_w, off);
+    st_n += __shfl_xor_sync(0xffffffffu, st_n, off);
+  }
+  if (lane == 0) { red[warp][0] = st_e2; red[warp][1] = st_w; red[warp][2] = st_n; }
+  tc_fence_before();
+  __syncthreads();
+  if (tid < 3) {
+    double s = 0.0;
+    for (int w = 0; w < 4; ++w) s += red[w][tid];
+    a.spart[(rt * a.nsplit + split) * 3 + tid] = s;
+  }
+  if (warp == 0) {
+    tc_fence_after();
+    tmem_dealloc(tbase, TMEM_COLS);
+  }
+}
+
+// ---------------------------------------------------------------------------------------
+// Pass 2: line-search denominator  den = sum_obs w (Lft_h . Rgt)^2  (w staged by pass 1)
+// ---------------------------------------------------------------------------------------
+template <int KP>
+__global__ void __launch_bounds__(128, 1) tc_pass2_kernel(TcArgs a) {
+  using L = TcLayout<KP>;
+  constexpr uint32_t TMEM_COLS = (TC_NT + KP <= 128) ? 128 : 256;
+  constexpr uint32_t COL_T = 0, COL_A = TC_NT;
+  extern __shared__ __align__(1024) unsigned char smem[];
+  __half* sB = reinterpret_cast<__half*>(smem);
+  float* dump = reinterpret_cast<float*>(sB + 2 * L::B_HALVES);
+  __shared__ uint64_t mbar;
+  __shared__ uint32_t tmem_slot;
+  __shared__ double red[4];
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t rt = blockIdx.x;
+  const int split = blockIdx.y;
+  const int64_t row = rt * TC_M + tid;
+  float* mydump = dump + tid * TC_DUMP_STRIDE;
+  const int64_t per = (a.n_col_tiles + a.nsplit - 1) / a.nsplit;
+  const int64_t t0 = (int64_t)split * per;
+  const int64_t t1 = min(a.n_col_tiles, t0 + per);
+
+  if (warp == 0) tmem_alloc(&tmem_slot, TMEM_COLS);
+  if (tid == 0) mbar_init(&mbar, 1);
+  if (t0 < t1) stage_b_async<KP>(a, t0, sB, tid);
+  cp_async_commit();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = tmem_slot;
+  const uint32_t lane_base = tbase + ((uint32_t)(warp * 32) << 16);
+  load_a_to_tmem<KP>(a, row, lane_base, COL_A);
+  tmem_wait_st();
+  cp_async_wait_all();
+  fence_proxy_async();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  double st_den = 0.0;
+  uint32_t phase = 0;
+
+  for (int64_t t = t0; t < t1; ++t) {
+    const int buf = (int)((t - t0) & 1);
+    const __half* sBc = sB + buf * L::B_HALVES;
+    if (tid == 0) {
+      tc_fence_after();
+      issue_split_gemm_ts<KP>(tbase + COL_T, tbase + COL_A, smem_u32(sBc));
+      mma_commit(&mbar);
+    }
+    const int64_t tile = rt * a.n_col_tiles + t;
+    const uint64_t bits = a.tbits[tile * TC_M + tid];
+    const int64_t vbase = (int64_t)a.tbase[tile] + a.troff[tile * TC_M + tid];
+    const int cnt = __popcll(bits);
+    float wr[TC_PREF];
+#pragma unroll
+    for (int q = 0; q < TC_PREF; ++q) wr[q] = q < cnt ? a.tw[vbase + q] : 0.f;
+    mbar_wait(&mbar, phase);
+    phase ^= 1;
+    tc_fence_after();
+    const bool has_next = t + 1 < t1;
+    if (has_next) stage_b_async<KP>(a, t + 1, sB + (buf ^ 1) * L::B_HALVES, tid);
+    cp_async_commit();
+    {
+      uint32_t tv[TC_NT];
+#pragma unroll
+      for (int q = 0; q < TC_NT / 16; ++q) tmem_ld16(lane_base + COL_T + q * 16, tv + q * 16);
+      tmem_wait_ld();
+#pragma unroll
+      for (int q = 0; q < TC_NT / 16; ++q) {
+        if ((bits >> (16 * q)) & 0xffffull) {
+          float4* d4 = reinterpret_cast<float4*>(mydump + 16 * q);
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            d4[u] = make_float4(__uint_as_float(tv[q * 16 + 4 * u]), __uint_as_float(tv[q * 16 + 4 * u + 1]),
+                                __uint_as_float(tv[q * 16 + 4 * u + 2]), __uint_as_float(tv[q * 16 + 4 * u + 3]));
+        }
+      }
+    }
+    uint64_t b = bits;
+#pragma unroll
+    for (int q = 0; q < TC_PREF; ++q) {
+      if (b) {
+        const int j = __ffsll((long long)b) - 1;
+        b &= b - 1;
+        const double tt = (double)mydump[j];
+        st_den += (double)wr[q] * tt * tt;
+      }
+    }
+    for (int q = TC_PREF; b; ++q) {
+      const int j = __ffsll((long long)b) - 1;
+      b &= b - 1;
+      const double tt = (double)mydump[j];
+      st_den += (double)a.tw[vbase + q] * tt * tt;
+    }
+    cp_async_wait_all();
+    fence_proxy_async();
+    tc_fence_before();
+    __syncthreads();   // T TMEM read, B(t+1) landed: the next tile's MMAs may start
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) st_den += __shfl_xor_sync(0xffffffffu, st_den, off);
+  if (lane == 0) red[warp] = st_den;
+  tc_fence_before();
+  __syncthreads();
+  if (tid == 0) a.denpart[rt * a.nsplit + split] = red[0] + red[1] + red[2] + red[3];
+  if (warp == 0) {
+    tc_fence_after();
+    tmem_dealloc(tbase, TMEM_COLS);
+  }
+}
+
+// ---------------------------------------------------------------------------------------
+// d(i_k)[o] = sum_split sum_jl contrib[split][row(i_k, jl)][o]  (fp64, fixed order) and the
+// pass-1 statistics -> dvec = [d | sum_e2 | welsch | n]
+// ---------------------------------------------------------------------------------------
+__global__ void tc_reduce_d_kernel(const float* __restrict__ contrib, const double* __restrict__ spart,
+                                   int64_t nparts, int nsplit, int64_t nrows_pad, int64_t nL, int64_t Ik,
+                                   int rowmode, int R2, double* __restrict__ dvec, DevScalars* sc,
+                                   int kblk) {
+  __shared__ double acc[1024];
+  const int64_t ik = blockIdx.x;
+  if (ik < Ik) {
+    const int G = max(1, (int)blockDim.x / R2);
+    const int o = threadIdx.x % R2, g = threadIdx.x / R2;
+    double s = 0.0;
+    if (g < G) {
+      for (int sp = 0; sp < nsplit; ++sp) {
+        for (int64_t jl = g; jl < nL; jl += G) {
+          const int64_t row = rowmode == 0 ? jl + nL * ik : ik + Ik * jl;
+          s += (double)contrib[((int64_t)sp * nrows_pad + row) * R2 + o];
+        }
+      }
+    }
+    acc[threadIdx.x] = s;
+    __syncthreads();
+    if (threadIdx.x < R2) {
+      double t = 0.0;
+      for (int gg = 0; gg < G; ++gg) t += acc[gg * R2 + threadIdx.x];
+      dvec[ik * R2 + threadIdx.x] = t;
+    }
+    return;
+  }
+  if (threadIdx.x < 3) {
+    double t = 0.0;
+    for (int64_t q = 0; q < nparts; ++q) t += spart[q * 3 + threadIdx.x];
+    dvec[Ik * R2 + threadIdx.x] = t;
+    if (threadIdx.x == 2 && sc && sc->prof_on) sc->prof_nobs[kblk] += t;
+  }
+}
+
+// ---------------------------------------------------------------------------------------
+// launchers
+// ---------------------------------------------------------------------------------------
+static int tc_grid(int64_t n) {
+  int64_t g = (n + 255) / 256;
+  return (int)std::max<int64_t>(1, std::min<int64_t>(g, 148 * 16));
+}
+
+void launch_tc_pack_rows(Context& c, const BlockPlan& bp, const float* src, __half* dst, cudaStream_t s) {
+  const int64_t pad = bp.n_row_tiles * TC_M;
+  tc_pack_rows_kernel<<<tc_grid(pad * bp.KP), 256, 0, s>>>(src, bp.nrows, bp.K, bp.KP, pad, dst);
+  c.launches++;
+}
+
+void launch_tc_pack_cols(Context& c, const BlockPlan& bp, cudaStream_t s) {
+  tc_pack_cols_kernel<<<tc_grid(bp.n_col_tiles * TC_NT * bp.KP), 256, 0, s>>>(c.rgtT, bp.ncols, bp.K, bp.KP,
+                                                                                bp.n_col_tiles, c.rgtHL);
+  c.launches++;
+}
+
+// Stage sketch for block bp into the staging buffers st (bits, offsets, prefix, values)
+void launch_tc_stage(Context& c, const BlockPlan& bp, TcStage& st, cudaStream_t s) {
+  StageArgs a;
+  a.nrows = bp.nrows; a.ncols = bp.ncols; a.n_col_tiles = bp.n_col_tiles;
+  a.n_tiles = bp.n_row_tiles * bp.n_col_tiles;
+  a.packed = c.packed;
+  a.row_off = c.row_off; a.col_off = c.col_off;
+  a.mask = c.mask; a.rank_prefix = c.rank_prefix; a.values = c.values;
+  a.tbits = st.tbits; a.troff = st.troff; a.tcount = st.tbase; a.tvals = st.tvals;
+  const int grid = (int)std::min<int64_t>(a.n_tiles, 148 * 16);
+  stage_bits_kernel<<<grid, TC_M, 0, s>>>(a);
+  cub::DeviceScan::ExclusiveSum(st.scan_tmp, st.scan_tmp_bytes, st.tbase, st.tbase, (int)a.n_tiles, s);
+  stage_vals_kernel<<<grid, TC_M, 0, s>>>(a);
+  c.launches += 3;
+}
+
+size_t tc_scan_tmp_bytes(int64_t n_tiles) {
+  size_t bytes = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, bytes, (uint64_t*)nullptr, (uint64_t*)nullptr, (int)n_tiles);
+  return bytes;
+}
+
+static TcArgs make_tc_args(const Context& c, const BlockPlan& bp, const TcStage& st, bool pass2) {
+  TcArgs a;
+  a.nrows = bp.nrows; a.ncols = bp.ncols; a.nL = bp.nL; a.Ik = bp.nrows / bp.nL;
+  a.n_col_tiles = bp.n_col_tiles; a.nrows_pad = bp.n_row_tiles * TC_M;
+  a.rowmode = bp.rowmode; a.K = bp.K; a.R2 = bp.R2; a.rk = bp.rk; a.rk1 = bp.rk1; a.rs = bp.rs;
+  a.p = bp.p; a.nsplit = bp.tc_nsplit;
+  a.sigma_inf = c.cfg.sigma_mode == TRD_SIGMA_INF;
+  a.arow = pass2 ? c.lfthHL : c.lftHL;
+  a.rgtHL = c.rgtHL;
+  a.mid = c.mid;
+  a.tbits = st.tbits; a.troff = st.troff; a.tbase = st.tbase; a.tvals = st.tvals;
+  a.tw = c.tw;
+  a.sc = c.sc;
+  a.contrib = c.contrib; a.spart = c.spart; a.denpart = c.denpart;
+  return a;
+}
+
+template <int KP>
+static size_t tc_smem1() {
+  using L = TcLayout<KP>;
+  size_t ab = (size_t)(2 * L::B_HALVES) * 2 + (size_t)TC_M * TC_DUMP_STRIDE * 4;
+  size_t dbuf = (size_t)TC_M * (KP + 1) * 4;
+  return std::max(ab, dbuf);
+}
+template <int KP>
+static size_t tc_smem2() {
+  using L = TcLayout<KP>;
+  return (size_t)(2 * L::B_HALVES) * 2 + (size_t)TC_M * TC_DUMP_STRIDE * 4;
+}
+
+template <int KP>
+static void launch_tc_pass_t(Context& c, const BlockPlan& bp, const TcStage& st, bool pass2, cudaStream_t s) {
+  TcArgs a = make_tc_args(c, bp, st, pass2);
+  dim3 grid((unsigned)bp.n_row_tiles, (unsigned)bp.tc_nsplit);
+  if (!pass2) {
+    const size_t sm = tc_smem1<KP>();
+    cudaFuncSetAttribute(tc_pass1_kernel<KP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    tc_pass1_kernel<KP><<<grid, TC_M, sm, s>>>(a);
+  } else {
+    const size_t sm = tc_smem2<KP>();
+    cudaFuncSetAttribute(tc_pass2_kernel<KP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    tc_pass2_kernel<KP><<<grid, TC_M, sm, s>>>(a);
+  }
+  c.launches++;
+}
+
+bool tc_supported_kp(int KP) { return KP >= 16 && KP <= 128 && KP % 16 == 0; }
+
+void launch_tc_pass(Context& c, const BlockPlan& bp, const TcStage& st, bool pass2, cudaStream_t s) {
+  switch (bp.KP) {
+    case 16: launch_tc_pass_t<16>(c, bp, st, pass2, s); break;
+    case 32: launch_tc_pass_t<32>(c, bp, st, pass2, s); break;
+    case 48: launch_tc_pass_t<48>(c, bp, st, pass2, s); break;
+    case 64: launch_tc_pass_t<64>(c, bp, st, pass2, s); break;
+    case 80: launch_tc_pass_t<80>(c, bp, st, pass2, s); break;
+    case 96: launch_tc_pass_t<96>(c, bp, st, pass2, s); break;
+    case 112: launch_tc_pass_t<112>(c, bp, st, pass2, s); break;
+    case 128: launch_tc_pass_t<128>(c, bp, st, pass2, s); break;
+    default: break;
+  }
+}
+
+void launch_tc_reduce_d(Context& c, const BlockPlan& bp, cudaStream_t s) {
+  const int64_t Ik = bp.nrows / bp.nL;
+  const int64_t nparts = bp.n_row_tiles * bp.tc_nsplit;
+  int threads = bp.R2 * std::max(1, 1024 / std::max(1, bp.R2));
+  threads = std::min(threads, 1024);
+  tc_reduce_d_kernel<<<(unsigned)(Ik + 1), threads, 0, s>>>(c.contrib, c.spart, nparts, bp.tc_nsplit,
+                                                            bp.n_row_tiles * TC_M, bp.nL, Ik, bp.rowmode,
+                                                            bp.R2, c.dvec, c.sc, bp.k);
+  c.launches++;
+}
+
+}  // namespace trd
