@@ -545,6 +545,10 @@ trd_status trd_init(const trd_config* cfg, const trd_shard* shard, const float* 
       max_v = std::max(max_v, sg.vcap);
     }
     if (max_v > 0 && (st = dalloc(c, &c->tw, (size_t)max_v))) return bail(st);
+    if (getenv("TRD_TC_TIMING")) {
+      if ((st = dalloc(c, &c->tc_dbg, 16))) return bail(st);
+      cudaMemset(c->tc_dbg, 0, 16 * 8);
+    }
   }
   if (shard->host) {
     if ((st = dalloc(c, &c->own_values, (size_t)c->n_values))) return bail(st);
@@ -798,6 +802,16 @@ void trd_destroy(trd_ctx* ctx) {
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->tw) cudaFree(c->tw);
+  if (c->tc_dbg) {
+    unsigned long long v[16];
+    cudaMemcpy(v, c->tc_dbg, sizeof(v), cudaMemcpyDeviceToHost);
+    const char* names[15] = {"prod_total", "prod_wait_bempty", "mma_total", "mma_idle", "epi_total",
+                             "epi_wait_bfull", "epi_wait_sfull", "epi_wait_pfree", "epi_compute",
+                             "epi_ldS", "epi_ldS+dump", "epi_setbits", "epi_Pstore", "mma_gemm1", "mma_gemm2"};
+    fprintf(stderr, "[trd tc timing] (cycles summed over CTAs / epilogue leaders)\n");
+    for (int i = 0; i < 15; ++i) fprintf(stderr, "  %-18s %.4e\n", names[i], (double)v[i]);
+    cudaFree(c->tc_dbg);
+  }
   for (int k = 0; k < kMaxN; ++k) {
     TcStage& sg = c->stage[k];
     void* sp[] = {sg.tbits, sg.troff, sg.tbase, sg.tvals, sg.scan_tmp};

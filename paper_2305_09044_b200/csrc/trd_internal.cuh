@@ -132,6 +132,7 @@ struct Context {
   __half* rgtHL = nullptr;             // [col tile][hi | lo][64 x KP] core-matrix layout
   float* contrib = nullptr;            // [split][row][R2]
   float* tw = nullptr;                 // staged HQ weights of the current block (pass 1 -> 2)
+  unsigned long long* tc_dbg = nullptr;  // TRD_TC_TIMING=1: per-role cycle counters
   TcStage stage[kMaxN];
   double* dpart = nullptr;             // pass-1 CTA partials of d
   double* spart = nullptr;             // pass-1 CTA partial stats (3 per CTA)

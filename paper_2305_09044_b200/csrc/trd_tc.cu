@@ -273,6 +273,7 @@ struct TcArgs {
   float* contrib;          // [split][nrows_pad][R2]
   double* spart;           // [row_tile][split][3]
   double* denpart;         // [row_tile][split]
+  unsigned long long* dbg; // optional per-role cycle counters (TRD_TC_TIMING)
 };
 
 template <int KP>
@@ -326,339 +327,7 @@ __device__ __forceinline__ void load_a_to_tmem(const TcArgs& a, int64_t row, uin
   }
 }
 
-// ---------------------------------------------------------------------------------------
-// Pass 1: gradient partials, residual statistics, staged weights
-// ---------------------------------------------------------------------------------------
-template <int KP>
-__global__ void __launch_bounds__(128, 1) tc_pass1_kernel(TcArgs a) {
-  using L = TcLayout<KP>;
-  constexpr uint32_t TMEM_COLS = (2 * TC_NT + 2 * KP <= 256) ? 256 : 512;
-  constexpr uint32_t COL_S = 0, COL_P = TC_NT, COL_D = 2 * TC_NT, COL_A = 2 * TC_NT + KP;
-  extern __shared__ __align__(1024) unsigned char smem[];
-  __half* sB = reinterpret_cast<__half*>(smem);                          // [2][B_HALVES]
-  float* dump = reinterpret_cast<float*>(sB + 2 * L::B_HALVES);          // [128][DUMP_STRIDE]
-  float* dbuf = reinterpret_cast<float*>(smem);                          // aliases sB at the end
-  __shared__ uint64_t mbar;
-  __shared__ uint32_t tmem_slot;
-  __shared__ double red[4][3];
-
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int64_t rt = blockIdx.x;
-  const int split = blockIdx.y;
-  const int64_t row = rt * TC_M + tid;
-  const bool row_ok = row < a.nrows;
-  float* mydump = dump + tid * TC_DUMP_STRIDE;
-
-  const int64_t per = (a.n_col_tiles + a.nsplit - 1) / a.nsplit;
-  const int64_t t0 = (int64_t)split * per;
-  const int64_t t1 = min(a.n_col_tiles, t0 + per);
-
-  if (warp == 0) tmem_alloc(&tmem_slot, TMEM_COLS);
-  if (tid == 0) mbar_init(&mbar, 1);
-  if (t0 < t1) stage_b_async<KP>(a, t0, sB, tid);
-  cp_async_commit();
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tbase = tmem_slot;
-  const uint32_t lane_base = tbase + ((uint32_t)(warp * 32) << 16);
-  load_a_to_tmem<KP>(a, row, lane_base, COL_A);
-  tmem_wait_st();
-  cp_async_wait_all();
-  fence_proxy_async();
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-
-  const double sigma = a.sc->sigma;
-  const float inv2s2 = a.sigma_inf ? 0.f : (float)(0.5 / (sigma * sigma));
-  const double s2 = sigma * sigma;
-  double st_e2 = 0.0, st_w = 0.0, st_n = 0.0;
-  uint32_t phase = 0;
-  bool d_acc = false;
-
-  for (int64_t t = t0; t < t1; ++t) {
-    const int buf = (int)((t - t0) & 1);
-    const __half* sBc = sB + buf * L::B_HALVES;
-    if (tid == 0) {
-      tc_fence_after();
-      issue_split_gemm_ts<KP>(tbase + COL_S, tbase + COL_A, smem_u32(sBc));
-      mma_commit(&mbar);
-    }
-    // staged tile data of this row (independent of S: overlaps the MMA)
-    const int64_t tile = rt * a.n_col_tiles + t;
-    const uint64_t bits = a.tbits[tile * TC_M + tid];
-    const int64_t vbase = (int64_t)a.tbase[tile] + a.troff[tile * TC_M + tid];
-    const int cnt = __popcll(bits);
-    float xr[TC_PREF];
-#pragma unroll
-    for (int q = 0; q < TC_PREF; ++q) xr[q] = q < cnt ? __ldg(a.tvals + vbase + q) : 0.f;
-    mbar_wait(&mbar, phase);       // S(t) ready; GEMM2(t-1) finished (in-order execution)
-    phase ^= 1;
-    tc_fence_after();
-    const bool has_next = t + 1 < t1;
-    if (has_next) stage_b_async<KP>(a, t + 1, sB + (buf ^ 1) * L::B_HALVES, tid);
-    cp_async_commit();
-    // S row -> dump (only 16-column chunks holding observed entries)
-    {
-      uint32_t sv[TC_NT];
-#pragma unroll
-      for (int q = 0; q < TC_NT / 16; ++q) tmem_ld16(lane_base + COL_S + q * 16, sv + q * 16);
-      tmem_wait_ld();
-#pragma unroll
-      for (int q = 0; q < TC_NT / 16; ++q) {
-        if ((bits >> (16 * q)) & 0xffffull) {
-          float4* d4 = reinterpret_cast<float4*>(mydump + 16 * q);
-#pragma unroll
-          for (int u = 0; u < 4; ++u)
-            d4[u] = make_float4(__uint_as_float(sv[q * 16 + 4 * u]), __uint_as_float(sv[q * 16 + 4 * u + 1]),
-                                __uint_as_float(sv[q * 16 + 4 * u + 2]), __uint_as_float(sv[q * 16 + 4 * u + 3]));
-        }
-      }
-    }
-    // observed entries: e = x - s, w, c = w e (in place of s), staged w
-    uint64_t b = bits;
-#pragma unroll
-    for (int q = 0; q < TC_PREF; ++q) {
-      if (b) {
-        const int j = __ffsll((long long)b) - 1;
-        b &= b - 1;
-        const float e = xr[q] - mydump[j];
-        const float w = a.sigma_inf ? 1.f : expf(-e * e * inv2s2);
-        mydump[j] = w * e;
-        a.tw[vbase + q] = w;
-        st_e2 += (double)e * (double)e;
-        st_n += 1.0;
-        st_w += s2 * (1.0 - (double)w);
-      }
-    }
-    for (int q = TC_PREF; b; ++q) {          // rare: more than TC_PREF entries in this row tile
-      const int j = __ffsll((long long)b) - 1;
-      b &= b - 1;
-      const float e = __ldg(a.tvals + vbase + q) - mydump[j];
-      const float w = a.sigma_inf ? 1.f : expf(-e * e * inv2s2);
-      mydump[j] = w * e;
-      a.tw[vbase + q] = w;
-      st_e2 += (double)e * (double)e;
-      st_n += 1.0;
-      st_w += s2 * (1.0 - (double)w);
-    }
-    // P = c_hi | c_lo (zero where unobserved) -> TMEM
-#pragma unroll
-    for (int q = 0; q < TC_NT / 16; ++q) {
-      const uint32_t chunk = (uint32_t)((bits >> (16 * q)) & 0xffffull);
-      uint32_t ph[8], pl[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) { ph[u] = 0u; pl[u] = 0u; }
-      if (chunk) {
-        const float4* d4 = reinterpret_cast<const float4*>(mydump + 16 * q);
-        float cv[16];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const float4 v = d4[u];
-          cv[4 * u] = v.x; cv[4 * u + 1] = v.y; cv[4 * u + 2] = v.z; cv[4 * u + 3] = v.w;
-        }
-#pragma unroll
-        for (int u = 0; u < 16; u += 2) {
-          const float c0 = ((chunk >> u) & 1u) ? cv[u] : 0.f;
-          const float c1 = ((chunk >> (u + 1)) & 1u) ? cv[u + 1] : 0.f;
-          const __half h0 = __float2half_rn(c0), h1 = __float2half_rn(c1);
-          ph[u / 2] = pack_half2(h0, h1);
-          pl[u / 2] = pack_half2(__float2half_rn(c0 - __half2float(h0)), __float2half_rn(c1 - __half2float(h1)));
-        }
-      }
-      tmem_st8(lane_base + COL_P + q * 8, ph);
-      tmem_st8(lane_base + COL_P + TC_NT / 2 + q * 8, pl);
-    }
-    tmem_wait_st();
-    cp_async_wait_all();           // B(t+1) has landed
-    fence_proxy_async();
-    tc_fence_before();
-    __syncthreads();
-    if (tid == 0) {
-      tc_fence_after();
-      const uint32_t bH = smem_u32(sBc);
-#pragma unroll
-      for (int term = 0; term < 3; ++term) {
-        const uint32_t pa = COL_P + (term == 2 ? TC_NT / 2 : 0);
-        const uint32_t bb = bH + (term == 1 ? L::B_LO_BYTES : 0u);
-#pragma unroll
-        for (int ks = 0; ks < TC_NT / 16; ++ks) {
-          // B as MN-major (N = kappa, K = columns): LBO = K-group stride, SBO = N-group stride
-          const uint64_t db = make_sdesc(bb + ks * 2 * L::HK * 128, L::HK * 128, 128);
-          mma_ts(tbase + COL_D, tbase + pa + ks * 8, db, L::IDESC_D, d_acc ? 1u : 0u);
-          d_acc = true;
-        }
-      }
-      if (!has_next) mma_commit(&mbar);
-    }
-  }
-  if (t1 > t0) {
-    mbar_wait(&mbar, phase);       // last GEMM2 done
-    tc_fence_after();
-  }
-  // ---- D(row) -> d contribution of this row: d[a + rk b] = sum_c Mid[b][c] D[a + rk c] ----
-  __syncthreads();
-  const bool have_d = t1 > t0;
-  float* drow = dbuf + (size_t)tid * (KP + 1);
-#pragma unroll
-  for (int q = 0; q < KP / 16; ++q) {
-    uint32_t v[16];
-    if (have_d) {
-      tmem_ld16(lane_base + COL_D + q * 16, v);
-      tmem_wait_ld();
-    }
-#pragma unroll
-    for (int u = 0; u < 16; ++u) drow[q * 16 + u] = have_d ? __uint_as_float(v[u]) : 0.f;
-  }
-  if (row_ok) {
-    const int64_t jl = a.rowmode == 0 ? row % a.nL : row / a.Ik;
-    float* out = a.contrib + ((int64_t)split * a.nrows_pad + row) * a.R2;
-    for (int o = 0; o < a.R2; ++o) {
-      const int aa = o % a.rk, bq = o / a.rk;
-      float v;
-      if (a.p == 0) {
-        v = drow[o];
-      } else {
-        const float* mr = a.mid + (jl * a.rk1 + bq) * a.rs;
-        v = 0.f;
-        for (int c = 0; c < a.rs; ++c) v = fmaf(__ldg(mr + c), drow[aa + a.rk * c], v);
-      }
-      out[o] = v;
-    }
-  }
-#pragma unroll
-  for (int off = 16; off > 0; off >>= 1) {
-    st_e2 += __shfl_xor_sync(0xffffffffu, st_e2, off);
-    st_w += __shfl_xor_sync(0xffffffffu, st_w, off);
-    st_n += __shfl_xor_sync(0xffffffffu, st_n, off);
-  }
-  if (lane == 0) { red[warp][0] = st_e2; red[warp][1] = st_w; red[warp][2] = st_n; }
-  tc_fence_before();
-  __syncthreads();
-  if (tid < 3) {
-    double s = 0.0;
-    for (int w = 0; w < 4; ++w) s += red[w][tid];
-    a.spart[(rt * a.nsplit + split) * 3 + tid] = s;
-  }
-  if (warp == 0) {
-    tc_fence_after();
-    tmem_dealloc(tbase, TMEM_COLS);
-  }
-}
-
-// ---------------------------------------------------------------------------------------
-// Pass 2: line-search denominator  den = sum_obs w (Lft_h . Rgt)^2  (w staged by pass 1)
-// ---------------------------------------------------------------------------------------
-template <int KP>
-__global__ void __launch_bounds__(128, 1) tc_pass2_kernel(TcArgs a) {
-  using L = TcLayout<KP>;
-  constexpr uint32_t TMEM_COLS = (TC_NT + KP <= 128) ? 128 : 256;
-  constexpr uint32_t COL_T = 0, COL_A = TC_NT;
-  extern __shared__ __align__(1024) unsigned char smem[];
-  __half* sB = reinterpret_cast<__half*>(smem);
-  float* dump = reinterpret_cast<float*>(sB + 2 * L::B_HALVES);
-  __shared__ uint64_t mbar;
-  __shared__ uint32_t tmem_slot;
-  __shared__ double red[4];
-
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int64_t rt = blockIdx.x;
-  const int split = blockIdx.y;
-  const int64_t row = rt * TC_M + tid;
-  float* mydump = dump + tid * TC_DUMP_STRIDE;
-  const int64_t per = (a.n_col_tiles + a.nsplit - 1) / a.nsplit;
-  const int64_t t0 = (int64_t)split * per;
-  const int64_t t1 = min(a.n_col_tiles, t0 + per);
-
-  if (warp == 0) tmem_alloc(&tmem_slot, TMEM_COLS);
-  if (tid == 0) mbar_init(&mbar, 1);
-  if (t0 < t1) stage_b_async<KP>(a, t0, sB, tid);
-  cp_async_commit();
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tbase = tmem_slot;
-  const uint32_t lane_base = tbase + ((uint32_t)(warp * 32) << 16);
-  load_a_to_tmem<KP>(a, row, lane_base, COL_A);
-  tmem_wait_st();
-  cp_async_wait_all();
-  fence_proxy_async();
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  double st_den = 0.0;
-  uint32_t phase = 0;
-
-  for (int64_t t = t0; t < t1; ++t) {
-    const int buf = (int)((t - t0) & 1);
-    const __half* sBc = sB + buf * L::B_HALVES;
-    if (tid == 0) {
-      tc_fence_after();
-      issue_split_gemm_ts<KP>(tbase + COL_T, tbase + COL_A, smem_u32(sBc));
-      mma_commit(&mbar);
-    }
-    const int64_t tile = rt * a.n_col_tiles + t;
-    const uint64_t bits = a.tbits[tile * TC_M + tid];
-    const int64_t vbase = (int64_t)a.tbase[tile] + a.troff[tile * TC_M + tid];
-    const int cnt = __popcll(bits);
-    float wr[TC_PREF];
-#pragma unroll
-    for (int q = 0; q < TC_PREF; ++q) wr[q] = q < cnt ? a.tw[vbase + q] : 0.f;
-    mbar_wait(&mbar, phase);
-    phase ^= 1;
-    tc_fence_after();
-    const bool has_next = t + 1 < t1;
-    if (has_next) stage_b_async<KP>(a, t + 1, sB + (buf ^ 1) * L::B_HALVES, tid);
-    cp_async_commit();
-    {
-      uint32_t tv[TC_NT];
-#pragma unroll
-      for (int q = 0; q < TC_NT / 16; ++q) tmem_ld16(lane_base + COL_T + q * 16, tv + q * 16);
-      tmem_wait_ld();
-#pragma unroll
-      for (int q = 0; q < TC_NT / 16; ++q) {
-        if ((bits >> (16 * q)) & 0xffffull) {
-          float4* d4 = reinterpret_cast<float4*>(mydump + 16 * q);
-#pragma unroll
-          for (int u = 0; u < 4; ++u)
-            d4[u] = make_float4(__uint_as_float(tv[q * 16 + 4 * u]), __uint_as_float(tv[q * 16 + 4 * u + 1]),
-                                __uint_as_float(tv[q * 16 + 4 * u + 2]), __uint_as_float(tv[q * 16 + 4 * u + 3]));
-        }
-      }
-    }
-    uint64_t b = bits;
-#pragma unroll
-    for (int q = 0; q < TC_PREF; ++q) {
-      if (b) {
-        const int j = __ffsll((long long)b) - 1;
-        b &= b - 1;
-        const double tt = (double)mydump[j];
-        st_den += (double)wr[q] * tt * tt;
-      }
-    }
-    for (int q = TC_PREF; b; ++q) {
-      const int j = __ffsll((long long)b) - 1;
-      b &= b - 1;
-      const double tt = (double)mydump[j];
-      st_den += (double)a.tw[vbase + q] * tt * tt;
-    }
-    cp_async_wait_all();
-    fence_proxy_async();
-    tc_fence_before();
-    __syncthreads();   // T TMEM read, B(t+1) landed: the next tile's MMAs may start
-  }
-#pragma unroll
-  for (int off = 16; off > 0; off >>= 1) st_den += __shfl_xor_sync(0xffffffffu, st_den, off);
-  if (lane == 0) red[warp] = st_den;
-  tc_fence_before();
-  __syncthreads();
-  if (tid == 0) a.denpart[rt * a.nsplit + split] = red[0] + red[1] + red[2] + red[3];
-  if (warp == 0) {
-    tc_fence_after();
-    tmem_dealloc(tbase, TMEM_COLS);
-  }
-}
+#include "tc_ws.inc"
 
 // ---------------------------------------------------------------------------------------
 // d(i_k)[o] = sum_split sum_jl contrib[split][row(i_k, jl)][o]  (fp64, fixed order) and the
@@ -730,14 +399,15 @@ void launch_tc_stage(Context& c, const BlockPlan& bp, TcStage& st, cudaStream_t 
   a.tbits = st.tbits; a.troff = st.troff; a.tcount = st.tbase; a.tvals = st.tvals;
   const int grid = (int)std::min<int64_t>(a.n_tiles, 148 * 16);
   stage_bits_kernel<<<grid, TC_M, 0, s>>>(a);
-  cub::DeviceScan::ExclusiveSum(st.scan_tmp, st.scan_tmp_bytes, st.tbase, st.tbase, (int)a.n_tiles, s);
+  cudaMemsetAsync(st.tbase + a.n_tiles, 0, sizeof(uint64_t), s);   // tbase[n_tiles] = total
+  cub::DeviceScan::ExclusiveSum(st.scan_tmp, st.scan_tmp_bytes, st.tbase, st.tbase, (int)a.n_tiles + 1, s);
   stage_vals_kernel<<<grid, TC_M, 0, s>>>(a);
   c.launches += 3;
 }
 
 size_t tc_scan_tmp_bytes(int64_t n_tiles) {
   size_t bytes = 0;
-  cub::DeviceScan::ExclusiveSum(nullptr, bytes, (uint64_t*)nullptr, (uint64_t*)nullptr, (int)n_tiles);
+  cub::DeviceScan::ExclusiveSum(nullptr, bytes, (uint64_t*)nullptr, (uint64_t*)nullptr, (int)n_tiles + 1);
   return bytes;
 }
 
@@ -755,20 +425,22 @@ static TcArgs make_tc_args(const Context& c, const BlockPlan& bp, const TcStage&
   a.tw = c.tw;
   a.sc = c.sc;
   a.contrib = c.contrib; a.spart = c.spart; a.denpart = c.denpart;
+  a.dbg = pass2 ? nullptr : c.tc_dbg;
   return a;
 }
 
 template <int KP>
 static size_t tc_smem1() {
   using L = TcLayout<KP>;
-  size_t ab = (size_t)(2 * L::B_HALVES) * 2 + (size_t)TC_M * TC_DUMP_STRIDE * 4;
-  size_t dbuf = (size_t)TC_M * (KP + 1) * 4;
-  return std::max(ab, dbuf);
+  (void)sizeof(L);
+  return (size_t)ws_nb<KP>() * ws_stage_bytes<KP>() + 2 * (size_t)TC_M * TC_DUMP_STRIDE * 4 +
+         2 * (size_t)TC_M * WS_PBUF_STRIDE * 4;
 }
 template <int KP>
 static size_t tc_smem2() {
   using L = TcLayout<KP>;
-  return (size_t)(2 * L::B_HALVES) * 2 + (size_t)TC_M * TC_DUMP_STRIDE * 4;
+  (void)sizeof(L);
+  return (size_t)ws_nb<KP>() * ws_stage_bytes<KP>() + 2 * (size_t)TC_M * TC_DUMP_STRIDE * 4;
 }
 
 template <int KP>
@@ -778,11 +450,11 @@ static void launch_tc_pass_t(Context& c, const BlockPlan& bp, const TcStage& st,
   if (!pass2) {
     const size_t sm = tc_smem1<KP>();
     cudaFuncSetAttribute(tc_pass1_kernel<KP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    tc_pass1_kernel<KP><<<grid, TC_M, sm, s>>>(a);
+    tc_pass1_kernel<KP><<<grid, WS_THREADS, sm, s>>>(a);
   } else {
     const size_t sm = tc_smem2<KP>();
     cudaFuncSetAttribute(tc_pass2_kernel<KP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    tc_pass2_kernel<KP><<<grid, TC_M, sm, s>>>(a);
+    tc_pass2_kernel<KP><<<grid, WS_THREADS, sm, s>>>(a);
   }
   c.launches++;
 }
