@@ -274,6 +274,7 @@ struct TcArgs {
   double* spart;           // [row_tile][split][3]
   double* denpart;         // [row_tile][split]
   unsigned long long* dbg; // optional per-role cycle counters (TRD_TC_TIMING)
+  int dbg_noepi;           // TRD_TC_NOEPI=1 (timing experiments only): epilogue skips its work
 };
 
 template <int KP>
@@ -426,21 +427,19 @@ static TcArgs make_tc_args(const Context& c, const BlockPlan& bp, const TcStage&
   a.sc = c.sc;
   a.contrib = c.contrib; a.spart = c.spart; a.denpart = c.denpart;
   a.dbg = pass2 ? nullptr : c.tc_dbg;
+  a.dbg_noepi = (a.dbg && getenv("TRD_TC_NOEPI")) ? 1 : 0;
   return a;
 }
 
 template <int KP>
 static size_t tc_smem1() {
-  using L = TcLayout<KP>;
-  (void)sizeof(L);
-  return (size_t)ws_nb<KP>() * ws_stage_bytes<KP>() + 2 * (size_t)TC_M * TC_DUMP_STRIDE * 4 +
-         2 * (size_t)TC_M * WS_PBUF_STRIDE * 4;
+  return (size_t)ws_nb<KP>() * ws_b_bytes<KP>() + (size_t)ws_ns<KP>() * WS_SK_BYTES +
+         2 * (size_t)TC_M * TC_DUMP_STRIDE * 4;
 }
 template <int KP>
 static size_t tc_smem2() {
-  using L = TcLayout<KP>;
-  (void)sizeof(L);
-  return (size_t)ws_nb<KP>() * ws_stage_bytes<KP>() + 2 * (size_t)TC_M * TC_DUMP_STRIDE * 4;
+  return (size_t)ws_nb<KP>() * ws_b_bytes<KP>() + (size_t)ws_ns<KP>() * WS_SK_BYTES +
+         2 * (size_t)TC_M * TC_DUMP_STRIDE * 4;
 }
 
 template <int KP>

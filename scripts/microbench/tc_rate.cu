@@ -84,8 +84,11 @@ __global__ void __launch_bounds__(128, 1) bench(long long* out, int iters) {
 
 // libtrd pass-1 tile sequence: GEMM1 (3 x 4 MMAs, N = 64, B K-major) into S, commit; GEMM2
 // (3 x 4 MMAs, N = KP = 64, B MN-major, A = P from TMEM) into D, commit x2 -- per tile
+__device__ volatile int g_stop;
+__device__ float g_src[64 * 4096 + 4096];
+
 template <int NT>
-__global__ void __launch_bounds__(128, 1) bench_seq(long long* out, int tiles) {
+__global__ void __launch_bounds__(384, 1) bench_seq(long long* out, int tiles, int mode) {
   extern __shared__ __align__(1024) unsigned char smem[];
   __shared__ uint64_t bar;
   __shared__ uint32_t slot;
@@ -129,6 +132,58 @@ __global__ void __launch_bounds__(128, 1) bench_seq(long long* out, int tiles) {
     }
     long long t1 = clock64();
     if (blockIdx.x == 0) { out[0] = t1 - t0; out[1] = t1 - t0; }
+    g_stop = 1;
+  } else if (tid >= 128 && mode != 0) {
+    // interfering warps (4..11): TMEM loads of columns 320..383 and/or smem traffic
+    const int w = (tid >> 5) & 3;
+    float acc = 0.f;
+    float4* sm4 = reinterpret_cast<float4*>(smem + 65536) + (tid - 128) * 4;
+    while (!g_stop) {
+      if (mode & 1) {
+        uint32_t v[16];
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+                     : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+                       "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+                     : "r"(tb + ((uint32_t)(w * 32) << 16) + 320));
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        acc += __uint_as_float(v[0]) + __uint_as_float(v[15]);
+      }
+      if (mode & 2) {
+        float4 x = sm4[0];
+        sm4[1] = make_float4(x.x + 1.f, x.y, x.z, x.w);
+        float4 y = sm4[2];
+        sm4[3] = y;
+        acc += x.x + y.y;
+      }
+      if (mode & 4) {
+        uint32_t v[16];
+        for (int u = 0; u < 16; ++u) v[u] = __float_as_uint(acc + u);
+        asm volatile("tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};"
+                     ::"r"(tb + ((uint32_t)(w * 32) << 16) + 384), "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]),
+                       "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]),
+                       "r"(v[13]), "r"(v[14]), "r"(v[15]));
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      }
+    }
+    if (acc == 12345.f) out[2] = 1;
+  } else if (tid == 96 && mode >= 8) {
+    // TMA bulk copies (16 KB) global -> smem, back to back
+    __shared__ uint64_t tbar;
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&tbar)), "r"(1));
+    asm volatile("fence.mbarrier_init.release.cluster;");
+    uint32_t ph = 0;
+    while (!g_stop) {
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&tbar)), "r"(16384) : "memory");
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                   ::"r"(smem_u32(smem + 65536 + 32768)), "l"(g_src + (blockIdx.x & 63) * 4096), "r"(16384),
+                     "r"(smem_u32(&tbar)) : "memory");
+      uint32_t ok = 0;
+      do {
+        asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+                     : "=r"(ok) : "r"(smem_u32(&tbar)), "r"(ph) : "memory");
+      } while (!ok);
+      ph ^= 1;
+    }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
@@ -138,14 +193,19 @@ __global__ void __launch_bounds__(128, 1) bench_seq(long long* out, int tiles) {
 template <int NT>
 void run_seq(int tiles) {
   long long* d;
-  cudaMalloc(&d, 16);
-  cudaFuncSetAttribute(bench_seq<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
-  bench_seq<NT><<<148, 128, 96 * 1024>>>(d, tiles);
-  cudaError_t err = cudaDeviceSynchronize();
-  long long h[2];
-  cudaMemcpy(h, d, 16, cudaMemcpyDeviceToHost);
-  printf("pass-1 tile sequence NT=%d: %.1f cycles per tile (24 MMAs + 3 commits) (%s)\n", NT,
-         (double)h[0] / tiles, cudaGetErrorString(err));
+  cudaMalloc(&d, 32);
+  cudaFuncSetAttribute(bench_seq<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 128 * 1024);
+  const char* names[9] = {"none", "TMEM ld", "smem", "TMEM ld + smem", "TMEM st", "", "", "all SIMT", "TMA bulk"};
+  for (int mode : {0, 1, 2, 3, 4, 7, 8}) {
+    int zero = 0;
+    cudaMemcpyToSymbol(g_stop, &zero, sizeof(int));
+    bench_seq<NT><<<148, 384, 128 * 1024>>>(d, tiles, mode);
+    cudaError_t err = cudaDeviceSynchronize();
+    long long h[2];
+    cudaMemcpy(h, d, 16, cudaMemcpyDeviceToHost);
+    printf("pass-1 tile sequence NT=%d, interference %-15s: %.1f cycles per tile (%s)\n", NT, names[mode],
+           (double)h[0] / tiles, cudaGetErrorString(err));
+  }
   cudaFree(d);
 }
 
