@@ -805,9 +805,9 @@ void trd_destroy(trd_ctx* ctx) {
   if (c->tc_dbg) {
     unsigned long long v[16];
     cudaMemcpy(v, c->tc_dbg, sizeof(v), cudaMemcpyDeviceToHost);
-    const char* names[15] = {"prod_total", "prod_wait_bempty", "mma_total", "mma_idle", "epi_total",
-                             "epi_wait_bfull", "epi_wait_sfull", "epi_wait_pfree", "epi_compute",
-                             "epi_ldS", "epi_ldS+dump", "epi_setbits", "epi_Pstore", "mma_gemm1", "mma_gemm2"};
+    const char* names[15] = {"cta_setup", "cta_tail", "mma_total", "mma_wait", "epi_total",
+                             "epi_wait_sketch", "epi_wait_sfull", "epi_wait_pfree", "epi_compute",
+                             "cta_total", "epi_ldS+dump", "epi_setbits", "epi_Pstore", "mma_gemm1", "mma_gemm2"};
     fprintf(stderr, "[trd tc timing] (cycles summed over CTAs / epilogue leaders)\n");
     for (int i = 0; i < 15; ++i) fprintf(stderr, "  %-18s %.4e\n", names[i], (double)v[i]);
     cudaFree(c->tc_dbg);
