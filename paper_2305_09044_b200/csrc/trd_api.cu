@@ -162,10 +162,29 @@ void build_plan(const Context& c, int k, const int64_t* s_in, BlockPlan& bp, boo
   bp.n_row_tiles = (bp.nrows + 127) / 128;
   bp.n_col_tiles = (bp.ncols + 63) / 64;
   {
-    int64_t ns = (2 * 148 + bp.n_row_tiles - 1) / bp.n_row_tiles;
-    ns = std::min<int64_t>(ns, bp.n_col_tiles);
-    ns = std::max<int64_t>(ns, 1);
-    bp.tc_nsplit = (int)std::min<int64_t>(ns, 65535);
+    // persistent pass kernels: one CTA per SM walking (row tile, column split) items; pick
+    // the split that minimises the busiest CTA's work (ties: fewer splits)
+    const int64_t nrt = bp.n_row_tiles, nct = bp.n_col_tiles;
+    double best = 1e300;
+    int64_t best_s = 1, best_per = nct;
+    for (int64_t sp = 1; sp <= std::min<int64_t>(nct, 64); ++sp) {
+      const int64_t per = (nct + sp - 1) / sp;
+      const int64_t se = (nct + per - 1) / per;             // no empty splits
+      const int64_t items = nrt * se;
+      const int64_t grid = std::min<int64_t>(items, (int64_t)c.num_sm);
+      // busiest CTA: its items x (tiles per item + ~1 tile of per-item cost: A load, D drain
+      // and the split's share of the d reduction)
+      const double cost = (double)((items + grid - 1) / grid) * ((double)per + 1.0);
+      if (cost < best - 1e-9) { best = cost; best_s = se; best_per = per; }
+    }
+    bp.tc_nsplit = (int)best_s;
+    bp.tc_per = best_per;
+    bp.tc_grid = (int)std::min<int64_t>(nrt * best_s, (int64_t)c.num_sm);
+    const int64_t Ikk = c.dims[k];
+    int64_t jc = (2 * (int64_t)c.num_sm + Ikk - 1) / Ikk;
+    jc = std::max<int64_t>(1, std::min<int64_t>(jc, bp.nL));
+    bp.tc_jl_chunk = (bp.nL + jc - 1) / jc;
+    bp.tc_jc = (bp.nL + bp.tc_jl_chunk - 1) / bp.tc_jl_chunk;
   }
   // geometry: 8 warps per CTA, one (row, column sub-range) item per warp
   if (bp.nL >= 8) { bp.jl_per_cta = 8; bp.ws_split = 1; }
@@ -409,6 +428,12 @@ trd_status trd_init(const trd_config* cfg, const trd_shard* shard, const float* 
   c->cfg.nccl_unique_id = nullptr;
   c->N = N;
   c->stream = (cudaStream_t)stream;
+  {
+    int dev = 0, nsm = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess &&
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess && nsm > 0)
+      c->num_sm = nsm;
+  }
   c->shard_begin = sb;
   c->shard_end = se;
   c->packed = shard->packed ? 1 : 0;
@@ -452,8 +477,9 @@ trd_status trd_init(const trd_config* cfg, const trd_shard* shard, const float* 
       st.vcap = bp.n_row_tiles * 128 * bp.n_col_tiles * 64;   // refined after the data is known
       max_lhl = std::max(max_lhl, (size_t)(bp.n_row_tiles * 2 * 128 * bp.KP));
       max_rhl = std::max(max_rhl, (size_t)(bp.n_col_tiles * 2 * 64 * bp.KP));
-      max_contrib = std::max(max_contrib, (size_t)bp.tc_nsplit * bp.n_row_tiles * 128 * bp.R2);
-      max_sp = std::max(max_sp, (size_t)(bp.n_row_tiles * bp.tc_nsplit * 3));
+      max_contrib = std::max(max_contrib, (size_t)bp.tc_nsplit * bp.n_row_tiles * 128 * bp.KP);
+      max_sp = std::max(max_sp, (size_t)bp.tc_grid * 3);
+      max_dp = std::max(max_dp, (size_t)(bp.tc_jc * c->dims[bp.k] * bp.R2));
     }
     max_rows = std::max(max_rows, (size_t)bp.nrows);
     max_cols = std::max(max_cols, (size_t)bp.ncols);
@@ -534,21 +560,17 @@ trd_status trd_init(const trd_config* cfg, const trd_shard* shard, const float* 
       if (!c->plan[k].use_tc) continue;
       TcStage& sg = c->stage[k];
       const int64_t obs_cap = c->packed ? c->n_values : c->n_local;
-      sg.vcap = std::max<int64_t>(1, std::min(sg.vcap, obs_cap));
+      sg.vcap = std::max<int64_t>(1, std::min(sg.vcap, obs_cap)) + 8 * sg.n_tiles;   // + tile padding
       sg.scan_tmp_bytes = tc_scan_tmp_bytes(sg.n_tiles);
       if ((st = dalloc(c, &sg.tbits, (size_t)sg.n_tiles * 128)) ||
           (st = dalloc(c, &sg.troff, (size_t)sg.n_tiles * 128)) ||
           (st = dalloc(c, &sg.tbase, (size_t)sg.n_tiles + 1)) ||
-          (st = dalloc(c, &sg.tvals, (size_t)sg.vcap)) ||
+          (st = dalloc(c, &sg.tvals, (size_t)sg.vcap)) || (st = dalloc(c, &sg.tidx, (size_t)sg.vcap)) ||
           (st = dalloc(c, reinterpret_cast<char**>(&sg.scan_tmp), sg.scan_tmp_bytes + 16)))
         return bail(st);
       max_v = std::max(max_v, sg.vcap);
     }
     if (max_v > 0 && (st = dalloc(c, &c->tw, (size_t)max_v))) return bail(st);
-    if (getenv("TRD_TC_TIMING")) {
-      if ((st = dalloc(c, &c->tc_dbg, 16))) return bail(st);
-      cudaMemset(c->tc_dbg, 0, 16 * 8);
-    }
   }
   if (shard->host) {
     if ((st = dalloc(c, &c->own_values, (size_t)c->n_values))) return bail(st);
@@ -802,19 +824,10 @@ void trd_destroy(trd_ctx* ctx) {
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->tw) cudaFree(c->tw);
-  if (c->tc_dbg) {
-    unsigned long long v[16];
-    cudaMemcpy(v, c->tc_dbg, sizeof(v), cudaMemcpyDeviceToHost);
-    const char* names[15] = {"cta_setup", "cta_tail", "mma_total", "mma_wait", "epi_total",
-                             "epi_wait_sketch", "epi_wait_sfull", "epi_wait_pfree", "epi_compute",
-                             "cta_total", "epi_ldS+dump", "epi_setbits", "epi_Pstore", "mma_gemm1", "mma_gemm2"};
-    fprintf(stderr, "[trd tc timing] (cycles summed over CTAs / epilogue leaders)\n");
-    for (int i = 0; i < 15; ++i) fprintf(stderr, "  %-18s %.4e\n", names[i], (double)v[i]);
-    cudaFree(c->tc_dbg);
-  }
+  if (getenv("TRD_TC_EXP")) tc_debug_dump();
   for (int k = 0; k < kMaxN; ++k) {
     TcStage& sg = c->stage[k];
-    void* sp[] = {sg.tbits, sg.troff, sg.tbase, sg.tvals, sg.scan_tmp};
+    void* sp[] = {sg.tbits, sg.troff, sg.tbase, sg.tvals, sg.tidx, sg.scan_tmp};
     for (void* p : sp)
       if (p) cudaFree(p);
   }

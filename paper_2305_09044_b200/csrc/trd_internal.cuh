@@ -69,7 +69,10 @@ struct BlockPlan {
   int use_tc;            // 1: tcgen05 pass kernels
   int KP;                // K padded to a multiple of 16
   int64_t n_row_tiles, n_col_tiles;
-  int tc_nsplit;         // column splits per row tile
+  int tc_nsplit;         // column splits per row tile (work item = (row tile, split))
+  int64_t tc_per;        // column tiles per split
+  int tc_grid;           // persistent CTAs of the pass kernels (<= SM count)
+  int64_t tc_jc, tc_jl_chunk;   // d reduction: jl chunks
 };
 
 // Staged working set of one block in tile order (trd_tc.cu "stage sketch", row a2)
@@ -77,7 +80,9 @@ struct TcStage {
   uint64_t* tbits = nullptr;     // [tile][128] observation mask of (row, 64 columns)
   uint16_t* troff = nullptr;     // [tile][128] row offset into the tile's compacted values
   uint64_t* tbase = nullptr;     // [tile] exclusive prefix of the tile counts
-  float* tvals = nullptr;        // compacted observed values, tile-major, row-major in a tile
+  float* tvals = nullptr;        // compacted observed values, tile-major, row-major in a tile,
+                                 // tile blocks padded to 8 entries
+  uint16_t* tidx = nullptr;      // entry list: row * 64 + column per value, 0xFFFF = padding
   void* scan_tmp = nullptr;
   size_t scan_tmp_bytes = 0;
   int64_t n_tiles = 0, vcap = 0;
@@ -95,6 +100,7 @@ struct Context {
   int64_t n_local, n_words;
   int packed;
   cudaStream_t stream;
+  int num_sm = 148;                    // SMs of the current device (persistent grids)
   std::string err;
   trd_status sticky = TRD_OK;
   long long launches = 0;
@@ -130,9 +136,8 @@ struct Context {
   __half* lftHL = nullptr;             // [row][hi KP | lo KP] (A operand, loaded into TMEM)
   __half* lfthHL = nullptr;            // same for the scaled gradient (pass 2)
   __half* rgtHL = nullptr;             // [col tile][hi | lo][64 x KP] core-matrix layout
-  float* contrib = nullptr;            // [split][row][R2]
+  float* contrib = nullptr;            // [split][row][KP] D rows of pass 1
   float* tw = nullptr;                 // staged HQ weights of the current block (pass 1 -> 2)
-  unsigned long long* tc_dbg = nullptr;  // TRD_TC_TIMING=1: per-role cycle counters
   TcStage stage[kMaxN];
   double* dpart = nullptr;             // pass-1 CTA partials of d
   double* spart = nullptr;             // pass-1 CTA partial stats (3 per CTA)
@@ -197,5 +202,6 @@ void launch_tc_pass(Context& c, const BlockPlan& bp, const TcStage& st, bool pas
 void launch_tc_reduce_d(Context& c, const BlockPlan& bp, cudaStream_t s);
 void launch_tc_stage(Context& c, const BlockPlan& bp, TcStage& st, cudaStream_t s);
 size_t tc_scan_tmp_bytes(int64_t n_tiles);
+void tc_debug_dump();   // TRD_TC_EXP diagnostics
 
 }  // namespace trd

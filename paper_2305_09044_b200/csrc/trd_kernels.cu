@@ -1058,7 +1058,7 @@ void launch_block_stats(Context& c, const BlockPlan& bp, cudaStream_t s) {
 void launch_reduce_den(Context& c, const BlockPlan& bp, cudaStream_t s) {
   const int64_t Ik = bp.nrows / bp.nL;
   const int64_t ncta = bp.grid_x * bp.nsplit;
-  const int64_t nden = bp.use_tc ? bp.n_row_tiles * bp.tc_nsplit : Ik * ncta;
+  const int64_t nden = bp.use_tc ? (int64_t)bp.tc_grid : Ik * ncta;
   reduce_den_kernel<<<1, 256, 0, s>>>(c.denpart, nden, c.numpart, Ik, c.red_ws);
   c.launches++;
 }

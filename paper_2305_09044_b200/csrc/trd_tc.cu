@@ -24,6 +24,7 @@
 // padded to KP (multiple of 16).  The B operand uses the canonical SWIZZLE_NONE core-matrix
 // layout (8 rows x 16 B per 128-byte core matrix, core matrix (g, h) at (g*HK + h)*128 B,
 // HK = KP/8); the same tile is the K-major B of S = A.B^T and the MN-major B of D += c.B.
+#include <cstdio>
 #include <cub/cub.cuh>
 #include <cuda_fp16.h>
 
@@ -33,7 +34,6 @@ namespace trd {
 
 constexpr int TC_M = 128;
 constexpr int TC_NT = 64;
-constexpr int TC_PREF = 12;          // observed entries per (row, tile) prefetched into registers
 constexpr int TC_DUMP_STRIDE = 68;   // floats per row of the S/T dump buffer (16-B aligned rows)
 
 // ---------------------------------------------------------------------------------------
@@ -57,12 +57,42 @@ __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 }
+// non-suspending poll (for the latency-critical single MMA warp)
+__device__ __forceinline__ void mbar_wait_spin(uint64_t* bar, uint32_t phase) {
+  const uint32_t addr = smem_u32(bar);
+  uint32_t ok = 0;
+  do {
+    asm volatile("{\n\t.reg .pred p;\n\tmbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+                 "selp.u32 %0, 1, 0, p;\n\t}" : "=r"(ok) : "r"(addr), "r"(phase) : "memory");
+  } while (!ok);
+}
+// try_wait with an explicit suspend-time hint (ns): the thread sleeps until the phase
+// completes or the hint elapses, instead of re-polling (keeps issue slots free for the MMA warp)
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t phase) {
+  const uint32_t addr = smem_u32(bar);
+  uint32_t ok = 0;
+  do {
+    asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+                 "selp.u32 %0, 1, 0, p;\n\t}" : "=r"(ok) : "r"(addr), "r"(phase), "r"(1000000u) : "memory");
+  } while (!ok);
+}
+#ifndef TRD_MBAR_SPIN
+#define TRD_MBAR_SPIN 0
+#endif
+// wait for the phase with the given parity to complete.  TRD_MBAR_SPIN=1 polls with the
+// non-suspending test_wait (hand-offs between the warp roles are latency critical);
+// 0 uses try_wait (may suspend the thread for an implementation-defined time)
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
   const uint32_t addr = smem_u32(bar);
   uint32_t ok = 0;
   do {
+#if TRD_MBAR_SPIN
+    asm volatile("{\n\t.reg .pred p;\n\tmbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+                 "selp.u32 %0, 1, 0, p;\n\t}" : "=r"(ok) : "r"(addr), "r"(phase) : "memory");
+#else
     asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
                  "selp.u32 %0, 1, 0, p;\n\t}" : "=r"(ok) : "r"(addr), "r"(phase) : "memory");
+#endif
   } while (!ok);
 }
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
@@ -173,7 +203,8 @@ struct StageArgs {
   uint64_t* tbits;        // [tile][128]
   uint16_t* troff;        // [tile][128]
   uint64_t* tcount;       // [tile]  (counts, then exclusive prefix)
-  float* tvals;           // compacted values
+  float* tvals;           // compacted values (tile blocks padded to 8 entries)
+  uint16_t* tidx;         // entry list: (row in tile) * 64 + column, 0xFFFF = padding
 };
 
 __global__ void __launch_bounds__(128) stage_bits_kernel(StageArgs s) {
@@ -216,7 +247,10 @@ __global__ void __launch_bounds__(128) stage_bits_kernel(StageArgs s) {
     const int excl = base + inc - cnt;
     s.tbits[tile * TC_M + tid] = bits;
     s.troff[tile * TC_M + tid] = (uint16_t)excl;
-    if (tid == TC_M - 1) s.tcount[tile] = (uint64_t)(excl + cnt);
+    // tile blocks of the compacted values are padded to 8 entries (32 B of values, 16 B of
+    // entry list) so that a tile's values / weights / list move by bulk copies without
+    // touching a neighbour's
+    if (tid == TC_M - 1) s.tcount[tile] = (uint64_t)((excl + cnt + 7) & ~7);
     __syncthreads();
   }
 }
@@ -233,9 +267,15 @@ __global__ void __launch_bounds__(128) stage_vals_kernel(StageArgs s) {
     __syncthreads();
     const int64_t row = rt * TC_M + tid;
     uint64_t bits = s.tbits[tile * TC_M + tid];
+    const int64_t base = (int64_t)s.tcount[tile] + s.troff[tile * TC_M + tid];
+    if (tid == TC_M - 1) {                    // padding entries of the tile block
+      const int64_t end = base + __popcll(bits);
+      for (int64_t e = end; e < (int64_t)s.tcount[tile + 1]; ++e) { s.tidx[e] = 0xFFFFu; s.tvals[e] = 0.f; }
+    }
     if (bits) {
       const int64_t ro = s.row_off[row];
-      float* out = s.tvals + s.tcount[tile] + s.troff[tile * TC_M + tid];
+      float* out = s.tvals + base;
+      uint16_t* oidx = s.tidx + base;
       int q = 0;
       int64_t cwi = -1;
       uint32_t cw = 0, cp = 0;
@@ -249,6 +289,7 @@ __global__ void __launch_bounds__(128) stage_vals_kernel(StageArgs s) {
           if (wi != cwi) { cw = __ldg(s.mask + wi); cp = __ldg(s.rank_prefix + wi); cwi = wi; }
           vi = (int64_t)cp + __popc(cw & ((1u << (lin & 31)) - 1u));
         }
+        oidx[q] = (uint16_t)(tid * TC_NT + j);
         out[q++] = __ldg(s.values + vi);
       }
     }
@@ -259,22 +300,24 @@ __global__ void __launch_bounds__(128) stage_vals_kernel(StageArgs s) {
 // ---------------------------------------------------------------------------------------
 struct TcArgs {
   int64_t nrows, ncols, nL, Ik, n_col_tiles, nrows_pad;
+  int64_t n_items, per;    // work items = (row tile, column split); per = column tiles per split
   int rowmode, K, R2, rk, rk1, rs, p, nsplit;
   int sigma_inf;
   const __half* arow;      // Lft (pass 1) or Lft_h (pass 2), row-major hi | lo
   const __half* rgtHL;
-  const float* mid;
   const uint64_t* tbits;
   const uint16_t* troff;
   const uint64_t* tbase;
   const float* tvals;
+  const uint16_t* tidx;    // staged entry lists
   float* tw;               // staged weights (pass 1 writes, pass 2 reads)
   const DevScalars* sc;
-  float* contrib;          // [split][nrows_pad][R2]
-  double* spart;           // [row_tile][split][3]
-  double* denpart;         // [row_tile][split]
-  unsigned long long* dbg; // optional per-role cycle counters (TRD_TC_TIMING)
-  int dbg_noepi;           // TRD_TC_NOEPI=1 (timing experiments only): epilogue skips its work
+  float* contrib;          // [split][nrows_pad][KP]  D rows of pass 1
+  double* spart;           // [cta][3]
+  double* denpart;         // [cta]
+  int exp;                 // TRD_TC_EXP (timing experiments only; results invalid if != 0):
+                           //   bit 0 = epilogue does the barrier handshakes only
+                           //   bit 1 = B producer skips the copies, bit 2 = sketch producer skips
 };
 
 template <int KP>
@@ -290,26 +333,24 @@ struct TcLayout {
 template <int KP>
 __device__ __forceinline__ void issue_split_gemm_ts(uint32_t dtmem, uint32_t acol, uint32_t bH) {
   using L = TcLayout<KP>;
-  uint32_t acc = 0;
+  // descriptor of the B tile start; K steps and the lo block are added to the address field
+  const uint64_t d0 = make_sdesc(bH, 128, L::HK * 128);
 #pragma unroll
   for (int term = 0; term < 3; ++term) {
     const uint32_t aa = acol + (term == 2 ? KP / 2 : 0);
-    const uint32_t bb = bH + (term == 1 ? L::B_LO_BYTES : 0u);
+    const uint64_t dt = d0 + (uint64_t)((term == 1 ? L::B_LO_BYTES : 0u) >> 4);
 #pragma unroll
-    for (int ks = 0; ks < KP / 16; ++ks) {
-      const uint64_t db = make_sdesc(bb + ks * 256, 128, L::HK * 128);
-      mma_ts(dtmem, aa + ks * 8, db, L::IDESC_S, acc);
-      acc = 1;
-    }
+    for (int ks = 0; ks < KP / 16; ++ks)
+      mma_ts(dtmem, aa + ks * 8, dt + (uint64_t)(ks * 16), L::IDESC_S, (term | ks) ? 1u : 0u);
   }
 }
 
-template <int KP>
-__device__ __forceinline__ void stage_b_async(const TcArgs& a, int64_t ct, __half* sBbuf, int tid) {
-  using L = TcLayout<KP>;
-  const char* g = reinterpret_cast<const char*>(a.rgtHL + ct * L::B_HALVES);
-  char* s = reinterpret_cast<char*>(sBbuf);
-  for (int i = tid; i < L::B_HALVES / 8; i += TC_M) cp_async16(s + i * 16, g + i * 16);
+// one lane of a converged warp (the MMA issuer runs warp-wide so that its operands live in
+// uniform registers; only the elected lane issues)
+__device__ __forceinline__ uint32_t elect_one() {
+  uint32_t pred = 0;
+  asm volatile("{\n\t.reg .pred P1;\n\telect.sync _|P1, 0xffffffff;\n\tselp.b32 %0, 1, 0, P1;\n\t}" : "=r"(pred));
+  return pred;
 }
 
 // this thread's row of A (hi | lo) -> TMEM columns [acol, acol + KP)
@@ -331,33 +372,77 @@ __device__ __forceinline__ void load_a_to_tmem(const TcArgs& a, int64_t row, uin
 #include "tc_ws.inc"
 
 // ---------------------------------------------------------------------------------------
-// d(i_k)[o] = sum_split sum_jl contrib[split][row(i_k, jl)][o]  (fp64, fixed order) and the
-// pass-1 statistics -> dvec = [d | sum_e2 | welsch | n]
+// a6 contraction + reduction, stage 1 (fp64, fixed order):
+//   d(i_k)[a + r_k b] = sum_split sum_jl sum_c Mid(jl)[b][c] D(split, row(i_k, jl))[a + r_k c]
+// (Eq. 9/15, P:152, 234 with S(j) = Mid(j_L) Rgt(j_R); p = 0: Mid = I).  grid (I_k, JC):
+// CTA (ik, jc) sums the jl chunk jc into dpart[jc][ik][R2].
 // ---------------------------------------------------------------------------------------
-__global__ void tc_reduce_d_kernel(const float* __restrict__ contrib, const double* __restrict__ spart,
-                                   int64_t nparts, int nsplit, int64_t nrows_pad, int64_t nL, int64_t Ik,
-                                   int rowmode, int R2, double* __restrict__ dvec, DevScalars* sc,
-                                   int kblk) {
-  __shared__ double acc[1024];
+constexpr int RD_ROWS = 32;   // jl rows staged per step
+__global__ void __launch_bounds__(256) tc_reduce_d_kernel(
+    const float* __restrict__ contrib, const float* __restrict__ mid, int nsplit, int64_t nrows_pad, int64_t nL,
+    int64_t Ik, int rowmode, int KP, int R2, int rk, int rs, int p, int64_t jl_chunk, double* __restrict__ dpart) {
+  extern __shared__ float rsm[];
+  const int KPp = KP + 1, MS = (R2 / rk) * rs;               // Mid(jl) is r_{k+1} x r_s
+  float* Dt = rsm;                                           // [RD_ROWS][KP + 1]
+  float* Mt = rsm + RD_ROWS * KPp;                           // [RD_ROWS][MS]
+  __shared__ double acc[256];
+  const int64_t ik = blockIdx.x, jc = blockIdx.y;
+  const int tid = threadIdx.x;
+  const int G = max(1, (int)blockDim.x / R2);
+  const int o = tid % R2, g = tid / R2;
+  const int aa = o % rk, bq = o / rk;
+  const int64_t j0 = jc * jl_chunk, j1 = min(nL, j0 + jl_chunk);
+  double s = 0.0;
+  for (int64_t jb = j0; jb < j1; jb += RD_ROWS) {
+    const int nr = (int)min((int64_t)RD_ROWS, j1 - jb);
+    if (p > 0) {
+      for (int idx = tid; idx < nr * MS; idx += blockDim.x) Mt[idx] = mid[jb * MS + idx];   // rows jb.. contiguous
+    }
+    for (int sp = 0; sp < nsplit; ++sp) {
+      for (int idx = tid; idx < nr * KP; idx += blockDim.x) {
+        const int rr = idx / KP, kk = idx - rr * KP;
+        const int64_t jl = jb + rr;
+        const int64_t row = rowmode == 0 ? jl + nL * ik : ik + Ik * jl;
+        Dt[rr * KPp + kk] = contrib[((int64_t)sp * nrows_pad + row) * KP + kk];
+      }
+      __syncthreads();
+      if (g < G) {
+        float t = 0.f;
+        for (int rr = g; rr < nr; rr += G) {
+          if (p == 0) {
+            t += Dt[rr * KPp + o];
+          } else {
+            const float* M = Mt + rr * MS + bq * rs;
+            const float* D = Dt + rr * KPp + aa;
+            float u = 0.f;
+            for (int c = 0; c < rs; ++c) u = fmaf(M[c], D[rk * c], u);
+            t += u;
+          }
+        }
+        s += (double)t;
+      }
+      __syncthreads();
+    }
+  }
+  acc[tid] = s;
+  __syncthreads();
+  if (tid < R2) {
+    double t = 0.0;
+    for (int gg = 0; gg < G; ++gg) t += acc[gg * R2 + tid];
+    dpart[(jc * Ik + ik) * R2 + tid] = t;
+  }
+}
+
+// stage 2: dvec = [d | sum_e2 | welsch | n] from the chunk partials and the per-CTA statistics
+__global__ void tc_reduce_final_kernel(const double* __restrict__ dpart, int64_t JC, int64_t Ik, int R2,
+                                       const double* __restrict__ spart, int64_t nparts,
+                                       double* __restrict__ dvec, DevScalars* sc, int kblk) {
   const int64_t ik = blockIdx.x;
   if (ik < Ik) {
-    const int G = max(1, (int)blockDim.x / R2);
-    const int o = threadIdx.x % R2, g = threadIdx.x / R2;
-    double s = 0.0;
-    if (g < G) {
-      for (int sp = 0; sp < nsplit; ++sp) {
-        for (int64_t jl = g; jl < nL; jl += G) {
-          const int64_t row = rowmode == 0 ? jl + nL * ik : ik + Ik * jl;
-          s += (double)contrib[((int64_t)sp * nrows_pad + row) * R2 + o];
-        }
-      }
-    }
-    acc[threadIdx.x] = s;
-    __syncthreads();
-    if (threadIdx.x < R2) {
+    for (int o = threadIdx.x; o < R2; o += blockDim.x) {
       double t = 0.0;
-      for (int gg = 0; gg < G; ++gg) t += acc[gg * R2 + threadIdx.x];
-      dvec[ik * R2 + threadIdx.x] = t;
+      for (int64_t jc = 0; jc < JC; ++jc) t += dpart[(jc * Ik + ik) * R2 + o];
+      dvec[ik * R2 + o] = t;
     }
     return;
   }
@@ -397,7 +482,7 @@ void launch_tc_stage(Context& c, const BlockPlan& bp, TcStage& st, cudaStream_t 
   a.packed = c.packed;
   a.row_off = c.row_off; a.col_off = c.col_off;
   a.mask = c.mask; a.rank_prefix = c.rank_prefix; a.values = c.values;
-  a.tbits = st.tbits; a.troff = st.troff; a.tcount = st.tbase; a.tvals = st.tvals;
+  a.tbits = st.tbits; a.troff = st.troff; a.tcount = st.tbase; a.tvals = st.tvals; a.tidx = st.tidx;
   const int grid = (int)std::min<int64_t>(a.n_tiles, 148 * 16);
   stage_bits_kernel<<<grid, TC_M, 0, s>>>(a);
   cudaMemsetAsync(st.tbase + a.n_tiles, 0, sizeof(uint64_t), s);   // tbase[n_tiles] = total
@@ -416,46 +501,56 @@ static TcArgs make_tc_args(const Context& c, const BlockPlan& bp, const TcStage&
   TcArgs a;
   a.nrows = bp.nrows; a.ncols = bp.ncols; a.nL = bp.nL; a.Ik = bp.nrows / bp.nL;
   a.n_col_tiles = bp.n_col_tiles; a.nrows_pad = bp.n_row_tiles * TC_M;
+  a.n_items = bp.n_row_tiles * bp.tc_nsplit; a.per = bp.tc_per;
   a.rowmode = bp.rowmode; a.K = bp.K; a.R2 = bp.R2; a.rk = bp.rk; a.rk1 = bp.rk1; a.rs = bp.rs;
   a.p = bp.p; a.nsplit = bp.tc_nsplit;
   a.sigma_inf = c.cfg.sigma_mode == TRD_SIGMA_INF;
   a.arow = pass2 ? c.lfthHL : c.lftHL;
   a.rgtHL = c.rgtHL;
-  a.mid = c.mid;
-  a.tbits = st.tbits; a.troff = st.troff; a.tbase = st.tbase; a.tvals = st.tvals;
+  a.tbits = st.tbits; a.troff = st.troff; a.tbase = st.tbase; a.tvals = st.tvals; a.tidx = st.tidx;
   a.tw = c.tw;
   a.sc = c.sc;
   a.contrib = c.contrib; a.spart = c.spart; a.denpart = c.denpart;
-  a.dbg = pass2 ? nullptr : c.tc_dbg;
-  a.dbg_noepi = (a.dbg && getenv("TRD_TC_NOEPI")) ? 1 : 0;
+  const char* ex = getenv("TRD_TC_EXP");
+  a.exp = ex ? atoi(ex) : 0;
   return a;
-}
-
-template <int KP>
-static size_t tc_smem1() {
-  return (size_t)ws_nb<KP>() * ws_b_bytes<KP>() + (size_t)ws_ns<KP>() * WS_SK_BYTES +
-         2 * (size_t)TC_M * TC_DUMP_STRIDE * 4;
-}
-template <int KP>
-static size_t tc_smem2() {
-  return (size_t)ws_nb<KP>() * ws_b_bytes<KP>() + (size_t)ws_ns<KP>() * WS_SK_BYTES +
-         2 * (size_t)TC_M * TC_DUMP_STRIDE * 4;
 }
 
 template <int KP>
 static void launch_tc_pass_t(Context& c, const BlockPlan& bp, const TcStage& st, bool pass2, cudaStream_t s) {
   TcArgs a = make_tc_args(c, bp, st, pass2);
-  dim3 grid((unsigned)bp.n_row_tiles, (unsigned)bp.tc_nsplit);
+  const dim3 grid((unsigned)bp.tc_grid);
   if (!pass2) {
-    const size_t sm = tc_smem1<KP>();
-    cudaFuncSetAttribute(tc_pass1_kernel<KP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    tc_pass1_kernel<KP><<<grid, WS_THREADS, sm, s>>>(a);
+    const int sm = Ws1<KP>::SMEM;
+    cudaFuncSetAttribute(tc_pass1_kernel<KP>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    tc_pass1_kernel<KP><<<grid, WsWarps<Ws1<KP>::NE>::THREADS, sm, s>>>(a);
   } else {
-    const size_t sm = tc_smem2<KP>();
-    cudaFuncSetAttribute(tc_pass2_kernel<KP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    tc_pass2_kernel<KP><<<grid, WS_THREADS, sm, s>>>(a);
+    const int sm = Ws2<KP>::SMEM;
+    cudaFuncSetAttribute(tc_pass2_kernel<KP>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    tc_pass2_kernel<KP><<<grid, WsWarps<Ws2<KP>::NE>::THREADS, sm, s>>>(a);
   }
   c.launches++;
+}
+
+void tc_debug_dump() {
+  static long long tr[256 * 16];
+  if (cudaMemcpyFromSymbol(tr, g_trace, sizeof(tr)) == cudaSuccess && tr[0] != 0) {
+    fprintf(stderr, "[trd tc trace] pass-1 CTA 0 (cycles rel. to tile 0 GEMM1 start)\n"
+                    "  tile | G1 start wait issue | G2 start wait issue | EPI start skfull sfull dumped ppfree done\n");
+    const long long t0 = tr[0];
+    for (int i = 0; i < 48; ++i) {
+      const long long* q = tr + i * 16;
+      auto f = [&](int k) { return q[k] ? q[k] - t0 : -1; };
+      fprintf(stderr, "  %4d | %7lld %5lld %5lld | %7lld %5lld %5lld | %7lld %5lld %5lld %5lld %5lld %5lld\n", i,
+              f(0), q[1] - q[0], q[2] - q[0], f(3), q[4] - q[3], q[5] - q[3], f(6), q[7] - q[6], q[8] - q[6],
+              q[9] - q[6], q[10] - q[6], q[11] - q[6]);
+    }
+  }
+  unsigned long long v[16];
+  if (cudaMemcpyFromSymbol(v, g_tc_dbg, sizeof(v)) != cudaSuccess) return;
+  const char* nm[6] = {"a_full_wait", "bf_full_wait", "t_free_wait", "issue", "tiles", "total"};
+  fprintf(stderr, "[trd tc exp] pass-2 MMA thread cycles summed over CTAs\n");
+  for (int i = 0; i < 6; ++i) fprintf(stderr, "  %-14s %.4e\n", nm[i], (double)v[i]);
 }
 
 bool tc_supported_kp(int KP) { return KP >= 16 && KP <= 128 && KP % 16 == 0; }
@@ -476,13 +571,15 @@ void launch_tc_pass(Context& c, const BlockPlan& bp, const TcStage& st, bool pas
 
 void launch_tc_reduce_d(Context& c, const BlockPlan& bp, cudaStream_t s) {
   const int64_t Ik = bp.nrows / bp.nL;
-  const int64_t nparts = bp.n_row_tiles * bp.tc_nsplit;
-  int threads = bp.R2 * std::max(1, 1024 / std::max(1, bp.R2));
-  threads = std::min(threads, 1024);
-  tc_reduce_d_kernel<<<(unsigned)(Ik + 1), threads, 0, s>>>(c.contrib, c.spart, nparts, bp.tc_nsplit,
-                                                            bp.n_row_tiles * TC_M, bp.nL, Ik, bp.rowmode,
-                                                            bp.R2, c.dvec, c.sc, bp.k);
-  c.launches++;
+  const int threads = bp.R2 * std::max(1, 256 / std::max(1, bp.R2));
+  const size_t smem = (size_t)RD_ROWS * ((bp.KP + 1) + (bp.R2 / bp.rk) * bp.rs) * sizeof(float);
+  cudaFuncSetAttribute(tc_reduce_d_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  tc_reduce_d_kernel<<<dim3((unsigned)Ik, (unsigned)bp.tc_jc), threads, smem, s>>>(
+      c.contrib, c.mid, bp.tc_nsplit, bp.n_row_tiles * TC_M, bp.nL, Ik, bp.rowmode, bp.KP, bp.R2, bp.rk,
+      bp.rs, bp.p, bp.tc_jl_chunk, c.dpart);
+  tc_reduce_final_kernel<<<(unsigned)(Ik + 1), 128, 0, s>>>(c.dpart, bp.tc_jc, Ik, bp.R2, c.spart, bp.tc_grid,
+                                                            c.dvec, c.sc, bp.k);
+  c.launches += 2;
 }
 
 }  // namespace trd
