@@ -181,8 +181,9 @@ void build_plan(const Context& c, int k, const int64_t* s_in, BlockPlan& bp, boo
     bp.tc_per = best_per;
     bp.tc_grid = (int)std::min<int64_t>(nrt * best_s, (int64_t)c.num_sm);
     const int64_t Ikk = c.dims[k];
-    int64_t jc = (2 * (int64_t)c.num_sm + Ikk - 1) / Ikk;
-    jc = std::max<int64_t>(1, std::min<int64_t>(jc, bp.nL));
+    // d reduction: >= 8 CTAs per SM worth of (i_k, jl-chunk) blocks, chunks of >= 32 rows
+    int64_t jc = (8 * (int64_t)c.num_sm + Ikk - 1) / Ikk;
+    jc = std::max<int64_t>(1, std::min<int64_t>(jc, (bp.nL + 31) / 32));
     bp.tc_jl_chunk = (bp.nL + jc - 1) / jc;
     bp.tc_jc = (bp.nL + bp.tc_jl_chunk - 1) / bp.tc_jl_chunk;
   }
@@ -231,10 +232,10 @@ trd_status block_pass1(Context* c, const BlockPlan& bp) {
   cudaStream_t s = c->stream;
   launch_sampler(*c, bp, s);
   launch_plan(*c, bp, s);
-  launch_lft(*c, bp, c->Z + c->zoff[bp.k], 0, c->lft, s);
+  if (!bp.use_tc) launch_lft(*c, bp, c->Z + c->zoff[bp.k], 0, c->lft, s);
   TcStage& stg = c->stage[bp.k];
-  if (bp.use_tc) {
-    launch_tc_pack_rows(*c, bp, c->lft, c->lftHL, s);
+  if (bp.use_tc) {                          // Lft built directly as the fp16 hi / lo A operand
+    launch_tc_lft(*c, bp, false, s);
     launch_tc_pack_cols(*c, bp, s);
     if (!stg.valid) {                       // a2: stage the sketch in tile order
       launch_tc_stage(*c, bp, stg, s);
@@ -262,8 +263,8 @@ trd_status block_pass2(Context* c, const BlockPlan& bp) {
   launch_gram(*c, bp, s);
   launch_solve(*c, bp, s);
   launch_h(*c, bp, s);
-  launch_lft(*c, bp, nullptr, 1, c->lfth, s);
-  if (bp.use_tc) launch_tc_pack_rows(*c, bp, c->lfth, c->lfthHL, s);
+  if (!bp.use_tc) launch_lft(*c, bp, nullptr, 1, c->lfth, s);
+  else launch_tc_lft(*c, bp, true, s);
   const int e0 = c->prof ? prof_event(c) : -1;
   if (bp.use_tc) launch_tc_pass(*c, bp, c->stage[bp.k], true, s);
   else launch_pass2(*c, bp, s);

@@ -716,6 +716,87 @@ solve_kernel(const double* __restrict__ G, int n, double lambda_rel, double* __r
   if (threadIdx.x == 0) sc->lambda = lam;
 }
 
+// Small-n path of a9 (R_k^2 <= kGjMaxN): the same filtered operator M = A^-1 G A^-1 with
+// A = G + lambda I (R5), A^-1 by in-place Gauss-Jordan elimination (A is SPD, so
+// no pivoting; a non-positive pivot means "not SPD" and triggers the lambda x10 retry like a
+// failed Cholesky), then two small GEMMs.  One CTA, everything in shared memory; 2n
+// barriers instead of the O(n) sequential triangular solves of solve_kernel.
+constexpr int kGjMaxN = 96;
+__global__ void __launch_bounds__(1024) gj_solve_kernel(const double* __restrict__ G, int n, double lambda_rel,
+                                                        double* __restrict__ Mout, DevScalars* __restrict__ sc) {
+  extern __shared__ double gsm[];
+  double* A = gsm;                 // n x n, becomes A^-1
+  double* Gs = gsm + n * n;        // n x n copy of G, then T = G A^-1
+  double* rowk = Gs + n * n;       // n
+  double* colk = rowk + n;         // n
+  __shared__ int fail_s;
+  __shared__ double tr_s;
+  const int nn = n * n;
+  for (int t = threadIdx.x; t < nn; t += blockDim.x) Gs[t] = G[t];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double tr = 0.0;
+    for (int i = 0; i < n; ++i) tr += Gs[i * n + i];
+    tr_s = tr;
+  }
+  __syncthreads();
+  double lam = lambda_rel * tr_s / n;
+  for (int attempt = 0;; ++attempt) {
+    for (int t = threadIdx.x; t < nn; t += blockDim.x) A[t] = Gs[t] + ((t / n == t % n) ? lam : 0.0);
+    if (threadIdx.x == 0) fail_s = 0;
+    __syncthreads();
+    for (int k = 0; k < n; ++k) {
+      const double p = A[k * n + k];
+      if (!(p > 0.0)) { if (threadIdx.x == 0) fail_s = 1; break; }   // uniform: all threads read p
+      const double ip = 1.0 / p;
+      for (int t = threadIdx.x; t < n; t += blockDim.x) {
+        rowk[t] = (t == k) ? ip : A[k * n + t] * ip;     // new row k
+        colk[t] = (t == k) ? 0.0 : A[t * n + k];         // old column k (pivot excluded)
+      }
+      __syncthreads();
+      for (int t = threadIdx.x; t < nn; t += blockDim.x) {
+        const int i = t / n, j = t - (t / n) * n;
+        double v;
+        if (i == k) v = rowk[j];
+        else if (j == k) v = -colk[i] * ip;
+        else v = fma(-colk[i], rowk[j], A[t]);
+        A[t] = v;
+      }
+      __syncthreads();
+    }
+    __syncthreads();
+    if (!fail_s || attempt >= 3) break;
+    lam *= 10.0;
+    __syncthreads();
+  }
+  if (fail_s) {
+    if (threadIdx.x == 0) { sc->not_spd = 1; sc->lambda = lam; }
+    for (int t = threadIdx.x; t < nn; t += blockDim.x) Mout[t] = 0.0;
+    return;
+  }
+  // T = G A^-1 (into Gs, row by row needs a copy: compute into registers first)
+  double acc[(kGjMaxN * kGjMaxN + 1023) / 1024];
+  int q = 0;
+  for (int t = threadIdx.x; t < nn; t += blockDim.x, ++q) {
+    const int i = t / n, j = t - (t / n) * n;
+    double v = 0.0;
+    for (int l = 0; l < n; ++l) v = fma(Gs[i * n + l], A[l * n + j], v);
+    acc[q] = v;
+  }
+  __syncthreads();
+  q = 0;
+  for (int t = threadIdx.x; t < nn; t += blockDim.x, ++q) Gs[t] = acc[q];
+  __syncthreads();
+  // M = A^-1 T
+  for (int t = threadIdx.x; t < nn; t += blockDim.x) {
+    const int i = t / n, j = t - (t / n) * n;
+    double v = 0.0;
+    for (int l = 0; l < n; ++l) v = fma(A[i * n + l], Gs[l * n + j], v);
+    Mout[t] = v;
+  }
+  if (threadIdx.x == 0) sc->lambda = lam;
+}
+
 // h = d M (row-wise), num partial per row = <d(i), h(i)>
 __global__ void h_kernel(const double* __restrict__ dvec, const double* __restrict__ M, int R2,
                          double* __restrict__ h, double* __restrict__ numpart) {
@@ -1093,6 +1174,18 @@ void launch_gram(Context& c, const BlockPlan& bp, cudaStream_t s) {
 
 void launch_solve(Context& c, const BlockPlan& bp, cudaStream_t s) {
   const int n = bp.R2;
+  if (n <= kGjMaxN) {
+    const size_t gneed = ((size_t)2 * n * n + 2 * n) * sizeof(double);
+    static bool gj_attr = false;
+    if (!gj_attr) {
+      cudaFuncSetAttribute(gj_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)(((size_t)2 * kGjMaxN * kGjMaxN + 2 * kGjMaxN) * sizeof(double)));
+      gj_attr = true;
+    }
+    gj_solve_kernel<<<1, 1024, gneed, s>>>(c.G, n, c.cfg.lambda_rel, c.Mop, c.sc);
+    c.launches++;
+    return;
+  }
   const size_t need = (size_t)2 * n * n * sizeof(double);
   const int use_smem = need <= 200 * 1024;
   static bool attr_set = false;

@@ -165,6 +165,63 @@ __global__ void tc_pack_rows_kernel(const float* __restrict__ src, int64_t nrows
   }
 }
 
+// a3 + the Lft half of the GEMM form, fused with the fp16 hi / lo split of
+// the A operand: Lft(row)[a + r_k c] = sum_b X(i_k)[a][b] Mid(j_L)[b][c]  (p = 0: Lft = X(i_k)),
+// X = core slice Z_k(i_k) (pass 1) or folded scaled gradient H(i_k) (pass 2).  One thread per
+// (row, 8 consecutive kappa): 16-byte stores of hi and lo.  Same fp32 arithmetic order as
+// lft_kernel (fmaf over b ascending).
+struct LftArgs {
+  int64_t nrows, nL, Ik;
+  int rowmode, rk, rk1, rs, K, KP, p;
+  const float* zk;       // Z_k[i][a][b]
+  const double* hk;      // h[i][a + r_k b]
+  const float* mid;      // Mid[jl][b][c]
+};
+__global__ void __launch_bounds__(256) tc_lft_pack_kernel(LftArgs a, int pass2, int64_t nrows_pad,
+                                                          __half* __restrict__ dst) {
+  const int per_row = a.KP / 8;
+  const int64_t tot = nrows_pad * per_row;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tot;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = t / per_row;
+    const int k0 = (int)(t - row * per_row) * 8;
+    __half hh[8], ll[8];
+    int64_t ik = -1, jl = 0;
+    if (row < a.nrows) {
+      if (a.rowmode == 0) { ik = row / a.nL; jl = row - ik * a.nL; }
+      else { jl = row / a.Ik; ik = row - jl * a.Ik; }
+    }
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const int kap = k0 + e;
+      float v = 0.f;
+      if (ik >= 0 && kap < a.K) {
+        const int aa = kap % a.rk, c = kap / a.rk;
+        if (a.p == 0) {
+          v = pass2 ? (float)__ldg(a.hk + ik * (a.rk * a.rk1) + aa + a.rk * c)
+                    : __ldg(a.zk + (ik * a.rk + aa) * a.rk1 + c);
+        } else {
+          const float* M = a.mid + (jl * a.rk1) * a.rs + c;
+          for (int b = 0; b < a.rk1; ++b) {
+            const float x = pass2 ? (float)__ldg(a.hk + ik * (a.rk * a.rk1) + aa + a.rk * b)
+                                  : __ldg(a.zk + (ik * a.rk + aa) * a.rk1 + b);
+            v = fmaf(x, __ldg(M + b * a.rs), v);
+          }
+        }
+      }
+      hh[e] = __float2half_rn(v);
+      ll[e] = __float2half_rn(v - __half2float(hh[e]));
+    }
+    uint4 hv, lv;
+    hv.x = pack_half2(hh[0], hh[1]); hv.y = pack_half2(hh[2], hh[3]);
+    hv.z = pack_half2(hh[4], hh[5]); hv.w = pack_half2(hh[6], hh[7]);
+    lv.x = pack_half2(ll[0], ll[1]); lv.y = pack_half2(ll[2], ll[3]);
+    lv.z = pack_half2(ll[4], ll[5]); lv.w = pack_half2(ll[6], ll[7]);
+    *reinterpret_cast<uint4*>(dst + row * 2 * a.KP + k0) = hv;
+    *reinterpret_cast<uint4*>(dst + row * 2 * a.KP + a.KP + k0) = lv;
+  }
+}
+
 __device__ __forceinline__ int64_t cm_offset(int r, int kap, int HK) {
   return ((int64_t)((r >> 3) * HK + (kap >> 3)) * 8 + (r & 7)) * 8 + (kap & 7);
 }
@@ -303,7 +360,10 @@ struct TcArgs {
   int64_t n_items, per;    // work items = (row tile, column split); per = column tiles per split
   int rowmode, K, R2, rk, rk1, rs, p, nsplit;
   int sigma_inf;
-  const __half* arow;      // Lft (pass 1) or Lft_h (pass 2), row-major hi | lo
+  const __half* arow;      // Lft (pass 1) or Lft_h (pass 2), row-major hi | lo (unused: built in-kernel)
+  const float* zk;         // core k, slice-major Z_k[i][a][b] (pass-1 A operand)
+  const double* hk;        // scaled gradient h[i][a + r_k b] (pass-2 A operand)
+  const float* mid;        // Mid(j_L): [jl][r_{k+1}][r_s]
   const __half* rgtHL;
   const uint64_t* tbits;
   const uint16_t* troff;
@@ -468,6 +528,18 @@ void launch_tc_pack_rows(Context& c, const BlockPlan& bp, const float* src, __ha
   c.launches++;
 }
 
+void launch_tc_lft(Context& c, const BlockPlan& bp, bool pass2, cudaStream_t s) {
+  LftArgs a;
+  a.nrows = bp.nrows; a.nL = bp.nL; a.Ik = bp.nrows / bp.nL;
+  a.rowmode = bp.rowmode; a.rk = bp.rk; a.rk1 = bp.rk1; a.rs = bp.rs; a.K = bp.K; a.KP = bp.KP; a.p = bp.p;
+  a.zk = c.Z + c.zoff[bp.k];
+  a.hk = c.h;
+  a.mid = c.mid;
+  const int64_t pad = bp.n_row_tiles * TC_M;
+  tc_lft_pack_kernel<<<tc_grid(pad * (bp.KP / 8)), 256, 0, s>>>(a, pass2 ? 1 : 0, pad, pass2 ? c.lfthHL : c.lftHL);
+  c.launches++;
+}
+
 void launch_tc_pack_cols(Context& c, const BlockPlan& bp, cudaStream_t s) {
   tc_pack_cols_kernel<<<tc_grid(bp.n_col_tiles * TC_NT * bp.KP), 256, 0, s>>>(c.rgtT, bp.ncols, bp.K, bp.KP,
                                                                                 bp.n_col_tiles, c.rgtHL);
@@ -506,6 +578,9 @@ static TcArgs make_tc_args(const Context& c, const BlockPlan& bp, const TcStage&
   a.p = bp.p; a.nsplit = bp.tc_nsplit;
   a.sigma_inf = c.cfg.sigma_mode == TRD_SIGMA_INF;
   a.arow = pass2 ? c.lfthHL : c.lftHL;
+  a.zk = c.Z + c.zoff[bp.k];
+  a.hk = c.h;
+  a.mid = c.mid;
   a.rgtHL = c.rgtHL;
   a.tbits = st.tbits; a.troff = st.troff; a.tbase = st.tbase; a.tvals = st.tvals; a.tidx = st.tidx;
   a.tw = c.tw;
