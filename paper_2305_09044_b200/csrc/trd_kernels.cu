@@ -721,7 +721,7 @@ solve_kernel(const double* __restrict__ G, int n, double lambda_rel, double* __r
 // no pivoting; a non-positive pivot means "not SPD" and triggers the lambda x10 retry like a
 // failed Cholesky), then two small GEMMs.  One CTA, everything in shared memory; 2n
 // barriers instead of the O(n) sequential triangular solves of solve_kernel.
-constexpr int kGjMaxN = 96;
+constexpr int kGjMaxN = 112;
 __global__ void __launch_bounds__(1024) gj_solve_kernel(const double* __restrict__ G, int n, double lambda_rel,
                                                         double* __restrict__ Mout, DevScalars* __restrict__ sc) {
   extern __shared__ double gsm[];
@@ -755,12 +755,9 @@ __global__ void __launch_bounds__(1024) gj_solve_kernel(const double* __restrict
       }
       __syncthreads();
       for (int t = threadIdx.x; t < nn; t += blockDim.x) {
-        const int i = t / n, j = t - (t / n) * n;
-        double v;
-        if (i == k) v = rowk[j];
-        else if (j == k) v = -colk[i] * ip;
-        else v = fma(-colk[i], rowk[j], A[t]);
-        A[t] = v;
+        const int i = t / n, j = t - i * n;
+        const double ci = colk[i], rj = rowk[j];
+        A[t] = (i == k) ? rj : ((j == k) ? -ci * ip : fma(-ci, rj, A[t]));
       }
       __syncthreads();
     }

@@ -177,48 +177,78 @@ struct LftArgs {
   const double* hk;      // h[i][a + r_k b]
   const float* mid;      // Mid[jl][b][c]
 };
+// CTA = one 128-row tile: the rows' X(i_k) and Mid(j_L) are staged in shared memory (row
+// stride padded to an odd word count: conflict-free across rows), then thread (row, half)
+// produces KP/2 consecutive kappa and stores them as 16-byte hi / lo vectors.
 __global__ void __launch_bounds__(256) tc_lft_pack_kernel(LftArgs a, int pass2, int64_t nrows_pad,
                                                           __half* __restrict__ dst) {
-  const int per_row = a.KP / 8;
-  const int64_t tot = nrows_pad * per_row;
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tot;
-       t += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t row = t / per_row;
-    const int k0 = (int)(t - row * per_row) * 8;
-    __half hh[8], ll[8];
-    int64_t ik = -1, jl = 0;
-    if (row < a.nrows) {
-      if (a.rowmode == 0) { ik = row / a.nL; jl = row - ik * a.nL; }
-      else { jl = row / a.Ik; ik = row - jl * a.Ik; }
-    }
-#pragma unroll
-    for (int e = 0; e < 8; ++e) {
-      const int kap = k0 + e;
-      float v = 0.f;
-      if (ik >= 0 && kap < a.K) {
-        const int aa = kap % a.rk, c = kap / a.rk;
-        if (a.p == 0) {
-          v = pass2 ? (float)__ldg(a.hk + ik * (a.rk * a.rk1) + aa + a.rk * c)
-                    : __ldg(a.zk + (ik * a.rk + aa) * a.rk1 + c);
-        } else {
-          const float* M = a.mid + (jl * a.rk1) * a.rs + c;
-          for (int b = 0; b < a.rk1; ++b) {
-            const float x = pass2 ? (float)__ldg(a.hk + ik * (a.rk * a.rk1) + aa + a.rk * b)
-                                  : __ldg(a.zk + (ik * a.rk + aa) * a.rk1 + b);
-            v = fmaf(x, __ldg(M + b * a.rs), v);
-          }
-        }
+  extern __shared__ float lsm[];
+  const int XS = a.rk * a.rk1, MS = a.rk1 * a.rs;
+  const int XP = XS | 1, MP = MS | 1;                       // odd strides
+  float* Xs = lsm;                                          // [128][XP]
+  float* Ms = lsm + TC_M * XP;                              // [128][MP]
+  const int tid = threadIdx.x;
+  for (int64_t rt = blockIdx.x; rt * TC_M < nrows_pad; rt += gridDim.x) {
+    // stage: threads 0-127 copy row r's X(i_k), threads 128-255 its Mid(j_L)
+    {
+      const int r = tid & (TC_M - 1);
+      const int64_t row = rt * TC_M + r;
+      int64_t ik = 0, jl = 0;
+      const bool ok = row < a.nrows;
+      if (ok) {
+        if (a.rowmode == 0) { ik = row / a.nL; jl = row - ik * a.nL; }
+        else { jl = row / a.Ik; ik = row - jl * a.Ik; }
       }
-      hh[e] = __float2half_rn(v);
-      ll[e] = __float2half_rn(v - __half2float(hh[e]));
+      if (tid < TC_M) {
+        float* xr = Xs + r * XP;
+        if (pass2) {
+          const double* hs = a.hk + ik * XS;
+          for (int aa = 0; aa < a.rk; ++aa)
+            for (int b = 0; b < a.rk1; ++b) xr[aa * a.rk1 + b] = ok ? (float)__ldg(hs + aa + a.rk * b) : 0.f;
+        } else {
+          const float* zs = a.zk + ik * XS;
+          for (int e = 0; e < XS; ++e) xr[e] = ok ? __ldg(zs + e) : 0.f;
+        }
+      } else if (a.p > 0) {
+        float* mr = Ms + r * MP;
+        const float* ms = a.mid + jl * MS;
+        for (int e = 0; e < MS; ++e) mr[e] = ok ? __ldg(ms + e) : 0.f;
+      }
     }
-    uint4 hv, lv;
-    hv.x = pack_half2(hh[0], hh[1]); hv.y = pack_half2(hh[2], hh[3]);
-    hv.z = pack_half2(hh[4], hh[5]); hv.w = pack_half2(hh[6], hh[7]);
-    lv.x = pack_half2(ll[0], ll[1]); lv.y = pack_half2(ll[2], ll[3]);
-    lv.z = pack_half2(ll[4], ll[5]); lv.w = pack_half2(ll[6], ll[7]);
-    *reinterpret_cast<uint4*>(dst + row * 2 * a.KP + k0) = hv;
-    *reinterpret_cast<uint4*>(dst + row * 2 * a.KP + a.KP + k0) = lv;
+    __syncthreads();
+    {
+      const int r = tid >> 1, hf = tid & 1;
+      const int64_t row = rt * TC_M + r;
+      const float* X = Xs + r * XP;
+      const float* M = Ms + r * MP;
+      const int kh = a.KP / 2;
+      for (int k0 = hf * kh; k0 < (hf + 1) * kh; k0 += 8) {
+        __half hh[8], ll[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const int kap = k0 + e;
+          float v = 0.f;
+          if (row < a.nrows && kap < a.K) {
+            const int aa = kap % a.rk, c = kap / a.rk;
+            if (a.p == 0) {
+              v = X[aa * a.rk1 + c];
+            } else {
+              for (int b = 0; b < a.rk1; ++b) v = fmaf(X[aa * a.rk1 + b], M[b * a.rs + c], v);
+            }
+          }
+          hh[e] = __float2half_rn(v);
+          ll[e] = __float2half_rn(v - __half2float(hh[e]));
+        }
+        uint4 hv, lv;
+        hv.x = pack_half2(hh[0], hh[1]); hv.y = pack_half2(hh[2], hh[3]);
+        hv.z = pack_half2(hh[4], hh[5]); hv.w = pack_half2(hh[6], hh[7]);
+        lv.x = pack_half2(ll[0], ll[1]); lv.y = pack_half2(ll[2], ll[3]);
+        lv.z = pack_half2(ll[4], ll[5]); lv.w = pack_half2(ll[6], ll[7]);
+        *reinterpret_cast<uint4*>(dst + row * 2 * a.KP + k0) = hv;
+        *reinterpret_cast<uint4*>(dst + row * 2 * a.KP + a.KP + k0) = lv;
+      }
+    }
+    __syncthreads();
   }
 }
 
@@ -437,13 +467,13 @@ __device__ __forceinline__ void load_a_to_tmem(const TcArgs& a, int64_t row, uin
 // (Eq. 9/15, P:152, 234 with S(j) = Mid(j_L) Rgt(j_R); p = 0: Mid = I).  grid (I_k, JC):
 // CTA (ik, jc) sums the jl chunk jc into dpart[jc][ik][R2].
 // ---------------------------------------------------------------------------------------
-constexpr int RD_ROWS = 32;   // jl rows staged per step
+constexpr int RD_ROWS = 64;   // jl rows staged per step
 __global__ void __launch_bounds__(256) tc_reduce_d_kernel(
     const float* __restrict__ contrib, const float* __restrict__ mid, int nsplit, int64_t nrows_pad, int64_t nL,
     int64_t Ik, int rowmode, int KP, int R2, int rk, int rs, int p, int64_t jl_chunk, double* __restrict__ dpart) {
   extern __shared__ float rsm[];
-  const int KPp = KP + 1, MS = (R2 / rk) * rs;               // Mid(jl) is r_{k+1} x r_s
-  float* Dt = rsm;                                           // [RD_ROWS][KP + 1]
+  const int KPp = KP + 4, MS = (R2 / rk) * rs;               // Mid(jl) is r_{k+1} x r_s
+  float* Dt = rsm;                                           // [RD_ROWS][KP + 4] (16-B rows)
   float* Mt = rsm + RD_ROWS * KPp;                           // [RD_ROWS][MS]
   __shared__ double acc[256];
   const int64_t ik = blockIdx.x, jc = blockIdx.y;
@@ -451,27 +481,31 @@ __global__ void __launch_bounds__(256) tc_reduce_d_kernel(
   const int G = max(1, (int)blockDim.x / R2);
   const int o = tid % R2, g = tid / R2;
   const int aa = o % rk, bq = o / rk;
+  const int q4 = KP / 4;                                     // float4 per D row
   const int64_t j0 = jc * jl_chunk, j1 = min(nL, j0 + jl_chunk);
   double s = 0.0;
   for (int64_t jb = j0; jb < j1; jb += RD_ROWS) {
     const int nr = (int)min((int64_t)RD_ROWS, j1 - jb);
-    if (p > 0) {
-      for (int idx = tid; idx < nr * MS; idx += blockDim.x) Mt[idx] = mid[jb * MS + idx];   // rows jb.. contiguous
+    if (p > 0) {                                             // Mid rows jb.. are contiguous
+      const float* src = mid + jb * MS;
+      for (int idx = tid; idx < nr * MS; idx += blockDim.x) Mt[idx] = __ldg(src + idx);
     }
     for (int sp = 0; sp < nsplit; ++sp) {
-      for (int idx = tid; idx < nr * KP; idx += blockDim.x) {
-        const int rr = idx / KP, kk = idx - rr * KP;
+      const float* base = contrib + (int64_t)sp * nrows_pad * KP;
+      for (int f = tid; f < nr * q4; f += blockDim.x) {
+        const int rr = f / q4, c4 = f - rr * q4;
         const int64_t jl = jb + rr;
         const int64_t row = rowmode == 0 ? jl + nL * ik : ik + Ik * jl;
-        Dt[rr * KPp + kk] = contrib[((int64_t)sp * nrows_pad + row) * KP + kk];
+        *reinterpret_cast<float4*>(Dt + rr * KPp + 4 * c4) =
+            __ldg(reinterpret_cast<const float4*>(base + row * KP) + c4);
       }
       __syncthreads();
       if (g < G) {
         float t = 0.f;
-        for (int rr = g; rr < nr; rr += G) {
-          if (p == 0) {
-            t += Dt[rr * KPp + o];
-          } else {
+        if (p == 0) {
+          for (int rr = g; rr < nr; rr += G) t += Dt[rr * KPp + o];
+        } else {
+          for (int rr = g; rr < nr; rr += G) {
             const float* M = Mt + rr * MS + bq * rs;
             const float* D = Dt + rr * KPp + aa;
             float u = 0.f;
@@ -536,7 +570,10 @@ void launch_tc_lft(Context& c, const BlockPlan& bp, bool pass2, cudaStream_t s) 
   a.hk = c.h;
   a.mid = c.mid;
   const int64_t pad = bp.n_row_tiles * TC_M;
-  tc_lft_pack_kernel<<<tc_grid(pad * (bp.KP / 8)), 256, 0, s>>>(a, pass2 ? 1 : 0, pad, pass2 ? c.lfthHL : c.lftHL);
+  const size_t smem = (size_t)TC_M * (((bp.rk * bp.rk1) | 1) + ((bp.rk1 * bp.rs) | 1)) * sizeof(float);
+  cudaFuncSetAttribute(tc_lft_pack_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const int grid = (int)std::min<int64_t>(bp.n_row_tiles, (int64_t)c.num_sm * 8);
+  tc_lft_pack_kernel<<<grid, 256, smem, s>>>(a, pass2 ? 1 : 0, pad, pass2 ? c.lfthHL : c.lftHL);
   c.launches++;
 }
 
@@ -647,7 +684,7 @@ void launch_tc_pass(Context& c, const BlockPlan& bp, const TcStage& st, bool pas
 void launch_tc_reduce_d(Context& c, const BlockPlan& bp, cudaStream_t s) {
   const int64_t Ik = bp.nrows / bp.nL;
   const int threads = bp.R2 * std::max(1, 256 / std::max(1, bp.R2));
-  const size_t smem = (size_t)RD_ROWS * ((bp.KP + 1) + (bp.R2 / bp.rk) * bp.rs) * sizeof(float);
+  const size_t smem = (size_t)RD_ROWS * ((bp.KP + 4) + (bp.R2 / bp.rk) * bp.rs) * sizeof(float);
   cudaFuncSetAttribute(tc_reduce_d_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   tc_reduce_d_kernel<<<dim3((unsigned)Ik, (unsigned)bp.tc_jc), threads, smem, s>>>(
       c.contrib, c.mid, bp.tc_nsplit, bp.n_row_tiles * TC_M, bp.nL, Ik, bp.rowmode, bp.KP, bp.R2, bp.rk,

@@ -8,5 +8,5 @@ CMD="python bench.py --config $CFG --steps 1 --warmup 3 --no-e2e --no-cpu-baseli
 timeout 600 $CMD > gpurun_out/${T}_plain.log 2>&1 || { echo plain failed; tail -20 gpurun_out/${T}_plain.log; exit 1; }
 tail -1 gpurun_out/${T}_plain.log | cut -c1-400
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${T}_launches.csv $CMD > gpurun_out/${T}_ncu_list.log 2>&1; echo list=$?
-timeout 900 ncu --set full --clock-control none --import-source on -k "regex:tc_pass|tc_reduce" -s 12 -c 4 -o gpurun_out/${T}_full $CMD > gpurun_out/${T}_ncu_full.log 2>&1; echo full=$?
+[ -n "$FULL" ] && { timeout 900 ncu --set full --clock-control none --import-source on -k "regex:$FULL" -s 12 -c 2 -o gpurun_out/${T}_full $CMD > gpurun_out/${T}_ncu_full.log 2>&1; echo full=$?; }
 python scripts/launch_share.py gpurun_out/${T}_launches.csv 2>&1 | head -40
