@@ -434,6 +434,12 @@ trd_status trd_init(const trd_config* cfg, const trd_shard* shard, const float* 
     if (cudaGetDevice(&dev) == cudaSuccess &&
         cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess && nsm > 0)
       c->num_sm = nsm;
+    // test knob: TRD_NUM_SM=n sizes the persistent grids for n SMs (n < SM count makes every
+    // CTA walk many work items; used by the parity tests of the item-boundary logic)
+    if (const char* e = getenv("TRD_NUM_SM")) {
+      const int v = atoi(e);
+      if (v > 0 && v < c->num_sm) c->num_sm = v;
+    }
   }
   c->shard_begin = sb;
   c->shard_end = se;

@@ -265,3 +265,72 @@ def test_stop_metric_matches_oracle():
     for t in (1, 2):
         assert abs(g[t]["stop_e"] - recs[t].stop_e) <= 1e-3 * recs[t].stop_e
     ctx.close()
+
+
+# ---------------------------------------------------------------- persistent-grid coverage
+MULTI_CASES = [
+    # C5-like order 5, rank 8 (KP = 64: two P buffers, double-buffered A), rho = 0.05: the
+    # staged entries of a tile fit the shared-memory sketch stage
+    ("C5b", [20, 18, 16, 12, 10], None, None),
+    # same shape at rho = 0.3: tiles overflow the stage, entries are read from global memory
+    ("C5b", [20, 18, 16, 12, 10], None, 0.3),
+    # rank 10 (KP = 112: single A buffer, shared P buffer), RStS sketch
+    ("C4", [24, 22, 20, 18], [12, 11, 10, 9], None),
+]
+
+
+@pytest.mark.parametrize("nsm", [None, 3, 1])
+@pytest.mark.parametrize("name,dims,sketch,rho", MULTI_CASES)
+def test_block_quantities_persistent_items(name, dims, sketch, rho, nsm, monkeypatch):
+    """The persistent pass kernels walk (row tile, column split) items; with TRD_NUM_SM = 3
+    or 1 every CTA crosses many item boundaries (A / D buffer rotation, ring phases).  The
+    block quantities must match the oracle at every grid size."""
+    _cuda()
+    if nsm is not None:
+        monkeypatch.setenv("TRD_NUM_SM", str(nsm))
+    over = {} if rho is None else {"observed": rho}
+    spec = small_spec(name, dims, sketch, **over)
+    prob = make_problem(spec)
+    src, _ = oracle_source(prob)
+    cfg = oracle_config(spec)
+    st = O.State(cfg, prob.init, src)
+    ctx = gpu_context(prob, packed=True)
+    for k in range(len(dims)):
+        g = ctx.block_probe(0, k)
+        sets = O.index_sets_for_block(cfg, 0, k)
+        Xk, Pk = O.working_set(src, k, sets)
+        S = O.subchain(st.cores, k, sets)
+        d, E, W = O.gradient_block(Xk, Pk, O.core_unfold2(st.cores[k]), S, st.sigma,
+                                   cfg.sigma_mode == O.SIGMA_INF)
+        G = O.gram_fgmc(st.Qs, k, spec.ranks)
+        h, _ = O.scaled_gradient(d, G, cfg.lambda_rel)
+        den = O.line_search_den(h, Pk, W, S)
+        assert g["n_obs"] == int(Pk.sum())
+        assert rel_fro(g["d"], d) <= 1e-4, (k, rel_fro(g["d"], d))
+        assert rel_fro(g["h"], h) <= 1e-4, k
+        assert abs(g["den"] - den) <= 1e-4 * abs(den), k
+    ctx.close()
+
+
+def test_persistent_grid_size_does_not_change_results(monkeypatch):
+    """Fixed-order reductions: the sweep result is bitwise independent of run-to-run timing
+    and equal (to rounding of the per-CTA partial order) across grid sizes."""
+    _cuda()
+    spec = small_spec("C5b", [24, 20, 16, 12, 10])
+    prob = make_problem(spec)
+    outs = []
+    for nsm in (None, 5):
+        if nsm is None:
+            monkeypatch.delenv("TRD_NUM_SM", raising=False)
+        else:
+            monkeypatch.setenv("TRD_NUM_SM", str(nsm))
+        runs = []
+        for _ in range(2):
+            ctx = gpu_context(prob, packed=True)
+            ctx.sweep(2, stats=False)
+            runs.append(ctx.get_cores())
+            ctx.close()
+        for a, b in zip(runs[0], runs[1]):
+            assert np.array_equal(a, b)                      # deterministic at a fixed grid
+        outs.append(runs[0])
+    assert cores_rel_err(outs[1], outs[0]) <= 1e-5
