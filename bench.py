@@ -346,6 +346,15 @@ def run_mine(args):
             "share_of_step": (prof["pass1_ms"] + prof["pass2_ms"]) / ms if ms > 0 else None,
             "pass1_ms_per_sweep": prof["pass1_ms"] / args.steps,
             "pass2_ms_per_sweep": prof["pass2_ms"] / args.steps}
+    # the same kernel seen as dense tensor-core work (what the tcgen05 pass kernels execute:
+    # 3-term fp16 split over every (row, column) of the working set, observed or not)
+    mma = prof.get(dom + "_mma_flops", 0.0) / n_l
+    if mma > 0:
+        pk = float(peaks.get("bf16_tflops", 1659.3))
+        ach = mma / (avg_ms / 1e3) / 1e12
+        roof["tensor_view"] = {"dense_mma_tflop_per_launch": mma / 1e12, "achieved": ach,
+                               "peak": pk, "unit": "TFLOP/s", "frac": ach / pk,
+                               "peak_source": f"{src} dense bf16 (fp16 kind::f16 runs at the bf16 rate)"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

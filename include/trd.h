@@ -181,6 +181,8 @@ typedef struct {
   double pass1_entries, pass2_entries;    /* observed entries processed (sum over launches) */
   double pass1_flops, pass2_flops;        /* algorithmic flops, SURVEY 8(d) per-entry count  */
   double pass1_bytes, pass2_bytes;        /* algorithmic bytes, SURVEY 8(d) per-entry count  */
+  double pass1_mma_flops, pass2_mma_flops;/* dense tensor-core flops the tcgen05 pass kernels
+                                             executed (3-term fp16 split, 128 x 64 tiles)     */
 } trd_profile;
 TRD_API trd_status trd_set_profiling(trd_ctx* ctx, int32_t enable);
 TRD_API trd_status trd_get_profile(trd_ctx* ctx, trd_profile* out);

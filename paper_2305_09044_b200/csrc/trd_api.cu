@@ -180,6 +180,7 @@ void build_plan(const Context& c, int k, const int64_t* s_in, BlockPlan& bp, boo
     bp.tc_nsplit = (int)best_s;
     bp.tc_per = best_per;
     bp.tc_grid = (int)std::min<int64_t>(nrt * best_s, (int64_t)c.num_sm);
+    bp.tc_grid1 = (int)std::max<int64_t>(1, std::min<int64_t>(nrt * best_s, (int64_t)c.num_sm - 1));
     const int64_t Ikk = c.dims[k];
     // d reduction: >= 8 CTAs per SM worth of (i_k, jl-chunk) blocks, chunks of >= 32 rows
     int64_t jc = (8 * (int64_t)c.num_sm + Ikk - 1) / Ikk;
@@ -230,6 +231,13 @@ int prof_event(Context* c) {
 // a1-a6 + a7 (pass 1 and the d/stat exchange) of block k
 trd_status block_pass1(Context* c, const BlockPlan& bp) {
   cudaStream_t s = c->stream;
+  // a8 + a9 (FGMC Gram, filtered operator M) depend only on the cores != k: run them on the
+  // side stream, overlapping the sampler / staging / pass 1 (which leaves one SM free)
+  CUDA_TRY(c, cudaEventRecord(c->ev_fork, s));
+  CUDA_TRY(c, cudaStreamWaitEvent(c->side, c->ev_fork, 0));
+  launch_gram(*c, bp, c->side);
+  launch_solve(*c, bp, c->side);
+  CUDA_TRY(c, cudaEventRecord(c->ev_join, c->side));
   launch_sampler(*c, bp, s);
   launch_plan(*c, bp, s);
   if (!bp.use_tc) launch_lft(*c, bp, c->Z + c->zoff[bp.k], 0, c->lft, s);
@@ -260,8 +268,7 @@ trd_status block_pass1(Context* c, const BlockPlan& bp) {
 // a8-a10 (FGMC, solve, scaled gradient, pass 2, den exchange)
 trd_status block_pass2(Context* c, const BlockPlan& bp) {
   cudaStream_t s = c->stream;
-  launch_gram(*c, bp, s);
-  launch_solve(*c, bp, s);
+  CUDA_TRY(c, cudaStreamWaitEvent(s, c->ev_join, 0));       // M of this block (side stream)
   launch_h(*c, bp, s);
   if (!bp.use_tc) launch_lft(*c, bp, nullptr, 1, c->lfth, s);
   else launch_tc_lft(*c, bp, true, s);
@@ -390,6 +397,15 @@ trd_status trd_get_profile(trd_ctx* ctx, trd_profile* out) {
     out->pass2_flops += n * (2.0 * R2 + 4.0);
     out->pass1_bytes += 8.0 * n + ws_bits;
     out->pass2_bytes += 4.0 * n + ws_bits;
+    const BlockPlan& bp = c->plan[k];
+    if (bp.use_tc) {
+      // per 128 x 64 tile: 3 split terms x 2 x 128 x 64 x KP flops per GEMM; pass 1 runs two
+      // GEMMs (S = A.B^T and D += P.B), pass 2 one
+      const double tile = 3.0 * 2.0 * 128.0 * 64.0 * (double)bp.KP;
+      const double tiles = (double)bp.n_row_tiles * (double)bp.n_col_tiles * per_block;
+      out->pass1_mma_flops += 2.0 * tile * tiles;
+      out->pass2_mma_flops += tile * tiles;
+    }
   }
   return TRD_OK;
 }
@@ -441,6 +457,13 @@ trd_status trd_init(const trd_config* cfg, const trd_shard* shard, const float* 
       if (v > 0 && v < c->num_sm) c->num_sm = v;
     }
   }
+  if (cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming) != cudaSuccess) {
+    trd_destroy(reinterpret_cast<trd_ctx*>(c));
+    return TRD_ERR_CUDA;
+  }
+
   c->shard_begin = sb;
   c->shard_end = se;
   c->packed = shard->packed ? 1 : 0;
@@ -823,6 +846,9 @@ void trd_destroy(trd_ctx* ctx) {
   if (c->stream) cudaStreamSynchronize(c->stream);
   if (c->nccl_comm && g_nccl.comm_destroy) g_nccl.comm_destroy(c->nccl_comm);
   for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
+  if (c->side) { cudaStreamSynchronize(c->side); cudaStreamDestroy(c->side); }
+  if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+  if (c->ev_join) cudaEventDestroy(c->ev_join);
   void* ptrs[] = {c->own_values, c->own_mask, c->rank_prefix, c->Z, c->Q, c->idx, c->doff,
                   c->row_off, c->col_off, c->mid, c->lft, c->lfth, c->rgtT, c->dpart, c->spart,
                   c->denpart, c->numpart, c->dvec, c->G, c->G_last, c->Mop, c->chol_ws,

@@ -71,7 +71,8 @@ struct BlockPlan {
   int64_t n_row_tiles, n_col_tiles;
   int tc_nsplit;         // column splits per row tile (work item = (row tile, split))
   int64_t tc_per;        // column tiles per split
-  int tc_grid;           // persistent CTAs of the pass kernels (<= SM count)
+  int tc_grid;           // persistent CTAs of pass 2 (<= SM count)
+  int tc_grid1;          // persistent CTAs of pass 1 (one SM left for the side-stream solve)
   int64_t tc_jc, tc_jl_chunk;   // d reduction: jl chunks
 };
 
@@ -100,6 +101,9 @@ struct Context {
   int64_t n_local, n_words;
   int packed;
   cudaStream_t stream;
+  cudaStream_t side = nullptr;         // FGMC Gram + filtered solve of a block (a8, a9) run here,
+                                       // concurrently with pass 1 (they need only cores != k)
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   int num_sm = 148;                    // SMs of the current device (persistent grids)
   std::string err;
   trd_status sticky = TRD_OK;

@@ -719,45 +719,60 @@ solve_kernel(const double* __restrict__ G, int n, double lambda_rel, double* __r
 // Small-n path of a9 (R_k^2 <= kGjMaxN): the same filtered operator M = A^-1 G A^-1 with
 // A = G + lambda I (R5), A^-1 by in-place Gauss-Jordan elimination (A is SPD, so
 // no pivoting; a non-positive pivot means "not SPD" and triggers the lambda x10 retry like a
-// failed Cholesky), then two small GEMMs.  One CTA, everything in shared memory; 2n
-// barriers instead of the O(n) sequential triangular solves of solve_kernel.
-constexpr int kGjMaxN = 112;
+// failed Cholesky), then two small GEMMs.  One CTA of 32 x 32 threads; thread (ty, tx) keeps
+// the elements (ty + 32 a, tx + 32 b), a, b < NB = ceil(n / 32), in registers.  Per pivot
+// step the owners of row / column k+1 publish them to a double-buffered shared array, so one
+// barrier separates consecutive steps.
+constexpr int kGjMaxN = 112;          // 2 n^2 doubles of dynamic smem must fit 227 KB
+template <int NB>
 __global__ void __launch_bounds__(1024) gj_solve_kernel(const double* __restrict__ G, int n, double lambda_rel,
                                                         double* __restrict__ Mout, DevScalars* __restrict__ sc) {
   extern __shared__ double gsm[];
-  double* A = gsm;                 // n x n, becomes A^-1
-  double* Gs = gsm + n * n;        // n x n copy of G, then T = G A^-1
-  double* rowk = Gs + n * n;       // n
-  double* colk = rowk + n;         // n
+  double* Ainv = gsm;              // n x n
+  double* Tm = gsm + n * n;        // n x n
+  __shared__ double rk_s[2][kGjMaxN], ck_s[2][kGjMaxN];
   __shared__ int fail_s;
   __shared__ double tr_s;
-  const int nn = n * n;
-  for (int t = threadIdx.x; t < nn; t += blockDim.x) Gs[t] = G[t];
-  __syncthreads();
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  double a[NB][NB];
   if (threadIdx.x == 0) {
     double tr = 0.0;
-    for (int i = 0; i < n; ++i) tr += Gs[i * n + i];
+    for (int i = 0; i < n; ++i) tr += G[i * n + i];
     tr_s = tr;
   }
   __syncthreads();
   double lam = lambda_rel * tr_s / n;
   for (int attempt = 0;; ++attempt) {
-    for (int t = threadIdx.x; t < nn; t += blockDim.x) A[t] = Gs[t] + ((t / n == t % n) ? lam : 0.0);
+#pragma unroll
+    for (int u = 0; u < NB; ++u)
+#pragma unroll
+      for (int v = 0; v < NB; ++v) {
+        const int i = ty + 32 * u, j = tx + 32 * v;
+        a[u][v] = (i < n && j < n) ? G[i * n + j] + (i == j ? lam : 0.0) : 0.0;
+        if (i == 0 && j < n) rk_s[0][j] = a[u][v];
+        if (j == 0 && i < n) ck_s[0][i] = a[u][v];
+      }
     if (threadIdx.x == 0) fail_s = 0;
     __syncthreads();
     for (int k = 0; k < n; ++k) {
-      const double p = A[k * n + k];
-      if (!(p > 0.0)) { if (threadIdx.x == 0) fail_s = 1; break; }   // uniform: all threads read p
+      const int b = k & 1;
+      const double p = rk_s[b][k];
+      if (!(p > 0.0)) { if (threadIdx.x == 0) fail_s = 1; break; }     // uniform
       const double ip = 1.0 / p;
-      for (int t = threadIdx.x; t < n; t += blockDim.x) {
-        rowk[t] = (t == k) ? ip : A[k * n + t] * ip;     // new row k
-        colk[t] = (t == k) ? 0.0 : A[t * n + k];         // old column k (pivot excluded)
-      }
-      __syncthreads();
-      for (int t = threadIdx.x; t < nn; t += blockDim.x) {
-        const int i = t / n, j = t - i * n;
-        const double ci = colk[i], rj = rowk[j];
-        A[t] = (i == k) ? rj : ((j == k) ? -ci * ip : fma(-ci, rj, A[t]));
+#pragma unroll
+      for (int u = 0; u < NB; ++u) {
+        const int i = ty + 32 * u;
+        const double ci = (i < n) ? ck_s[b][i] : 0.0;
+#pragma unroll
+        for (int v = 0; v < NB; ++v) {
+          const int j = tx + 32 * v;
+          if (i >= n || j >= n) continue;
+          const double rj = (j == k) ? ip : rk_s[b][j] * ip;         // new row k
+          const double val = (i == k) ? rj : ((j == k) ? -ci * ip : fma(-ci, rj, a[u][v]));
+          a[u][v] = val;
+          if (i == k + 1) rk_s[b ^ 1][j] = val;
+          if (j == k + 1) ck_s[b ^ 1][i] = val;
+        }
       }
       __syncthreads();
     }
@@ -768,29 +783,39 @@ __global__ void __launch_bounds__(1024) gj_solve_kernel(const double* __restrict
   }
   if (fail_s) {
     if (threadIdx.x == 0) { sc->not_spd = 1; sc->lambda = lam; }
-    for (int t = threadIdx.x; t < nn; t += blockDim.x) Mout[t] = 0.0;
+    for (int t = threadIdx.x; t < n * n; t += blockDim.x) Mout[t] = 0.0;
     return;
   }
-  // T = G A^-1 (into Gs, row by row needs a copy: compute into registers first)
-  double acc[(kGjMaxN * kGjMaxN + 1023) / 1024];
-  int q = 0;
-  for (int t = threadIdx.x; t < nn; t += blockDim.x, ++q) {
-    const int i = t / n, j = t - (t / n) * n;
-    double v = 0.0;
-    for (int l = 0; l < n; ++l) v = fma(Gs[i * n + l], A[l * n + j], v);
-    acc[q] = v;
-  }
+#pragma unroll
+  for (int u = 0; u < NB; ++u)
+#pragma unroll
+    for (int v = 0; v < NB; ++v) {
+      const int i = ty + 32 * u, j = tx + 32 * v;
+      if (i < n && j < n) Ainv[i * n + j] = a[u][v];
+    }
   __syncthreads();
-  q = 0;
-  for (int t = threadIdx.x; t < nn; t += blockDim.x, ++q) Gs[t] = acc[q];
+  // T = G A^-1 (G from global / L1), then M = A^-1 T
+#pragma unroll
+  for (int u = 0; u < NB; ++u)
+#pragma unroll
+    for (int v = 0; v < NB; ++v) {
+      const int i = ty + 32 * u, j = tx + 32 * v;
+      if (i >= n || j >= n) continue;
+      double acc = 0.0;
+      for (int l = 0; l < n; ++l) acc = fma(__ldg(G + i * n + l), Ainv[l * n + j], acc);
+      Tm[i * n + j] = acc;
+    }
   __syncthreads();
-  // M = A^-1 T
-  for (int t = threadIdx.x; t < nn; t += blockDim.x) {
-    const int i = t / n, j = t - (t / n) * n;
-    double v = 0.0;
-    for (int l = 0; l < n; ++l) v = fma(A[i * n + l], Gs[l * n + j], v);
-    Mout[t] = v;
-  }
+#pragma unroll
+  for (int u = 0; u < NB; ++u)
+#pragma unroll
+    for (int v = 0; v < NB; ++v) {
+      const int i = ty + 32 * u, j = tx + 32 * v;
+      if (i >= n || j >= n) continue;
+      double acc = 0.0;
+      for (int l = 0; l < n; ++l) acc = fma(Ainv[i * n + l], Tm[l * n + j], acc);
+      Mout[i * n + j] = acc;
+    }
   if (threadIdx.x == 0) sc->lambda = lam;
 }
 
@@ -1172,14 +1197,21 @@ void launch_gram(Context& c, const BlockPlan& bp, cudaStream_t s) {
 void launch_solve(Context& c, const BlockPlan& bp, cudaStream_t s) {
   const int n = bp.R2;
   if (n <= kGjMaxN) {
-    const size_t gneed = ((size_t)2 * n * n + 2 * n) * sizeof(double);
+    const size_t gneed = (size_t)2 * n * n * sizeof(double);
     static bool gj_attr = false;
+    const int maxs = (int)((size_t)2 * kGjMaxN * kGjMaxN * sizeof(double));
     if (!gj_attr) {
-      cudaFuncSetAttribute(gj_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)(((size_t)2 * kGjMaxN * kGjMaxN + 2 * kGjMaxN) * sizeof(double)));
+      cudaFuncSetAttribute(gj_solve_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxs);
+      cudaFuncSetAttribute(gj_solve_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxs);
+      cudaFuncSetAttribute(gj_solve_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxs);
+      cudaFuncSetAttribute(gj_solve_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxs);
       gj_attr = true;
     }
-    gj_solve_kernel<<<1, 1024, gneed, s>>>(c.G, n, c.cfg.lambda_rel, c.Mop, c.sc);
+    const int nb = (n + 31) / 32;
+    if (nb == 1) gj_solve_kernel<1><<<1, 1024, gneed, s>>>(c.G, n, c.cfg.lambda_rel, c.Mop, c.sc);
+    else if (nb == 2) gj_solve_kernel<2><<<1, 1024, gneed, s>>>(c.G, n, c.cfg.lambda_rel, c.Mop, c.sc);
+    else if (nb == 3) gj_solve_kernel<3><<<1, 1024, gneed, s>>>(c.G, n, c.cfg.lambda_rel, c.Mop, c.sc);
+    else gj_solve_kernel<4><<<1, 1024, gneed, s>>>(c.G, n, c.cfg.lambda_rel, c.Mop, c.sc);
     c.launches++;
     return;
   }

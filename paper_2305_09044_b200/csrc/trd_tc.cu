@@ -252,6 +252,71 @@ __global__ void __launch_bounds__(256) tc_lft_pack_kernel(LftArgs a, int pass2, 
   }
 }
 
+// Register-blocked variant for compile-time ranks (RK = r_k, RK1 = r_{k+1}, RS = r_s, p > 0):
+// one thread per row holds X(i_k) (RK x RK1) and Mid(j_L) (RK1 x RS) and produces the whole
+// row, Lft[a + RK c] = sum_b X[a][b] Mid[b][c] (fmaf over b ascending, as lft_kernel).
+template <int RK, int RK1, int RS>
+__global__ void __launch_bounds__(128) tc_lft_pack_rb_kernel(LftArgs a, int pass2, int64_t nrows_pad,
+                                                             __half* __restrict__ dst) {
+  constexpr int K = RK * RS;
+  constexpr int KP = (K + 15) / 16 * 16;
+  for (int64_t row = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; row < nrows_pad;
+       row += (int64_t)gridDim.x * blockDim.x) {
+    float out[KP];
+#pragma unroll
+    for (int q = 0; q < KP; ++q) out[q] = 0.f;
+    if (row < a.nrows) {
+      int64_t ik, jl;
+      if (a.rowmode == 0) { ik = row / a.nL; jl = row - ik * a.nL; }
+      else { jl = row / a.Ik; ik = row - jl * a.Ik; }
+      float X[RK][RK1], M[RK1][RS];
+      if (pass2) {
+        const double* hs = a.hk + ik * (RK * RK1);
+#pragma unroll
+        for (int aa = 0; aa < RK; ++aa)
+#pragma unroll
+          for (int b = 0; b < RK1; ++b) X[aa][b] = (float)__ldg(hs + aa + RK * b);
+      } else {
+        const float* zs = a.zk + ik * (RK * RK1);
+#pragma unroll
+        for (int aa = 0; aa < RK; ++aa)
+#pragma unroll
+          for (int b = 0; b < RK1; ++b) X[aa][b] = __ldg(zs + aa * RK1 + b);
+      }
+      const float* ms = a.mid + jl * (RK1 * RS);
+#pragma unroll
+      for (int b = 0; b < RK1; ++b)
+#pragma unroll
+        for (int c = 0; c < RS; ++c) M[b][c] = __ldg(ms + b * RS + c);
+#pragma unroll
+      for (int aa = 0; aa < RK; ++aa)
+#pragma unroll
+        for (int c = 0; c < RS; ++c) {
+          float v = 0.f;
+#pragma unroll
+          for (int b = 0; b < RK1; ++b) v = fmaf(X[aa][b], M[b][c], v);
+          out[aa + RK * c] = v;
+        }
+    }
+#pragma unroll
+    for (int k0 = 0; k0 < KP; k0 += 8) {
+      __half hh[8], ll[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        hh[e] = __float2half_rn(out[k0 + e]);
+        ll[e] = __float2half_rn(out[k0 + e] - __half2float(hh[e]));
+      }
+      uint4 hv, lv;
+      hv.x = pack_half2(hh[0], hh[1]); hv.y = pack_half2(hh[2], hh[3]);
+      hv.z = pack_half2(hh[4], hh[5]); hv.w = pack_half2(hh[6], hh[7]);
+      lv.x = pack_half2(ll[0], ll[1]); lv.y = pack_half2(ll[2], ll[3]);
+      lv.z = pack_half2(ll[4], ll[5]); lv.w = pack_half2(ll[6], ll[7]);
+      *reinterpret_cast<uint4*>(dst + row * 2 * KP + k0) = hv;
+      *reinterpret_cast<uint4*>(dst + row * 2 * KP + KP + k0) = lv;
+    }
+  }
+}
+
 __device__ __forceinline__ int64_t cm_offset(int r, int kap, int HK) {
   return ((int64_t)((r >> 3) * HK + (kap >> 3)) * 8 + (r & 7)) * 8 + (kap & 7);
 }
@@ -570,6 +635,12 @@ void launch_tc_lft(Context& c, const BlockPlan& bp, bool pass2, cudaStream_t s) 
   a.hk = c.h;
   a.mid = c.mid;
   const int64_t pad = bp.n_row_tiles * TC_M;
+  if (bp.p > 0 && bp.rk == 8 && bp.rk1 == 8 && bp.rs == 8) {
+    const int grid = (int)std::min<int64_t>((pad + 127) / 128, (int64_t)c.num_sm * 16);
+    tc_lft_pack_rb_kernel<8, 8, 8><<<grid, 128, 0, s>>>(a, pass2 ? 1 : 0, pad, pass2 ? c.lfthHL : c.lftHL);
+    c.launches++;
+    return;
+  }
   const size_t smem = (size_t)TC_M * (((bp.rk * bp.rk1) | 1) + ((bp.rk1 * bp.rs) | 1)) * sizeof(float);
   cudaFuncSetAttribute(tc_lft_pack_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int grid = (int)std::min<int64_t>(bp.n_row_tiles, (int64_t)c.num_sm * 8);
@@ -631,7 +702,7 @@ static TcArgs make_tc_args(const Context& c, const BlockPlan& bp, const TcStage&
 template <int KP>
 static void launch_tc_pass_t(Context& c, const BlockPlan& bp, const TcStage& st, bool pass2, cudaStream_t s) {
   TcArgs a = make_tc_args(c, bp, st, pass2);
-  const dim3 grid((unsigned)bp.tc_grid);
+  const dim3 grid((unsigned)(pass2 ? bp.tc_grid : bp.tc_grid1));
   if (!pass2) {
     const int sm = Ws1<KP>::SMEM;
     cudaFuncSetAttribute(tc_pass1_kernel<KP>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
@@ -689,7 +760,7 @@ void launch_tc_reduce_d(Context& c, const BlockPlan& bp, cudaStream_t s) {
   tc_reduce_d_kernel<<<dim3((unsigned)Ik, (unsigned)bp.tc_jc), threads, smem, s>>>(
       c.contrib, c.mid, bp.tc_nsplit, bp.n_row_tiles * TC_M, bp.nL, Ik, bp.rowmode, bp.KP, bp.R2, bp.rk,
       bp.rs, bp.p, bp.tc_jl_chunk, c.dpart);
-  tc_reduce_final_kernel<<<(unsigned)(Ik + 1), 128, 0, s>>>(c.dpart, bp.tc_jc, Ik, bp.R2, c.spart, bp.tc_grid,
+  tc_reduce_final_kernel<<<(unsigned)(Ik + 1), 128, 0, s>>>(c.dpart, bp.tc_jc, Ik, bp.R2, c.spart, bp.tc_grid1,
                                                             c.dvec, c.sc, bp.k);
   c.launches += 2;
 }

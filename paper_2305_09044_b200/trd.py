@@ -80,7 +80,8 @@ class trd_profile(ctypes.Structure):
                 ("pass1_launches", ctypes.c_int64), ("pass2_launches", ctypes.c_int64),
                 ("pass1_entries", ctypes.c_double), ("pass2_entries", ctypes.c_double),
                 ("pass1_flops", ctypes.c_double), ("pass2_flops", ctypes.c_double),
-                ("pass1_bytes", ctypes.c_double), ("pass2_bytes", ctypes.c_double)]
+                ("pass1_bytes", ctypes.c_double), ("pass2_bytes", ctypes.c_double),
+                ("pass1_mma_flops", ctypes.c_double), ("pass2_mma_flops", ctypes.c_double)]
 
 
 _lib = None
