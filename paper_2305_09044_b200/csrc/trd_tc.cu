@@ -373,16 +373,22 @@ __global__ void __launch_bounds__(128) stage_bits_kernel(StageArgs s) {
     const int64_t row = rt * TC_M + tid;
     const int64_t ro = row < s.nrows ? s.row_off[row] : -1;
     uint64_t bits = 0;
-    int64_t cwi = -1;
-    uint32_t cw = 0;
     if (ro >= 0) {
-      for (int j = 0; j < TC_NT; ++j) {
-        const int64_t co = sco[j];
-        if (co < 0) continue;
-        const int64_t lin = ro + co;
-        const int64_t wi = lin >> 5;
-        if (wi != cwi) { cw = __ldg(s.mask + wi); cwi = wi; }
-        if ((cw >> (lin & 31)) & 1u) bits |= 1ull << j;
+      // 8 independent mask-word loads in flight per step (L1 serves the words shared by
+      // neighbouring rows / columns)
+#pragma unroll 1
+      for (int j0 = 0; j0 < TC_NT; j0 += 8) {
+        uint32_t w[8];
+        int sh[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int64_t co = sco[j0 + u];
+          const int64_t lin = ro + (co < 0 ? 0 : co);
+          w[u] = co < 0 ? 0u : __ldg(s.mask + (lin >> 5));
+          sh[u] = (int)(lin & 31);
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) bits |= (uint64_t)((w[u] >> sh[u]) & 1u) << (j0 + u);
       }
     }
     const int cnt = __popcll(bits);
