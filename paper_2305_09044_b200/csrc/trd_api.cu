@@ -556,7 +556,8 @@ trd_status trd_init(const trd_config* cfg, const trd_shard* shard, const float* 
     return bail(st);
   if (max_lhl > 0) {
     if ((st = dalloc(c, &c->lftHL, max_lhl)) || (st = dalloc(c, &c->lfthHL, max_lhl)) ||
-        (st = dalloc(c, &c->rgtHL, max_rhl)) || (st = dalloc(c, &c->contrib, max_contrib)))
+        (st = dalloc(c, &c->rgtHL, max_rhl)) || (st = dalloc(c, &c->rgtHL2, max_rhl)) ||
+        (st = dalloc(c, &c->contrib, max_contrib)))
       return bail(st);
   }
   if ((st = ensure_stats(c, 4))) return bail(st);
@@ -853,7 +854,7 @@ void trd_destroy(trd_ctx* ctx) {
                   c->row_off, c->col_off, c->mid, c->lft, c->lfth, c->rgtT, c->dpart, c->spart,
                   c->denpart, c->numpart, c->dvec, c->G, c->G_last, c->Mop, c->chol_ws,
                   c->chain_ws, c->h, c->Dcur, c->Dprev, c->sc, c->stats, c->red_ws,
-                  c->lftHL, c->lfthHL, c->rgtHL, c->contrib};
+                  c->lftHL, c->lfthHL, c->rgtHL, c->rgtHL2, c->contrib};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->tw) cudaFree(c->tw);

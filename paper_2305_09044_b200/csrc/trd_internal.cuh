@@ -139,7 +139,8 @@ struct Context {
   int want_tc = 1;                     // TRD_PASS=simt disables the tcgen05 pass kernels
   __half* lftHL = nullptr;             // [row][hi KP | lo KP] (A operand, loaded into TMEM)
   __half* lfthHL = nullptr;            // same for the scaled gradient (pass 2)
-  __half* rgtHL = nullptr;             // [col tile][hi | lo][64 x KP] core-matrix layout
+  __half* rgtHL = nullptr;             // [col tile][hi | lo][64 x KP] core-matrix layout (L1)
+  __half* rgtHL2 = nullptr;            // same tiles, layout L2 ([hi KP | lo KP] per column)
   float* contrib = nullptr;            // [split][row][KP] D rows of pass 1
   float* tw = nullptr;                 // staged HQ weights of the current block (pass 1 -> 2)
   TcStage stage[kMaxN];

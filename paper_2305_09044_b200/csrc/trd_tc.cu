@@ -68,12 +68,37 @@ __device__ __forceinline__ void mbar_wait_spin(uint64_t* bar, uint32_t phase) {
 }
 // try_wait with an explicit suspend-time hint (ns): the thread sleeps until the phase
 // completes or the hint elapses, instead of re-polling (keeps issue slots free for the MMA warp)
+// Build with -DTRD_DEBUG_HANG=1 and run with TRD_DEBUG_HANG=1: a wait that spins for ~4 s
+// reports its barrier (smem offset, parity, thread) -- debugging aid for the pipeline barriers
+#ifndef TRD_DEBUG_HANG
+#define TRD_DEBUG_HANG 0
+#endif
+__device__ int g_debug_hang;
+__device__ int g_prog[160][24];     // per (block, warp): 1000 * tile + stage code
+__device__ __noinline__ void mbar_hang_report(uint32_t addr, uint32_t phase) {
+  printf("[trd hang] block %d thread %d waits on mbarrier smem+%u parity %u\n", blockIdx.x, threadIdx.x,
+         addr & 0xFFFFFu, phase);
+  if ((threadIdx.x & 31) == 0 && blockIdx.x < 160)
+    printf("[trd prog] block %d warps 4-15: %d %d %d %d | %d %d %d %d | %d %d %d %d\n", blockIdx.x,
+           g_prog[blockIdx.x][4], g_prog[blockIdx.x][5], g_prog[blockIdx.x][6], g_prog[blockIdx.x][7],
+           g_prog[blockIdx.x][8], g_prog[blockIdx.x][9], g_prog[blockIdx.x][10], g_prog[blockIdx.x][11],
+           g_prog[blockIdx.x][12], g_prog[blockIdx.x][13], g_prog[blockIdx.x][14], g_prog[blockIdx.x][15]);
+}
 __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t phase) {
   const uint32_t addr = smem_u32(bar);
   uint32_t ok = 0;
+  uint32_t spins = 0;
+  long long t0 = 0;
   do {
     asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
                  "selp.u32 %0, 1, 0, p;\n\t}" : "=r"(ok) : "r"(addr), "r"(phase), "r"(1000000u) : "memory");
+#if TRD_DEBUG_HANG
+    if (!ok && g_debug_hang && (++spins & 255u) == 0u) {
+      const long long now = clock64();
+      if (spins == 256u) t0 = now;
+      else if (now - t0 > (1ll << 33)) { mbar_hang_report(addr, phase); t0 = now + (1ll << 40); }
+    }
+#endif
   } while (!ok);
 }
 #ifndef TRD_MBAR_SPIN
@@ -85,6 +110,8 @@ __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t phase) {
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
   const uint32_t addr = smem_u32(bar);
   uint32_t ok = 0;
+  uint32_t spins = 0;
+  long long t0 = 0;
   do {
 #if TRD_MBAR_SPIN
     asm volatile("{\n\t.reg .pred p;\n\tmbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
@@ -92,6 +119,13 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
 #else
     asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
                  "selp.u32 %0, 1, 0, p;\n\t}" : "=r"(ok) : "r"(addr), "r"(phase) : "memory");
+#endif
+#if TRD_DEBUG_HANG
+    if (!ok && g_debug_hang && (++spins & 4095u) == 0u) {
+      const long long now = clock64();
+      if (spins == 4096u) t0 = now;
+      else if (now - t0 > (1ll << 33)) { mbar_hang_report(addr, phase); t0 = now + (1ll << 40); }
+    }
 #endif
   } while (!ok);
 }
@@ -323,7 +357,7 @@ __device__ __forceinline__ int64_t cm_offset(int r, int kap, int HK) {
 
 // B (Rgt) core-matrix tiles: [col tile][hi | lo][64 x KP]
 __global__ void tc_pack_cols_kernel(const float* __restrict__ rgtT, int64_t ncols, int K, int KP,
-                                    int64_t ntiles, __half* __restrict__ dst) {
+                                    int64_t ntiles, __half* __restrict__ dst, __half* __restrict__ dst2) {
   const int HK = KP / 8;
   const int64_t tot = ntiles * TC_NT * KP;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tot;
@@ -338,6 +372,10 @@ __global__ void tc_pack_cols_kernel(const float* __restrict__ rgtT, int64_t ncol
     __half* base = dst + tile * (2LL * TC_NT * KP);
     base[off] = hi;
     base[(int64_t)TC_NT * KP + off] = lo;
+    // layout L2: K = 2 KP per column ([hi KP | lo KP]), core matrix (g, h') at (g * 2HK + h')
+    __half* base2 = dst2 + tile * (2LL * TC_NT * KP);
+    base2[cm_offset((int)(col % TC_NT), kap, 2 * HK)] = hi;
+    base2[cm_offset((int)(col % TC_NT), KP + kap, 2 * HK)] = lo;
   }
 }
 
@@ -465,7 +503,7 @@ struct TcArgs {
   const float* zk;         // core k, slice-major Z_k[i][a][b] (pass-1 A operand)
   const double* hk;        // scaled gradient h[i][a + r_k b] (pass-2 A operand)
   const float* mid;        // Mid(j_L): [jl][r_{k+1}][r_s]
-  const __half* rgtHL;
+  const __half* rgtHL;     // B tiles, layout L1 (pass 2) or L2 (pass 1)
   const uint64_t* tbits;
   const uint16_t* troff;
   const uint64_t* tbase;
@@ -487,7 +525,9 @@ struct TcLayout {
   static constexpr int B_HALVES = 2 * TC_NT * KP;    // hi block then lo block
   static constexpr uint32_t B_LO_BYTES = TC_NT * KP * 2;
   static constexpr uint32_t IDESC_S = make_idesc(TC_M, TC_NT, 0);   // S = A . B^T
+  static constexpr uint32_t IDESC_S2 = make_idesc(TC_M, 2 * TC_NT, 0);  // S' = A_hi [B_hi ; B_lo]^T
   static constexpr uint32_t IDESC_D = make_idesc(TC_M, KP, 1);      // D += P . B (B MN-major)
+  static constexpr uint32_t IDESC_D2 = make_idesc(TC_M, 2 * KP, 1); // D' += P_hi [B_hi | B_lo]
 };
 
 // S[tmem] = A_hi.B_hi + A_hi.B_lo + A_lo.B_hi with A in TMEM (hi at acol, lo at acol + KP/2)
@@ -506,6 +546,44 @@ __device__ __forceinline__ void issue_split_gemm_ts(uint32_t dtmem, uint32_t aco
   }
 }
 
+// Merged split terms, layout L1 ([hi block | lo block] per 64-column tile; the lo block sits
+// 8 row groups after the hi block, so one N = 128 MMA covers rows hi 0..63, lo 0..63):
+//   S'[:, 0:64]   = A_hi.B_hi^T + A_lo.B_hi^T
+//   S'[:, 64:128] = A_hi.B_lo^T                     (S = S'[:, 0:64] + S'[:, 64:128])
+// 4 N = 128 + 4 N = 64 MMAs (KP = 64) instead of 12 N = 64 ones.
+template <int KP>
+__device__ __forceinline__ void issue_split_gemm_ts_merged(uint32_t dtmem, uint32_t acol, uint32_t bH) {
+  using L = TcLayout<KP>;
+  const uint64_t d0 = make_sdesc(bH, 128, L::HK * 128);
+#pragma unroll
+  for (int ks = 0; ks < KP / 16; ++ks)
+    mma_ts(dtmem, acol + ks * 8, d0 + (uint64_t)(ks * 16), L::IDESC_S2, ks ? 1u : 0u);
+#pragma unroll
+  for (int ks = 0; ks < KP / 16; ++ks)
+    mma_ts(dtmem, acol + KP / 2 + ks * 8, d0 + (uint64_t)(ks * 16), L::IDESC_S, 1u);
+}
+
+// Layout L2 (pass 1): per 64-column tile, each column's row of 2 KP halves is [hi KP | lo KP];
+// core matrix (g, h') at (g * 2HK + h') * 128 B, h' < HK hi, h' >= HK lo.  GEMM1 reads it
+// K-major with the three split terms (lo = +HK core matrices); GEMM2 reads it MN-major with
+// N = 2 KP for the P_hi terms (D' = P_hi [B_hi | B_lo]) and N = KP for P_lo.B_hi.
+template <int KP>
+__device__ __forceinline__ void issue_split_gemm_ts_l2(uint32_t dtmem, uint32_t acol, uint32_t bH) {
+  using L = TcLayout<KP>;
+  const uint64_t d0 = make_sdesc(bH, 128, 2 * L::HK * 128);
+#pragma unroll
+  for (int term = 0; term < 3; ++term) {
+    const uint32_t aa = acol + (term == 2 ? KP / 2 : 0);
+    const uint64_t dt = d0 + (uint64_t)((term == 1 ? L::HK * 128 : 0) >> 4);
+#pragma unroll
+    for (int ks = 0; ks < KP / 16; ++ks)
+      mma_ts(dtmem, aa + ks * 8, dt + (uint64_t)(ks * 16), L::IDESC_S, (term | ks) ? 1u : 0u);
+  }
+}
+
+#ifndef TRD_P1_MERGE
+#define TRD_P1_MERGE 0
+#endif
 // one lane of a converged warp (the MMA issuer runs warp-wide so that its operands live in
 // uniform registers; only the elected lane issues)
 __device__ __forceinline__ uint32_t elect_one() {
@@ -656,7 +734,7 @@ void launch_tc_lft(Context& c, const BlockPlan& bp, bool pass2, cudaStream_t s) 
 
 void launch_tc_pack_cols(Context& c, const BlockPlan& bp, cudaStream_t s) {
   tc_pack_cols_kernel<<<tc_grid(bp.n_col_tiles * TC_NT * bp.KP), 256, 0, s>>>(c.rgtT, bp.ncols, bp.K, bp.KP,
-                                                                                bp.n_col_tiles, c.rgtHL);
+                                                                                bp.n_col_tiles, c.rgtHL, c.rgtHL2);
   c.launches++;
 }
 
@@ -695,7 +773,7 @@ static TcArgs make_tc_args(const Context& c, const BlockPlan& bp, const TcStage&
   a.zk = c.Z + c.zoff[bp.k];
   a.hk = c.h;
   a.mid = c.mid;
-  a.rgtHL = c.rgtHL;
+  a.rgtHL = (pass2 || !TRD_P1_MERGE) ? c.rgtHL : c.rgtHL2;
   a.tbits = st.tbits; a.troff = st.troff; a.tbase = st.tbase; a.tvals = st.tvals; a.tidx = st.tidx;
   a.tw = c.tw;
   a.sc = c.sc;
@@ -707,6 +785,12 @@ static TcArgs make_tc_args(const Context& c, const BlockPlan& bp, const TcStage&
 
 template <int KP>
 static void launch_tc_pass_t(Context& c, const BlockPlan& bp, const TcStage& st, bool pass2, cudaStream_t s) {
+  static bool hang_flag_set = false;
+  if (!hang_flag_set) {
+    const int on = getenv("TRD_DEBUG_HANG") ? 1 : 0;
+    cudaMemcpyToSymbol(g_debug_hang, &on, sizeof(int));
+    hang_flag_set = true;
+  }
   TcArgs a = make_tc_args(c, bp, st, pass2);
   const dim3 grid((unsigned)(pass2 ? bp.tc_grid : bp.tc_grid1));
   if (!pass2) {
@@ -719,6 +803,11 @@ static void launch_tc_pass_t(Context& c, const BlockPlan& bp, const TcStage& st,
     tc_pass2_kernel<KP><<<grid, WsWarps<Ws2<KP>::NE>::THREADS, sm, s>>>(a);
   }
   c.launches++;
+  if (getenv("TRD_DEBUG_SYNC")) {            // debugging aid: serialise and report each pass launch
+    const cudaError_t e = cudaStreamSynchronize(s);
+    fprintf(stderr, "[trd debug] block %d pass %d KP %d grid %u items %lld per %lld: %s\n", bp.k, pass2 ? 2 : 1, KP,
+            grid.x, (long long)a.n_items, (long long)a.per, cudaGetErrorString(e));
+  }
 }
 
 void tc_debug_dump() {
