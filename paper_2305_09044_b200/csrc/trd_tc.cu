@@ -294,8 +294,10 @@ __global__ void __launch_bounds__(128) tc_lft_pack_rb_kernel(LftArgs a, int pass
                                                              __half* __restrict__ dst) {
   constexpr int K = RK * RS;
   constexpr int KP = (K + 15) / 16 * 16;
-  for (int64_t row = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; row < nrows_pad;
-       row += (int64_t)gridDim.x * blockDim.x) {
+  constexpr int ROWB = 2 * KP * 2;                 // bytes of one packed row (hi | lo)
+  __shared__ __align__(16) unsigned char stage[128 * ROWB];
+  for (int64_t row0 = blockIdx.x * (int64_t)blockDim.x; row0 < nrows_pad; row0 += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = row0 + threadIdx.x;
     float out[KP];
 #pragma unroll
     for (int q = 0; q < KP; ++q) out[q] = 0.f;
@@ -345,9 +347,21 @@ __global__ void __launch_bounds__(128) tc_lft_pack_rb_kernel(LftArgs a, int pass
       hv.z = pack_half2(hh[4], hh[5]); hv.w = pack_half2(hh[6], hh[7]);
       lv.x = pack_half2(ll[0], ll[1]); lv.y = pack_half2(ll[2], ll[3]);
       lv.z = pack_half2(ll[4], ll[5]); lv.w = pack_half2(ll[6], ll[7]);
-      *reinterpret_cast<uint4*>(dst + row * 2 * KP + k0) = hv;
-      *reinterpret_cast<uint4*>(dst + row * 2 * KP + KP + k0) = lv;
+      // row-major staging, 16-B chunks rotated by the row so a warp's stores hit all banks
+      const int c0 = k0 / 8, cq = ROWB / 16;
+      *reinterpret_cast<uint4*>(stage + threadIdx.x * ROWB + ((c0 + threadIdx.x) % cq) * 16) = hv;
+      *reinterpret_cast<uint4*>(stage + threadIdx.x * ROWB + ((c0 + KP / 8 + threadIdx.x) % cq) * 16) = lv;
     }
+    __syncthreads();
+    // the block's rows are consecutive in dst: one contiguous, coalesced copy
+    const int64_t nr = min((int64_t)blockDim.x, nrows_pad - row0);
+    uint4* gdst = reinterpret_cast<uint4*>(dst + row0 * 2 * KP);
+    const int cq = ROWB / 16;
+    for (int q = threadIdx.x; q < nr * cq; q += blockDim.x) {
+      const int r = q / cq, c = q - r * cq;
+      gdst[q] = *reinterpret_cast<const uint4*>(stage + r * ROWB + ((c + r) % cq) * 16);
+    }
+    __syncthreads();
   }
 }
 
@@ -582,7 +596,7 @@ __device__ __forceinline__ void issue_split_gemm_ts_l2(uint32_t dtmem, uint32_t 
 }
 
 #ifndef TRD_P1_MERGE
-#define TRD_P1_MERGE 0
+#define TRD_P1_MERGE 1
 #endif
 // one lane of a converged warp (the MMA issuer runs warp-wide so that its operands live in
 // uniform registers; only the elected lane issues)
