@@ -307,23 +307,29 @@ __global__ void __launch_bounds__(128) tc_lft_pack_rb_kernel(LftArgs a, int pass
       else { jl = row / a.Ik; ik = row - jl * a.Ik; }
       float X[RK][RK1], M[RK1][RS];
       if (pass2) {
-        const double* hs = a.hk + ik * (RK * RK1);
+        const double2* hs = reinterpret_cast<const double2*>(a.hk + ik * (RK * RK1));   // h[a + RK b]
 #pragma unroll
-        for (int aa = 0; aa < RK; ++aa)
-#pragma unroll
-          for (int b = 0; b < RK1; ++b) X[aa][b] = (float)__ldg(hs + aa + RK * b);
+        for (int q = 0; q < RK * RK1 / 2; ++q) {
+          const double2 v = __ldg(hs + q);
+          X[(2 * q) % RK][(2 * q) / RK] = (float)v.x;
+          X[(2 * q + 1) % RK][(2 * q + 1) / RK] = (float)v.y;
+        }
       } else {
-        const float* zs = a.zk + ik * (RK * RK1);
+        const float4* zs = reinterpret_cast<const float4*>(a.zk + ik * (RK * RK1));     // Z[a][b]
 #pragma unroll
-        for (int aa = 0; aa < RK; ++aa)
-#pragma unroll
-          for (int b = 0; b < RK1; ++b) X[aa][b] = __ldg(zs + aa * RK1 + b);
+        for (int q = 0; q < RK * RK1 / 4; ++q) {
+          const float4 v = __ldg(zs + q);
+          reinterpret_cast<float*>(X)[4 * q] = v.x; reinterpret_cast<float*>(X)[4 * q + 1] = v.y;
+          reinterpret_cast<float*>(X)[4 * q + 2] = v.z; reinterpret_cast<float*>(X)[4 * q + 3] = v.w;
+        }
       }
-      const float* ms = a.mid + jl * (RK1 * RS);
+      const float4* ms = reinterpret_cast<const float4*>(a.mid + jl * (RK1 * RS));
 #pragma unroll
-      for (int b = 0; b < RK1; ++b)
-#pragma unroll
-        for (int c = 0; c < RS; ++c) M[b][c] = __ldg(ms + b * RS + c);
+      for (int q = 0; q < RK1 * RS / 4; ++q) {
+        const float4 v = __ldg(ms + q);
+        reinterpret_cast<float*>(M)[4 * q] = v.x; reinterpret_cast<float*>(M)[4 * q + 1] = v.y;
+        reinterpret_cast<float*>(M)[4 * q + 2] = v.z; reinterpret_cast<float*>(M)[4 * q + 3] = v.w;
+      }
 #pragma unroll
       for (int aa = 0; aa < RK; ++aa)
 #pragma unroll
@@ -690,6 +696,64 @@ __global__ void __launch_bounds__(256) tc_reduce_d_kernel(
   }
 }
 
+// Register-blocked stage 1 for compile-time ranks (RK, RK1, RS) with KP == RK * RS: thread per
+// GEMM row, Mid(jl) (RK1 x RS) and the D row (RK x RS, column a + RK c) loaded as float4 into
+// registers, acc[a][b] += sum_c D[a + RK c] Mid[b][c] (outer products over c), fp32 per
+// thread; then a fixed-order fp64 reduction over the CTA's threads.  CTA = (i_k, jl chunk).
+template <int RK, int RK1, int RS>
+__global__ void __launch_bounds__(128) tc_reduce_d_rb_kernel(const float* __restrict__ contrib,
+                                                             const float* __restrict__ mid, int nsplit,
+                                                             int64_t nrows_pad, int64_t nL, int64_t Ik, int rowmode,
+                                                             int64_t jl_chunk, double* __restrict__ dpart) {
+  constexpr int KP = RK * RS, MS = RK1 * RS, R2 = RK * RK1;
+  static_assert(KP % 16 == 0 && MS % 4 == 0, "vector loads");
+  __shared__ float red[128][R2 + 1];
+  const int64_t ik = blockIdx.x, jc = blockIdx.y;
+  const int64_t j0 = jc * jl_chunk, j1 = min(nL, j0 + jl_chunk);
+  float acc[RK][RK1];
+#pragma unroll
+  for (int a = 0; a < RK; ++a)
+#pragma unroll
+    for (int b = 0; b < RK1; ++b) acc[a][b] = 0.f;
+  for (int64_t jl = j0 + threadIdx.x; jl < j1; jl += blockDim.x) {
+    float M[RK1][RS];
+    const float4* m4 = reinterpret_cast<const float4*>(mid + jl * MS);
+#pragma unroll
+    for (int q = 0; q < MS / 4; ++q) {
+      const float4 v = __ldg(m4 + q);
+      reinterpret_cast<float*>(M)[4 * q + 0] = v.x; reinterpret_cast<float*>(M)[4 * q + 1] = v.y;
+      reinterpret_cast<float*>(M)[4 * q + 2] = v.z; reinterpret_cast<float*>(M)[4 * q + 3] = v.w;
+    }
+    const int64_t row = rowmode == 0 ? jl + nL * ik : ik + Ik * jl;
+    for (int sp = 0; sp < nsplit; ++sp) {
+      const float4* d4 = reinterpret_cast<const float4*>(contrib + ((int64_t)sp * nrows_pad + row) * KP);
+#pragma unroll
+      for (int c = 0; c < RS; ++c) {
+        float D[RK];
+#pragma unroll
+        for (int q = 0; q < RK / 4; ++q) {
+          const float4 v = __ldg(d4 + (RK * c) / 4 + q);
+          D[4 * q] = v.x; D[4 * q + 1] = v.y; D[4 * q + 2] = v.z; D[4 * q + 3] = v.w;
+        }
+#pragma unroll
+        for (int a = 0; a < RK; ++a)
+#pragma unroll
+          for (int b = 0; b < RK1; ++b) acc[a][b] = fmaf(D[a], M[b][c], acc[a][b]);
+      }
+    }
+  }
+#pragma unroll
+  for (int a = 0; a < RK; ++a)
+#pragma unroll
+    for (int b = 0; b < RK1; ++b) red[threadIdx.x][a + RK * b] = acc[a][b];
+  __syncthreads();
+  if (threadIdx.x < R2) {
+    double t = 0.0;
+    for (int q = 0; q < (int)blockDim.x; ++q) t += (double)red[q][threadIdx.x];
+    dpart[(jc * Ik + ik) * R2 + threadIdx.x] = t;
+  }
+}
+
 // stage 2: dvec = [d | sum_e2 | welsch | n] from the chunk partials and the per-CTA statistics
 __global__ void tc_reduce_final_kernel(const double* __restrict__ dpart, int64_t JC, int64_t Ik, int R2,
                                        const double* __restrict__ spart, int64_t nparts,
@@ -863,6 +927,14 @@ void launch_tc_pass(Context& c, const BlockPlan& bp, const TcStage& st, bool pas
 
 void launch_tc_reduce_d(Context& c, const BlockPlan& bp, cudaStream_t s) {
   const int64_t Ik = bp.nrows / bp.nL;
+  if (bp.p > 0 && bp.rk == 8 && bp.rk1 == 8 && bp.rs == 8 && bp.KP == 64) {
+    tc_reduce_d_rb_kernel<8, 8, 8><<<dim3((unsigned)Ik, (unsigned)bp.tc_jc), 128, 0, s>>>(
+        c.contrib, c.mid, bp.tc_nsplit, bp.n_row_tiles * TC_M, bp.nL, Ik, bp.rowmode, bp.tc_jl_chunk, c.dpart);
+    tc_reduce_final_kernel<<<(unsigned)(Ik + 1), 128, 0, s>>>(c.dpart, bp.tc_jc, Ik, bp.R2, c.spart, bp.tc_grid1,
+                                                              c.dvec, c.sc, bp.k);
+    c.launches += 2;
+    return;
+  }
   const int threads = bp.R2 * std::max(1, 256 / std::max(1, bp.R2));
   const size_t smem = (size_t)RD_ROWS * ((bp.KP + 4) + (bp.R2 / bp.rk) * bp.rs) * sizeof(float);
   cudaFuncSetAttribute(tc_reduce_d_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
