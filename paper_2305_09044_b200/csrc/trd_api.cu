@@ -179,8 +179,15 @@ void build_plan(const Context& c, int k, const int64_t* s_in, BlockPlan& bp, boo
     }
     bp.tc_nsplit = (int)best_s;
     bp.tc_per = best_per;
-    bp.tc_grid = (int)std::min<int64_t>(nrt * best_s, (int64_t)c.num_sm);
-    bp.tc_grid1 = (int)std::max<int64_t>(1, std::min<int64_t>(nrt * best_s, (int64_t)c.num_sm - 1));
+    // CTA pairs (clusters of 2) share each B tile (half each, multicast); TRD_CLUSTER=1 disables
+    const char* ce = getenv("TRD_CLUSTER");
+    bp.tc_cl = (ce && atoi(ce) == 1) || c.num_sm < 4 ? 1 : 2;
+    const int64_t groups = (nrt + bp.tc_cl - 1) / bp.tc_cl;      // row-tile groups
+    const int64_t citems = groups * best_s;                          // items per cluster walk
+    const int64_t ncl2 = ((int64_t)c.num_sm / bp.tc_cl);             // clusters that fit
+    const int64_t ncl1 = (((int64_t)c.num_sm - 1) / bp.tc_cl);       // one SM left (side stream)
+    bp.tc_grid = (int)(std::max<int64_t>(1, std::min<int64_t>(citems, ncl2)) * bp.tc_cl);
+    bp.tc_grid1 = (int)(std::max<int64_t>(1, std::min<int64_t>(citems, ncl1)) * bp.tc_cl);
     const int64_t Ikk = c.dims[k];
     // d reduction: >= 8 CTAs per SM worth of (i_k, jl-chunk) blocks, chunks of >= 32 rows
     int64_t jc = (8 * (int64_t)c.num_sm + Ikk - 1) / Ikk;

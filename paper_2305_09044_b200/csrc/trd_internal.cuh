@@ -72,7 +72,8 @@ struct BlockPlan {
   int tc_nsplit;         // column splits per row tile (work item = (row tile, split))
   int64_t tc_per;        // column tiles per split
   int tc_grid;           // persistent CTAs of pass 2 (<= SM count)
-  int tc_grid1;          // persistent CTAs of pass 1 (one SM left for the side-stream solve)
+  int tc_grid1;          // persistent CTAs of pass 1 (SMs left for the side-stream solve)
+  int tc_cl;             // CTAs per cluster of the pass kernels (2: B tiles multicast to a pair)
   int64_t tc_jc, tc_jl_chunk;   // d reduction: jl chunks
 };
 

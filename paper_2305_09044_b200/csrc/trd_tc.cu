@@ -516,7 +516,9 @@ __global__ void __launch_bounds__(128) stage_vals_kernel(StageArgs s) {
 // ---------------------------------------------------------------------------------------
 struct TcArgs {
   int64_t nrows, ncols, nL, Ik, n_col_tiles, nrows_pad;
-  int64_t n_items, per;    // work items = (row tile, column split); per = column tiles per split
+  int64_t n_items, per;    // work items = (row-tile group, column split); per = column tiles per split
+  int cl;                  // CTAs per cluster (1, or 2: a pair shares B tiles via multicast)
+  int64_t n_row_tiles;
   int rowmode, K, R2, rk, rk1, rs, p, nsplit;
   int sigma_inf;
   const __half* arow;      // Lft (pass 1) or Lft_h (pass 2), row-major hi | lo (unused: built in-kernel)
@@ -537,6 +539,7 @@ struct TcArgs {
   int exp;                 // TRD_TC_EXP (timing experiments only; results invalid if != 0):
                            //   bit 0 = epilogue does the barrier handshakes only
                            //   bit 1 = B producer skips the copies, bit 2 = sketch producer skips
+                           //   bit 3 = trace, bit 4 = pass-2 epilogue skips the TMEM loads
 };
 
 template <int KP>
@@ -843,7 +846,9 @@ static TcArgs make_tc_args(const Context& c, const BlockPlan& bp, const TcStage&
   TcArgs a;
   a.nrows = bp.nrows; a.ncols = bp.ncols; a.nL = bp.nL; a.Ik = bp.nrows / bp.nL;
   a.n_col_tiles = bp.n_col_tiles; a.nrows_pad = bp.n_row_tiles * TC_M;
-  a.n_items = bp.n_row_tiles * bp.tc_nsplit; a.per = bp.tc_per;
+  a.cl = bp.tc_cl;
+  a.n_row_tiles = bp.n_row_tiles;
+  a.n_items = ((bp.n_row_tiles + a.cl - 1) / a.cl) * bp.tc_nsplit; a.per = bp.tc_per;
   a.rowmode = bp.rowmode; a.K = bp.K; a.R2 = bp.R2; a.rk = bp.rk; a.rk1 = bp.rk1; a.rs = bp.rs;
   a.p = bp.p; a.nsplit = bp.tc_nsplit;
   a.sigma_inf = c.cfg.sigma_mode == TRD_SIGMA_INF;
@@ -871,14 +876,28 @@ static void launch_tc_pass_t(Context& c, const BlockPlan& bp, const TcStage& st,
   }
   TcArgs a = make_tc_args(c, bp, st, pass2);
   const dim3 grid((unsigned)(pass2 ? bp.tc_grid : bp.tc_grid1));
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = (unsigned)a.cl;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.gridDim = grid;
+  cfg.stream = s;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
   if (!pass2) {
     const int sm = Ws1<KP>::SMEM;
     cudaFuncSetAttribute(tc_pass1_kernel<KP>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
-    tc_pass1_kernel<KP><<<grid, WsWarps<Ws1<KP>::NE>::THREADS, sm, s>>>(a);
+    cfg.blockDim = dim3(WsWarps<Ws1<KP>::NE>::THREADS);
+    cfg.dynamicSmemBytes = sm;
+    cudaLaunchKernelEx(&cfg, tc_pass1_kernel<KP>, a);
   } else {
     const int sm = Ws2<KP>::SMEM;
     cudaFuncSetAttribute(tc_pass2_kernel<KP>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
-    tc_pass2_kernel<KP><<<grid, WsWarps<Ws2<KP>::NE>::THREADS, sm, s>>>(a);
+    cfg.blockDim = dim3(WsWarps<Ws2<KP>::NE>::THREADS);
+    cfg.dynamicSmemBytes = sm;
+    cudaLaunchKernelEx(&cfg, tc_pass2_kernel<KP>, a);
   }
   c.launches++;
   if (getenv("TRD_DEBUG_SYNC")) {            // debugging aid: serialise and report each pass launch
