@@ -187,6 +187,34 @@ def gradient_block(Xk, Pk, Zk2, S, sigma, sigma_inf=False):
     return Y @ S, E, W
 
 
+def gradient_entries(cores, k, index, x, sigma, sigma_inf=False):
+    """Eq. (7) + Eq. (9) summed entry by entry, for a list of observed
+    entries: index (n x N int, the multi-indices), x (n,) their values.  For each entry j,
+    S(j) = Z_{k+1}(i_{k+1}) .. Z_{k-1}(i_{k-1}) (Thm 1), e = x - Tr(Z_k(i_k) S(j)),
+    w = exp(-e^2 / 2 sigma^2) (reading R1), and d[i_k, c + r_k b] += w e S(j)[b, c].
+    Same quantity as gradient_block restricted to the given entries (pinned against it);
+    used to check single rows of d at sizes where the dense unfolding does not fit.
+    Returns (d, sum_e2) with d of shape (I_k, r_k * r_{k+1})."""
+    N = len(cores)
+    index = np.asarray(index, dtype=np.int64)
+    x = np.asarray(x, dtype=np.float64)
+    rk, Ik, rk1 = cores[k].shape
+    order = [(k + 1 + q) % N for q in range(N - 1)]
+    S = cores[order[0]][:, index[:, order[0]], :].transpose(1, 0, 2)        # (n, r, r')
+    for m in order[1:]:
+        S = np.einsum('nab,nbc->nac', S, cores[m][:, index[:, m], :].transpose(1, 0, 2))
+    # S[n] = S(j) in R^{r_{k+1} x r_k};  Tr(Z_k(i_k) S(j)) = sum_{a,b} Z_k[a, i_k, b] S(j)[b, a]
+    Zs = cores[k][:, index[:, k], :].transpose(1, 0, 2)                    # (n, r_k, r_{k+1})
+    xhat = np.einsum('nab,nba->n', Zs, S)
+    e = x - xhat
+    w = hq_weight(e, sigma, sigma_inf)
+    y = w * e
+    d = np.zeros((Ik, rk * rk1))
+    contrib = (y[:, None, None] * S).reshape(len(x), rk1 * rk)             # column b*r_k + c
+    np.add.at(d, index[:, k], contrib)
+    return d, float(np.sum(e * e))
+
+
 def scaled_gradient(d, G, lambda_rel):
     """Eq. (10)/(16) with reading R5:
     lambda = lambda_rel * tr(G) / R^2, A = G + lambda I = L L^T and the filtered solve

@@ -537,3 +537,22 @@ def test_psnr_and_relative_error():
     X = np.zeros((4, 4))
     assert abs(O.psnr(X, X + 0.1) - 20.0) <= 1e-12
     assert O.psnr(X, X) == float('inf')
+
+
+def test_gradient_entries_equals_dense_gradient_block():
+    """The entry-wise form of Eq. (9) (used for full-size row checks) equals the dense
+    unfolding form on a small random instance, for every block, including sigma = inf."""
+    rng = np.random.default_rng(7)
+    dims, ranks = [5, 4, 6, 3], [2, 3, 2, 3]
+    cores = [rng.standard_normal((ranks[m], dims[m], ranks[(m + 1) % 4])) for m in range(4)]
+    X = rng.standard_normal(dims)
+    P = rng.random(dims) < 0.4
+    idx = np.argwhere(P)
+    for k in range(4):
+        for sigma, sinf in ((0.7, False), (1.0, True)):
+            Xk, Pk = O.unfold_shifted(X, k), O.unfold_shifted(P, k)
+            S = O.subchain(cores, k)
+            d_dense, E, W = O.gradient_block(Xk, Pk, O.core_unfold2(cores[k]), S, sigma, sinf)
+            d_ent, se2 = O.gradient_entries(cores, k, idx, X[P], sigma, sinf)
+            assert np.allclose(d_ent, d_dense, rtol=1e-12, atol=1e-12)
+            assert abs(se2 - float(np.sum(E[Pk] ** 2))) <= 1e-10 * float(np.sum(E[Pk] ** 2))
