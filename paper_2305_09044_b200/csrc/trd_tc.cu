@@ -87,8 +87,10 @@ __device__ __noinline__ void mbar_hang_report(uint32_t addr, uint32_t phase) {
 __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t phase) {
   const uint32_t addr = smem_u32(bar);
   uint32_t ok = 0;
+#if TRD_DEBUG_HANG
   uint32_t spins = 0;
   long long t0 = 0;
+#endif
   do {
     asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
                  "selp.u32 %0, 1, 0, p;\n\t}" : "=r"(ok) : "r"(addr), "r"(phase), "r"(1000000u) : "memory");
@@ -110,8 +112,10 @@ __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t phase) {
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
   const uint32_t addr = smem_u32(bar);
   uint32_t ok = 0;
+#if TRD_DEBUG_HANG
   uint32_t spins = 0;
   long long t0 = 0;
+#endif
   do {
 #if TRD_MBAR_SPIN
     asm volatile("{\n\t.reg .pred p;\n\tmbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
