@@ -202,7 +202,6 @@ void launch_fill_full_sets(Context& c, const BlockPlan& bp, cudaStream_t s);
 
 // ---- tensor-core pass kernels (trd_tc.cu) ---------------------------------------------
 bool tc_supported_kp(int KP);
-void launch_tc_pack_rows(Context& c, const BlockPlan& bp, const float* src, __half* dst, cudaStream_t s);
 void launch_tc_pack_cols(Context& c, const BlockPlan& bp, cudaStream_t s);
 void launch_tc_lft(Context& c, const BlockPlan& bp, bool pass2, cudaStream_t s);
 void launch_tc_pass(Context& c, const BlockPlan& bp, const TcStage& st, bool pass2, cudaStream_t s);

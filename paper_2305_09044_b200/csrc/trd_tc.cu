@@ -187,22 +187,6 @@ __device__ __forceinline__ uint32_t pack_half2(__half lo, __half hi) {
 // ---------------------------------------------------------------------------------------
 // Operand packing
 // ---------------------------------------------------------------------------------------
-// A (Lft or Lft_h) row-major: [row][hi KP | lo KP] halves, rows padded to the tile count
-__global__ void tc_pack_rows_kernel(const float* __restrict__ src, int64_t nrows, int K, int KP,
-                                    int64_t nrows_pad, __half* __restrict__ dst) {
-  const int64_t tot = nrows_pad * KP;
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tot;
-       t += (int64_t)gridDim.x * blockDim.x) {
-    const int kap = (int)(t % KP);
-    const int64_t row = t / KP;
-    const float v = (row < nrows && kap < K) ? src[row * K + kap] : 0.f;
-    const __half hi = __float2half_rn(v);
-    const __half lo = __float2half_rn(v - __half2float(hi));
-    dst[row * 2 * KP + kap] = hi;
-    dst[row * 2 * KP + KP + kap] = lo;
-  }
-}
-
 // a3 + the Lft half of the GEMM form, fused with the fp16 hi / lo split of
 // the A operand: Lft(row)[a + r_k c] = sum_b X(i_k)[a][b] Mid(j_L)[b][c]  (p = 0: Lft = X(i_k)),
 // X = core slice Z_k(i_k) (pass 1) or folded scaled gradient H(i_k) (pass 2).  One thread per
@@ -552,7 +536,6 @@ struct TcLayout {
   static constexpr int B_HALVES = 2 * TC_NT * KP;    // hi block then lo block
   static constexpr uint32_t B_LO_BYTES = TC_NT * KP * 2;
   static constexpr uint32_t IDESC_S = make_idesc(TC_M, TC_NT, 0);   // S = A . B^T
-  static constexpr uint32_t IDESC_S2 = make_idesc(TC_M, 2 * TC_NT, 0);  // S' = A_hi [B_hi ; B_lo]^T
   static constexpr uint32_t IDESC_D = make_idesc(TC_M, KP, 1);      // D += P . B (B MN-major)
   static constexpr uint32_t IDESC_D2 = make_idesc(TC_M, 2 * KP, 1); // D' += P_hi [B_hi | B_lo]
 };
@@ -571,23 +554,6 @@ __device__ __forceinline__ void issue_split_gemm_ts(uint32_t dtmem, uint32_t aco
     for (int ks = 0; ks < KP / 16; ++ks)
       mma_ts(dtmem, aa + ks * 8, dt + (uint64_t)(ks * 16), L::IDESC_S, (term | ks) ? 1u : 0u);
   }
-}
-
-// Merged split terms, layout L1 ([hi block | lo block] per 64-column tile; the lo block sits
-// 8 row groups after the hi block, so one N = 128 MMA covers rows hi 0..63, lo 0..63):
-//   S'[:, 0:64]   = A_hi.B_hi^T + A_lo.B_hi^T
-//   S'[:, 64:128] = A_hi.B_lo^T                     (S = S'[:, 0:64] + S'[:, 64:128])
-// 4 N = 128 + 4 N = 64 MMAs (KP = 64) instead of 12 N = 64 ones.
-template <int KP>
-__device__ __forceinline__ void issue_split_gemm_ts_merged(uint32_t dtmem, uint32_t acol, uint32_t bH) {
-  using L = TcLayout<KP>;
-  const uint64_t d0 = make_sdesc(bH, 128, L::HK * 128);
-#pragma unroll
-  for (int ks = 0; ks < KP / 16; ++ks)
-    mma_ts(dtmem, acol + ks * 8, d0 + (uint64_t)(ks * 16), L::IDESC_S2, ks ? 1u : 0u);
-#pragma unroll
-  for (int ks = 0; ks < KP / 16; ++ks)
-    mma_ts(dtmem, acol + KP / 2 + ks * 8, d0 + (uint64_t)(ks * 16), L::IDESC_S, 1u);
 }
 
 // Layout L2 (pass 1): per 64-column tile, each column's row of 2 KP halves is [hi KP | lo KP];
@@ -788,12 +754,6 @@ __global__ void tc_reduce_final_kernel(const double* __restrict__ dpart, int64_t
 static int tc_grid(int64_t n) {
   int64_t g = (n + 255) / 256;
   return (int)std::max<int64_t>(1, std::min<int64_t>(g, 148 * 16));
-}
-
-void launch_tc_pack_rows(Context& c, const BlockPlan& bp, const float* src, __half* dst, cudaStream_t s) {
-  const int64_t pad = bp.n_row_tiles * TC_M;
-  tc_pack_rows_kernel<<<tc_grid(pad * bp.KP), 256, 0, s>>>(src, bp.nrows, bp.K, bp.KP, pad, dst);
-  c.launches++;
 }
 
 void launch_tc_lft(Context& c, const BlockPlan& bp, bool pass2, cudaStream_t s) {
