@@ -165,6 +165,11 @@ void build_plan(const Context& c, int k, const int64_t* s_in, BlockPlan& bp, boo
     // persistent pass kernels: one CTA per SM walking (row tile, column split) items; pick
     // the split that minimises the busiest CTA's work (ties: fewer splits)
     const int64_t nrt = bp.n_row_tiles, nct = bp.n_col_tiles;
+    // tile pairs (N = 128 GEMMs) for KP <= 64 unless there is a single column tile;
+    // TRD_UNIT=1 forces single tiles
+    const char* ue = getenv("TRD_UNIT");
+    bp.tc_u = (bp.KP <= 64 && nct >= 2 && !(ue && atoi(ue) == 1)) ? 2 : 1;
+    const int64_t U = bp.tc_u;
     double best = 1e300;
     int64_t best_s = 1, best_per = nct;
     for (int64_t sp = 1; sp <= std::min<int64_t>(nct, 64); ++sp) {
@@ -174,7 +179,8 @@ void build_plan(const Context& c, int k, const int64_t* s_in, BlockPlan& bp, boo
       const int64_t grid = std::min<int64_t>(items, (int64_t)c.num_sm);
       // busiest CTA: its items x (tiles per item + ~1 tile of per-item cost: A load, D drain
       // and the split's share of the d reduction)
-      const double cost = (double)((items + grid - 1) / grid) * ((double)per + 1.0);
+      // (an odd split with tile pairs ends in a phantom half, costed as a whole tile)
+      const double cost = (double)((items + grid - 1) / grid) * ((double)((per + U - 1) / U * U) + 1.0);
       if (cost < best - 1e-9) { best = cost; best_s = se; best_per = per; }
     }
     bp.tc_nsplit = (int)best_s;

@@ -74,6 +74,7 @@ struct BlockPlan {
   int tc_grid;           // persistent CTAs of pass 2 (<= SM count)
   int tc_grid1;          // persistent CTAs of pass 1 (SMs left for the side-stream solve)
   int tc_cl;             // CTAs per cluster of the pass kernels (2: B tiles multicast to a pair)
+  int tc_u;              // column tiles per ring unit of the pass kernels (2: N = 128 GEMMs)
   int64_t tc_jc, tc_jl_chunk;   // d reduction: jl chunks
 };
 

@@ -392,6 +392,7 @@ __global__ void tc_pack_cols_kernel(const float* __restrict__ rgtT, int64_t ncol
 // ---------------------------------------------------------------------------------------
 struct StageArgs {
   int64_t nrows, ncols, n_col_tiles, n_tiles;
+  int64_t n_words;        // 32-bit words of the observation mask
   int packed;
   const int64_t* row_off;
   const int64_t* col_off;
@@ -405,36 +406,118 @@ struct StageArgs {
   uint16_t* tidx;         // entry list: (row in tile) * 64 + column, 0xFFFF = padding
 };
 
+// The working-set tile (128 GEMM rows x 64 columns) reads the observation bits at linear
+// positions row_off[row] + col_off[col].  Two structures make this cheap:
+//  * column runs: consecutive columns with consecutive linear positions (mode 0 is the fastest
+//    column digit) -> one funnel-shifted bit window per run and row;
+//  * contiguous rows (k = 0: rows enumerate i_0 fastest): the 32 rows of a warp are one 32-bit
+//    window per column; lane j extracts column j's window and a warp bit-matrix transpose
+//    turns the columns into the rows' 64-bit masks.
+// Sampled (RStS) index sets fall back to runs of length 1.
+__device__ __forceinline__ uint32_t mask_word(const StageArgs& s, int64_t w) {
+  return w < s.n_words ? __ldg(s.mask + w) : 0u;
+}
+// 32 bits of the mask starting at linear position lin
+__device__ __forceinline__ uint32_t mask_bits32(const StageArgs& s, int64_t lin) {
+  const int64_t w = lin >> 5;
+  const uint32_t sh = (uint32_t)(lin & 31);
+  const uint32_t lo = mask_word(s, w);
+  const uint32_t hi = sh ? mask_word(s, w + 1) : 0u;
+  return __funnelshift_r(lo, hi, sh);
+}
+// len (1..64) bits of the mask starting at linear position lin
+__device__ __forceinline__ uint64_t mask_bits(const StageArgs& s, int64_t lin, int len) {
+  const int64_t w = lin >> 5;
+  const uint32_t sh = (uint32_t)(lin & 31);
+  const uint32_t w0 = mask_word(s, w);
+  const uint32_t w1 = (sh + len > 32) ? mask_word(s, w + 1) : 0u;
+  const uint32_t w2 = (sh + len > 64) ? mask_word(s, w + 2) : 0u;
+  uint64_t v = ((((uint64_t)w1) << 32) | w0) >> sh;
+  if (sh) v |= ((uint64_t)w2) << (64 - sh);
+  return len >= 64 ? v : (v & ((1ull << len) - 1ull));
+}
+// rank of linear position lin among the observed entries (packed value index)
+__device__ __forceinline__ int64_t mask_rank(const StageArgs& s, int64_t lin) {
+  const int64_t w = lin >> 5;
+  return (int64_t)__ldg(s.rank_prefix + w) + __popc(__ldg(s.mask + w) & ((1u << (lin & 31)) - 1u));
+}
+// 32 x 32 bit-matrix transpose across a warp: in, lane i holds row i (bit j = element (i, j));
+// out, lane i holds column i (bit j = element (j, i))
+__device__ __forceinline__ uint32_t warp_transpose32(uint32_t x, int lane) {
+  const uint32_t M[5] = {0x0000FFFFu, 0x00FF00FFu, 0x0F0F0F0Fu, 0x33333333u, 0x55555555u};
+#pragma unroll
+  for (int q = 0; q < 5; ++q) {
+    const int sft = 16 >> q;
+    const uint32_t t = __shfl_xor_sync(0xffffffffu, x, sft);
+    x = (lane & sft) ? ((x & ~M[q]) | ((t & ~M[q]) >> sft)) : ((x & M[q]) | ((t & M[q]) << sft));
+  }
+  return x;
+}
+// per tile: column offsets and the run-start mask (bit j: column j starts a run)
+__device__ __forceinline__ void stage_tile_cols(const StageArgs& s, int64_t ct, int tid, int64_t* sco,
+                                                uint32_t* sstart) {
+  if (tid < TC_NT) {
+    const int64_t col = ct * TC_NT + tid;
+    sco[tid] = col < s.ncols ? s.col_off[col] : -1;
+  }
+  __syncthreads();
+  if (tid < TC_NT) {
+    const int64_t c0 = sco[tid];
+    const bool start = tid == 0 || c0 < 0 || sco[tid - 1] < 0 || c0 != sco[tid - 1] + 1;
+    const uint32_t b = __ballot_sync(0xffffffffu, start);
+    if ((tid & 31) == 0) sstart[tid >> 5] = b;
+  }
+  __syncthreads();
+}
+// rows of this warp at most two contiguous ranges of linear positions (lanes [0, b) from
+// baseA, lanes [b, 32) from baseB; b = 32: one range)?  Row digit orders put i_0 first, so a
+// warp's rows break at most once (every dims[0] >= 32 rows)
+struct WarpRows {
+  int64_t baseA, baseB;
+  int b;
+};
+__device__ __forceinline__ bool warp_row_segments(int64_t ro, int lane, WarpRows& w) {
+  const int64_t prev = __shfl_up_sync(0xffffffffu, ro, 1);
+  const uint32_t brk = __ballot_sync(0xffffffffu, lane > 0 && ro != prev + 1);
+  if (!__all_sync(0xffffffffu, ro >= 0) || __popc(brk) > 1) return false;
+  w.b = brk ? __ffs(brk) - 1 : 32;
+  w.baseA = __shfl_sync(0xffffffffu, ro, 0);
+  w.baseB = __shfl_sync(0xffffffffu, ro, w.b & 31);
+  return true;
+}
+// the warp's 32 row bits of column offset co (bit r = row r)
+__device__ __forceinline__ uint32_t warp_col_bits(const StageArgs& s, const WarpRows& w, int64_t co) {
+  uint32_t a = mask_bits32(s, w.baseA + co);
+  if (w.b < 32) a = (a & ((1u << w.b) - 1u)) | (mask_bits32(s, w.baseB + co) << w.b);
+  return a;
+}
+
 __global__ void __launch_bounds__(128) stage_bits_kernel(StageArgs s) {
   __shared__ int64_t sco[TC_NT];
+  __shared__ uint32_t sstart[2];
   __shared__ int wsum[4];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   for (int64_t tile = blockIdx.x; tile < s.n_tiles; tile += gridDim.x) {
     const int64_t rt = tile / s.n_col_tiles, ct = tile % s.n_col_tiles;
-    if (tid < TC_NT) {
-      const int64_t col = ct * TC_NT + tid;
-      sco[tid] = col < s.ncols ? s.col_off[col] : -1;
-    }
-    __syncthreads();
+    stage_tile_cols(s, ct, tid, sco, sstart);
     const int64_t row = rt * TC_M + tid;
     const int64_t ro = row < s.nrows ? s.row_off[row] : -1;
     uint64_t bits = 0;
-    if (ro >= 0) {
-      // 8 independent mask-word loads in flight per step (L1 serves the words shared by
-      // neighbouring rows / columns)
-#pragma unroll 1
-      for (int j0 = 0; j0 < TC_NT; j0 += 8) {
-        uint32_t w[8];
-        int sh[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const int64_t co = sco[j0 + u];
-          const int64_t lin = ro + (co < 0 ? 0 : co);
-          w[u] = co < 0 ? 0u : __ldg(s.mask + (lin >> 5));
-          sh[u] = (int)(lin & 31);
-        }
-#pragma unroll
-        for (int u = 0; u < 8; ++u) bits |= (uint64_t)((w[u] >> sh[u]) & 1u) << (j0 + u);
+    WarpRows wr;
+    if (warp_row_segments(ro, lane, wr)) {
+      // lane j: column j's and column (j + 32)'s bits over the warp's 32 rows, then transpose
+      const int64_t c0 = sco[lane], c1 = sco[lane + 32];
+      const uint32_t w0 = c0 >= 0 ? warp_col_bits(s, wr, c0) : 0u;
+      const uint32_t w1 = c1 >= 0 ? warp_col_bits(s, wr, c1) : 0u;
+      bits = (uint64_t)warp_transpose32(w0, lane) | ((uint64_t)warp_transpose32(w1, lane) << 32);
+    } else {
+      uint64_t st = (uint64_t)sstart[0] | ((uint64_t)sstart[1] << 32);   // warp-uniform
+      while (st) {
+        const int j0 = __ffsll((long long)st) - 1;
+        st &= st - 1;
+        const int j1 = st ? __ffsll((long long)st) - 1 : TC_NT;
+        const int64_t co = sco[j0];
+        if (ro >= 0 && co >= 0) bits |= mask_bits(s, ro + co, j1 - j0) << j0;
       }
     }
     const int cnt = __popcll(bits);
@@ -461,40 +544,85 @@ __global__ void __launch_bounds__(128) stage_bits_kernel(StageArgs s) {
 
 __global__ void __launch_bounds__(128) stage_vals_kernel(StageArgs s) {
   __shared__ int64_t sco[TC_NT];
-  const int tid = threadIdx.x;
+  __shared__ uint32_t sstart[2];
+  __shared__ uint64_t sbits[TC_M];
+  __shared__ int soff[TC_M];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   for (int64_t tile = blockIdx.x; tile < s.n_tiles; tile += gridDim.x) {
     const int64_t rt = tile / s.n_col_tiles, ct = tile % s.n_col_tiles;
-    if (tid < TC_NT) {
-      const int64_t col = ct * TC_NT + tid;
-      sco[tid] = col < s.ncols ? s.col_off[col] : -1;
-    }
-    __syncthreads();
     const int64_t row = rt * TC_M + tid;
-    uint64_t bits = s.tbits[tile * TC_M + tid];
-    const int64_t base = (int64_t)s.tcount[tile] + s.troff[tile * TC_M + tid];
+    const uint64_t bits = s.tbits[tile * TC_M + tid];
+    const int roff = s.troff[tile * TC_M + tid];
+    const int64_t tb = (int64_t)s.tcount[tile];          // tile block start (after the scan)
+    sbits[tid] = bits;
+    soff[tid] = roff;
+    stage_tile_cols(s, ct, tid, sco, sstart);            // (its barriers also publish sbits / soff)
     if (tid == TC_M - 1) {                    // padding entries of the tile block
-      const int64_t end = base + __popcll(bits);
-      for (int64_t e = end; e < (int64_t)s.tcount[tile + 1]; ++e) { s.tidx[e] = 0xFFFFu; s.tvals[e] = 0.f; }
+      for (int64_t e = tb + roff + __popcll(bits); e < (int64_t)s.tcount[tile + 1]; ++e) {
+        s.tidx[e] = 0xFFFFu;
+        s.tvals[e] = 0.f;
+      }
     }
-    if (bits) {
-      const int64_t ro = s.row_off[row];
-      float* out = s.tvals + base;
-      uint16_t* oidx = s.tidx + base;
-      int q = 0;
-      int64_t cwi = -1;
-      uint32_t cw = 0, cp = 0;
-      while (bits) {
-        const int j = __ffsll((long long)bits) - 1;
-        bits &= bits - 1;
-        const int64_t lin = ro + sco[j];
-        int64_t vi = lin;
-        if (s.packed) {
-          const int64_t wi = lin >> 5;
-          if (wi != cwi) { cw = __ldg(s.mask + wi); cp = __ldg(s.rank_prefix + wi); cwi = wi; }
-          vi = (int64_t)cp + __popc(cw & ((1u << (lin & 31)) - 1u));
+    const int64_t ro = row < s.nrows ? s.row_off[row] : -1;
+    WarpRows wr;
+    if (warp_row_segments(ro, lane, wr)) {
+      // column-wise: lane j takes columns j and j + 32; each row range of the warp is one run of
+      // linear positions per column, so its packed values are consecutive
+#pragma unroll 1
+      for (int h = 0; h < 2; ++h) {
+        const int j = lane + 32 * h;
+        const int64_t co = sco[j];
+        if (co < 0) continue;
+        uint32_t cw = warp_col_bits(s, wr, co);
+        if (!cw) continue;
+        const int64_t la = wr.baseA + co, lb = wr.baseB + co;   // linear positions of lanes 0, b
+        const int64_t va = s.packed ? mask_rank(s, la) : la;
+        const int64_t vb = (s.packed && wr.b < 32) ? mask_rank(s, lb) : lb;
+        int qa = 0, qb = 0;
+        while (cw) {
+          const int r = __ffs(cw) - 1;
+          cw &= cw - 1;
+          const int rr = warp * 32 + r;                   // row in the tile
+          const int64_t pos = tb + soff[rr] + __popcll(sbits[rr] & ((1ull << j) - 1ull));
+          int64_t vi;
+          if (r < wr.b) vi = s.packed ? va + qa++ : la + r;
+          else vi = s.packed ? vb + qb++ : lb + (r - wr.b);
+          s.tvals[pos] = __ldg(s.values + vi);
+          s.tidx[pos] = (uint16_t)(rr * TC_NT + j);
         }
-        oidx[q] = (uint16_t)(tid * TC_NT + j);
-        out[q++] = __ldg(s.values + vi);
+      }
+    } else if (bits) {
+      // row-wise over the column runs: a run's observed values are consecutive
+      float* out = s.tvals + tb + roff;
+      uint16_t* oidx = s.tidx + tb + roff;
+      int q = 0;
+      uint64_t st = (uint64_t)sstart[0] | ((uint64_t)sstart[1] << 32);
+      while (st) {
+        const int j0 = __ffsll((long long)st) - 1;
+        st &= st - 1;
+        const int j1 = st ? __ffsll((long long)st) - 1 : TC_NT;
+        const uint64_t rb = (bits >> j0) & (j1 - j0 >= 64 ? ~0ull : ((1ull << (j1 - j0)) - 1ull));
+        if (!rb) continue;
+        const int64_t lin0 = ro + sco[j0];
+        if (s.packed) {
+          const int64_t v0 = mask_rank(s, lin0);
+          const int n = __popcll(rb);
+          uint64_t b = rb;
+          for (int u = 0; u < n; ++u) {
+            const int jj = __ffsll((long long)b) - 1;
+            b &= b - 1;
+            oidx[q] = (uint16_t)(tid * TC_NT + j0 + jj);
+            out[q++] = __ldg(s.values + v0 + u);
+          }
+        } else {
+          uint64_t b = rb;
+          while (b) {
+            const int jj = __ffsll((long long)b) - 1;
+            b &= b - 1;
+            oidx[q] = (uint16_t)(tid * TC_NT + j0 + jj);
+            out[q++] = __ldg(s.values + lin0 + jj);
+          }
+        }
       }
     }
     __syncthreads();
@@ -560,9 +688,12 @@ __device__ __forceinline__ void issue_split_gemm_ts(uint32_t dtmem, uint32_t aco
 // core matrix (g, h') at (g * 2HK + h') * 128 B, h' < HK hi, h' >= HK lo.  GEMM1 reads it
 // K-major with the three split terms (lo = +HK core matrices); GEMM2 reads it MN-major with
 // N = 2 KP for the P_hi terms (D' = P_hi [B_hi | B_lo]) and N = KP for P_lo.B_hi.
-template <int KP>
+// NCOL = 64 U columns: U consecutive L2 tiles are one canonical K-major operand of N = 64 U
+// rows (the 8-column groups of tile t + 1 follow those of tile t at the same stride)
+template <int KP, int NCOL = TC_NT>
 __device__ __forceinline__ void issue_split_gemm_ts_l2(uint32_t dtmem, uint32_t acol, uint32_t bH) {
   using L = TcLayout<KP>;
+  constexpr uint32_t IDESC = make_idesc(TC_M, NCOL, 0);
   const uint64_t d0 = make_sdesc(bH, 128, 2 * L::HK * 128);
 #pragma unroll
   for (int term = 0; term < 3; ++term) {
@@ -570,7 +701,7 @@ __device__ __forceinline__ void issue_split_gemm_ts_l2(uint32_t dtmem, uint32_t 
     const uint64_t dt = d0 + (uint64_t)((term == 1 ? L::HK * 128 : 0) >> 4);
 #pragma unroll
     for (int ks = 0; ks < KP / 16; ++ks)
-      mma_ts(dtmem, aa + ks * 8, dt + (uint64_t)(ks * 16), L::IDESC_S, (term | ks) ? 1u : 0u);
+      mma_ts(dtmem, aa + ks * 8, dt + (uint64_t)(ks * 16), IDESC, (term | ks) ? 1u : 0u);
   }
 }
 
@@ -788,6 +919,7 @@ void launch_tc_stage(Context& c, const BlockPlan& bp, TcStage& st, cudaStream_t 
   StageArgs a;
   a.nrows = bp.nrows; a.ncols = bp.ncols; a.n_col_tiles = bp.n_col_tiles;
   a.n_tiles = bp.n_row_tiles * bp.n_col_tiles;
+  a.n_words = c.n_words;
   a.packed = c.packed;
   a.row_off = c.row_off; a.col_off = c.col_off;
   a.mask = c.mask; a.rank_prefix = c.rank_prefix; a.values = c.values;
@@ -820,17 +952,17 @@ static TcArgs make_tc_args(const Context& c, const BlockPlan& bp, const TcStage&
   a.zk = c.Z + c.zoff[bp.k];
   a.hk = c.h;
   a.mid = c.mid;
-  a.rgtHL = (pass2 || !TRD_P1_MERGE) ? c.rgtHL : c.rgtHL2;
+  const char* ex = getenv("TRD_TC_EXP");
+  a.exp = ex ? atoi(ex) : 0;
+  a.rgtHL = ((!pass2 && !TRD_P1_MERGE) || (pass2 && (a.exp & 32))) ? c.rgtHL : c.rgtHL2;
   a.tbits = st.tbits; a.troff = st.troff; a.tbase = st.tbase; a.tvals = st.tvals; a.tidx = st.tidx;
   a.tw = c.tw;
   a.sc = c.sc;
   a.contrib = c.contrib; a.spart = c.spart; a.denpart = c.denpart;
-  const char* ex = getenv("TRD_TC_EXP");
-  a.exp = ex ? atoi(ex) : 0;
   return a;
 }
 
-template <int KP>
+template <int KP, int U>
 static void launch_tc_pass_t(Context& c, const BlockPlan& bp, const TcStage& st, bool pass2, cudaStream_t s) {
   static bool hang_flag_set = false;
   if (!hang_flag_set) {
@@ -851,23 +983,23 @@ static void launch_tc_pass_t(Context& c, const BlockPlan& bp, const TcStage& st,
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   if (!pass2) {
-    const int sm = Ws1<KP>::SMEM;
-    cudaFuncSetAttribute(tc_pass1_kernel<KP>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
-    cfg.blockDim = dim3(WsWarps<Ws1<KP>::NE>::THREADS);
+    const int sm = Ws1<KP, U>::SMEM;
+    cudaFuncSetAttribute(tc_pass1_kernel<KP, U>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    cfg.blockDim = dim3(WsWarps<Ws1<KP, U>::NE>::THREADS);
     cfg.dynamicSmemBytes = sm;
-    cudaLaunchKernelEx(&cfg, tc_pass1_kernel<KP>, a);
+    cudaLaunchKernelEx(&cfg, tc_pass1_kernel<KP, U>, a);
   } else {
-    const int sm = Ws2<KP>::SMEM;
-    cudaFuncSetAttribute(tc_pass2_kernel<KP>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
-    cfg.blockDim = dim3(WsWarps<Ws2<KP>::NE>::THREADS);
+    const int sm = Ws2<KP, U>::SMEM;
+    cudaFuncSetAttribute(tc_pass2_kernel<KP, U>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    cfg.blockDim = dim3(WsWarps<Ws2<KP, U>::NE>::THREADS);
     cfg.dynamicSmemBytes = sm;
-    cudaLaunchKernelEx(&cfg, tc_pass2_kernel<KP>, a);
+    cudaLaunchKernelEx(&cfg, tc_pass2_kernel<KP, U>, a);
   }
   c.launches++;
   if (getenv("TRD_DEBUG_SYNC")) {            // debugging aid: serialise and report each pass launch
     const cudaError_t e = cudaStreamSynchronize(s);
-    fprintf(stderr, "[trd debug] block %d pass %d KP %d grid %u items %lld per %lld: %s\n", bp.k, pass2 ? 2 : 1, KP,
-            grid.x, (long long)a.n_items, (long long)a.per, cudaGetErrorString(e));
+    fprintf(stderr, "[trd debug] block %d pass %d KP %d U %d grid %u items %lld per %lld: %s\n", bp.k, pass2 ? 2 : 1,
+            KP, U, grid.x, (long long)a.n_items, (long long)a.per, cudaGetErrorString(e));
   }
 }
 
@@ -895,15 +1027,20 @@ void tc_debug_dump() {
 bool tc_supported_kp(int KP) { return KP >= 16 && KP <= 128 && KP % 16 == 0; }
 
 void launch_tc_pass(Context& c, const BlockPlan& bp, const TcStage& st, bool pass2, cudaStream_t s) {
+  // U = 2 (tile pairs, N = 128 GEMMs) for KP <= 64 as chosen by build_plan: pass 2 only by
+  // default -- pass 1 with pairs runs its two epilogue warpgroups in lockstep on the halves
+  // of a pair and measured slower on C5b (13.8 vs 12.4 ms per sweep); TRD_P1_UNIT=2 enables it
+  static const int p1_unit = getenv("TRD_P1_UNIT") ? atoi(getenv("TRD_P1_UNIT")) : 1;
+  const bool pair = bp.tc_u == 2 && (pass2 || p1_unit == 2);
   switch (bp.KP) {
-    case 16: launch_tc_pass_t<16>(c, bp, st, pass2, s); break;
-    case 32: launch_tc_pass_t<32>(c, bp, st, pass2, s); break;
-    case 48: launch_tc_pass_t<48>(c, bp, st, pass2, s); break;
-    case 64: launch_tc_pass_t<64>(c, bp, st, pass2, s); break;
-    case 80: launch_tc_pass_t<80>(c, bp, st, pass2, s); break;
-    case 96: launch_tc_pass_t<96>(c, bp, st, pass2, s); break;
-    case 112: launch_tc_pass_t<112>(c, bp, st, pass2, s); break;
-    case 128: launch_tc_pass_t<128>(c, bp, st, pass2, s); break;
+    case 16: pair ? launch_tc_pass_t<16, 2>(c, bp, st, pass2, s) : launch_tc_pass_t<16, 1>(c, bp, st, pass2, s); break;
+    case 32: pair ? launch_tc_pass_t<32, 2>(c, bp, st, pass2, s) : launch_tc_pass_t<32, 1>(c, bp, st, pass2, s); break;
+    case 48: pair ? launch_tc_pass_t<48, 2>(c, bp, st, pass2, s) : launch_tc_pass_t<48, 1>(c, bp, st, pass2, s); break;
+    case 64: pair ? launch_tc_pass_t<64, 2>(c, bp, st, pass2, s) : launch_tc_pass_t<64, 1>(c, bp, st, pass2, s); break;
+    case 80: launch_tc_pass_t<80, 1>(c, bp, st, pass2, s); break;
+    case 96: launch_tc_pass_t<96, 1>(c, bp, st, pass2, s); break;
+    case 112: launch_tc_pass_t<112, 1>(c, bp, st, pass2, s); break;
+    case 128: launch_tc_pass_t<128, 1>(c, bp, st, pass2, s); break;
     default: break;
   }
 }

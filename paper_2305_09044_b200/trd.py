@@ -11,7 +11,7 @@ from typing import List, Optional
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libtrd.so")
+LIB_PATH = os.environ.get("TRD_LIB_PATH") or os.path.join(HERE, "libtrd.so")   # override: A/B experiments
 HEADER = os.path.join(os.path.dirname(HERE), "include", "trd.h")
 
 TRD_MAX_ORDER = 8

@@ -52,6 +52,9 @@ __global__ void __launch_bounds__(128, 1) bench(long long* out, int iters) {
       if (LAYOUT == 0) {
         db = make_sdesc(b_s + ks * 256, 128, 8 * 128, 0);
         da = make_sdesc(a_s + ks * 256, 128, 8 * 128, 0);
+      } else if (LAYOUT == 1) {   // libtrd layout L2: [hi KP | lo KP] per row, SBO = 2 HK * 128
+        db = make_sdesc(b_s + ks * 256, 128, 16 * 128, 0);
+        da = make_sdesc(a_s + ks * 256, 128, 16 * 128, 0);
       } else {  // SWIZZLE_128B K-major: rows of 128 B, 8-row atoms of 1024 B, SBO = 1024
         db = make_sdesc(b_s + ks * 32, 16, 1024, 2);
         da = make_sdesc(a_s + ks * 32, 16, 1024, 2);
@@ -230,8 +233,17 @@ void run(const char* name, int iters) {
   cudaFree(d);
 }
 
-int main() {
+int main(int argc, char** argv) {
   const int it = 20000;
+  if (argc > 1) {   // layout comparison only
+    run<64, true, 0>("TS none SBO1024", it);
+    run<64, true, 1>("TS none SBO2048", it);
+    run<128, true, 0>("TS none SBO1024", it);
+    run<128, true, 1>("TS none SBO2048", it);
+    run<64, false, 0>("SS none SBO1024", it);
+    run<64, false, 1>("SS none SBO2048", it);
+    return 0;
+  }
   run<64, true, 0>("TS none", it);
   run<128, true, 0>("TS none", it);
   run<256, true, 0>("TS none", it);
