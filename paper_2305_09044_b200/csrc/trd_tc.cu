@@ -510,6 +510,24 @@ __global__ void __launch_bounds__(128) stage_bits_kernel(StageArgs s) {
       const uint32_t w0 = c0 >= 0 ? warp_col_bits(s, wr, c0) : 0u;
       const uint32_t w1 = c1 >= 0 ? warp_col_bits(s, wr, c1) : 0u;
       bits = (uint64_t)warp_transpose32(w0, lane) | ((uint64_t)warp_transpose32(w1, lane) << 32);
+    } else if (__popcll((uint64_t)sstart[0] | ((uint64_t)sstart[1] << 32)) > 16) {
+      // scattered columns (sampled index sets): one bit per column, 8 loads in flight per step
+      if (ro >= 0) {
+#pragma unroll 1
+        for (int j0 = 0; j0 < TC_NT; j0 += 8) {
+          uint32_t w[8];
+          int sh[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int64_t co = sco[j0 + u];
+            const int64_t lin = ro + (co < 0 ? 0 : co);
+            w[u] = co < 0 ? 0u : __ldg(s.mask + (lin >> 5));
+            sh[u] = (int)(lin & 31);
+          }
+#pragma unroll
+          for (int u = 0; u < 8; ++u) bits |= (uint64_t)((w[u] >> sh[u]) & 1u) << (j0 + u);
+        }
+      }
     } else {
       uint64_t st = (uint64_t)sstart[0] | ((uint64_t)sstart[1] << 32);   // warp-uniform
       while (st) {
@@ -590,6 +608,28 @@ __global__ void __launch_bounds__(128) stage_vals_kernel(StageArgs s) {
           s.tvals[pos] = __ldg(s.values + vi);
           s.tidx[pos] = (uint16_t)(rr * TC_NT + j);
         }
+      }
+    } else if (bits && __popcll((uint64_t)sstart[0] | ((uint64_t)sstart[1] << 32)) > 16) {
+      // scattered columns: per entry, the rank from its mask word (cached across entries)
+      const int64_t rof = s.row_off[row];
+      float* out = s.tvals + tb + roff;
+      uint16_t* oidx = s.tidx + tb + roff;
+      int q = 0;
+      int64_t cwi = -1;
+      uint32_t cwd = 0, cp = 0;
+      uint64_t b = bits;
+      while (b) {
+        const int j = __ffsll((long long)b) - 1;
+        b &= b - 1;
+        const int64_t lin = rof + sco[j];
+        int64_t vi = lin;
+        if (s.packed) {
+          const int64_t wi = lin >> 5;
+          if (wi != cwi) { cwd = __ldg(s.mask + wi); cp = __ldg(s.rank_prefix + wi); cwi = wi; }
+          vi = (int64_t)cp + __popc(cwd & ((1u << (lin & 31)) - 1u));
+        }
+        oidx[q] = (uint16_t)(tid * TC_NT + j);
+        out[q++] = __ldg(s.values + vi);
       }
     } else if (bits) {
       // row-wise over the column runs: a run's observed values are consecutive
