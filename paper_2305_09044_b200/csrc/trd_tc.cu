@@ -1047,14 +1047,14 @@ void tc_debug_dump() {
   static long long tr[256 * 16];
   if (cudaMemcpyFromSymbol(tr, g_trace, sizeof(tr)) == cudaSuccess && tr[0] != 0) {
     fprintf(stderr, "[trd tc trace] pass-1 CTA 0 (cycles rel. to tile 0 GEMM1 start)\n"
-                    "  tile | G1 start wait issue | G2 start wait issue | EPI start skfull sfull dumped ppfree done\n");
+                    "  tile | G1 start wait issue | G2 start wait issue | EPI start skfull sfull dumped ppfree done fenced barred\n");
     const long long t0 = tr[0];
     for (int i = 0; i < 48; ++i) {
       const long long* q = tr + i * 16;
       auto f = [&](int k) { return q[k] ? q[k] - t0 : -1; };
-      fprintf(stderr, "  %4d | %7lld %5lld %5lld | %7lld %5lld %5lld | %7lld %5lld %5lld %5lld %5lld %5lld\n", i,
+      fprintf(stderr, "  %4d | %7lld %5lld %5lld | %7lld %5lld %5lld | %7lld %5lld %5lld %5lld %5lld %5lld %5lld %5lld\n", i,
               f(0), q[1] - q[0], q[2] - q[0], f(3), q[4] - q[3], q[5] - q[3], f(6), q[7] - q[6], q[8] - q[6],
-              q[9] - q[6], q[10] - q[6], q[11] - q[6]);
+              q[9] - q[6], q[10] - q[6], q[11] - q[6], q[12] - q[6], q[13] - q[6]);
     }
   }
   unsigned long long v[16];
