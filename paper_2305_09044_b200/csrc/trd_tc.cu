@@ -84,6 +84,9 @@ __device__ __noinline__ void mbar_hang_report(uint32_t addr, uint32_t phase) {
            g_prog[blockIdx.x][8], g_prog[blockIdx.x][9], g_prog[blockIdx.x][10], g_prog[blockIdx.x][11],
            g_prog[blockIdx.x][12], g_prog[blockIdx.x][13], g_prog[blockIdx.x][14], g_prog[blockIdx.x][15]);
 }
+#ifndef TRD_SLEEP_NS
+#define TRD_SLEEP_NS 1000000u
+#endif
 __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t phase) {
   const uint32_t addr = smem_u32(bar);
   uint32_t ok = 0;
@@ -93,7 +96,7 @@ __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t phase) {
 #endif
   do {
     asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
-                 "selp.u32 %0, 1, 0, p;\n\t}" : "=r"(ok) : "r"(addr), "r"(phase), "r"(1000000u) : "memory");
+                 "selp.u32 %0, 1, 0, p;\n\t}" : "=r"(ok) : "r"(addr), "r"(phase), "r"(TRD_SLEEP_NS) : "memory");
 #if TRD_DEBUG_HANG
     if (!ok && g_debug_hang && (++spins & 255u) == 0u) {
       const long long now = clock64();
@@ -1045,6 +1048,20 @@ static void launch_tc_pass_t(Context& c, const BlockPlan& bp, const TcStage& st,
 
 void tc_debug_dump() {
   static long long tr[256 * 16];
+  if (getenv("TRD_TC_EXP") && (atoi(getenv("TRD_TC_EXP")) & 64) &&
+      cudaMemcpyFromSymbol(tr, g_trace, sizeof(tr)) == cudaSuccess) {
+    fprintf(stderr, "[trd tc trace2] pass-2 CTA 0 units (cycles rel. to unit 0 issue start)\n"
+                    "  unit | MMA start bfull tfree issued | EPI start | h0: skfull dumped entries barred | h1: ...\n");
+    const long long t0 = tr[0];
+    for (int i = 0; i < 40; ++i) {
+      const long long* q = tr + i * 16;
+      auto f = [&](int k) { return q[k] ? q[k] - t0 : -1; };
+      fprintf(stderr, "  %4d | %7lld %5lld %5lld %5lld | %7lld | %5lld %5lld %5lld %5lld | %5lld %5lld %5lld %5lld\n", i,
+              f(0), q[1] - q[0], q[2] - q[0], q[3] - q[0], f(4), q[5] - q[4], q[6] - q[4], q[7] - q[4], q[8] - q[4],
+              q[9] - q[4], q[10] - q[4], q[11] - q[4], q[12] - q[4]);
+    }
+    return;
+  }
   if (cudaMemcpyFromSymbol(tr, g_trace, sizeof(tr)) == cudaSuccess && tr[0] != 0) {
     fprintf(stderr, "[trd tc trace] pass-1 CTA 0 (cycles rel. to tile 0 GEMM1 start)\n"
                     "  tile | G1 start wait issue | G2 start wait issue | EPI start skfull sfull dumped ppfree done fenced barred\n");
