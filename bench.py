@@ -342,7 +342,8 @@ def run_mine(args):
             traffic = json.load(open(tp)).get(spec.name, {}).get(dom)
         except Exception:
             traffic = None
-    roof = {"bound": "alu", "kernel": f"{dom} (trd pass_kernel)", "achieved": achieved,
+    kname = {"pass1": "tc_pass1_kernel", "pass2": "tc_pass2_kernel"}[dom]
+    roof = {"bound": "alu", "kernel": f"{dom} ({kname}, libtrd)", "achieved": achieved,
             "peak": p_fp32, "unit": "TFLOP/s", "frac": achieved / p_fp32, "traffic": traffic,
             "peak_source": f"FP32 FMA: {SM_COUNT} SM x {FP32_LANES_PER_SM} lanes x 2 x "
                            f"{sm_max:.0f} MHz ({src} sm_max_mhz)",
