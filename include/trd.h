@@ -23,7 +23,9 @@
  * sticky error state in which only trd_get_cores / trd_last_error / trd_destroy are valid.
  *
  * Threading: a context is used by one host thread at a time.  All device work is enqueued
- * on the stream given to trd_init.  No call keeps pointers to caller host memory.
+ * on the stream given to trd_init (trd_upload's copies: on a library copy stream ordered
+ * against it).  No call keeps pointers to caller host memory, except that trd_upload's
+ * asynchronous copy reads its host buffers until the call that consumes the upload returns.
  */
 #ifndef TRD_H
 #define TRD_H
@@ -129,9 +131,13 @@ typedef struct {
 TRD_API trd_status trd_init(const trd_config* cfg, const trd_shard* shard,
                     const float* const* init_cores, void* stream, trd_ctx** out);
 
-/* Re-copy host-resident X / P into the context's device buffers (shard.host == 1 only):
- * the host->device leg of an end-to-end step.  Asynchronous on the context stream;
- * host memory should be pinned for overlap.  Same layout and sizes as at trd_init. */
+/* Copy host-resident X / P (shard.host == 1 only) for a later sweep: the host->device leg of
+ * an end-to-end step.  The copy runs on the library's copy stream into one of two device
+ * buffer sets, so it overlaps the sweeps already enqueued; the next trd_sweep consumes the
+ * oldest pending upload (waits for its copy, restages, recomputes the packed rank prefix).
+ * At most two uploads may be pending (TRD_ERR_STATE otherwise).  Same layout and sizes as at
+ * trd_init (packed: same number of observed entries).  The host buffers (pinned for overlap)
+ * must stay unmodified until the trd_sweep that consumes them returns. */
 TRD_API trd_status trd_upload(trd_ctx* ctx, const float* values_host, const uint32_t* mask_host);
 
 /* Write the RStS index sets of sweep `sweep`, block k (Alg. 1 line 4; reading R11)

@@ -662,11 +662,46 @@ trd_status trd_upload(trd_ctx* ctx, const float* values_host, const uint32_t* ma
   if (!c || !values_host || !mask_host) return TRD_ERR_INVALID_ARG;
   if (c->sticky) return c->sticky;
   if (!c->own_values || !c->own_mask) return fail(c, TRD_ERR_STATE, "shard is not host-resident");
-  CUDA_TRY(c, cudaMemcpyAsync(c->own_mask, mask_host, c->n_words * 4, cudaMemcpyHostToDevice, c->stream));
-  CUDA_TRY(c, cudaMemcpyAsync(c->own_values, values_host, c->n_values * 4, cudaMemcpyHostToDevice, c->stream));
+  if (c->up_npend >= 2) return fail(c, TRD_ERR_STATE, "two uploads already pending (run a sweep first)");
+  trd_status st;
+  if (!c->copy) {                            // lazily: copy stream, events, second buffer set
+    CUDA_TRY(c, cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking));
+    for (int b = 0; b < 2; ++b) CUDA_TRY(c, cudaEventCreateWithFlags(&c->ev_up_ready[b], cudaEventDisableTiming));
+    CUDA_TRY(c, cudaEventCreateWithFlags(&c->ev_up_free, cudaEventDisableTiming));
+    c->up_values[0] = c->own_values;
+    c->up_mask[0] = c->own_mask;
+    if ((st = dalloc(c, &c->up_values[1], (size_t)c->n_values))) return st;
+    if ((st = dalloc(c, &c->up_mask[1], (size_t)c->n_words))) return st;
+  }
+  // target: the set that is neither the active one nor pending (with one upload pending,
+  // the active set -- the next sweep switches away from it before any later use)
+  const int b = c->up_npend == 0 ? 1 - c->up_active : 1 - c->up_pend[0];
+  // the copy may only overwrite b after all work enqueued so far (which may read it) is done
+  CUDA_TRY(c, cudaEventRecord(c->ev_up_free, c->stream));
+  CUDA_TRY(c, cudaStreamWaitEvent(c->copy, c->ev_up_free, 0));
+  CUDA_TRY(c, cudaMemcpyAsync(c->up_mask[b], mask_host, c->n_words * 4, cudaMemcpyHostToDevice, c->copy));
+  CUDA_TRY(c, cudaMemcpyAsync(c->up_values[b], values_host, c->n_values * 4, cudaMemcpyHostToDevice, c->copy));
+  CUDA_TRY(c, cudaEventRecord(c->ev_up_ready[b], c->copy));
+  c->up_pend[c->up_npend++] = b;
+  return check_launch(c, "upload");
+}
+
+// start of a sweep: switch to the oldest pending upload (its copy finished before any kernel
+// of this sweep reads it), rebuild the packed rank prefix, invalidate the staged sketches
+static trd_status consume_upload(Context* c) {
+  if (c->up_npend == 0) return TRD_OK;
+  const int b = c->up_pend[0];
+  c->up_pend[0] = c->up_pend[1];
+  --c->up_npend;
+  CUDA_TRY(c, cudaStreamWaitEvent(c->stream, c->ev_up_ready[b], 0));
+  c->up_active = b;
+  c->own_values = c->up_values[b];
+  c->own_mask = c->up_mask[b];
+  c->values = c->own_values;
+  c->mask = c->own_mask;
   if (c->packed) launch_rank_prefix(*c, c->stream);
   for (int k = 0; k < c->N; ++k) c->stage[k].valid = false;   // staged sketches are stale
-  return check_launch(c, "upload");
+  return check_launch(c, "upload consume");
 }
 
 trd_status trd_sketch(trd_ctx* ctx, int32_t sweep, int32_t k, int32_t* idx_dev, int64_t* sizes_host) {
@@ -700,6 +735,7 @@ trd_status trd_sweep(trd_ctx* ctx, int32_t n_sweeps, trd_sweep_stats* stats) {
   if (n_sweeps == 0) return TRD_OK;
   trd_status st = ensure_stats(c, n_sweeps);
   if (st) return st;
+  if ((st = consume_upload(c))) return st;
   cudaStream_t s = c->stream;
   std::vector<cudaEvent_t> ev;
   if (stats) {
@@ -755,6 +791,7 @@ trd_status trd_block_probe(trd_ctx* ctx, int32_t sweep, int32_t k, double* d_hos
   if (!c) return TRD_ERR_INVALID_ARG;
   if (c->sticky) return c->sticky;
   if (k < 0 || k >= c->N || sweep < 0) return TRD_ERR_INVALID_ARG;
+  if (trd_status su = consume_upload(c)) return su;
   const BlockPlan& bp = c->plan[k];
   cudaStream_t s = c->stream;
   int saved = 0;
@@ -796,6 +833,7 @@ trd_status trd_error(trd_ctx* ctx, const float* ref_dev, const uint32_t* eval_bi
   Context* c = reinterpret_cast<Context*>(ctx);
   if (!c || !ref_dev || !out) return TRD_ERR_INVALID_ARG;
   if (c->sticky) return c->sticky;
+  if (trd_status su = consume_upload(c)) return su;
   const BlockPlan& bp = c->full_plan;
   cudaStream_t s = c->stream;
   launch_sampler(*c, bp, s);
@@ -861,6 +899,19 @@ void trd_destroy(trd_ctx* ctx) {
   if (c->nccl_comm && g_nccl.comm_destroy) g_nccl.comm_destroy(c->nccl_comm);
   for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
   if (c->side) { cudaStreamSynchronize(c->side); cudaStreamDestroy(c->side); }
+  if (c->copy) { cudaStreamSynchronize(c->copy); cudaStreamDestroy(c->copy); }
+  for (int b = 0; b < 2; ++b)
+    if (c->ev_up_ready[b]) cudaEventDestroy(c->ev_up_ready[b]);
+  if (c->ev_up_free) cudaEventDestroy(c->ev_up_free);
+  // own_values / own_mask point at one of the two sets: free both sets once
+  if (c->up_values[0]) {
+    for (int b = 0; b < 2; ++b) {
+      if (c->up_values[b]) cudaFree(c->up_values[b]);
+      if (c->up_mask[b]) cudaFree(c->up_mask[b]);
+    }
+    c->own_values = nullptr;
+    c->own_mask = nullptr;
+  }
   if (c->ev_fork) cudaEventDestroy(c->ev_fork);
   if (c->ev_join) cudaEventDestroy(c->ev_join);
   void* ptrs[] = {c->own_values, c->own_mask, c->rank_prefix, c->Z, c->Q, c->idx, c->doff,
@@ -871,6 +922,7 @@ void trd_destroy(trd_ctx* ctx) {
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->tw) cudaFree(c->tw);
+  if (c->rp_tmp) cudaFree(c->rp_tmp);
   if (getenv("TRD_TC_EXP")) tc_debug_dump();
   for (int k = 0; k < kMaxN; ++k) {
     TcStage& sg = c->stage[k];

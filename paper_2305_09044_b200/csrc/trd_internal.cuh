@@ -116,8 +116,17 @@ struct Context {
   const uint32_t* mask = nullptr;
   float* own_values = nullptr;         // host-resident shards: library-owned copies
   uint32_t* own_mask = nullptr;
+  // double-buffered uploads (host-resident shards): buffer set b = (up_values[b], up_mask[b]);
+  // set 0 aliases own_values / own_mask.  `active` feeds the sweeps; pending uploads form a FIFO
+  float* up_values[2] = {nullptr, nullptr};
+  uint32_t* up_mask[2] = {nullptr, nullptr};
+  int up_active = 0, up_npend = 0, up_pend[2] = {0, 0};
+  cudaStream_t copy = nullptr;
+  cudaEvent_t ev_up_ready[2] = {nullptr, nullptr}, ev_up_free = nullptr;
   int64_t n_values = 0;
   uint32_t* rank_prefix = nullptr;     // packed layout: exclusive popcount prefix per word
+  void* rp_tmp = nullptr;              // its scan's scratch (allocated once)
+  size_t rp_tmp_bytes = 0;
 
   // model (device)
   float* Z = nullptr;                  // cores, slice-major: Z_k[i][a][b]

@@ -1291,10 +1291,13 @@ void launch_rank_prefix(Context& c, cudaStream_t s) {
   c.launches++;
   size_t tmp = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, tmp, c.rank_prefix, c.rank_prefix, c.n_words, s);
-  void* dtmp = nullptr;
-  cudaMallocAsync(&dtmp, tmp, s);
-  cub::DeviceScan::ExclusiveSum(dtmp, tmp, c.rank_prefix, c.rank_prefix, c.n_words, s);
-  cudaFreeAsync(dtmp, s);
+  if (tmp > c.rp_tmp_bytes) {                 // once per context (no allocation per upload)
+    if (c.rp_tmp) cudaFree(c.rp_tmp);
+    c.rp_tmp = nullptr;
+    c.rp_tmp_bytes = 0;
+    if (cudaMalloc(&c.rp_tmp, tmp) == cudaSuccess) c.rp_tmp_bytes = tmp;
+  }
+  cub::DeviceScan::ExclusiveSum(c.rp_tmp, tmp, c.rank_prefix, c.rank_prefix, c.n_words, s);
   c.launches += 1;
 }
 

@@ -223,6 +223,49 @@ def test_packed_equals_dense_bitwise_and_deterministic():
         ctx.close()
 
 
+def test_pipelined_uploads_are_consumed_in_order():
+    """trd_upload copies into one of two device buffer sets on a copy stream and each sweep
+    consumes the oldest pending upload.  Two uploads queued ahead of two sweeps give the same
+    cores, bit for bit, as one upload per sweep, and the first of them the same cores as a
+    context created on that data (fixed sigma: no init-time dependence on the data)."""
+    _cuda()
+    import torch
+    spec = small_spec("C4", [16, 16, 16, 16], [8, 8, 8, 8])
+    prob = make_problem(spec)
+    over = dict(sigma_mode=O.SIGMA_FIXED, sigma=0.7)
+    v1 = prob.packed_values().cpu().pin_memory()
+    m = prob.mask.cpu().pin_memory()
+    v2 = (v1 * 0.5 + 0.25).pin_memory()
+    a = gpu_context(prob, packed=True, host=True, **over)
+    a.upload(v2, m)
+    a.upload(v1, m)
+    from paper_2305_09044_b200.trd import TrdError
+    with pytest.raises(TrdError):
+        a.upload(v1, m)                                   # at most two pending
+    a.sweep(1, stats=False)
+    a1 = a.get_cores()
+    a.sweep(1, stats=False)
+    a2 = a.get_cores()
+    b = gpu_context(prob, packed=True, host=True, **over)
+    b.upload(v2, m)
+    b.sweep(1, stats=False)
+    b.upload(v1, m)
+    b.sweep(1, stats=False)
+    b2 = b.get_cores()
+    from paper_2305_09044_b200 import TRD
+    c = TRD(spec.dims, spec.ranks, v2.cuda(), m.cuda(), prob.init, packed=True,
+            sketch=spec.sketch, seed=spec.sampler_seed, **over)
+    c.sweep(1, stats=False)
+    c1 = c.get_cores()
+    torch.cuda.synchronize()
+    for x, y in zip(a1, c1):
+        assert np.array_equal(x, y)
+    for x, y in zip(a2, b2):
+        assert np.array_equal(x, y)
+    for ctx in (a, b, c):
+        ctx.close()
+
+
 def test_sigma_inf_and_fixed_step_modes():
     """sigma = inf (W == 1) and a fixed step eta (config step > 0) vs the oracle."""
     _cuda()
