@@ -563,11 +563,16 @@ __global__ void __launch_bounds__(128) stage_bits_kernel(StageArgs s) {
   }
 }
 
+// the tile block is assembled in shared memory (scattered entry positions) and written out
+// coalesced; tiles with more than SV_OUT entries write to global memory directly
+constexpr int SV_OUT = 1024;
 __global__ void __launch_bounds__(128) stage_vals_kernel(StageArgs s) {
   __shared__ int64_t sco[TC_NT];
   __shared__ uint32_t sstart[2];
   __shared__ uint64_t sbits[TC_M];
   __shared__ int soff[TC_M];
+  __shared__ __align__(16) float sov[SV_OUT];
+  __shared__ __align__(16) uint16_t soi[SV_OUT];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   for (int64_t tile = blockIdx.x; tile < s.n_tiles; tile += gridDim.x) {
     const int64_t rt = tile / s.n_col_tiles, ct = tile % s.n_col_tiles;
@@ -575,13 +580,17 @@ __global__ void __launch_bounds__(128) stage_vals_kernel(StageArgs s) {
     const uint64_t bits = s.tbits[tile * TC_M + tid];
     const int roff = s.troff[tile * TC_M + tid];
     const int64_t tb = (int64_t)s.tcount[tile];          // tile block start (after the scan)
+    const int nt = (int)((int64_t)s.tcount[tile + 1] - tb);   // padded entry count of the tile
+    const bool in_smem = nt <= SV_OUT;
+    float* ov = in_smem ? sov : s.tvals + tb;            // tile-relative output positions
+    uint16_t* oi = in_smem ? soi : s.tidx + tb;
     sbits[tid] = bits;
     soff[tid] = roff;
     stage_tile_cols(s, ct, tid, sco, sstart);            // (its barriers also publish sbits / soff)
     if (tid == TC_M - 1) {                    // padding entries of the tile block
-      for (int64_t e = tb + roff + __popcll(bits); e < (int64_t)s.tcount[tile + 1]; ++e) {
-        s.tidx[e] = 0xFFFFu;
-        s.tvals[e] = 0.f;
+      for (int e = roff + __popcll(bits); e < nt; ++e) {
+        oi[e] = 0xFFFFu;
+        ov[e] = 0.f;
       }
     }
     const int64_t ro = row < s.nrows ? s.row_off[row] : -1;
@@ -604,19 +613,19 @@ __global__ void __launch_bounds__(128) stage_vals_kernel(StageArgs s) {
           const int r = __ffs(cw) - 1;
           cw &= cw - 1;
           const int rr = warp * 32 + r;                   // row in the tile
-          const int64_t pos = tb + soff[rr] + __popcll(sbits[rr] & ((1ull << j) - 1ull));
+          const int pos = soff[rr] + __popcll(sbits[rr] & ((1ull << j) - 1ull));
           int64_t vi;
           if (r < wr.b) vi = s.packed ? va + qa++ : la + r;
           else vi = s.packed ? vb + qb++ : lb + (r - wr.b);
-          s.tvals[pos] = __ldg(s.values + vi);
-          s.tidx[pos] = (uint16_t)(rr * TC_NT + j);
+          ov[pos] = __ldg(s.values + vi);
+          oi[pos] = (uint16_t)(rr * TC_NT + j);
         }
       }
     } else if (bits && __popcll((uint64_t)sstart[0] | ((uint64_t)sstart[1] << 32)) > 16) {
       // scattered columns: per entry, the rank from its mask word (cached across entries)
       const int64_t rof = s.row_off[row];
-      float* out = s.tvals + tb + roff;
-      uint16_t* oidx = s.tidx + tb + roff;
+      float* out = ov + roff;
+      uint16_t* oidx = oi + roff;
       int q = 0;
       int64_t cwi = -1;
       uint32_t cwd = 0, cp = 0;
@@ -636,8 +645,8 @@ __global__ void __launch_bounds__(128) stage_vals_kernel(StageArgs s) {
       }
     } else if (bits) {
       // row-wise over the column runs: a run's observed values are consecutive
-      float* out = s.tvals + tb + roff;
-      uint16_t* oidx = s.tidx + tb + roff;
+      float* out = ov + roff;
+      uint16_t* oidx = oi + roff;
       int q = 0;
       uint64_t st = (uint64_t)sstart[0] | ((uint64_t)sstart[1] << 32);
       while (st) {
@@ -667,6 +676,13 @@ __global__ void __launch_bounds__(128) stage_vals_kernel(StageArgs s) {
           }
         }
       }
+    }
+    if (in_smem) {                              // (block-uniform)
+      __syncthreads();
+      float4* gv = reinterpret_cast<float4*>(s.tvals + tb);     // tile blocks: 8-entry aligned
+      uint4* gi = reinterpret_cast<uint4*>(s.tidx + tb);
+      for (int q = tid; q < nt / 4; q += TC_M) gv[q] = reinterpret_cast<const float4*>(sov)[q];
+      for (int q = tid; q < nt / 8; q += TC_M) gi[q] = reinterpret_cast<const uint4*>(soi)[q];
     }
     __syncthreads();
   }
