@@ -597,14 +597,15 @@ __global__ void __launch_bounds__(128) stage_vals_kernel(StageArgs s) {
     WarpRows wr;
     if (warp_row_segments(ro, lane, wr)) {
       // column-wise: lane j takes columns j and j + 32; each row range of the warp is one run of
-      // linear positions per column, so its packed values are consecutive
+      // linear positions per column, so its packed values are consecutive.  The columns' row
+      // masks come from the staged row masks by a warp bit-matrix transpose (no mask reads)
+      const uint32_t cws[2] = {warp_transpose32((uint32_t)bits, lane), warp_transpose32((uint32_t)(bits >> 32), lane)};
 #pragma unroll 1
       for (int h = 0; h < 2; ++h) {
         const int j = lane + 32 * h;
         const int64_t co = sco[j];
-        if (co < 0) continue;
-        uint32_t cw = warp_col_bits(s, wr, co);
-        if (!cw) continue;
+        uint32_t cw = cws[h];
+        if (co < 0 || !cw) continue;
         const int64_t la = wr.baseA + co, lb = wr.baseB + co;   // linear positions of lanes 0, b
         const int64_t va = s.packed ? mask_rank(s, la) : la;
         const int64_t vb = (s.packed && wr.b < 32) ? mask_rank(s, lb) : lb;

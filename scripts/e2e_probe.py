@@ -59,11 +59,10 @@ for i in range(4):
     t2 = time.perf_counter()
     print("call %d: wall %.2f ms, wall+sync %.2f ms, events %.2f ms" % (i, (t1 - t0) * 1e3, (t2 - t0) * 1e3,
                                                                      e0.elapsed_time(e1)))
-print("upload only      %.2f ms" % timed(lambda: ctx.upload(vals_h, words_h)))
 print("sweep (cached)   %.2f ms" % timed(lambda: ctx.sweep(1, stats=True)))
 print("sweep x3 / 3     %.2f ms" % timed(lambda: ctx.sweep(3, stats=True), n=1) + " (per 3)")
 print("sweep no stats   %.2f ms" % timed(lambda: ctx.sweep(1, stats=False)))
-print("upload + sweep   %.2f ms" % timed(lambda: (ctx.upload(vals_h, words_h), ctx.sweep(1, stats=True))))
+print("upload + sweep   %.2f ms (copy in line)" % timed(lambda: (ctx.upload(vals_h, words_h), ctx.sweep(1, stats=True))))
 x = torch.empty(vals_h.numel() + words_h.numel(), dtype=torch.float32, device="cuda")
 h = torch.empty(x.numel(), dtype=torch.float32).pin_memory()
 print("torch H2D copy   %.2f ms" % timed(lambda: x.copy_(h, non_blocking=True)))
