@@ -83,7 +83,19 @@ typedef struct {
   int32_t world, rank;              /* data-parallel group; world == 1: no NCCL             */
   const void* nccl_unique_id;       /* 128 bytes from trd_nccl_unique_id() on rank 0,
                                        broadcast by the caller; NULL when world == 1         */
+  int32_t scaling;                  /* operator of the update direction (ablation arms of
+                                       Sec. 6.1): TRD_SCALING_GLOBAL h = d M with the
+                                       FGMC Gram (Eq. 16, default); TRD_SCALING_NONE h = d
+                                       ('gradient descent'); TRD_SCALING_LOCAL the Gram of the
+                                       sampled cores (Z_k)_{I_k} ('local scaled term').  The
+                                       stop metric (Alg. 1 l.12) always uses the FGMC Gram.  */
 } trd_config;
+
+typedef enum {
+  TRD_SCALING_GLOBAL = 0,
+  TRD_SCALING_NONE = 1,
+  TRD_SCALING_LOCAL = 2
+} trd_scaling;
 
 /* Local shard of X and P.  Local tensor = global X restricted to
  * i_{shard_mode} in [shard_begin, shard_end), stored in its own linear order (same formula

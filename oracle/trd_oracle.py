@@ -31,6 +31,9 @@ import numpy as np
 from .philox import sample_indices
 
 SIGMA_FIXED, SIGMA_INF, SIGMA_RMS = 0, 1, 2
+# operator of the update direction: the paper's scaled gradient (Eq. 16) and the two
+# ablation arms of Sec. 6.1 built on the same sketch
+SCALING_GLOBAL, SCALING_NONE, SCALING_LOCAL = 0, 1, 2
 
 
 # ----------------------------------------------------------------------------------------
@@ -287,7 +290,8 @@ class Config:
     """Algorithm 1 inputs plus the readings' parameters."""
 
     def __init__(self, dims, ranks, sigma_mode=SIGMA_RMS, sigma=1.0, sigma_theta=1.0,
-                 sigma_min=1e-3, lambda_rel=1e-6, step=0.0, sketch=None, seed=0, eps=0.0):
+                 sigma_min=1e-3, lambda_rel=1e-6, step=0.0, sketch=None, seed=0, eps=0.0,
+                 scaling=SCALING_GLOBAL):
         self.dims = list(dims)
         self.ranks = list(ranks)
         self.sigma_mode = sigma_mode
@@ -299,6 +303,29 @@ class Config:
         self.sketch = list(sketch) if sketch is not None else [0] * len(dims)
         self.seed = seed
         self.eps = eps
+        self.scaling = scaling
+
+
+def gram_local(cores, k, sets, ranks):
+    """'Local scaled term' ablation arm: the Gram G_{Z_I^{!=k}} of the
+    subchain of the sampled cores {(Z_m)_{I_m}}, computed as Eq. (13) with
+    each Q_m summed over the sampled slices only."""
+    N = len(cores)
+    Qs = [q_matrix(cores[m][:, sets[m], :]) if m != k else None for m in range(N)]
+    return gram_fgmc(Qs, k, ranks)
+
+
+def update_direction(cfg, d, G_global, cores, k, sets):
+    """Update direction of block k: h = d (G + lambda I)^-1-filtered (Eq. 16) with the FGMC
+    Gram, or an ablation arm of Sec. 6.1: 'gradient descent' h = d (Eq. 15's
+    d_I instead of h_I), 'local scaled term' the same filtered solve with gram_local."""
+    if cfg.scaling == SCALING_NONE:
+        return d.copy()
+    if cfg.scaling == SCALING_LOCAL:
+        h, _ = scaled_gradient(d, gram_local(cores, k, sets, cfg.ranks), cfg.lambda_rel)
+        return h
+    h, _ = scaled_gradient(d, G_global, cfg.lambda_rel)
+    return h
 
 
 def index_sets_for_block(cfg, t, k):
@@ -374,8 +401,9 @@ def block_update(cfg, st, source, k, rec, check_gram=False):
         Sf = subchain(st.cores, k)
         Gx = gram_explicit(Sf)
         assert np.linalg.norm(G - Gx) <= 1e-10 * max(np.linalg.norm(Gx), 1e-300)
-    # line 9: scaled gradient (Eq. 10/16), step (Eq. 12/18), update (Eq. 11/17, reading R2)
-    h, _ = scaled_gradient(d, G, cfg.lambda_rel)
+    # line 9: scaled gradient (Eq. 10/16; or an ablation arm), step (Eq. 12/18), update
+    # (Eq. 11/17, reading R2)
+    h = update_direction(cfg, d, G, st.cores, k, sets)
     num = float(np.sum(d * h))
     den = line_search_den(h, Pk, W, S)
     rec.num[k], rec.den[k] = num, den

@@ -246,12 +246,21 @@ trd_status block_pass1(Context* c, const BlockPlan& bp) {
   cudaStream_t s = c->stream;
   // a8 + a9 (FGMC Gram, filtered operator M) depend only on the cores != k: run them on the
   // side stream, overlapping the sampler / staging / pass 1 (which leaves one SM free)
+  // (the sampler first: the local-scaled-term arm builds its Gram from the sampled slices)
+  launch_sampler(*c, bp, s);
   CUDA_TRY(c, cudaEventRecord(c->ev_fork, s));
   CUDA_TRY(c, cudaStreamWaitEvent(c->side, c->ev_fork, 0));
-  launch_gram(*c, bp, c->side);
-  launch_solve(*c, bp, c->side);
+  launch_gram(*c, bp, c->side, c->Q, c->G);             // FGMC Gram (also the stop metric's)
+  if (c->cfg.scaling == TRD_SCALING_GLOBAL) {
+    launch_solve(*c, bp, c->side, c->G);
+  } else if (c->cfg.scaling == TRD_SCALING_NONE) {
+    launch_identity_op(*c, bp, c->side);                 // h = d ('gradient descent' arm)
+  } else {                                               // 'local scaled term' arm
+    launch_q_sampled(*c, bp, c->side);
+    launch_gram(*c, bp, c->side, c->Qloc, c->Gloc);
+    launch_solve(*c, bp, c->side, c->Gloc);
+  }
   CUDA_TRY(c, cudaEventRecord(c->ev_join, c->side));
-  launch_sampler(*c, bp, s);
   launch_plan(*c, bp, s);
   if (!bp.use_tc) launch_lft(*c, bp, c->Z + c->zoff[bp.k], 0, c->lft, s);
   TcStage& stg = c->stage[bp.k];
@@ -442,6 +451,7 @@ trd_status trd_init(const trd_config* cfg, const trd_shard* shard, const float* 
   if (cfg->sigma_mode == TRD_SIGMA_RMS && (!(cfg->sigma_theta > 0.0) || !(cfg->sigma_min > 0.0)))
     return TRD_ERR_INVALID_ARG;
   if (!(cfg->lambda_rel >= 0.0) || !(cfg->step >= 0.0)) return TRD_ERR_INVALID_ARG;
+  if (cfg->scaling < TRD_SCALING_GLOBAL || cfg->scaling > TRD_SCALING_LOCAL) return TRD_ERR_INVALID_ARG;
   if (cfg->world < 1 || cfg->rank < 0 || cfg->rank >= cfg->world) return TRD_ERR_INVALID_ARG;
   if (cfg->shard_mode < 0 || cfg->shard_mode >= N) return TRD_ERR_SHAPE;
   if (cfg->world > 1 && !cfg->nccl_unique_id) return TRD_ERR_INVALID_ARG;
@@ -566,6 +576,9 @@ trd_status trd_init(const trd_config* cfg, const trd_shard* shard, const float* 
       (st = dalloc(c, &c->chain_ws, chain_cap)) || (st = dalloc(c, &c->h, max_h)) ||
       (st = dalloc(c, &c->Dcur, (size_t)(In * In))) || (st = dalloc(c, &c->Dprev, (size_t)(In * In))) ||
       (st = dalloc(c, &c->sc, 1)) || (st = dalloc(c, &c->red_ws, 1024)))
+    return bail(st);
+  if (cfg->scaling == TRD_SCALING_LOCAL &&
+      ((st = dalloc(c, &c->Qloc, (size_t)qtot)) || (st = dalloc(c, &c->Gloc, (size_t)kMaxR2 * kMaxR2))))
     return bail(st);
   if (max_lhl > 0) {
     if ((st = dalloc(c, &c->lftHL, max_lhl)) || (st = dalloc(c, &c->lfthHL, max_lhl)) ||
@@ -918,7 +931,7 @@ void trd_destroy(trd_ctx* ctx) {
                   c->row_off, c->col_off, c->mid, c->lft, c->lfth, c->rgtT, c->dpart, c->spart,
                   c->denpart, c->numpart, c->dvec, c->G, c->G_last, c->Mop, c->chol_ws,
                   c->chain_ws, c->h, c->Dcur, c->Dprev, c->sc, c->stats, c->red_ws,
-                  c->lftHL, c->lfthHL, c->rgtHL, c->rgtHL2, c->contrib};
+                  c->lftHL, c->lfthHL, c->rgtHL, c->rgtHL2, c->contrib, c->Qloc, c->Gloc};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->tw) cudaFree(c->tw);

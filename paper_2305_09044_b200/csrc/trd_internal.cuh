@@ -132,6 +132,8 @@ struct Context {
   float* Z = nullptr;                  // cores, slice-major: Z_k[i][a][b]
   int64_t zoff[kMaxN + 1];
   double* Q = nullptr;                 // FGMC Q_k (r_k^2 x r_{k+1}^2)
+  double* Qloc = nullptr;              // 'local scaled term' arm: Q_m over the sampled slices
+  double* Gloc = nullptr;              //   and its Gram
   int64_t qoff[kMaxN + 1];
 
   // plans and per-block workspaces (device)
@@ -193,8 +195,10 @@ void launch_pass1(Context& c, const BlockPlan& bp, int stats_only, cudaStream_t 
 void launch_reduce_d(Context& c, const BlockPlan& bp, cudaStream_t s);
 void launch_block_stats(Context& c, const BlockPlan& bp, cudaStream_t s);
 void launch_q(Context& c, int k, cudaStream_t s);
-void launch_gram(Context& c, const BlockPlan& bp, cudaStream_t s);
-void launch_solve(Context& c, const BlockPlan& bp, cudaStream_t s);
+void launch_gram(Context& c, const BlockPlan& bp, cudaStream_t s, const double* Qsrc, double* Gout);
+void launch_solve(Context& c, const BlockPlan& bp, cudaStream_t s, const double* G);
+void launch_q_sampled(Context& c, const BlockPlan& bp, cudaStream_t s);
+void launch_identity_op(Context& c, const BlockPlan& bp, cudaStream_t s);
 void launch_h(Context& c, const BlockPlan& bp, cudaStream_t s);
 void launch_pass2(Context& c, const BlockPlan& bp, cudaStream_t s);
 void launch_reduce_den(Context& c, const BlockPlan& bp, cudaStream_t s);

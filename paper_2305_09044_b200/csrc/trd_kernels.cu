@@ -1173,10 +1173,48 @@ void launch_q(Context& c, int k, cudaStream_t s) {
   c.launches++;
 }
 
-void launch_gram(Context& c, const BlockPlan& bp, cudaStream_t s) {
+// Q_m over a subset of slices (the 'local scaled term' ablation arm: the Gram of the
+// sampled cores (Z_m)_{I_m}): Q[(a r + a'), (b r' + b')] = sum_{i in idx} Z(i)[a][b] Z(i)[a'][b']
+__global__ void q_idx_kernel(const float* __restrict__ Zk, const int* __restrict__ idx, int64_t n_idx, int r0,
+                             int r1, double* __restrict__ Qk) {
+  const int n0 = r0 * r0, n1 = r1 * r1;
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n0 * n1; t += gridDim.x * blockDim.x) {
+    const int row = t / n1, col = t % n1;
+    const int a = row / r0, ap = row % r0, b = col / r1, bp = col % r1;
+    double acc = 0.0;
+    for (int64_t q = 0; q < n_idx; ++q) {
+      const float* S = Zk + (int64_t)idx[q] * r0 * r1;
+      acc += (double)S[a * r1 + b] * (double)S[ap * r1 + bp];
+    }
+    Qk[t] = acc;
+  }
+}
+
+void launch_q_sampled(Context& c, const BlockPlan& bp, cudaStream_t s) {
+  for (int m = 0; m < c.N; ++m) {
+    if (m == bp.k) continue;
+    const int r0 = c.ranks[m], r1 = c.ranks[(m + 1) % c.N];
+    q_idx_kernel<<<grid_for((int64_t)r0 * r0 * r1 * r1), 256, 0, s>>>(c.Z + c.zoff[m], c.idx + c.idx_off[m], bp.s[m],
+                                                                       r0, r1, c.Qloc + c.qoff[m]);
+    c.launches++;
+  }
+}
+
+__global__ void identity_kernel(double* __restrict__ M, int n) {
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n * n; t += gridDim.x * blockDim.x)
+    M[t] = (t / n == t % n) ? 1.0 : 0.0;
+}
+
+// M = I: h = d M = d (the 'gradient descent' ablation arm)
+void launch_identity_op(Context& c, const BlockPlan& bp, cudaStream_t s) {
+  identity_kernel<<<grid_for((int64_t)bp.R2 * bp.R2), 256, 0, s>>>(c.Mop, bp.R2);
+  c.launches++;
+}
+
+void launch_gram(Context& c, const BlockPlan& bp, cudaStream_t s, const double* Qsrc, double* Gout) {
   const int N = c.N, k = bp.k;
   // C = Q_{k+1} Q_{k+2} ... Q_{k-1}
-  const double* cur = c.Q + c.qoff[(k + 1) % N];
+  const double* cur = Qsrc + c.qoff[(k + 1) % N];
   int m_rows = bp.rk1 * bp.rk1;
   double* bufs[2] = {c.chain_ws, c.chain_ws + kMaxR2 * kMaxR2};
   int which = 0;
@@ -1185,16 +1223,16 @@ void launch_gram(Context& c, const BlockPlan& bp, cudaStream_t s) {
     const int qcols = c.ranks[(mm + 1) % N] * c.ranks[(mm + 1) % N];
     const int qin = c.ranks[mm] * c.ranks[mm];
     dim3 grid((qcols + 15) / 16, (m_rows + 15) / 16);
-    matmul_f64_kernel<<<grid, dim3(16, 16), 0, s>>>(cur, c.Q + c.qoff[mm], bufs[which], m_rows, qcols, qin);
+    matmul_f64_kernel<<<grid, dim3(16, 16), 0, s>>>(cur, Qsrc + c.qoff[mm], bufs[which], m_rows, qcols, qin);
     c.launches++;
     cur = bufs[which];
     which ^= 1;
   }
-  phi_kernel<<<grid_for((int64_t)bp.R2 * bp.R2), 256, 0, s>>>(cur, bp.rk, bp.rk1, c.G);
+  phi_kernel<<<grid_for((int64_t)bp.R2 * bp.R2), 256, 0, s>>>(cur, bp.rk, bp.rk1, Gout);
   c.launches++;
 }
 
-void launch_solve(Context& c, const BlockPlan& bp, cudaStream_t s) {
+void launch_solve(Context& c, const BlockPlan& bp, cudaStream_t s, const double* G) {
   const int n = bp.R2;
   if (n <= kGjMaxN) {
     const size_t gneed = (size_t)2 * n * n * sizeof(double);
@@ -1208,10 +1246,10 @@ void launch_solve(Context& c, const BlockPlan& bp, cudaStream_t s) {
       gj_attr = true;
     }
     const int nb = (n + 31) / 32;
-    if (nb == 1) gj_solve_kernel<1><<<1, 1024, gneed, s>>>(c.G, n, c.cfg.lambda_rel, c.Mop, c.sc);
-    else if (nb == 2) gj_solve_kernel<2><<<1, 1024, gneed, s>>>(c.G, n, c.cfg.lambda_rel, c.Mop, c.sc);
-    else if (nb == 3) gj_solve_kernel<3><<<1, 1024, gneed, s>>>(c.G, n, c.cfg.lambda_rel, c.Mop, c.sc);
-    else gj_solve_kernel<4><<<1, 1024, gneed, s>>>(c.G, n, c.cfg.lambda_rel, c.Mop, c.sc);
+    if (nb == 1) gj_solve_kernel<1><<<1, 1024, gneed, s>>>(G, n, c.cfg.lambda_rel, c.Mop, c.sc);
+    else if (nb == 2) gj_solve_kernel<2><<<1, 1024, gneed, s>>>(G, n, c.cfg.lambda_rel, c.Mop, c.sc);
+    else if (nb == 3) gj_solve_kernel<3><<<1, 1024, gneed, s>>>(G, n, c.cfg.lambda_rel, c.Mop, c.sc);
+    else gj_solve_kernel<4><<<1, 1024, gneed, s>>>(G, n, c.cfg.lambda_rel, c.Mop, c.sc);
     c.launches++;
     return;
   }
@@ -1222,7 +1260,7 @@ void launch_solve(Context& c, const BlockPlan& bp, cudaStream_t s) {
     cudaFuncSetAttribute(solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attr_set = true;
   }
-  solve_kernel<<<1, kSolveThreads, use_smem ? need : 0, s>>>(c.G, n, c.cfg.lambda_rel, c.Mop,
+  solve_kernel<<<1, kSolveThreads, use_smem ? need : 0, s>>>(G, n, c.cfg.lambda_rel, c.Mop,
                                                              c.chol_ws, use_smem, c.sc);
   c.launches++;
 }

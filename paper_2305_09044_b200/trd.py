@@ -27,6 +27,9 @@ class TrdError(RuntimeError):
         super().__init__(f"{STATUS.get(status, status)}: {msg}")
 
 
+TRD_SCALING_GLOBAL, TRD_SCALING_NONE, TRD_SCALING_LOCAL = 0, 1, 2   # trd_scaling (ablation arms)
+
+
 class trd_config(ctypes.Structure):
     _fields_ = [("order", ctypes.c_int32),
                 ("dims", ctypes.c_int64 * TRD_MAX_ORDER),
@@ -42,7 +45,8 @@ class trd_config(ctypes.Structure):
                 ("shard_mode", ctypes.c_int32),
                 ("world", ctypes.c_int32),
                 ("rank", ctypes.c_int32),
-                ("nccl_unique_id", ctypes.c_void_p)]
+                ("nccl_unique_id", ctypes.c_void_p),
+                ("scaling", ctypes.c_int32)]
 
 
 class trd_shard(ctypes.Structure):
@@ -157,7 +161,8 @@ class TRD:
     def __init__(self, dims, ranks, values, mask, init_cores, *, sigma_mode=TRD_SIGMA_RMS,
                  sigma=1.0, sigma_theta=1.0, sigma_min=1e-3, lambda_rel=1e-6, step=0.0,
                  sketch=None, seed=0, shard_mode=0, shard_range=None, world=1, rank=0,
-                 nccl_id: Optional[bytes] = None, packed=False, host=False, stream=None):
+                 nccl_id: Optional[bytes] = None, packed=False, host=False, stream=None,
+                 scaling=0):
         import torch
         self.lib = load_library()
         N = len(dims)
@@ -177,6 +182,7 @@ class TRD:
         cfg.shard_mode = int(shard_mode)
         cfg.world = int(world)
         cfg.rank = int(rank)
+        cfg.scaling = int(scaling)
         self._nccl_buf = None
         if nccl_id is not None:
             self._nccl_buf = ctypes.create_string_buffer(nccl_id, 128)

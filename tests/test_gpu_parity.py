@@ -132,6 +132,39 @@ def test_block_quantities_match_oracle(name, dims, sketch, packed):
     ctx.close()
 
 
+@pytest.mark.parametrize("scaling", [O.SCALING_NONE, O.SCALING_LOCAL])
+def test_ablation_arms_match_oracle(scaling):
+    """Sec. 6.1 ablation arms on an RStS sketch: 'gradient descent' (h = d) and
+    'local scaled term' (Gram of the sampled cores): d, h, num, den per block at t = 0, and
+    the cores after two sweeps."""
+    _cuda()
+    spec = small_spec("C4", [12, 11, 10, 9], [4, 5, 3, 4])
+    prob = make_problem(spec)
+    src, _ = oracle_source(prob)
+    cfg = oracle_config(spec, scaling=scaling)
+    st = O.State(cfg, prob.init, src)
+    ctx = gpu_context(prob, packed=True, scaling=scaling)
+    for k in range(len(spec.dims)):
+        g = ctx.block_probe(0, k)
+        sets = O.index_sets_for_block(cfg, 0, k)
+        Xk, Pk = O.working_set(src, k, sets)
+        S = O.subchain(st.cores, k, sets)
+        d, E, W = O.gradient_block(Xk, Pk, O.core_unfold2(st.cores[k]), S, st.sigma, False)
+        h = O.update_direction(cfg, d, O.gram_fgmc(st.Qs, k, spec.ranks), st.cores, k, sets)
+        num = float(np.sum(d * h))
+        den = O.line_search_den(h, Pk, W, S)
+        assert rel_fro(g["d"], d) <= 1e-4, k
+        assert rel_fro(g["h"], h) <= 1e-4, k
+        assert abs(g["num"] - num) <= 1e-4 * abs(num), k
+        assert abs(g["den"] - den) <= 1e-4 * abs(den), k
+    ctx.close()
+    st2, _ = O.run(cfg, prob.init, src, 2)
+    ctx = gpu_context(prob, packed=True, scaling=scaling)
+    ctx.sweep(2, stats=False)
+    assert cores_rel_err(ctx.get_cores(), st2.cores) <= 1e-4
+    ctx.close()
+
+
 # ---------------------------------------------------------------------------- sweeps
 SWEEP_CASES = [
     ("C1", [32, 32, 32], None),

@@ -556,3 +556,68 @@ def test_gradient_entries_equals_dense_gradient_block():
             d_ent, se2 = O.gradient_entries(cores, k, idx, X[P], sigma, sinf)
             assert np.allclose(d_ent, d_dense, rtol=1e-12, atol=1e-12)
             assert abs(se2 - float(np.sum(E[Pk] ** 2))) <= 1e-10 * float(np.sum(E[Pk] ** 2))
+
+
+# ---------------------------------------------------------------- ablation arms (Sec. 6.1)
+@pytest.mark.parametrize("seed", range(3))
+def test_local_gram_equals_explicit_gram_of_sampled_subchain(seed):
+    """'Local scaled term' arm: the Gram of the subchain of the sampled cores
+    (P:239), built as Eq. (13) over the sampled slices, equals S_I^T S_I formed explicitly
+    from the sampled subchain rows."""
+    dims, ranks = [5, 4, 6, 3], [2, 3, 2, 2]
+    cores = rand_cores(dims, ranks, seed + 300)
+    rng = np.random.default_rng(seed)
+    for k in range(4):
+        sets = [np.arange(dims[m]) if m == k else np.sort(rng.choice(dims[m], 2, replace=False))
+                for m in range(4)]
+        G = O.gram_local(cores, k, sets, ranks)
+        Gx = O.gram_explicit(O.subchain(cores, k, sets))
+        assert np.linalg.norm(G - Gx) <= 1e-12 * np.linalg.norm(Gx)
+
+
+def test_local_gram_with_full_sets_is_the_fgmc_gram():
+    dims, ranks = [4, 3, 5], [2, 3, 2]
+    cores = rand_cores(dims, ranks, 7)
+    sets = [np.arange(I) for I in dims]
+    Qs = [O.q_matrix(Z) for Z in cores]
+    for k in range(3):
+        assert np.allclose(O.gram_local(cores, k, sets, ranks), O.gram_fgmc(Qs, k, ranks),
+                           rtol=1e-13, atol=0.0)
+
+
+@pytest.mark.parametrize("scaling", [O.SCALING_NONE, O.SCALING_LOCAL])
+def test_ablation_arm_steps_are_exact_line_searches(scaling):
+    """Both arms keep Eq. (12)'s exact line search along their own direction: the block step
+    minimises the weighted residual along +h (cost(eta) <= cost(0.99 eta), cost(1.01 eta));
+    'gradient descent' moves along d itself (d_I instead of h_I)."""
+    dims, ranks = [6, 5, 4], [2, 3, 2]
+    gt = rand_cores(dims, ranks, 11)
+    rng = np.random.default_rng(12)
+    X = O.tr_reconstruct(gt) + 0.05 * rng.standard_normal(dims)
+    P = rng.random(dims) < 0.7
+    cfg = O.Config(dims, ranks, sigma_mode=O.SIGMA_FIXED, sigma=0.8, sketch=[4, 3, 3], seed=5,
+                   scaling=scaling)
+    src = O.DenseSource(X, P)
+    st = O.State(cfg, rand_cores(dims, ranks, 13), src)
+    for k in range(3):
+        sets = O.index_sets_for_block(cfg, st.t, k)
+        Xk, Pk = O.working_set(src, k, sets)
+        S = O.subchain(st.cores, k, sets)
+        Zk2 = O.core_unfold2(st.cores[k])
+        d, E, W = O.gradient_block(Xk, Pk, Zk2, S, st.sigma, False)
+        h = O.update_direction(cfg, d, O.gram_fgmc(st.Qs, k, ranks), st.cores, k, sets)
+        if scaling == O.SCALING_NONE:
+            assert np.array_equal(h, d)
+        num, den = float(np.sum(d * h)), O.line_search_den(h, Pk, W, S)
+        assert num > 0 and den > 0
+        eta = num / den
+
+        def cost(t):
+            Et = Xk - (Zk2 + t * h) @ S.T
+            return 0.5 * np.sum(W * Pk * Et * Et)
+        c0 = cost(eta)
+        assert c0 <= cost(0.99 * eta) + 1e-12 and c0 <= cost(1.01 * eta) + 1e-12
+        assert c0 < cost(0.0)
+        rec = O.SweepRecord(3)
+        O.block_update(cfg, st, src, k, rec)
+        assert abs(rec.eta[k] - eta) <= 1e-12 * eta
