@@ -62,7 +62,11 @@ typedef enum {
 typedef enum {
   TRD_SIGMA_FIXED = 0,  /* Alg. 1 input sigma, kept fixed                        */
   TRD_SIGMA_INF = 1,    /* sigma -> inf: W == 1, the masked LS problem Eq. 2     */
-  TRD_SIGMA_RMS = 2     /* reading R9: sigma_{t+1} = max(sigma_min, theta * RMS(e))      */
+  TRD_SIGMA_RMS = 2,    /* reading R9: sigma_{t+1} = max(sigma_min, theta * RMS(e))      */
+  TRD_SIGMA_MAD = 3     /* reading R21 (robust rule): sigma_{t+1} = max(sigma_min,
+                           theta * 1.4826 * median |e|) over the sweep's pass-1 residuals, the
+                           median from a 512-bin histogram of |e| (16 linear sub-bins per
+                           octave over 2^-20 .. 2^12) with linear interpolation in its bin   */
 } trd_sigma_mode;
 
 typedef struct {
@@ -138,7 +142,7 @@ typedef struct {
 
 /* Create a context.  init_cores: host pointers, N arrays float[r_k][I_k][r_{k+1}] (Alg. 1
  * line 1).  stream: a cudaStream_t (NULL = legacy default stream).  Builds the FGMC
- * cache Q_k and, for TRD_SIGMA_RMS, sigma_0 from all local observed residuals
+ * cache Q_k and, for TRD_SIGMA_RMS / MAD, sigma_0 from all local observed residuals
  * (allreduced).  Synchronises the stream once.  *out is NULL on failure. */
 TRD_API trd_status trd_init(const trd_config* cfg, const trd_shard* shard,
                     const float* const* init_cores, void* stream, trd_ctx** out);

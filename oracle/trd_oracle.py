@@ -30,7 +30,12 @@ import numpy as np
 
 from .philox import sample_indices
 
-SIGMA_FIXED, SIGMA_INF, SIGMA_RMS = 0, 1, 2
+SIGMA_FIXED, SIGMA_INF, SIGMA_RMS, SIGMA_MAD = 0, 1, 2, 3
+# robust sigma (reading R21): sigma = max(sigma_min, theta * MAD_C * median |e|), the median
+# estimated from a histogram of |e| with 16 linear sub-bins per octave over 2^-20 .. 2^12
+MAD_C = 1.4826                     # 1 / Phi^-1(3/4): MAD -> standard deviation for Gaussians
+HIST_E0, HIST_OCT, HIST_SUB = -20, 32, 16
+HIST_BINS = HIST_OCT * HIST_SUB
 # operator of the update direction: the paper's scaled gradient (Eq. 16) and the two
 # ablation arms of Sec. 6.1 built on the same sketch
 SCALING_GLOBAL, SCALING_NONE, SCALING_LOCAL = 0, 1, 2
@@ -340,13 +345,51 @@ def index_sets_for_block(cfg, t, k):
     return sets
 
 
+def hist_bin(ae):
+    """Bin of |e| (reading R21): bin (E - E0) * 16 + m covers [(1 + m/16) 2^E, (1 + (m+1)/16) 2^E);
+    values below 2^E0 (and 0) fall in bin 0, values >= 2^(E0 + 32) in the last bin."""
+    ae = np.asarray(ae, dtype=np.float64)
+    f, x = np.frexp(ae)                        # ae = f 2^x, f in [0.5, 1)
+    E = x - 1
+    m = np.floor((2.0 * f - 1.0) * HIST_SUB).astype(np.int64)
+    b = (E - HIST_E0) * HIST_SUB + m
+    b = np.where(E < HIST_E0, 0, b)
+    b = np.where(E >= HIST_E0 + HIST_OCT, HIST_BINS - 1, b)
+    return np.where(ae > 0.0, b, 0)
+
+
+def hist_median(counts):
+    """Median from the |e| histogram: the bin where the cumulative count reaches n/2, linear
+    interpolation inside it (reading R21)."""
+    counts = np.asarray(counts, dtype=np.float64)
+    target = 0.5 * float(counts.sum())
+    cum = 0.0
+    for b in range(HIST_BINS):
+        c = float(counts[b])
+        if c > 0.0 and cum + c >= target:
+            E, m = HIST_E0 + b // HIST_SUB, b % HIST_SUB
+            lo = (1.0 + m / HIST_SUB) * 2.0 ** E
+            return lo + (target - cum) / c * (2.0 ** E / HIST_SUB)
+        cum += c
+    return 0.0
+
+
+def mad_sigma(cfg, abs_e):
+    """R21: sigma = max(sigma_min, theta * 1.4826 * histogram median of |e|)."""
+    counts = np.bincount(hist_bin(abs_e), minlength=HIST_BINS)
+    return max(cfg.sigma_min, cfg.sigma_theta * MAD_C * hist_median(counts))
+
+
 def initial_sigma(cfg, cores, source):
-    """sigma_0 for the RMS reading R9: max(sigma_min, theta * RMS of the observed residuals
-    at the initial cores), over all observed entries."""
-    if cfg.sigma_mode != SIGMA_RMS:
+    """sigma_0 for the RMS reading R9 (or the MAD reading R21): max(sigma_min, theta * RMS
+    (or 1.4826 median |e|)) of the observed residuals at the initial cores, over all
+    observed entries."""
+    if cfg.sigma_mode not in (SIGMA_RMS, SIGMA_MAD):
         return cfg.sigma
     Xhat = tr_reconstruct([c.astype(np.float64) for c in cores])
     E = (source.X - Xhat)[source.P]
+    if cfg.sigma_mode == SIGMA_MAD:
+        return mad_sigma(cfg, np.abs(E))
     return max(cfg.sigma_min, cfg.sigma_theta * math.sqrt(float(np.mean(E * E))))
 
 
@@ -362,6 +405,7 @@ class SweepRecord:
         self.den = [0.0] * N
         self.nnz = [0] * N
         self.skipped = [False] * N
+        self.abs_e = []                      # |e| of every pass-1 residual (MAD rule, R21)
 
 
 class State:
@@ -390,6 +434,8 @@ def block_update(cfg, st, source, k, rec, check_gram=False):
     d, E, W = gradient_block(Xk, Pk, Zk2, S, st.sigma, sigma_inf)
     e_obs = E[Pk]
     rec.sum_e2 += float(np.sum(e_obs * e_obs))
+    if cfg.sigma_mode == SIGMA_MAD:
+        rec.abs_e.append(np.abs(e_obs))
     rec.n_obs += int(e_obs.size)
     rec.nnz[k] = int(e_obs.size)
     s2 = st.sigma * st.sigma if abs(st.sigma) < 1e150 else float('inf')
@@ -440,6 +486,9 @@ def sweep(cfg, st, source, check_gram=False):
     # sigma for the next sweep (reading R9)
     if cfg.sigma_mode == SIGMA_RMS and rec.n_obs > 0:
         st.sigma = max(cfg.sigma_min, cfg.sigma_theta * math.sqrt(rec.sum_e2 / rec.n_obs))
+    elif cfg.sigma_mode == SIGMA_MAD and rec.n_obs > 0:
+        st.sigma = mad_sigma(cfg, np.concatenate(rec.abs_e))
+        rec.abs_e = []
     st.t += 1
     return rec
 

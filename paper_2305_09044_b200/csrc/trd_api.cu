@@ -317,6 +317,7 @@ trd_status ensure_stats(Context* c, int n) {
 trd_status sigma0_pass(Context* c) {
   const BlockPlan& bp = c->full_plan;
   cudaStream_t s = c->stream;
+  if (c->hist) CUDA_TRY(c, cudaMemsetAsync(c->hist, 0, kHistBins * sizeof(double), s));
   launch_sampler(*c, bp, s);
   launch_plan(*c, bp, s);
   launch_lft(*c, bp, c->Z + c->zoff[bp.k], 0, c->lft, s);
@@ -332,6 +333,7 @@ trd_status sigma0_pass(Context* c) {
   if (st) return st;
   st = allreduce(c, c->red_ws, 3);
   if (st) return st;
+  if (c->hist && (st = allreduce(c, c->hist, (size_t)kHistBins))) return st;
   launch_sigma0(*c, s);
   return check_launch(c, "sigma0");
 }
@@ -446,9 +448,10 @@ trd_status trd_init(const trd_config* cfg, const trd_shard* shard, const float* 
     if (!init_cores[m]) return TRD_ERR_INVALID_ARG;
     if (cfg->sketch[m] > 0 && cfg->sketch[m] < cfg->dims[m] && cfg->dims[m] > 16384) return TRD_ERR_SHAPE;
   }
-  if (cfg->sigma_mode < 0 || cfg->sigma_mode > 2) return TRD_ERR_INVALID_ARG;
+  if (cfg->sigma_mode < 0 || cfg->sigma_mode > TRD_SIGMA_MAD) return TRD_ERR_INVALID_ARG;
   if (cfg->sigma_mode == TRD_SIGMA_FIXED && !(cfg->sigma > 0.0)) return TRD_ERR_INVALID_ARG;
-  if (cfg->sigma_mode == TRD_SIGMA_RMS && (!(cfg->sigma_theta > 0.0) || !(cfg->sigma_min > 0.0)))
+  if ((cfg->sigma_mode == TRD_SIGMA_RMS || cfg->sigma_mode == TRD_SIGMA_MAD) &&
+      (!(cfg->sigma_theta > 0.0) || !(cfg->sigma_min > 0.0)))
     return TRD_ERR_INVALID_ARG;
   if (!(cfg->lambda_rel >= 0.0) || !(cfg->step >= 0.0)) return TRD_ERR_INVALID_ARG;
   if (cfg->scaling < TRD_SCALING_GLOBAL || cfg->scaling > TRD_SCALING_LOCAL) return TRD_ERR_INVALID_ARG;
@@ -577,6 +580,7 @@ trd_status trd_init(const trd_config* cfg, const trd_shard* shard, const float* 
       (st = dalloc(c, &c->Dcur, (size_t)(In * In))) || (st = dalloc(c, &c->Dprev, (size_t)(In * In))) ||
       (st = dalloc(c, &c->sc, 1)) || (st = dalloc(c, &c->red_ws, 1024)))
     return bail(st);
+  if (cfg->sigma_mode == TRD_SIGMA_MAD && (st = dalloc(c, &c->hist, (size_t)kHistBins))) return bail(st);
   if (cfg->scaling == TRD_SCALING_LOCAL &&
       ((st = dalloc(c, &c->Qloc, (size_t)qtot)) || (st = dalloc(c, &c->Gloc, (size_t)kMaxR2 * kMaxR2))))
     return bail(st);
@@ -662,7 +666,7 @@ trd_status trd_init(const trd_config* cfg, const trd_shard* shard, const float* 
     int r = g_nccl.comm_init_rank(&c->nccl_comm, cfg->world, id, cfg->rank);
     if (r != 0) return bail(fail(c, TRD_ERR_NCCL, "ncclCommInitRank failed (%d)", r));
   }
-  if (cfg->sigma_mode == TRD_SIGMA_RMS) {
+  if (cfg->sigma_mode == TRD_SIGMA_RMS || cfg->sigma_mode == TRD_SIGMA_MAD) {
     if ((st = sigma0_pass(c))) return bail(st);
   }
   CUDA_TRY(c, cudaStreamSynchronize(s));
@@ -758,6 +762,7 @@ trd_status trd_sweep(trd_ctx* ctx, int32_t n_sweeps, trd_sweep_stats* stats) {
   }
   for (int t = 0; t < n_sweeps; ++t) {
     launch_sweep_begin(*c, t, s);
+    if (c->hist) CUDA_TRY(c, cudaMemsetAsync(c->hist, 0, kHistBins * sizeof(double), s));
     for (int k = 0; k < c->N; ++k) {
       const BlockPlan& bp = c->plan[k];
       if ((st = block_pass1(c, bp))) return st;
@@ -768,6 +773,7 @@ trd_status trd_sweep(trd_ctx* ctx, int32_t n_sweeps, trd_sweep_stats* stats) {
       launch_q(*c, k, s);
       if ((st = check_launch(c, "update"))) return st;
     }
+    if (c->hist && (st = allreduce(c, c->hist, (size_t)kHistBins))) return st;   // (world > 1)
     launch_sweep_end(*c, t, s);
     if ((st = check_launch(c, "sweep end"))) return st;
     if (stats) CUDA_TRY(c, cudaEventRecord(ev[(size_t)t + 1], s));
@@ -931,7 +937,7 @@ void trd_destroy(trd_ctx* ctx) {
                   c->row_off, c->col_off, c->mid, c->lft, c->lfth, c->rgtT, c->dpart, c->spart,
                   c->denpart, c->numpart, c->dvec, c->G, c->G_last, c->Mop, c->chol_ws,
                   c->chain_ws, c->h, c->Dcur, c->Dprev, c->sc, c->stats, c->red_ws,
-                  c->lftHL, c->lfthHL, c->rgtHL, c->rgtHL2, c->contrib, c->Qloc, c->Gloc};
+                  c->lftHL, c->lfthHL, c->rgtHL, c->rgtHL2, c->contrib, c->Qloc, c->Gloc, c->hist};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->tw) cudaFree(c->tw);

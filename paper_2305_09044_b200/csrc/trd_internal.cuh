@@ -26,6 +26,19 @@ struct DevStats {
 };
 
 // Scalars shared by the kernels of one block (device memory).
+// |e| histogram of the robust sigma rule (reading R21, TRD_SIGMA_MAD): bin (E - E0) * 16 + m
+// covers [(1 + m/16) 2^E, (1 + (m+1)/16) 2^E), E in [E0, E0 + 32); below -> bin 0, above ->
+// the last bin.  Read off the fp32 exponent and the top 4 mantissa bits.
+constexpr int kHistBins = 512, kHistE0 = -20;
+__device__ __forceinline__ int mad_bin(float ae) {
+  if (!(ae > 0.f)) return 0;
+  const uint32_t b = __float_as_uint(ae);
+  const int E = (int)(b >> 23) - 127;
+  if (E < kHistE0) return 0;
+  if (E >= kHistE0 + 32) return kHistBins - 1;
+  return (E - kHistE0) * 16 + (int)((b >> 19) & 15u);
+}
+
 struct DevScalars {
   double sigma;          // kernel width of the current sweep
   double num, den;       // <d,h> and the line-search denominator of the current block
@@ -132,6 +145,7 @@ struct Context {
   float* Z = nullptr;                  // cores, slice-major: Z_k[i][a][b]
   int64_t zoff[kMaxN + 1];
   double* Q = nullptr;                 // FGMC Q_k (r_k^2 x r_{k+1}^2)
+  double* hist = nullptr;              // TRD_SIGMA_MAD: |e| histogram of the sweep (counts)
   double* Qloc = nullptr;              // 'local scaled term' arm: Q_m over the sampled slices
   double* Gloc = nullptr;              //   and its Gram
   int64_t qoff[kMaxN + 1];

@@ -305,6 +305,7 @@ struct PassArgs {
   double* dpart;      // [ik][cta][R2]
   double* spart;      // [ik][cta][3]
   double* denpart;    // [ik][cta]
+  double* hist;       // TRD_SIGMA_MAD: |e| histogram (pass 1), else nullptr
 };
 
 __device__ __forceinline__ float warp_sum_f(float v) {
@@ -340,7 +341,12 @@ pass_kernel(PassArgs a) {
   __shared__ float lfhS[kPassWarps][PASS2 ? KT : 1];
   __shared__ float dS[kPassWarps][KT];
   __shared__ double redS[kPassWarps][kMaxR2 + 3];
+  __shared__ uint32_t histS[PASS2 ? 1 : kHistBins];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (!PASS2 && a.hist) {
+    for (int b = threadIdx.x; b < kHistBins; b += blockDim.x) histS[b] = 0u;
+    __syncthreads();
+  }
   const int64_t ik = blockIdx.y;
   const int64_t jl0 = (int64_t)blockIdx.x * a.jl_per_cta;
   const int jlc = (int)min((int64_t)a.jl_per_cta, a.nL - jl0);
@@ -401,6 +407,7 @@ pass_kernel(PassArgs a) {
           st_e2 += (double)e * (double)e;
           st_n += 1.0;
           st_w += s2 * (1.0 - (double)w);
+          if (a.hist) atomicAdd(&histS[mad_bin(fabsf(e))], 1u);
         }
         if (!STATS_ONLY) {
           const float cv = obs ? w * e : 0.f;
@@ -455,6 +462,11 @@ pass_kernel(PassArgs a) {
     }
     return;
   }
+  if (a.hist) {                              // (PASS2 returned above)
+    __syncthreads();
+    for (int b = threadIdx.x; b < kHistBins; b += blockDim.x)
+      if (histS[b]) atomicAdd(&a.hist[b], (double)histS[b]);   // integer counts: exact in any order
+  }
   {
     double v0 = warp_sum_d(st_e2), v1 = warp_sum_d(st_w), v2 = warp_sum_d(st_n);
     if (lane == 0) { redS[warp][kMaxR2] = v0; redS[warp][kMaxR2 + 1] = v1; redS[warp][kMaxR2 + 2] = v2; }
@@ -494,6 +506,7 @@ static PassArgs make_pass_args(const Context& c, const BlockPlan& bp) {
   a.values = c.values; a.mask = c.mask; a.rank_prefix = c.rank_prefix;
   a.sc = c.sc;
   a.dpart = c.dpart; a.spart = c.spart; a.denpart = c.denpart;
+  a.hist = c.cfg.sigma_mode == TRD_SIGMA_MAD ? c.hist : nullptr;
   return a;
 }
 
@@ -940,9 +953,28 @@ __global__ void dt_D_kernel(const float* __restrict__ Zn, int64_t In, int rk, in
   }
 }
 
+// R21: 1.4826 x the histogram median of |e| (bin reaching n/2, linear inside it)
+__device__ double hist_median_sigma(const double* __restrict__ hist, double theta, double sigma_min) {
+  double n = 0.0;
+  for (int b = 0; b < kHistBins; ++b) n += hist[b];
+  const double target = 0.5 * n;
+  double cum = 0.0, med = 0.0;
+  for (int b = 0; b < kHistBins; ++b) {
+    const double c = hist[b];
+    if (c > 0.0 && cum + c >= target) {
+      const int E = kHistE0 + b / 16, m = b % 16;
+      const double lo = (1.0 + m / 16.0) * ldexp(1.0, E);
+      med = lo + (target - cum) / c * ldexp(1.0, E) / 16.0;
+      break;
+    }
+    cum += c;
+  }
+  return fmax(sigma_min, theta * 1.4826 * med);
+}
+
 __global__ void sweep_end_kernel(double* __restrict__ D, double* __restrict__ Dprev, int64_t n2,
                                  DevScalars* sc, DevStats* stats, int slot, int sigma_mode,
-                                 double theta, double sigma_min) {
+                                 double theta, double sigma_min, const double* __restrict__ hist) {
   __shared__ double a1[1024], a2[1024];
   double s1 = 0.0, s2 = 0.0;
   for (int64_t t = threadIdx.x; t < n2; t += blockDim.x) {
@@ -961,6 +993,7 @@ __global__ void sweep_end_kernel(double* __restrict__ D, double* __restrict__ Dp
     stats[slot].stop_e = e;
     if (sigma_mode == TRD_SIGMA_RMS && sc->acc_n > 0.0)
       sc->sigma = fmax(sigma_min, theta * sqrt(sc->acc_e2 / sc->acc_n));
+    if (sigma_mode == TRD_SIGMA_MAD && sc->acc_n > 0.0) sc->sigma = hist_median_sigma(hist, theta, sigma_min);
     sc->have_prev_D = 1;
     sc->sweep += 1;
   }
@@ -970,9 +1003,10 @@ __global__ void sweep_end_kernel(double* __restrict__ D, double* __restrict__ Dp
 
 // sigma_0 = max(sigma_min, theta * RMS) from [sum_e2, welsch, n] (after allreduce)
 __global__ void sigma0_kernel(const double* __restrict__ s3, DevScalars* sc, double theta,
-                              double sigma_min) {
+                              double sigma_min, const double* __restrict__ hist) {
   if (threadIdx.x == 0 && blockIdx.x == 0)
-    sc->sigma = fmax(sigma_min, theta * sqrt(s3[0] / fmax(s3[2], 1.0)));
+    sc->sigma = hist ? hist_median_sigma(hist, theta, sigma_min)
+                     : fmax(sigma_min, theta * sqrt(s3[0] / fmax(s3[2], 1.0)));
 }
 
 // ----------------------------------------------------------------------------------------
@@ -1294,14 +1328,15 @@ void launch_sweep_end(Context& c, int slot, cudaStream_t s) {
   dt_T_kernel<<<(unsigned)In, 128, 0, s>>>(c.Z + c.zoff[n], In, rk, rk1, c.G_last, T);
   dt_D_kernel<<<grid_for(In * In), 256, 0, s>>>(c.Z + c.zoff[n], In, rk, rk1, T, c.Dcur);
   sweep_end_kernel<<<1, 1024, 0, s>>>(c.Dcur, c.Dprev, In * In, c.sc, c.stats, slot,
-                                      c.cfg.sigma_mode, c.cfg.sigma_theta, c.cfg.sigma_min);
+                                      c.cfg.sigma_mode, c.cfg.sigma_theta, c.cfg.sigma_min, c.hist);
   c.launches += 3;
 }
 
 void launch_sigma0(Context& c, cudaStream_t s) {
   // dvec[Ik*R2 .. +3] of the stats-only full pass hold [sum_e2, welsch, n]; the caller
   // reduced them into red_ws[0..2]
-  sigma0_kernel<<<1, 32, 0, s>>>(c.red_ws, c.sc, c.cfg.sigma_theta, c.cfg.sigma_min);
+  sigma0_kernel<<<1, 32, 0, s>>>(c.red_ws, c.sc, c.cfg.sigma_theta, c.cfg.sigma_min,
+                                 c.cfg.sigma_mode == TRD_SIGMA_MAD ? c.hist : nullptr);
   c.launches++;
 }
 

@@ -708,6 +708,7 @@ struct TcArgs {
   const float* tvals;
   const uint16_t* tidx;    // staged entry lists
   float* tw;               // staged weights (pass 1 writes, pass 2 reads)
+  double* hist;            // TRD_SIGMA_MAD: |e| histogram (pass 1), else nullptr
   const DevScalars* sc;
   float* contrib;          // [split][nrows_pad][KP]  D rows of pass 1
   double* spart;           // [cta][3]
@@ -1019,6 +1020,7 @@ static TcArgs make_tc_args(const Context& c, const BlockPlan& bp, const TcStage&
   a.tw = c.tw;
   a.sc = c.sc;
   a.contrib = c.contrib; a.spart = c.spart; a.denpart = c.denpart;
+  a.hist = (!pass2 && c.cfg.sigma_mode == TRD_SIGMA_MAD) ? c.hist : nullptr;
   return a;
 }
 

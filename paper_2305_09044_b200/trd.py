@@ -15,7 +15,7 @@ LIB_PATH = os.environ.get("TRD_LIB_PATH") or os.path.join(HERE, "libtrd.so")   #
 HEADER = os.path.join(os.path.dirname(HERE), "include", "trd.h")
 
 TRD_MAX_ORDER = 8
-TRD_SIGMA_FIXED, TRD_SIGMA_INF, TRD_SIGMA_RMS = 0, 1, 2
+TRD_SIGMA_FIXED, TRD_SIGMA_INF, TRD_SIGMA_RMS, TRD_SIGMA_MAD = 0, 1, 2, 3
 STATUS = {0: "TRD_OK", 1: "TRD_ERR_INVALID_ARG", 2: "TRD_ERR_SHAPE", 3: "TRD_ERR_OOM",
           4: "TRD_ERR_CUDA", 5: "TRD_ERR_NCCL", 6: "TRD_ERR_NOT_SPD", 7: "TRD_ERR_NONFINITE",
           8: "TRD_ERR_STATE"}

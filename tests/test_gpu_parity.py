@@ -165,6 +165,25 @@ def test_ablation_arms_match_oracle(scaling):
     ctx.close()
 
 
+@pytest.mark.parametrize("name,dims,sketch", [("C1", [32, 32, 32], None), ("C4", [16, 16, 16, 16], [8, 8, 8, 8])])
+def test_robust_sigma_rule_matches_oracle(name, dims, sketch):
+    """Reading R21 (TRD_SIGMA_MAD): sigma_0 and each sweep's sigma from the |e| histogram
+    median (same bins on both sides), and the cores after two sweeps."""
+    _cuda()
+    spec = small_spec(name, dims, sketch)
+    prob = make_problem(spec)
+    src, _ = oracle_source(prob)
+    cfg = oracle_config(spec, sigma_mode=O.SIGMA_MAD)
+    st, recs = O.run(cfg, prob.init, src, 2)
+    ctx = gpu_context(prob, packed=True, sigma_mode=O.SIGMA_MAD)
+    g = ctx.sweep(2)
+    for t in range(2):
+        assert abs(g[t]["sigma"] - recs[t].sigma) <= 1e-5 * recs[t].sigma, (t, g[t]["sigma"], recs[t].sigma)
+    assert abs(g[1]["sigma"] - g[0]["sigma"]) > 0.0
+    assert cores_rel_err(ctx.get_cores(), st.cores) <= 1e-4
+    ctx.close()
+
+
 # ---------------------------------------------------------------------------- sweeps
 SWEEP_CASES = [
     ("C1", [32, 32, 32], None),
