@@ -807,28 +807,39 @@ __global__ void __launch_bounds__(1024) gj_solve_kernel(const double* __restrict
       if (i < n && j < n) Ainv[i * n + j] = a[u][v];
     }
   __syncthreads();
-  // T = G A^-1 (G from global / L1), then M = A^-1 T
+  // M = A^-1 G A^-1 = X - lam X^2 with X = A^-1 (G = A - lam I): one product X.X, all of
+  // this thread's NB x NB outputs accumulated together (independent FMA chains)
+  {
+    double acc[NB][NB];
 #pragma unroll
-  for (int u = 0; u < NB; ++u)
+    for (int u = 0; u < NB; ++u)
 #pragma unroll
-    for (int v = 0; v < NB; ++v) {
-      const int i = ty + 32 * u, j = tx + 32 * v;
-      if (i >= n || j >= n) continue;
-      double acc = 0.0;
-      for (int l = 0; l < n; ++l) acc = fma(__ldg(G + i * n + l), Ainv[l * n + j], acc);
-      Tm[i * n + j] = acc;
+      for (int v = 0; v < NB; ++v) acc[u][v] = 0.0;
+    for (int l = 0; l < n; ++l) {
+      double xr[NB], xc[NB];
+#pragma unroll
+      for (int u = 0; u < NB; ++u) {
+        const int i = ty + 32 * u;
+        xr[u] = i < n ? Ainv[i * n + l] : 0.0;
+      }
+#pragma unroll
+      for (int v = 0; v < NB; ++v) {
+        const int j = tx + 32 * v;
+        xc[v] = j < n ? Ainv[l * n + j] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < NB; ++u)
+#pragma unroll
+        for (int v = 0; v < NB; ++v) acc[u][v] = fma(xr[u], xc[v], acc[u][v]);
     }
-  __syncthreads();
 #pragma unroll
-  for (int u = 0; u < NB; ++u)
+    for (int u = 0; u < NB; ++u)
 #pragma unroll
-    for (int v = 0; v < NB; ++v) {
-      const int i = ty + 32 * u, j = tx + 32 * v;
-      if (i >= n || j >= n) continue;
-      double acc = 0.0;
-      for (int l = 0; l < n; ++l) acc = fma(Ainv[i * n + l], Tm[l * n + j], acc);
-      Mout[i * n + j] = acc;
-    }
+      for (int v = 0; v < NB; ++v) {
+        const int i = ty + 32 * u, j = tx + 32 * v;
+        if (i < n && j < n) Mout[i * n + j] = fma(-lam, acc[u][v], Ainv[i * n + j]);
+      }
+  }
   if (threadIdx.x == 0) sc->lambda = lam;
 }
 
