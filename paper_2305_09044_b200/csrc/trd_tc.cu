@@ -281,7 +281,7 @@ __global__ void __launch_bounds__(256) tc_lft_pack_kernel(LftArgs a, int pass2, 
 // one thread per row holds X(i_k) (RK x RK1) and Mid(j_L) (RK1 x RS) and produces the whole
 // row, Lft[a + RK c] = sum_b X[a][b] Mid[b][c] (fmaf over b ascending, as lft_kernel).
 template <int RK, int RK1, int RS>
-__global__ void __launch_bounds__(128) tc_lft_pack_rb_kernel(LftArgs a, int pass2, int64_t nrows_pad,
+__global__ void __launch_bounds__(128, 4) tc_lft_pack_rb_kernel(LftArgs a, int pass2, int64_t nrows_pad,
                                                              __half* __restrict__ dst) {
   constexpr int K = RK * RS;
   constexpr int KP = (K + 15) / 16 * 16;

@@ -132,6 +132,22 @@ def test_block_quantities_match_oracle(name, dims, sketch, packed):
     ctx.close()
 
 
+def test_large_ranks_use_the_simt_and_cholesky_paths():
+    """Ranks up to TRD_MAX_RANK: K = r_k r_s > 128 has no tensor-core kernel (SIMT pass
+    kernels) and R^2 > 112 takes the Cholesky solve instead of Gauss-Jordan; cores after one
+    sweep vs the oracle."""
+    _cuda()
+    spec = small_spec("C1", [14, 13, 12])
+    spec.ranks = [12, 14, 16]
+    prob = make_problem(spec)
+    src, _ = oracle_source(prob)
+    st, _ = O.run(oracle_config(spec), prob.init, src, 1)
+    ctx = gpu_context(prob, packed=True)
+    ctx.sweep(1)
+    assert cores_rel_err(ctx.get_cores(), st.cores) <= 1e-4
+    ctx.close()
+
+
 @pytest.mark.parametrize("scaling", [O.SCALING_NONE, O.SCALING_LOCAL])
 def test_ablation_arms_match_oracle(scaling):
     """Sec. 6.1 ablation arms on an RStS sketch: 'gradient descent' (h = d) and
