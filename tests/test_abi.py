@@ -52,3 +52,68 @@ def test_invalid_arguments_rejected_without_gpu():
     assert lib.trd_init(ctypes.byref(cfg), ctypes.byref(sh), arr, None, ctypes.byref(ctx)) in (1, 2)
     assert lib.trd_sweep(None, 1, None) == 1
     assert lib.trd_destroy(None) is None
+
+
+def test_ctypes_structs_match_the_c_header(tmp_path):
+    """trd_config / trd_shard / trd_sweep_stats / trd_error_stats / trd_profile: sizes and
+    field offsets of the ctypes mirrors equal the C header's (compiled with gcc here)."""
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    structs = {"trd_config": T.trd_config, "trd_shard": T.trd_shard,
+               "trd_sweep_stats": T.trd_sweep_stats}
+    for extra in ("trd_error_stats", "trd_profile"):
+        if hasattr(T, extra):
+            structs[extra] = getattr(T, extra)
+    lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "trd.h"', "int main(void) {"]
+    for name, cls in structs.items():
+        lines.append(f'  printf("{name} size %zu\\n", sizeof({name}));')
+        for fname, _ in cls._fields_:
+            lines.append(f'  printf("{name} {fname} %zu\\n", offsetof({name}, {fname}));')
+    lines += ["  return 0;", "}"]
+    src = tmp_path / "layout.c"
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "layout"
+    subprocess.run(["gcc", "-I", os.path.join(root, "include"), str(src), "-o", str(exe)], check=True)
+    out = subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.split("\n")
+    got = {}
+    for line in out:
+        if line.strip():
+            a, b, v = line.split()
+            got[(a, b)] = int(v)
+    for name, cls in structs.items():
+        assert got[(name, "size")] == ctypes.sizeof(cls), name
+        for fname, _ in cls._fields_:
+            assert got[(name, fname)] == getattr(cls, fname).offset, (name, fname)
+
+
+def test_new_config_values_are_validated_without_gpu():
+    """sigma_mode beyond TRD_SIGMA_MAD and scaling beyond TRD_SCALING_LOCAL are rejected."""
+    lib = T.load_library()
+    sh = T.trd_shard()
+    dummy = (ctypes.c_float * 16)()
+    sh.values = ctypes.cast(dummy, ctypes.c_void_p)
+    sh.mask_bits = ctypes.cast(dummy, ctypes.c_void_p)
+    sh.shard_begin, sh.shard_end = 0, 4
+    ctx = ctypes.c_void_p()
+    core = (ctypes.c_float * 64)()
+    arr = (ctypes.c_void_p * 8)(*([ctypes.cast(core, ctypes.c_void_p).value] * 8))
+    for field, bad in ((None, None), ("sigma_mode", 4), ("scaling", 3), ("scaling", -1)):
+        cfg = T.trd_config()
+        cfg.order = 3
+        for m in range(3):
+            cfg.dims[m] = 4
+            cfg.ranks[m] = 2
+        cfg.sigma_mode, cfg.sigma, cfg.sigma_theta, cfg.sigma_min = 2, 1.0, 1.0, 1e-3
+        cfg.world = 1
+        if field is None:                # a valid config gets past validation (then no GPU)
+            import torch
+            if torch.cuda.is_available():    # (dummy pointers: only probe without a device)
+                continue
+            st = lib.trd_init(ctypes.byref(cfg), ctypes.byref(sh), arr, None, ctypes.byref(ctx))
+            assert st != 1
+            if ctx.value:
+                lib.trd_destroy(ctx)
+            ctx = ctypes.c_void_p()
+            continue
+        setattr(cfg, field, bad)
+        assert lib.trd_init(ctypes.byref(cfg), ctypes.byref(sh), arr, None, ctypes.byref(ctx)) == 1, field
+        assert ctx.value is None
