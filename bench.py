@@ -40,6 +40,11 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget-s", type=float, default=15.0)
+    # variants of the method (defaults: the config's sigma rule, the paper's scaled gradient)
+    ap.add_argument("--sigma-mode", default=None, choices=["fixed", "inf", "rms", "mad"],
+                    help="sigma rule (mad: robust rule R21)")
+    ap.add_argument("--scaling", default="global", choices=["global", "none", "local"],
+                    help="update operator: Eq. 16 (global) or the Sec. 6.1 ablation arms")
     return ap.parse_args()
 
 
@@ -254,8 +259,14 @@ def run_mine(args):
         dist.broadcast_object_list(obj, src=0)
         nid = obj[0]
     stream = torch.cuda.current_stream()
-    kw = dict(sigma_mode=spec.sigma_mode, sketch=spec.sketch, seed=spec.sampler_seed,
-              shard_mode=0, shard_range=(b, e), world=world, rank=rank, nccl_id=nid, packed=True)
+    sigma_mode = spec.sigma_mode if args.sigma_mode is None else \
+        {"fixed": 0, "inf": 1, "rms": 2, "mad": 3}[args.sigma_mode]
+    scaling = {"global": 0, "none": 1, "local": 2}[args.scaling]
+    kw = dict(sigma_mode=sigma_mode, sketch=spec.sketch, seed=spec.sampler_seed,
+              shard_mode=0, shard_range=(b, e), world=world, rank=rank, nccl_id=nid, packed=True,
+              scaling=scaling)
+    if sigma_mode == 0:
+        kw["sigma"] = 1.0
     ctx = TRD(spec.dims, spec.ranks, vals, words, prob.init, **kw)
 
     # warm-up
@@ -388,7 +399,9 @@ def run_mine(args):
                            "storage": "packed observed values + bitmask",
                            "l2": "inputs larger than L2 (packed values + mask > 126 MB)"
                            if (vals.numel() + words.numel()) * 4 > 126e6 else "inputs fit in L2",
-                           "parallelism": f"dp{world} (X sharded along mode 0, NCCL allreduce)"},
+                           "parallelism": f"dp{world} (X sharded along mode 0, NCCL allreduce)",
+                           "sigma_rule": ["fixed", "inf", "rms", "mad"][sigma_mode],
+                           "update_operator": args.scaling},
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
                 "clocks": clk.summary(),
                 "per_sweep_ms": [r["ms"] for r in recs]}
