@@ -45,6 +45,8 @@ def parse():
                     help="sigma rule (mad: robust rule R21)")
     ap.add_argument("--scaling", default="global", choices=["global", "none", "local"],
                     help="update operator: Eq. 16 (global) or the Sec. 6.1 ablation arms")
+    ap.add_argument("--sampling", default="rsts", choices=["rsts", "rows"],
+                    help="working set: RStS subtensor or the uniform-row-sampling arm")
     return ap.parse_args()
 
 
@@ -264,7 +266,7 @@ def run_mine(args):
     scaling = {"global": 0, "none": 1, "local": 2}[args.scaling]
     kw = dict(sigma_mode=sigma_mode, sketch=spec.sketch, seed=spec.sampler_seed,
               shard_mode=0, shard_range=(b, e), world=world, rank=rank, nccl_id=nid, packed=True,
-              scaling=scaling)
+              scaling=scaling, sampling={"rsts": 0, "rows": 1}[args.sampling])
     if sigma_mode == 0:
         kw["sigma"] = 1.0
     ctx = TRD(spec.dims, spec.ranks, vals, words, prob.init, **kw)
@@ -401,7 +403,7 @@ def run_mine(args):
                            if (vals.numel() + words.numel()) * 4 > 126e6 else "inputs fit in L2",
                            "parallelism": f"dp{world} (X sharded along mode 0, NCCL allreduce)",
                            "sigma_rule": ["fixed", "inf", "rms", "mad"][sigma_mode],
-                           "update_operator": args.scaling},
+                           "update_operator": args.scaling, "sampling": args.sampling},
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
                 "clocks": clk.summary(),
                 "per_sweep_ms": [r["ms"] for r in recs]}

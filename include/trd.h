@@ -93,7 +93,17 @@ typedef struct {
                                        ('gradient descent'); TRD_SCALING_LOCAL the Gram of the
                                        sampled cores (Z_k)_{I_k} ('local scaled term').  The
                                        stop metric (Alg. 1 l.12) always uses the FGMC Gram.  */
+  int32_t sampling;                 /* working set of a block: TRD_SAMPLING_RSTS the RStS
+                                       subtensor (Eq. 14, default); TRD_SAMPLING_ROWS the
+                                       'uniform row sampling' ablation arm (reading R22):
+                                       J = prod_{m!=k} s_m rows of X_[k] drawn uniformly with
+                                       replacement (not with TRD_SCALING_LOCAL)               */
 } trd_config;
+
+typedef enum {
+  TRD_SAMPLING_RSTS = 0,
+  TRD_SAMPLING_ROWS = 1
+} trd_sampling;
 
 typedef enum {
   TRD_SCALING_GLOBAL = 0,
@@ -158,7 +168,9 @@ TRD_API trd_status trd_upload(trd_ctx* ctx, const float* values_host, const uint
 
 /* Write the RStS index sets of sweep `sweep`, block k (Alg. 1 line 4; reading R11)
  * to idx_dev (device, int32, sum_m sizes[m] entries, mode-major, each set ascending) and
- * their sizes to sizes_host[N] (host).  Mode k gets 0..I_k-1.  Synchronises the stream. */
+ * their sizes to sizes_host[N] (host).  Mode k gets 0..I_k-1.  With TRD_SAMPLING_ROWS every
+ * other mode gets the J draws in draw order (entry q of each list = draw q; idx_dev must
+ * hold I_k + (N-1) J entries).  Synchronises the stream. */
 TRD_API trd_status trd_sketch(trd_ctx* ctx, int32_t sweep, int32_t k, int32_t* idx_dev,
                       int64_t* sizes_host);
 

@@ -28,7 +28,7 @@ trajectory is pinned only through those invariants.
 import math
 import numpy as np
 
-from .philox import sample_indices
+from .philox import philox4x32_10, sample_indices
 
 SIGMA_FIXED, SIGMA_INF, SIGMA_RMS, SIGMA_MAD = 0, 1, 2, 3
 # robust sigma (reading R21): sigma = max(sigma_min, theta * MAD_C * median |e|), the median
@@ -39,6 +39,9 @@ HIST_BINS = HIST_OCT * HIST_SUB
 # operator of the update direction: the paper's scaled gradient (Eq. 16) and the two
 # ablation arms of Sec. 6.1 built on the same sketch
 SCALING_GLOBAL, SCALING_NONE, SCALING_LOCAL = 0, 1, 2
+# working set of a block: the RStS subtensor (Eq. 14) or the 'uniform row sampling' arm
+SAMPLING_RSTS, SAMPLING_ROWS = 0, 1
+ROW_TAG = 0x524F5753                 # Philox counter word of the row sampler ('ROWS')
 
 
 # ----------------------------------------------------------------------------------------
@@ -296,7 +299,7 @@ class Config:
 
     def __init__(self, dims, ranks, sigma_mode=SIGMA_RMS, sigma=1.0, sigma_theta=1.0,
                  sigma_min=1e-3, lambda_rel=1e-6, step=0.0, sketch=None, seed=0, eps=0.0,
-                 scaling=SCALING_GLOBAL):
+                 scaling=SCALING_GLOBAL, sampling=SAMPLING_RSTS):
         self.dims = list(dims)
         self.ranks = list(ranks)
         self.sigma_mode = sigma_mode
@@ -309,6 +312,9 @@ class Config:
         self.seed = seed
         self.eps = eps
         self.scaling = scaling
+        self.sampling = sampling
+        if sampling == SAMPLING_ROWS and scaling == SCALING_LOCAL:
+            raise ValueError("the local scaled term needs RStS index sets")
 
 
 def gram_local(cores, k, sets, ranks):
@@ -331,6 +337,52 @@ def update_direction(cfg, d, G_global, cores, k, sets):
         return h
     h, _ = scaled_gradient(d, G_global, cfg.lambda_rel)
     return h
+
+
+def row_samples(cfg, t, k):
+    """'Uniform row sampling' ablation arm (reading R22): J = prod_{m != k} s_m
+    rows of the shifted unfolding X_[k] drawn uniformly with replacement.  Draw q:
+    kappa_q = (out0 << 32) | out1 of Philox(key = seed, ctr = (q, ROW_TAG, k, t)), row
+    rho_q = floor(kappa_q R / 2^64) with R = prod_{m != k} I_m, decoded with i_{k+1} fastest
+    (Thm 1's column order of X_[k]).  Returns per-mode index lists: mode k all of I_k, the
+    others J entries each (entry q of every list belongs to draw q)."""
+    N = len(cfg.dims)
+    order = [(k + 1 + q) % N for q in range(N - 1)]
+    J, R = 1, 1
+    for m in order:
+        s_m = cfg.sketch[m]
+        J *= cfg.dims[m] if (s_m <= 0 or s_m >= cfg.dims[m]) else s_m
+        R *= cfg.dims[m]
+    q = np.arange(J, dtype=np.uint64)
+    seed = int(cfg.seed)
+    o0, o1, _, _ = philox4x32_10(q, ROW_TAG, k, t, seed & 0xFFFFFFFF, (seed >> 32) & 0xFFFFFFFF)
+    kappa = (o0 << np.uint64(32)) | o1
+    rho = [(int(x) * R) >> 64 for x in kappa]
+    lists = [None] * N
+    lists[k] = np.arange(cfg.dims[k], dtype=np.int64)
+    for m in order:
+        lists[m] = np.array([r % cfg.dims[m] for r in rho], dtype=np.int64)
+        rho = [r // cfg.dims[m] for r in rho]
+    return lists
+
+
+def working_set_rows(source, k, lists):
+    """X_I and P_I for explicit rows (draw q = column q): X_k[i_k, q] = X[.., i_k, .., lists[m][q], ..]."""
+    N = len(lists)
+    idx = [lists[m][None, :] if m != k else lists[k][:, None] for m in range(N)]
+    return source.X[tuple(idx)], source.P[tuple(idx)]
+
+
+def subchain_rows(cores, k, lists):
+    """Subchain rows S(j_q) = Z_{k+1}(i_{k+1}^q) .. Z_{k-1}(i_{k-1}^q) for explicit multi-indices
+    (Thm 1, one row per draw); S_[2][q, c + r_k b] = S(j_q)[b, c]."""
+    N = len(cores)
+    order = [(k + 1 + q) % N for q in range(N - 1)]
+    M = cores[order[0]][:, lists[order[0]], :]
+    for m in order[1:]:
+        M = np.einsum('ajb,bjc->ajc', M, cores[m][:, lists[m], :])
+    rk1, J, rk = M.shape
+    return M.transpose(1, 0, 2).reshape(J, rk1 * rk)
 
 
 def index_sets_for_block(cfg, t, k):
@@ -425,10 +477,15 @@ def block_update(cfg, st, source, k, rec, check_gram=False):
     ranks = cfg.ranks
     rk, rk1 = ranks[k], ranks[(k + 1) % N]
     sigma_inf = cfg.sigma_mode == SIGMA_INF
-    # line 4-5: index sets and sketch
-    sets = index_sets_for_block(cfg, st.t, k)
-    Xk, Pk = working_set(source, k, sets)
-    S = subchain(st.cores, k, sets)
+    # line 4-5: index sets and sketch (or the uniform-row-sampling arm)
+    if cfg.sampling == SAMPLING_ROWS:
+        sets = row_samples(cfg, st.t, k)
+        Xk, Pk = working_set_rows(source, k, sets)
+        S = subchain_rows(st.cores, k, sets)
+    else:
+        sets = index_sets_for_block(cfg, st.t, k)
+        Xk, Pk = working_set(source, k, sets)
+        S = subchain(st.cores, k, sets)
     Zk2 = core_unfold2(st.cores[k])
     # lines 6-7: weights (Eq. 7) and gradient (Eq. 9/15)
     d, E, W = gradient_block(Xk, Pk, Zk2, S, st.sigma, sigma_inf)

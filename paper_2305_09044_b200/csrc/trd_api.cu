@@ -109,7 +109,7 @@ double plan_cost_tc(int64_t K, int64_t ncols) {
   return KP * waste * (1.0 + 0.02 * shape);
 }
 
-void build_plan(const Context& c, int k, const int64_t* s_in, BlockPlan& bp, bool want_tc) {
+void build_plan(const Context& c, int k, const int64_t* s_in, BlockPlan& bp, bool want_tc, bool rows = false) {
   const int N = c.N;
   memset(&bp, 0, sizeof(bp));
   bp.k = k;
@@ -118,9 +118,15 @@ void build_plan(const Context& c, int k, const int64_t* s_in, BlockPlan& bp, boo
     if (m == k || s <= 0 || s >= c.dims[m]) s = c.dims[m];
     bp.s[m] = s;
   }
+  int64_t J = 1;                             // row sampling: J = prod_{m != k} s_m draws
+  if (rows) {
+    for (int m = 0; m < N; ++m) if (m != k) J *= bp.s[m];
+    for (int m = 0; m < N; ++m) if (m != k) bp.s[m] = J;
+    bp.explicit_cols = 1;
+  }
   double best = 1e300;
   int best_p = 0;
-  for (int p = 0; p <= N - 2; ++p) {
+  for (int p = 0; p <= (rows ? 0 : N - 2); ++p) {
     const int rs = c.ranks[(k + p + 1) % N];
     const int64_t K = (int64_t)c.ranks[k] * rs;
     int64_t ncols = 1;
@@ -136,6 +142,7 @@ void build_plan(const Context& c, int k, const int64_t* s_in, BlockPlan& bp, boo
   for (int q = 0; q < p; ++q) { bp.left[q] = (k + 1 + q) % N; bp.nL *= bp.s[bp.left[q]]; }
   bp.ncols = 1;
   for (int q = 0; q < bp.nright; ++q) { bp.right[q] = (k + 1 + p + q) % N; bp.ncols *= bp.s[bp.right[q]]; }
+  if (rows) bp.ncols = J;
   // digit orders: mode 0 (unit stride in memory) becomes the fastest digit of its group, and
   // for k == 0 the rows enumerate i_0 fastest, so that the bitmask / packed values of
   // consecutive rows or columns are contiguous (coalesced in the pass kernels)
@@ -455,6 +462,8 @@ trd_status trd_init(const trd_config* cfg, const trd_shard* shard, const float* 
     return TRD_ERR_INVALID_ARG;
   if (!(cfg->lambda_rel >= 0.0) || !(cfg->step >= 0.0)) return TRD_ERR_INVALID_ARG;
   if (cfg->scaling < TRD_SCALING_GLOBAL || cfg->scaling > TRD_SCALING_LOCAL) return TRD_ERR_INVALID_ARG;
+  if (cfg->sampling < TRD_SAMPLING_RSTS || cfg->sampling > TRD_SAMPLING_ROWS) return TRD_ERR_INVALID_ARG;
+  if (cfg->sampling == TRD_SAMPLING_ROWS && cfg->scaling == TRD_SCALING_LOCAL) return TRD_ERR_INVALID_ARG;
   if (cfg->world < 1 || cfg->rank < 0 || cfg->rank >= cfg->world) return TRD_ERR_INVALID_ARG;
   if (cfg->shard_mode < 0 || cfg->shard_mode >= N) return TRD_ERR_SHAPE;
   if (cfg->world > 1 && !cfg->nccl_unique_id) return TRD_ERR_INVALID_ARG;
@@ -521,7 +530,7 @@ trd_status trd_init(const trd_config* cfg, const trd_shard* shard, const float* 
   }
   for (int k = 0; k <= N; ++k) {
     BlockPlan& bp = (k < N) ? c->plan[k] : c->full_plan;
-    if (k < N) build_plan(*c, k, cfg->sketch, bp, c->want_tc != 0);
+    if (k < N) build_plan(*c, k, cfg->sketch, bp, c->want_tc != 0, cfg->sampling == TRD_SAMPLING_ROWS);
     else build_plan(*c, 0, full_s, bp, false);
     if (bp.use_tc && !tc_supported_kp(bp.KP)) bp.use_tc = 0;
     if (bp.use_tc) {
@@ -530,6 +539,7 @@ trd_status trd_init(const trd_config* cfg, const trd_shard* shard, const float* 
       st.invariant = true;
       for (int m = 0; m < N; ++m)
         if (m != k && bp.s[m] < c->dims[m]) st.invariant = false;
+      if (bp.explicit_cols) st.invariant = false;          // rows are redrawn every sweep
       st.vcap = bp.n_row_tiles * 128 * bp.n_col_tiles * 64;   // refined after the data is known
       max_lhl = std::max(max_lhl, (size_t)(bp.n_row_tiles * 2 * 128 * bp.KP));
       max_rhl = std::max(max_rhl, (size_t)(bp.n_col_tiles * 2 * 64 * bp.KP));
@@ -548,7 +558,19 @@ trd_status trd_init(const trd_config* cfg, const trd_shard* shard, const float* 
     max_dvec = std::max(max_dvec, Ik * (size_t)bp.R2 + 3);
     max_h = std::max(max_h, Ik * (size_t)bp.R2);
   }
-  for (int m = 0; m < N; ++m) { c->idx_off[m] = (int64_t)idx_total; idx_total += (size_t)c->dims[m]; }
+  // index lists per mode: the RStS sets (<= I_m) or, with row sampling, J_k draws
+  int64_t jmax = 0;
+  if (cfg->sampling == TRD_SAMPLING_ROWS)
+    for (int k = 0; k < N; ++k) {
+      int64_t J = 1;
+      for (int m = 0; m < N; ++m)
+        if (m != k) J *= (cfg->sketch[m] <= 0 || cfg->sketch[m] >= c->dims[m]) ? c->dims[m] : cfg->sketch[m];
+      jmax = std::max(jmax, J);
+    }
+  for (int m = 0; m < N; ++m) {
+    c->idx_off[m] = (int64_t)idx_total;
+    idx_total += (size_t)std::max<int64_t>(c->dims[m], jmax);
+  }
   c->idx_off[N] = (int64_t)idx_total;
   max_dp = std::max(max_dp, (size_t)(148 * 4 * 6));
 

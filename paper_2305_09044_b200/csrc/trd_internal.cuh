@@ -75,6 +75,8 @@ struct BlockPlan {
   // so that mode 0 (contiguous in memory) is the fastest digit of rows or columns
   int rowmode;
   int ldig[kMaxN], rdig[kMaxN];
+  int explicit_cols;     // 'uniform row sampling' (R22): p = 0, column q = draw q, whose index in
+                         // right mode m is idx[idx_off[m] + q] (all s[m] = ncols = J)
   // pass-kernel geometry (v1 SIMT)
   int jl_per_cta, ws_split, nsplit;
   int64_t grid_x;        // ceil(nL / jl_per_cta)

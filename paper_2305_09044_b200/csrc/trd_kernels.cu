@@ -90,6 +90,37 @@ __global__ void sampler_kernel(SamplerArgs sa, const DevScalars* __restrict__ sc
   }
 }
 
+// 'Uniform row sampling' arm (reading R22): draw q of block k, sweep t is row
+// rho = floor(kappa R / 2^64) of X_[k] (kappa from Philox(seed, (q, ROWS, k, t)), R = prod_{m!=k}
+// I_m), decoded with i_{k+1} fastest into entry q of every mode's list; mode k: all indices
+__device__ __forceinline__ void row_put(const SamplerArgs& sa, int m, int64_t q, int64_t g, int32_t* idx,
+                                        int64_t* doff) {
+  idx[sa.idx_off[m] + q] = (int32_t)g;
+  int64_t loc = g;
+  if (m == sa.shard_mode) loc = (g >= sa.shard_begin && g < sa.shard_end) ? g - sa.shard_begin : -1;
+  doff[sa.idx_off[m] + q] = loc < 0 ? -1 : loc * sa.lstride[m];
+}
+__global__ void row_sampler_kernel(SamplerArgs sa, int64_t J, const DevScalars* __restrict__ sc,
+                                   int32_t* __restrict__ idx, int64_t* __restrict__ doff) {
+  const int N = sa.N, k = sa.k;
+  const uint32_t t = (uint32_t)sc->sweep;
+  uint64_t R = 1;
+  for (int q = 1; q < N; ++q) R *= (uint64_t)sa.dims[(k + q) % N];
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < J + sa.dims[k];
+       q += (int64_t)gridDim.x * blockDim.x) {
+    if (q >= J) { row_put(sa, k, q - J, q - J, idx, doff); continue; }
+    uint32_t c[4] = {(uint32_t)q, 0x524F5753u, (uint32_t)k, t};
+    philox10(c, (uint32_t)(sa.seed & 0xffffffffu), (uint32_t)(sa.seed >> 32));
+    const uint64_t kappa = ((uint64_t)c[0] << 32) | c[1];
+    uint64_t rho = __umul64hi(kappa, R);
+    for (int d = 1; d < N; ++d) {
+      const int m = (k + d) % N;
+      row_put(sa, m, q, (int64_t)(rho % (uint64_t)sa.dims[m]), idx, doff);
+      rho /= (uint64_t)sa.dims[m];
+    }
+  }
+}
+
 // ----------------------------------------------------------------------------------------
 // Plan kernels: row/col data offsets and the chain products Mid, Lft, Rgt (Thm 1 subchain,
 // P:63-66; Def. 2 merging).  Slice of core m at index i: Z + zoff[m] + i*r_m*r_{m+1}.
@@ -99,6 +130,7 @@ struct PlanArgs {
   int left[kMaxN], right[kMaxN];
   int ldig[kMaxN], rdig[kMaxN];        // digit order (fastest first) as indices into left/right
   int rowmode;                         // 0: row = jl + nL*ik ; 1: row = ik + Ik*jl
+  int explicit_cols;                   // row sampling (R22): column col = draw col in every list
   int64_t sL[kMaxN], sR[kMaxN];        // sizes of the left/right index sets
   int64_t offL[kMaxN], offR[kMaxN];    // offsets into idx/doff
   int64_t off_k;
@@ -120,6 +152,7 @@ static PlanArgs make_plan_args(const Context& c, const BlockPlan& bp) {
     a.rdig[q] = bp.rdig[q];
   }
   a.rowmode = bp.rowmode;
+  a.explicit_cols = bp.explicit_cols;
   a.off_k = c.idx_off[bp.k];
   a.nL = bp.nL; a.nrows = bp.nrows; a.ncols = bp.ncols; a.Ik = bp.nrows / bp.nL;
   a.rk = bp.rk; a.rk1 = bp.rk1; a.rs = bp.rs; a.K = bp.K;
@@ -141,6 +174,10 @@ __device__ __forceinline__ void left_digits(const PlanArgs& a, int64_t jl, int64
   }
 }
 __device__ __forceinline__ void right_digits(const PlanArgs& a, int64_t col, int64_t* dq) {
+  if (a.explicit_cols) {                     // draw col: entry col of every right mode's list
+    for (int d = 0; d < a.nright; ++d) dq[d] = col;
+    return;
+  }
   for (int d = 0; d < a.nright; ++d) {
     const int q = a.rdig[d];
     dq[q] = col % a.sR[q];
@@ -224,14 +261,15 @@ __global__ void mid_kernel(PlanArgs a, const int32_t* __restrict__ idx, const fl
 }
 
 // Rgt(j_R) = Z_{k+p+1}(.) .. Z_{k-1}(.)  (r_s x r_k); stored RgtT[(a + r_k c) * ncols + col]
-// = Rgt[c][a].  One thread per (col, c).
+// = Rgt[c][a].  One thread per (col, c); the r_s threads of a column are adjacent so that
+// their slice reads coincide (columns of explicit draws hit unrelated slices)
 __global__ void rgt_kernel(PlanArgs a, const int32_t* __restrict__ idx, const float* __restrict__ Z,
                            float* __restrict__ rgtT) {
   const int64_t tot = a.ncols * a.rs;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tot;
        t += (int64_t)gridDim.x * blockDim.x) {
-    int64_t col = t % a.ncols;
-    int cc = (int)(t / a.ncols);
+    int64_t col = t / a.rs;
+    int cc = (int)(t % a.rs);
     int64_t dq[kMaxN];
     right_digits(a, col, dq);
     float v[kMaxR];
@@ -1153,6 +1191,12 @@ void launch_sampler(Context& c, const BlockPlan& bp, cudaStream_t s) {
   if (!attr_set) {
     cudaFuncSetAttribute(sampler_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
     attr_set = true;
+  }
+  if (bp.explicit_cols) {
+    const int64_t J = bp.ncols;
+    row_sampler_kernel<<<grid_for(J + c.dims[bp.k]), 256, 0, s>>>(sa, J, c.sc, c.idx, c.doff);
+    c.launches++;
+    return;
   }
   size_t smem = (size_t)maxI * 9 + 16;
   sampler_kernel<<<c.N, 256, smem, s>>>(sa, c.sc, c.idx, c.doff);

@@ -28,6 +28,7 @@ class TrdError(RuntimeError):
 
 
 TRD_SCALING_GLOBAL, TRD_SCALING_NONE, TRD_SCALING_LOCAL = 0, 1, 2   # trd_scaling (ablation arms)
+TRD_SAMPLING_RSTS, TRD_SAMPLING_ROWS = 0, 1                          # trd_sampling
 
 
 class trd_config(ctypes.Structure):
@@ -46,7 +47,8 @@ class trd_config(ctypes.Structure):
                 ("world", ctypes.c_int32),
                 ("rank", ctypes.c_int32),
                 ("nccl_unique_id", ctypes.c_void_p),
-                ("scaling", ctypes.c_int32)]
+                ("scaling", ctypes.c_int32),
+                ("sampling", ctypes.c_int32)]
 
 
 class trd_shard(ctypes.Structure):
@@ -162,7 +164,7 @@ class TRD:
                  sigma=1.0, sigma_theta=1.0, sigma_min=1e-3, lambda_rel=1e-6, step=0.0,
                  sketch=None, seed=0, shard_mode=0, shard_range=None, world=1, rank=0,
                  nccl_id: Optional[bytes] = None, packed=False, host=False, stream=None,
-                 scaling=0):
+                 scaling=0, sampling=0):
         import torch
         self.lib = load_library()
         N = len(dims)
@@ -183,6 +185,7 @@ class TRD:
         cfg.world = int(world)
         cfg.rank = int(rank)
         cfg.scaling = int(scaling)
+        cfg.sampling = int(sampling)
         self._nccl_buf = None
         if nccl_id is not None:
             self._nccl_buf = ctypes.create_string_buffer(nccl_id, 128)
@@ -198,6 +201,8 @@ class TRD:
         self._keep = (values, mask)
         self.N = N
         self.dims = [int(x) for x in dims]
+        self.sampling = int(sampling)
+        self.sketch_sizes = [int(sketch[m]) if sketch is not None else 0 for m in range(N)]
         self.ranks = [int(x) for x in ranks]
         cores = [np.ascontiguousarray(c, dtype=np.float32) for c in init_cores]
         arr = (ctypes.c_void_p * N)(*[c.ctypes.data for c in cores])
@@ -232,6 +237,13 @@ class TRD:
     def sketch(self, t: int, k: int):
         import torch
         total = sum(self.dims)
+        if self.sampling == TRD_SAMPLING_ROWS:         # J draws in every mode but k
+            J = 1
+            for m in range(self.N):
+                if m != k:
+                    s_m = self.sketch_sizes[m]
+                    J *= self.dims[m] if (s_m <= 0 or s_m >= self.dims[m]) else s_m
+            total = self.dims[k] + (self.N - 1) * J
         buf = torch.empty(total, dtype=torch.int32, device="cuda")
         sizes = (ctypes.c_int64 * TRD_MAX_ORDER)()
         self._check(self.lib.trd_sketch(self.ctx, int(t), int(k), ctypes.c_void_p(buf.data_ptr()),

@@ -148,6 +148,42 @@ def test_large_ranks_use_the_simt_and_cholesky_paths():
     ctx.close()
 
 
+@pytest.mark.parametrize("name,dims,sketch", [("C4", [12, 11, 10, 9], [4, 5, 3, 4]),
+                                               ("C5a", [7, 6, 5, 6, 5], [3, 4, 2, 3, 2])])
+def test_uniform_row_sampling_arm_matches_oracle(name, dims, sketch):
+    """'Uniform row sampling' arm (reading R22): the drawn rows (bit-exact), d, h, num,
+    den per block at t = 0, and the cores after two sweeps."""
+    _cuda()
+    spec = small_spec(name, dims, sketch)
+    prob = make_problem(spec)
+    src, _ = oracle_source(prob)
+    cfg = oracle_config(spec, sampling=O.SAMPLING_ROWS)
+    st = O.State(cfg, prob.init, src)
+    ctx = gpu_context(prob, packed=True, sampling=O.SAMPLING_ROWS)
+    for k in range(len(dims)):
+        L = O.row_samples(cfg, 0, k)
+        got = ctx.sketch(0, k)
+        for m in range(len(dims)):
+            assert np.array_equal(got[m], L[m]), (k, m)
+        g = ctx.block_probe(0, k)
+        Xk, Pk = O.working_set_rows(src, k, L)
+        S = O.subchain_rows(st.cores, k, L)
+        d, E, W = O.gradient_block(Xk, Pk, O.core_unfold2(st.cores[k]), S, st.sigma, False)
+        h = O.update_direction(cfg, d, O.gram_fgmc(st.Qs, k, spec.ranks), st.cores, k, L)
+        num, den = float(np.sum(d * h)), O.line_search_den(h, Pk, W, S)
+        assert g["n_obs"] == int(Pk.sum())
+        assert rel_fro(g["d"], d) <= 1e-4, k
+        assert rel_fro(g["h"], h) <= 1e-4, k
+        assert abs(g["num"] - num) <= 1e-4 * abs(num), k
+        assert abs(g["den"] - den) <= 1e-4 * abs(den), k
+    ctx.close()
+    st2, _ = O.run(cfg, prob.init, src, 2)
+    ctx = gpu_context(prob, packed=True, sampling=O.SAMPLING_ROWS)
+    ctx.sweep(2, stats=False)
+    assert cores_rel_err(ctx.get_cores(), st2.cores) <= 1e-4
+    ctx.close()
+
+
 @pytest.mark.parametrize("scaling", [O.SCALING_NONE, O.SCALING_LOCAL])
 def test_ablation_arms_match_oracle(scaling):
     """Sec. 6.1 ablation arms on an RStS sketch: 'gradient descent' (h = d) and

@@ -662,3 +662,72 @@ def test_mad_sigma_is_consistent_for_gaussian_residuals_and_robust_to_outliers()
     mad = O.mad_sigma(cfg, np.abs(out))
     rms = float(np.sqrt(np.mean(out * out)))
     assert mad < 0.2 and rms > 2.0
+
+
+# ---------------------------------------------------------------- uniform row sampling (R22)
+def test_rows_of_a_full_enumeration_equal_the_subtensor_forms():
+    """Explicit-row working set and subchain: listing every multi-index of a product set in
+    Thm 1's order (i_{k+1} fastest) reproduces working_set / subchain of that set."""
+    dims, ranks = [4, 3, 5, 2], [2, 3, 2, 2]
+    cores = rand_cores(dims, ranks, 21)
+    rng = np.random.default_rng(22)
+    X = rng.standard_normal(dims)
+    P = rng.random(dims) < 0.6
+    src = O.DenseSource(X, P)
+    for k in range(4):
+        sets = [np.arange(I) for I in dims]
+        order = [(k + 1 + q) % 4 for q in range(3)]
+        grids = np.meshgrid(*[sets[m] for m in order[::-1]], indexing="ij")   # slowest first
+        lists = [None] * 4
+        lists[k] = sets[k]
+        for g, m in zip(grids, order[::-1]):
+            lists[m] = g.reshape(-1)
+        Xr, Pr = O.working_set_rows(src, k, lists)
+        Xs, Ps = O.working_set(src, k, sets)
+        assert np.array_equal(Xr, Xs) and np.array_equal(Pr, Ps)
+        assert np.allclose(O.subchain_rows(cores, k, lists), O.subchain(cores, k, sets), rtol=1e-13, atol=1e-14)
+
+
+def test_row_samples_are_uniform_with_replacement_and_decode_in_thm1_order():
+    cfg = O.Config([3, 4, 5], [1, 1, 1], sketch=[0, 4, 5], seed=9, sampling=O.SAMPLING_ROWS)
+    counts = np.zeros((4, 5))
+    for t in range(300):
+        L = O.row_samples(cfg, t, 0)
+        assert len(L[1]) == len(L[2]) == 20 and np.array_equal(L[0], np.arange(3))
+        np.add.at(counts, (L[1], L[2]), 1)
+    expected = 300 * 20 / 20.0
+    chi2 = float(np.sum((counts - expected) ** 2 / expected))
+    assert chi2 < 60.0                                   # 19 dof, p ~ 1e-5
+    # decode: the same Philox word, i_{k+1} fastest
+    L = O.row_samples(cfg, 7, 1)                        # k = 1: modes 2 (fastest), then 0
+    o0, o1, _, _ = O.philox4x32_10(np.arange(len(L[2]), dtype=np.uint64), O.ROW_TAG, 1, 7, 9, 0)
+    rho = [(int((a << np.uint64(32)) | b) * 15) >> 64 for a, b in zip(o0, o1)]
+    assert [r % 5 for r in rho] == list(L[2]) and [r // 5 for r in rho] == list(L[0])
+
+
+def test_row_sampling_block_step_is_an_exact_line_search():
+    dims, ranks = [6, 5, 4], [2, 3, 2]
+    gt = rand_cores(dims, ranks, 31)
+    rng = np.random.default_rng(32)
+    X = O.tr_reconstruct(gt) + 0.05 * rng.standard_normal(dims)
+    P = rng.random(dims) < 0.7
+    src = O.DenseSource(X, P)
+    cfg = O.Config(dims, ranks, sigma_mode=O.SIGMA_FIXED, sigma=0.8, sketch=[4, 3, 3], seed=5,
+                   sampling=O.SAMPLING_ROWS)
+    st = O.State(cfg, rand_cores(dims, ranks, 33), src)
+    for k in range(3):
+        L = O.row_samples(cfg, st.t, k)
+        Xk, Pk = O.working_set_rows(src, k, L)
+        S = O.subchain_rows(st.cores, k, L)
+        Zk2 = O.core_unfold2(st.cores[k])
+        d, E, W = O.gradient_block(Xk, Pk, Zk2, S, st.sigma, False)
+        h = O.update_direction(cfg, d, O.gram_fgmc(st.Qs, k, ranks), st.cores, k, L)
+        eta = float(np.sum(d * h)) / O.line_search_den(h, Pk, W, S)
+
+        def cost(t):
+            Et = Xk - (Zk2 + t * h) @ S.T
+            return 0.5 * np.sum(W * Pk * Et * Et)
+        assert cost(eta) <= min(cost(0.99 * eta), cost(1.01 * eta)) + 1e-12
+        rec = O.SweepRecord(3)
+        O.block_update(cfg, st, src, k, rec)
+        assert abs(rec.eta[k] - eta) <= 1e-12 * eta
