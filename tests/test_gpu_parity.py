@@ -421,8 +421,12 @@ MULTI_CASES = [
     ("C5b", [20, 18, 16, 12, 10], None, None),
     # same shape at rho = 0.3: tiles overflow the stage, entries are read from global memory
     ("C5b", [20, 18, 16, 12, 10], None, 0.3),
-    # rho = 0.6: > 1024 entries per tile, pass 1 compacts the S values in chunks (S re-read)
+    # rho = 0.6: > 512 entries per tile (values from global memory, P cleared by groups)
     ("C5b", [20, 18, 16, 12, 10], None, 0.6),
+    # rho = 1: every entry observed (full tiles: staging writes straight to global memory)
+    ("C5b", [20, 18, 16, 12, 10], None, 1.0),
+    # rho = 0.002: mostly empty tiles and rows
+    ("C5b", [20, 18, 16, 12, 10], None, 0.002),
     # rank 10 (KP = 112: single A buffer, shared P buffer), RStS sketch
     ("C4", [24, 22, 20, 18], [12, 11, 10, 9], None),
 ]
