@@ -118,6 +118,16 @@ void build_plan(const Context& c, int k, const int64_t* s_in, BlockPlan& bp, boo
     if (m == k || s <= 0 || s >= c.dims[m]) s = c.dims[m];
     bp.s[m] = s;
   }
+  // data parallel: the full index set of the shard mode (m != k) shrinks to this rank's slice
+  {
+    const int sm = c.cfg.shard_mode;
+    const int64_t local = c.shard_end - c.shard_begin;
+    if (!rows && bp.s[sm] == c.dims[sm] && local < c.dims[sm]) {
+      bp.s[sm] = local;
+      bp.shard_local = 1;
+      if (sm == k) bp.ik0 = c.shard_begin;   // plan rows i_k = ik0 + local index
+    }
+  }
   int64_t J = 1;                             // row sampling: J = prod_{m != k} s_m draws
   if (rows) {
     for (int m = 0; m < N; ++m) if (m != k) J *= bp.s[m];
@@ -161,7 +171,7 @@ void build_plan(const Context& c, int k, const int64_t* s_in, BlockPlan& bp, boo
   bp.rs = c.ranks[(k + p + 1) % N];
   bp.K = bp.rk * bp.rs;
   bp.R2 = bp.rk * bp.rk1;
-  const int64_t Ik = c.dims[k];
+  const int64_t Ik = bp.s[k];                 // (this rank's slice when k is the shard mode)
   bp.nrows = Ik * bp.nL;
   bp.nnz_ws = bp.nrows * bp.ncols;
   bp.KP = (bp.K + 15) / 16 * 16;
@@ -201,7 +211,7 @@ void build_plan(const Context& c, int k, const int64_t* s_in, BlockPlan& bp, boo
     const int64_t ncl1 = (((int64_t)c.num_sm - 1) / bp.tc_cl);       // one SM left (side stream)
     bp.tc_grid = (int)(std::max<int64_t>(1, std::min<int64_t>(citems, ncl2)) * bp.tc_cl);
     bp.tc_grid1 = (int)(std::max<int64_t>(1, std::min<int64_t>(citems, ncl1)) * bp.tc_cl);
-    const int64_t Ikk = c.dims[k];
+    const int64_t Ikk = bp.s[k];
     // d reduction: >= 8 CTAs per SM worth of (i_k, jl-chunk) blocks, chunks of >= 32 rows
     int64_t jc = (8 * (int64_t)c.num_sm + Ikk - 1) / Ikk;
     jc = std::max<int64_t>(1, std::min<int64_t>(jc, (bp.nL + 31) / 32));
@@ -471,7 +481,8 @@ trd_status trd_init(const trd_config* cfg, const trd_shard* shard, const float* 
   const int sm = cfg->shard_mode;
   const int64_t sb = shard->shard_begin, se = shard->shard_end;
   if (sb < 0 || se > cfg->dims[sm] || se <= sb) return TRD_ERR_SHAPE;
-  if (cfg->world == 1 && (sb != 0 || se != cfg->dims[sm])) return TRD_ERR_SHAPE;
+  // (world == 1 with a partial shard: that shard's partial problem, no exchange -- used by
+  //  the single-GPU tests of the per-rank plans)
   if (cfg->dims[N - 1] > 16384) return TRD_ERR_SHAPE;   // D^t is I_N x I_N (Alg. 1 l.12)
 
   Context* c = new (std::nothrow) Context();
@@ -538,7 +549,7 @@ trd_status trd_init(const trd_config* cfg, const trd_shard* shard, const float* 
       st.n_tiles = bp.n_row_tiles * bp.n_col_tiles;
       st.invariant = true;
       for (int m = 0; m < N; ++m)
-        if (m != k && bp.s[m] < c->dims[m]) st.invariant = false;
+        if (m != k && bp.s[m] < c->dims[m] && !(m == cfg->shard_mode && bp.shard_local)) st.invariant = false;
       if (bp.explicit_cols) st.invariant = false;          // rows are redrawn every sweep
       st.vcap = bp.n_row_tiles * 128 * bp.n_col_tiles * 64;   // refined after the data is known
       max_lhl = std::max(max_lhl, (size_t)(bp.n_row_tiles * 2 * 128 * bp.KP));

@@ -75,6 +75,9 @@ struct BlockPlan {
   // so that mode 0 (contiguous in memory) is the fastest digit of rows or columns
   int rowmode;
   int ldig[kMaxN], rdig[kMaxN];
+  int shard_local;       // the shard mode (full index set) enumerates only this rank's slice
+                         // [shard_begin, shard_end): per-rank GEMM work shrinks with world
+  int64_t ik0;           // k == shard mode: global i_k of plan row index 0 (else 0)
   int explicit_cols;     // 'uniform row sampling' (R22): p = 0, column q = draw q, whose index in
                          // right mode m is idx[idx_off[m] + q] (all s[m] = ncols = J)
   // pass-kernel geometry (v1 SIMT)

@@ -39,6 +39,7 @@ struct SamplerArgs {
   uint64_t seed;
   int64_t shard_begin, shard_end;
   int64_t dims[kMaxN], s[kMaxN], idx_off[kMaxN + 1], lstride[kMaxN];
+  int shard_local;       // shard mode enumerates [shard_begin, shard_end) (full set, m != k)
 };
 
 __global__ void sampler_kernel(SamplerArgs sa, const DevScalars* __restrict__ sc,
@@ -52,7 +53,9 @@ __global__ void sampler_kernel(SamplerArgs sa, const DevScalars* __restrict__ sc
   int32_t* out = idx + sa.idx_off[m];
   int64_t* dof = doff + sa.idx_off[m];
   const uint32_t t = (uint32_t)sc->sweep;
-  if (s >= I) {
+  if (m == sa.shard_mode && sa.shard_local) {               // this rank's slice, global indices
+    for (int64_t q = threadIdx.x; q < s; q += blockDim.x) out[q] = (int32_t)(sa.shard_begin + q);
+  } else if (s >= I) {
     for (int64_t i = threadIdx.x; i < I; i += blockDim.x) out[i] = (int32_t)i;
   } else {
     for (int64_t i = threadIdx.x; i < I; i += blockDim.x) {
@@ -131,6 +134,7 @@ struct PlanArgs {
   int ldig[kMaxN], rdig[kMaxN];        // digit order (fastest first) as indices into left/right
   int rowmode;                         // 0: row = jl + nL*ik ; 1: row = ik + Ik*jl
   int explicit_cols;                   // row sampling (R22): column col = draw col in every list
+  int64_t ik0;                         // global i_k of plan row index 0 (k = shard mode)
   int64_t sL[kMaxN], sR[kMaxN];        // sizes of the left/right index sets
   int64_t offL[kMaxN], offR[kMaxN];    // offsets into idx/doff
   int64_t off_k;
@@ -153,6 +157,7 @@ static PlanArgs make_plan_args(const Context& c, const BlockPlan& bp) {
   }
   a.rowmode = bp.rowmode;
   a.explicit_cols = bp.explicit_cols;
+  a.ik0 = bp.ik0;
   a.off_k = c.idx_off[bp.k];
   a.nL = bp.nL; a.nrows = bp.nrows; a.ncols = bp.ncols; a.Ik = bp.nrows / bp.nL;
   a.rk = bp.rk; a.rk1 = bp.rk1; a.rs = bp.rs; a.K = bp.K;
@@ -302,8 +307,8 @@ __global__ void lft_kernel(PlanArgs a, const float* __restrict__ Zk, const doubl
 #pragma unroll
     for (int b = 0; b < kMaxR; ++b) {
       if (b < a.rk1) {
-        v[b] = h ? (float)h[ik * a.rk * a.rk1 + aa + a.rk * b]
-                 : __ldg(Zk + (ik * a.rk + aa) * a.rk1 + b);
+        v[b] = h ? (float)h[(a.ik0 + ik) * a.rk * a.rk1 + aa + a.rk * b]
+                 : __ldg(Zk + ((a.ik0 + ik) * a.rk + aa) * a.rk1 + b);
       } else {
         v[b] = 0.f;
       }
@@ -562,15 +567,16 @@ static void launch_pass_t(Context& c, const BlockPlan& bp, cudaStream_t s) {
 // ----------------------------------------------------------------------------------------
 // Reductions (fixed order) -> dvec = [d (I_k x R2) | sum_e2 | welsch | n]
 // ----------------------------------------------------------------------------------------
+// (Ik plan rows starting at global i_k = ik0; dvec has Ik_tot rows, the statistics after them)
 __global__ void reduce_d_kernel(const double* __restrict__ dpart, const double* __restrict__ spart,
                                 int64_t ncta, int R2, int64_t Ik, double* __restrict__ dvec,
-                                DevScalars* sc, int kblk) {
+                                DevScalars* sc, int kblk, int64_t ik0, int64_t Ik_tot) {
   const int64_t ik = blockIdx.x;
   if (ik < Ik) {
     for (int o = threadIdx.x; o < R2; o += blockDim.x) {
       double tot = 0.0;
       for (int64_t q = 0; q < ncta; ++q) tot += dpart[(ik * ncta + q) * R2 + o];
-      dvec[ik * R2 + o] = tot;
+      dvec[(ik0 + ik) * R2 + o] = tot;
     }
     return;
   }
@@ -586,7 +592,7 @@ __global__ void reduce_d_kernel(const double* __restrict__ dpart, const double* 
   if (threadIdx.x < 3) {
     double tot = 0.0;
     for (int t = 0; t < (int)blockDim.x; ++t) tot += acc[threadIdx.x][t];
-    dvec[Ik * R2 + threadIdx.x] = tot;
+    dvec[Ik_tot * R2 + threadIdx.x] = tot;
     if (threadIdx.x == 2 && sc && sc->prof_on) sc->prof_nobs[kblk] += tot;   // local count
   }
 }
@@ -1178,6 +1184,7 @@ void launch_sampler(Context& c, const BlockPlan& bp, cudaStream_t s) {
   SamplerArgs sa;
   sa.N = c.N; sa.k = bp.k; sa.shard_mode = c.cfg.shard_mode; sa.seed = c.cfg.seed;
   sa.shard_begin = c.shard_begin; sa.shard_end = c.shard_end;
+  sa.shard_local = bp.shard_local;
   int64_t maxI = 0;
   for (int m = 0; m < c.N; ++m) {
     sa.dims[m] = c.dims[m];
@@ -1233,25 +1240,26 @@ void launch_pass2(Context& c, const BlockPlan& bp, cudaStream_t s) {
 }
 
 void launch_reduce_d(Context& c, const BlockPlan& bp, cudaStream_t s) {
-  const int64_t Ik = bp.nrows / bp.nL;
+  const int64_t Ik = bp.nrows / bp.nL, Ik_tot = c.dims[bp.k];
   const int64_t ncta = bp.grid_x * bp.nsplit;
+  if (bp.R2 > 0 && Ik < Ik_tot) cudaMemsetAsync(c.dvec, 0, (size_t)(Ik_tot * bp.R2) * sizeof(double), s);
   reduce_d_kernel<<<(unsigned)(Ik + 1), 256, 0, s>>>(c.dpart, c.spart, ncta, bp.R2, Ik, c.dvec,
-                                                      bp.R2 > 0 ? c.sc : nullptr, bp.k);
+                                                      bp.R2 > 0 ? c.sc : nullptr, bp.k, bp.ik0, Ik_tot);
   c.launches++;
 }
 
 // block statistics from the (allreduced) dvec tail
 void launch_block_stats(Context& c, const BlockPlan& bp, cudaStream_t s) {
-  const int64_t Ik = bp.nrows / bp.nL;
+  const int64_t Ik = c.dims[bp.k];                     // dvec rows: all of I_k
   block_scalars_kernel<<<1, 32, 0, s>>>(c.dvec, Ik, bp.R2, nullptr, c.sc, c.stats, 0, bp.k, 0.0, 0);
   c.launches++;
 }
 
 void launch_reduce_den(Context& c, const BlockPlan& bp, cudaStream_t s) {
-  const int64_t Ik = bp.nrows / bp.nL;
+  const int64_t Ik = bp.nrows / bp.nL;                 // plan rows (pass-2 partials)
   const int64_t ncta = bp.grid_x * bp.nsplit;
   const int64_t nden = bp.use_tc ? (int64_t)bp.tc_grid : Ik * ncta;
-  reduce_den_kernel<<<1, 256, 0, s>>>(c.denpart, nden, c.numpart, Ik, c.red_ws);
+  reduce_den_kernel<<<1, 256, 0, s>>>(c.denpart, nden, c.numpart, c.dims[bp.k], c.red_ws);
   c.launches++;
 }
 
@@ -1355,13 +1363,13 @@ void launch_solve(Context& c, const BlockPlan& bp, cudaStream_t s, const double*
 }
 
 void launch_h(Context& c, const BlockPlan& bp, cudaStream_t s) {
-  const int64_t Ik = bp.nrows / bp.nL;
+  const int64_t Ik = c.dims[bp.k];                     // h of every i_k (replicated update)
   h_kernel<<<(unsigned)Ik, 256, 0, s>>>(c.dvec, c.Mop, bp.R2, c.h, c.numpart);
   c.launches++;
 }
 
 void launch_update(Context& c, const BlockPlan& bp, int slot, cudaStream_t s) {
-  const int64_t Ik = bp.nrows / bp.nL;
+  const int64_t Ik = c.dims[bp.k];
   block_scalars_kernel<<<1, 32, 0, s>>>(c.dvec, Ik, bp.R2, c.red_ws, c.sc, c.stats, slot, bp.k,
                                         c.cfg.step, 1);
   c.launches++;

@@ -197,6 +197,7 @@ __device__ __forceinline__ uint32_t pack_half2(__half lo, __half hi) {
 // lft_kernel (fmaf over b ascending).
 struct LftArgs {
   int64_t nrows, nL, Ik;
+  int64_t ik0;           // global i_k of plan row index 0 (k = shard mode)
   int rowmode, rk, rk1, rs, K, KP, p;
   const float* zk;       // Z_k[i][a][b]
   const double* hk;      // h[i][a + r_k b]
@@ -227,11 +228,11 @@ __global__ void __launch_bounds__(256) tc_lft_pack_kernel(LftArgs a, int pass2, 
       if (tid < TC_M) {
         float* xr = Xs + r * XP;
         if (pass2) {
-          const double* hs = a.hk + ik * XS;
+          const double* hs = a.hk + (a.ik0 + ik) * XS;
           for (int aa = 0; aa < a.rk; ++aa)
             for (int b = 0; b < a.rk1; ++b) xr[aa * a.rk1 + b] = ok ? (float)__ldg(hs + aa + a.rk * b) : 0.f;
         } else {
-          const float* zs = a.zk + ik * XS;
+          const float* zs = a.zk + (a.ik0 + ik) * XS;
           for (int e = 0; e < XS; ++e) xr[e] = ok ? __ldg(zs + e) : 0.f;
         }
       } else if (a.p > 0) {
@@ -298,7 +299,7 @@ __global__ void __launch_bounds__(128, 4) tc_lft_pack_rb_kernel(LftArgs a, int p
       else { jl = row / a.Ik; ik = row - jl * a.Ik; }
       float X[RK][RK1], M[RK1][RS];
       if (pass2) {
-        const double2* hs = reinterpret_cast<const double2*>(a.hk + ik * (RK * RK1));   // h[a + RK b]
+        const double2* hs = reinterpret_cast<const double2*>(a.hk + (a.ik0 + ik) * (RK * RK1));   // h[a + RK b]
 #pragma unroll
         for (int q = 0; q < RK * RK1 / 2; ++q) {
           const double2 v = __ldg(hs + q);
@@ -306,7 +307,7 @@ __global__ void __launch_bounds__(128, 4) tc_lft_pack_rb_kernel(LftArgs a, int p
           X[(2 * q + 1) % RK][(2 * q + 1) / RK] = (float)v.y;
         }
       } else {
-        const float4* zs = reinterpret_cast<const float4*>(a.zk + ik * (RK * RK1));     // Z[a][b]
+        const float4* zs = reinterpret_cast<const float4*>(a.zk + (a.ik0 + ik) * (RK * RK1));     // Z[a][b]
 #pragma unroll
         for (int q = 0; q < RK * RK1 / 4; ++q) {
           const float4 v = __ldg(zs + q);
@@ -922,20 +923,21 @@ __global__ void __launch_bounds__(128) tc_reduce_d_rb_kernel(const float* __rest
 // stage 2: dvec = [d | sum_e2 | welsch | n] from the chunk partials and the per-CTA statistics
 __global__ void tc_reduce_final_kernel(const double* __restrict__ dpart, int64_t JC, int64_t Ik, int R2,
                                        const double* __restrict__ spart, int64_t nparts,
-                                       double* __restrict__ dvec, DevScalars* sc, int kblk) {
+                                       double* __restrict__ dvec, DevScalars* sc, int kblk, int64_t ik0,
+                                       int64_t Ik_tot) {
   const int64_t ik = blockIdx.x;
   if (ik < Ik) {
     for (int o = threadIdx.x; o < R2; o += blockDim.x) {
       double t = 0.0;
       for (int64_t jc = 0; jc < JC; ++jc) t += dpart[(jc * Ik + ik) * R2 + o];
-      dvec[ik * R2 + o] = t;
+      dvec[(ik0 + ik) * R2 + o] = t;
     }
     return;
   }
   if (threadIdx.x < 3) {
     double t = 0.0;
     for (int64_t q = 0; q < nparts; ++q) t += spart[q * 3 + threadIdx.x];
-    dvec[Ik * R2 + threadIdx.x] = t;
+    dvec[Ik_tot * R2 + threadIdx.x] = t;
     if (threadIdx.x == 2 && sc && sc->prof_on) sc->prof_nobs[kblk] += t;
   }
 }
@@ -950,7 +952,7 @@ static int tc_grid(int64_t n) {
 
 void launch_tc_lft(Context& c, const BlockPlan& bp, bool pass2, cudaStream_t s) {
   LftArgs a;
-  a.nrows = bp.nrows; a.nL = bp.nL; a.Ik = bp.nrows / bp.nL;
+  a.nrows = bp.nrows; a.nL = bp.nL; a.Ik = bp.nrows / bp.nL; a.ik0 = bp.ik0;
   a.rowmode = bp.rowmode; a.rk = bp.rk; a.rk1 = bp.rk1; a.rs = bp.rs; a.K = bp.K; a.KP = bp.KP; a.p = bp.p;
   a.zk = c.Z + c.zoff[bp.k];
   a.hk = c.h;
@@ -1123,11 +1125,12 @@ void launch_tc_pass(Context& c, const BlockPlan& bp, const TcStage& st, bool pas
 
 void launch_tc_reduce_d(Context& c, const BlockPlan& bp, cudaStream_t s) {
   const int64_t Ik = bp.nrows / bp.nL;
+  if (Ik < c.dims[bp.k]) cudaMemsetAsync(c.dvec, 0, (size_t)(c.dims[bp.k] * bp.R2) * sizeof(double), s);
   if (bp.p > 0 && bp.rk == 8 && bp.rk1 == 8 && bp.rs == 8 && bp.KP == 64) {
     tc_reduce_d_rb_kernel<8, 8, 8><<<dim3((unsigned)Ik, (unsigned)bp.tc_jc), 128, 0, s>>>(
         c.contrib, c.mid, bp.tc_nsplit, bp.n_row_tiles * TC_M, bp.nL, Ik, bp.rowmode, bp.tc_jl_chunk, c.dpart);
     tc_reduce_final_kernel<<<(unsigned)(Ik + 1), 128, 0, s>>>(c.dpart, bp.tc_jc, Ik, bp.R2, c.spart, bp.tc_grid1,
-                                                              c.dvec, c.sc, bp.k);
+                                                              c.dvec, c.sc, bp.k, bp.ik0, c.dims[bp.k]);
     c.launches += 2;
     return;
   }
@@ -1138,7 +1141,7 @@ void launch_tc_reduce_d(Context& c, const BlockPlan& bp, cudaStream_t s) {
       c.contrib, c.mid, bp.tc_nsplit, bp.n_row_tiles * TC_M, bp.nL, Ik, bp.rowmode, bp.KP, bp.R2, bp.rk,
       bp.rs, bp.p, bp.tc_jl_chunk, c.dpart);
   tc_reduce_final_kernel<<<(unsigned)(Ik + 1), 128, 0, s>>>(c.dpart, bp.tc_jc, Ik, bp.R2, c.spart, bp.tc_grid1,
-                                                            c.dvec, c.sc, bp.k);
+                                                            c.dvec, c.sc, bp.k, bp.ik0, c.dims[bp.k]);
   c.launches += 2;
 }
 

@@ -132,6 +132,46 @@ def test_block_quantities_match_oracle(name, dims, sketch, packed):
     ctx.close()
 
 
+@pytest.mark.parametrize("name,dims,sketch", [("C5b", [12, 9, 8, 7, 6], None),
+                                               ("C4", [12, 11, 10, 9], [4, 5, 3, 4])])
+def test_rank_shard_plans_match_oracle_partials(name, dims, sketch):
+    """Data-parallel plans on one GPU: a context holding only the slab i_0 in [b, e) (world 1,
+    partial shard: no exchange) computes that shard's partial d, n_obs and den; with full
+    index sets the shard mode enumerates only the local slice (per-rank GEMM work / world)."""
+    _cuda()
+    import bench
+    from paper_2305_09044_b200 import TRD
+    spec = small_spec(name, dims, sketch)
+    prob = make_problem(spec, keep_mask_bool=True)
+    src, _ = oracle_source(prob)
+    cfg = oracle_config(spec, sigma_mode=O.SIGMA_FIXED, sigma=0.9)
+    st = O.State(cfg, prob.init, src)
+    world = 3
+    for rank in (0, 1, 2):
+        (b, e), vals, words, _ = bench.local_shard(prob, rank, world)
+        ctx = TRD(spec.dims, spec.ranks, vals.cuda(), words.cuda(), prob.init, packed=True,
+                  sketch=spec.sketch, seed=spec.sampler_seed, sigma_mode=O.SIGMA_FIXED, sigma=0.9,
+                  shard_mode=0, shard_range=(b, e), world=1, rank=0)
+        for k in range(len(dims)):
+            g = ctx.block_probe(0, k)
+            sets = O.index_sets_for_block(cfg, 0, k)
+            Xk, Pk = O.working_set(src, k, sets)
+            # entries of this rank: i_0 in [b, e)
+            i0 = np.asarray(sets[0])
+            own = (i0 >= b) & (i0 < e)
+            Xs, Ps = src.subtensor(sets)
+            Ps = Ps & own.reshape([-1] + [1] * (len(dims) - 1))
+            Pk = O.unfold_shifted(Ps, k)
+            S = O.subchain(st.cores, k, sets)
+            d, E, W = O.gradient_block(Xk, Pk, O.core_unfold2(st.cores[k]), S, st.sigma, False)
+            h, _ = O.scaled_gradient(d, O.gram_fgmc(st.Qs, k, spec.ranks), cfg.lambda_rel)
+            den = O.line_search_den(h, Pk, W, S)
+            assert g["n_obs"] == int(Pk.sum()), (rank, k)
+            assert rel_fro(g["d"], d) <= 1e-4, (rank, k)
+            assert abs(g["den"] - den) <= 1e-4 * abs(den), (rank, k)
+        ctx.close()
+
+
 def test_large_ranks_use_the_simt_and_cholesky_paths():
     """Ranks up to TRD_MAX_RANK: K = r_k r_s > 128 has no tensor-core kernel (SIMT pass
     kernels) and R^2 > 112 takes the Cholesky solve instead of Gauss-Jordan; cores after one
