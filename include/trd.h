@@ -111,7 +111,8 @@ typedef enum {
   TRD_SCALING_LOCAL = 2
 } trd_scaling;
 
-/* Local shard of X and P.  Local tensor = global X restricted to
+/* Local shard of X and P (world == 1 with a partial shard: that shard's partial problem, no
+ * exchange).  Local tensor = global X restricted to
  * i_{shard_mode} in [shard_begin, shard_end), stored in its own linear order (same formula
  * with the local extent of the shard mode).  Device pointers, caller owned, read only,
  * must stay valid and unmodified until trd_destroy (or until trd_upload replaces them when
