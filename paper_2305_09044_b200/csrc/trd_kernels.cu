@@ -1173,6 +1173,16 @@ __global__ void popc_kernel(const uint32_t* __restrict__ mask, int64_t nw, uint3
 // ----------------------------------------------------------------------------------------
 // Launchers
 // ----------------------------------------------------------------------------------------
+// kernel attributes are per device: remember which devices a launcher has configured
+static bool first_on_device(uint64_t& done_mask) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const uint64_t bit = 1ull << (dev & 63);
+  if (done_mask & bit) return false;
+  done_mask |= bit;
+  return true;
+}
+
 static int grid_for(int64_t n, int threads = 256, int cap = 148 * 16) {
   int64_t g = (n + threads - 1) / threads;
   if (g < 1) g = 1;
@@ -1194,11 +1204,9 @@ void launch_sampler(Context& c, const BlockPlan& bp, cudaStream_t s) {
     if (bp.s[m] < c.dims[m] && c.dims[m] > maxI) maxI = c.dims[m];
   }
   sa.idx_off[c.N] = c.idx_off[c.N];
-  static bool attr_set = false;
-  if (!attr_set) {
+  static uint64_t attr_set = 0;
+  if (first_on_device(attr_set))
     cudaFuncSetAttribute(sampler_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
-    attr_set = true;
-  }
   if (bp.explicit_cols) {
     const int64_t J = bp.ncols;
     row_sampler_kernel<<<grid_for(J + c.dims[bp.k]), 256, 0, s>>>(sa, J, c.sc, c.idx, c.doff);
@@ -1333,14 +1341,13 @@ void launch_solve(Context& c, const BlockPlan& bp, cudaStream_t s, const double*
   const int n = bp.R2;
   if (n <= kGjMaxN) {
     const size_t gneed = (size_t)2 * n * n * sizeof(double);
-    static bool gj_attr = false;
+    static uint64_t gj_attr = 0;
     const int maxs = (int)((size_t)2 * kGjMaxN * kGjMaxN * sizeof(double));
-    if (!gj_attr) {
+    if (first_on_device(gj_attr)) {
       cudaFuncSetAttribute(gj_solve_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxs);
       cudaFuncSetAttribute(gj_solve_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxs);
       cudaFuncSetAttribute(gj_solve_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxs);
       cudaFuncSetAttribute(gj_solve_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxs);
-      gj_attr = true;
     }
     const int nb = (n + 31) / 32;
     if (nb == 1) gj_solve_kernel<1><<<1, 1024, gneed, s>>>(G, n, c.cfg.lambda_rel, c.Mop, c.sc);
@@ -1352,11 +1359,9 @@ void launch_solve(Context& c, const BlockPlan& bp, cudaStream_t s, const double*
   }
   const size_t need = (size_t)2 * n * n * sizeof(double);
   const int use_smem = need <= 200 * 1024;
-  static bool attr_set = false;
-  if (!attr_set) {
+  static uint64_t attr_set = 0;
+  if (first_on_device(attr_set))
     cudaFuncSetAttribute(solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr_set = true;
-  }
   solve_kernel<<<1, kSolveThreads, use_smem ? need : 0, s>>>(G, n, c.cfg.lambda_rel, c.Mop,
                                                              c.chol_ws, use_smem, c.sc);
   c.launches++;
