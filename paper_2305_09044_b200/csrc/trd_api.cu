@@ -122,10 +122,14 @@ void build_plan(const Context& c, int k, const int64_t* s_in, BlockPlan& bp, boo
   {
     const int sm = c.cfg.shard_mode;
     const int64_t local = c.shard_end - c.shard_begin;
+    for (int m = 0; m < N; ++m) bp.s_samp[m] = bp.s[m];
     if (!rows && bp.s[sm] == c.dims[sm] && local < c.dims[sm]) {
       bp.s[sm] = local;
       bp.shard_local = 1;
       if (sm == k) bp.ik0 = c.shard_begin;   // plan rows i_k = ik0 + local index
+    } else if (!rows && sm != k && bp.s[sm] < c.dims[sm] && std::min<int64_t>(bp.s[sm], local) < bp.s[sm]) {
+      bp.s[sm] = std::min<int64_t>(bp.s[sm], local);   // capacity for this rank's sampled indices
+      bp.shard_sampled = 1;
     }
   }
   int64_t J = 1;                             // row sampling: J = prod_{m != k} s_m draws

@@ -78,6 +78,9 @@ struct BlockPlan {
   int shard_local;       // the shard mode (full index set) enumerates only this rank's slice
                          // [shard_begin, shard_end): per-rank GEMM work shrinks with world
   int64_t ik0;           // k == shard mode: global i_k of plan row index 0 (else 0)
+  int shard_sampled;     // sampled shard-mode set (m != k): only the rank's sampled indices,
+                         // compacted into a list of capacity min(s_m, slice) (rest padding)
+  int64_t s_samp[kMaxN]; // sample size of the RStS draw per mode (s[m] may be the capacity)
   int explicit_cols;     // 'uniform row sampling' (R22): p = 0, column q = draw q, whose index in
                          // right mode m is idx[idx_off[m] + q] (all s[m] = ncols = J)
   // pass-kernel geometry (v1 SIMT)

@@ -39,7 +39,9 @@ struct SamplerArgs {
   uint64_t seed;
   int64_t shard_begin, shard_end;
   int64_t dims[kMaxN], s[kMaxN], idx_off[kMaxN + 1], lstride[kMaxN];
-  int shard_local;       // shard mode enumerates [shard_begin, shard_end) (full set, m != k)
+  int shard_local;       // shard mode enumerates [shard_begin, shard_end) (full set)
+  int shard_sampled;     // shard mode: this rank's sampled indices, compacted, capacity s[m]
+  int64_t s_samp[kMaxN]; // RStS sample sizes (the draw; s[m] may be a smaller capacity)
 };
 
 __global__ void sampler_kernel(SamplerArgs sa, const DevScalars* __restrict__ sc,
@@ -50,12 +52,16 @@ __global__ void sampler_kernel(SamplerArgs sa, const DevScalars* __restrict__ sc
   const uint64_t seed = sa.seed;
   const int64_t I = sa.dims[m];
   const int64_t s = sa.s[m] <= 0 ? I : sa.s[m];
+  const int64_t s_draw = sa.s_samp[m] <= 0 ? I : sa.s_samp[m];      // selection size of the draw
+  const bool compact = m == sa.shard_mode && sa.shard_sampled;
   int32_t* out = idx + sa.idx_off[m];
   int64_t* dof = doff + sa.idx_off[m];
   const uint32_t t = (uint32_t)sc->sweep;
+  __shared__ int64_t n_local;                                         // (compacted lists)
+  if (threadIdx.x == 0) n_local = s;
   if (m == sa.shard_mode && sa.shard_local) {               // this rank's slice, global indices
     for (int64_t q = threadIdx.x; q < s; q += blockDim.x) out[q] = (int32_t)(sa.shard_begin + q);
-  } else if (s >= I) {
+  } else if (s >= I && !compact) {
     for (int64_t i = threadIdx.x; i < I; i += blockDim.x) out[i] = (int32_t)i;
   } else {
     for (int64_t i = threadIdx.x; i < I; i += blockDim.x) {
@@ -73,7 +79,8 @@ __global__ void sampler_kernel(SamplerArgs sa, const DevScalars* __restrict__ sc
         const unsigned long long kj = keys[j];
         rank += (kj < ki) || (kj == ki && j < i);
       }
-      sel[i] = rank < s;
+      // the draw selects s_draw of I; a compacted shard-mode list keeps this rank's ones
+      sel[i] = rank < s_draw && (!compact || (i >= sa.shard_begin && i < sa.shard_end));
     }
     __syncthreads();
     for (int64_t i = threadIdx.x; i < I; i += blockDim.x) {
@@ -82,6 +89,13 @@ __global__ void sampler_kernel(SamplerArgs sa, const DevScalars* __restrict__ sc
       for (int64_t j = 0; j < i; ++j) pos += sel[j];
       out[pos] = (int32_t)i;
     }
+    if (compact && threadIdx.x == 0) {
+      int64_t nl = 0;
+      for (int64_t j = 0; j < I; ++j) nl += sel[j];
+      n_local = nl;
+    }
+    __syncthreads();
+    for (int64_t q = n_local + threadIdx.x; q < s; q += blockDim.x) out[q] = (int32_t)sa.shard_begin;   // padding
   }
   __syncthreads();
   const int64_t cnt = s >= I ? I : s;
@@ -89,6 +103,7 @@ __global__ void sampler_kernel(SamplerArgs sa, const DevScalars* __restrict__ sc
     int64_t g = out[q];
     int64_t loc = g;
     if (m == sa.shard_mode) loc = (g >= sa.shard_begin && g < sa.shard_end) ? g - sa.shard_begin : -1;
+    if (q >= n_local) loc = -1;                                       // padding of a compacted list
     dof[q] = loc < 0 ? -1 : loc * sa.lstride[m];
   }
 }
@@ -1195,10 +1210,12 @@ void launch_sampler(Context& c, const BlockPlan& bp, cudaStream_t s) {
   sa.N = c.N; sa.k = bp.k; sa.shard_mode = c.cfg.shard_mode; sa.seed = c.cfg.seed;
   sa.shard_begin = c.shard_begin; sa.shard_end = c.shard_end;
   sa.shard_local = bp.shard_local;
+  sa.shard_sampled = bp.shard_sampled;
   int64_t maxI = 0;
   for (int m = 0; m < c.N; ++m) {
     sa.dims[m] = c.dims[m];
     sa.s[m] = bp.s[m];
+    sa.s_samp[m] = bp.s_samp[m];
     sa.idx_off[m] = c.idx_off[m];
     sa.lstride[m] = c.lstride[m];
     if (bp.s[m] < c.dims[m] && c.dims[m] > maxI) maxI = c.dims[m];

@@ -133,11 +133,13 @@ def test_block_quantities_match_oracle(name, dims, sketch, packed):
 
 
 @pytest.mark.parametrize("name,dims,sketch", [("C5b", [12, 9, 8, 7, 6], None),
-                                               ("C4", [12, 11, 10, 9], [4, 5, 3, 4])])
+                                               ("C4", [12, 11, 10, 9], [4, 5, 3, 4]),
+                                               ("C4", [12, 11, 10, 9], [9, 5, 3, 4])])
 def test_rank_shard_plans_match_oracle_partials(name, dims, sketch):
     """Data-parallel plans on one GPU: a context holding only the slab i_0 in [b, e) (world 1,
     partial shard: no exchange) computes that shard's partial d, n_obs and den; with full
-    index sets the shard mode enumerates only the local slice (per-rank GEMM work / world)."""
+    index sets the shard mode enumerates only the local slice, with sampled sets only the
+    rank's sampled indices (capacity min(s, slice), padded): per-rank GEMM work / world."""
     _cuda()
     import bench
     from paper_2305_09044_b200 import TRD
