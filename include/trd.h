@@ -171,7 +171,10 @@ TRD_API trd_status trd_upload(trd_ctx* ctx, const float* values_host, const uint
  * to idx_dev (device, int32, sum_m sizes[m] entries, mode-major, each set ascending) and
  * their sizes to sizes_host[N] (host).  Mode k gets 0..I_k-1.  With TRD_SAMPLING_ROWS every
  * other mode gets the J draws in draw order (entry q of each list = draw q; idx_dev must
- * hold I_k + (N-1) J entries).  Synchronises the stream. */
+ * hold I_k + (N-1) J entries).  With a partial shard (world > 1) the shard mode's list is
+ * this rank's part: its slice for a full set, its sampled indices (ascending, then padding
+ * entries equal to shard_begin that carry no data) for an RStS set, whose sizes[m] is the
+ * capacity min(s_m, slice).  Synchronises the stream. */
 TRD_API trd_status trd_sketch(trd_ctx* ctx, int32_t sweep, int32_t k, int32_t* idx_dev,
                       int64_t* sizes_host);
 
