@@ -199,10 +199,16 @@ void build_plan(const Context& c, int k, const int64_t* s_in, BlockPlan& bp, boo
       const int64_t items = nrt * se;
       const int64_t grid = std::min<int64_t>(items, (int64_t)c.num_sm);
       // busiest CTA: its items x (tiles per item + ~1 tile of per-item cost: A load, D drain
-      // and the split's share of the d reduction)
+      // and the split's share of the d reduction).  C5b (TRD_NSPLIT): 1 and 2 splits equal
+      // within run-to-run noise, 3 splits +3 %, 4 splits +6 %
       // (an odd split with tile pairs ends in a phantom half, costed as a whole tile)
       const double cost = (double)((items + grid - 1) / grid) * ((double)((per + U - 1) / U * U) + 1.0);
       if (cost < best - 1e-9) { best = cost; best_s = se; best_per = per; }
+    }
+    if (const char* e = getenv("TRD_NSPLIT")) {    // experiment knob: fixed column split count
+      const int64_t sp = std::max<int64_t>(1, std::min<int64_t>(atoll(e), nct));
+      best_per = (nct + sp - 1) / sp;
+      best_s = (nct + best_per - 1) / best_per;
     }
     bp.tc_nsplit = (int)best_s;
     bp.tc_per = best_per;
