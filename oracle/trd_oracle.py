@@ -31,11 +31,9 @@ import numpy as np
 from .philox import philox4x32_10, sample_indices
 
 SIGMA_FIXED, SIGMA_INF, SIGMA_RMS, SIGMA_MAD = 0, 1, 2, 3
-# robust sigma (reading R21): sigma = max(sigma_min, theta * MAD_C * median |e|), the median
-# estimated from a histogram of |e| with 16 linear sub-bins per octave over 2^-20 .. 2^12
+# robust sigma (reading R21): sigma = max(sigma_min, theta * MAD_C * median |e|), the exact
+# median of the sweep's pass-1 residual magnitudes
 MAD_C = 1.4826                     # 1 / Phi^-1(3/4): MAD -> standard deviation for Gaussians
-HIST_E0, HIST_OCT, HIST_SUB = -20, 32, 16
-HIST_BINS = HIST_OCT * HIST_SUB
 # operator of the update direction: the paper's scaled gradient (Eq. 16) and the two
 # ablation arms of Sec. 6.1 built on the same sketch
 SCALING_GLOBAL, SCALING_NONE, SCALING_LOCAL = 0, 1, 2
@@ -226,15 +224,34 @@ def gradient_entries(cores, k, index, x, sigma, sigma_inf=False):
     return d, float(np.sum(e * e))
 
 
+class NotSPD(ArithmeticError):
+    """G + lambda I stayed not positive definite through the retries (reading R23)."""
+
+
+LAMBDA_RETRIES = 3
+LAMBDA_FLOOR = 2.0 ** -40          # R23: first retry when lambda_rel = 0, relative to tr(G)/R^2
+
+
 def scaled_gradient(d, G, lambda_rel):
     """Eq. (10)/(16) with reading R5:
     lambda = lambda_rel * tr(G) / R^2, A = G + lambda I = L L^T and the filtered solve
     h = d A^{-1} G A^{-1} (= d (G + lambda I)^{-1} up to O(lambda/mu) on range(G)).
+    Reading R23: if the Cholesky factorisation of A fails, lambda <- 10 lambda
+    (from 2^-40 tr(G)/R^2 when lambda = 0), at most 3 retries, then NotSPD.
     Returns (h, lambda)."""
     R2 = G.shape[0]
-    lam = lambda_rel * float(np.trace(G)) / R2
-    A = G + lam * np.eye(R2)
-    L = np.linalg.cholesky(A)
+    scale = float(np.trace(G)) / R2
+    lam = lambda_rel * scale
+    for attempt in range(LAMBDA_RETRIES + 1):
+        if attempt > 0:
+            lam = 10.0 * lam if lam > 0.0 else LAMBDA_FLOOR * scale
+        try:
+            L = np.linalg.cholesky(G + lam * np.eye(R2))
+            break
+        except np.linalg.LinAlgError:
+            L = None
+    if L is None:
+        raise NotSPD(f"G + lambda I not positive definite (lambda = {lam:g})")
     # row-wise h = d A^{-1} G A^{-1}: solve A u^T = d^T, then A h^T = G u^T (A, G symmetric)
     U = _chol_solve(L, d.T)
     H = _chol_solve(L, G @ U)
@@ -397,39 +414,10 @@ def index_sets_for_block(cfg, t, k):
     return sets
 
 
-def hist_bin(ae):
-    """Bin of |e| (reading R21): bin (E - E0) * 16 + m covers [(1 + m/16) 2^E, (1 + (m+1)/16) 2^E);
-    values below 2^E0 (and 0) fall in bin 0, values >= 2^(E0 + 32) in the last bin."""
-    ae = np.asarray(ae, dtype=np.float64)
-    f, x = np.frexp(ae)                        # ae = f 2^x, f in [0.5, 1)
-    E = x - 1
-    m = np.floor((2.0 * f - 1.0) * HIST_SUB).astype(np.int64)
-    b = (E - HIST_E0) * HIST_SUB + m
-    b = np.where(E < HIST_E0, 0, b)
-    b = np.where(E >= HIST_E0 + HIST_OCT, HIST_BINS - 1, b)
-    return np.where(ae > 0.0, b, 0)
-
-
-def hist_median(counts):
-    """Median from the |e| histogram: the bin where the cumulative count reaches n/2, linear
-    interpolation inside it (reading R21)."""
-    counts = np.asarray(counts, dtype=np.float64)
-    target = 0.5 * float(counts.sum())
-    cum = 0.0
-    for b in range(HIST_BINS):
-        c = float(counts[b])
-        if c > 0.0 and cum + c >= target:
-            E, m = HIST_E0 + b // HIST_SUB, b % HIST_SUB
-            lo = (1.0 + m / HIST_SUB) * 2.0 ** E
-            return lo + (target - cum) / c * (2.0 ** E / HIST_SUB)
-        cum += c
-    return 0.0
-
-
 def mad_sigma(cfg, abs_e):
-    """R21: sigma = max(sigma_min, theta * 1.4826 * histogram median of |e|)."""
-    counts = np.bincount(hist_bin(abs_e), minlength=HIST_BINS)
-    return max(cfg.sigma_min, cfg.sigma_theta * MAD_C * hist_median(counts))
+    """R21: sigma = max(sigma_min, theta * 1.4826 * median |e|) -- the exact median (numpy's:
+    the middle value, or the mean of the two middle values of an even count)."""
+    return max(cfg.sigma_min, cfg.sigma_theta * MAD_C * float(np.median(np.asarray(abs_e, dtype=np.float64))))
 
 
 def initial_sigma(cfg, cores, source):
@@ -438,6 +426,14 @@ def initial_sigma(cfg, cores, source):
     observed entries."""
     if cfg.sigma_mode not in (SIGMA_RMS, SIGMA_MAD):
         return cfg.sigma
+    if hasattr(source, "pass1"):                  # entry-wise source: all observed entries
+        N = len(cfg.dims)
+        sets = [np.arange(cfg.dims[m], dtype=np.int64) for m in range(N)]
+        _, sum_e2, _, n, abs_e = source.pass1([np.asarray(c, dtype=np.float64) for c in cores], 0, sets,
+                                              cfg.ranks, 1.0, True, want_abs=cfg.sigma_mode == SIGMA_MAD)
+        if cfg.sigma_mode == SIGMA_MAD:
+            return mad_sigma(cfg, abs_e)
+        return max(cfg.sigma_min, cfg.sigma_theta * math.sqrt(sum_e2 / n))
     Xhat = tr_reconstruct([c.astype(np.float64) for c in cores])
     E = (source.X - Xhat)[source.P]
     if cfg.sigma_mode == SIGMA_MAD:
@@ -477,6 +473,8 @@ def block_update(cfg, st, source, k, rec, check_gram=False):
     ranks = cfg.ranks
     rk, rk1 = ranks[k], ranks[(k + 1) % N]
     sigma_inf = cfg.sigma_mode == SIGMA_INF
+    if hasattr(source, "pass1"):
+        return block_update_entries(cfg, st, source, k, rec)
     # line 4-5: index sets and sketch (or the uniform-row-sampling arm)
     if cfg.sampling == SAMPLING_ROWS:
         sets = row_samples(cfg, st.t, k)
@@ -523,6 +521,47 @@ def block_update(cfg, st, source, k, rec, check_gram=False):
         st.cores[k] = st.cores[k] + eta * core_fold2(h, rk, rk1)
     # line 10: refresh Q_k
     st.Qs[k] = q_matrix(st.cores[k])
+    return G
+
+
+def block_update_entries(cfg, st, source, k, rec):
+    """block_update with the two per-entry sums taken entry by entry (oracle/entries.py):
+    same lines 4-10 of Alg. 1 in the same order, for problems whose sketch does not fit the
+    dense unfolding (RStS subtensors only)."""
+    if cfg.sampling != SAMPLING_RSTS:
+        raise ValueError("entry-wise source: RStS index sets only")
+    N = len(cfg.dims)
+    rk, rk1 = cfg.ranks[k], cfg.ranks[(k + 1) % N]
+    sigma_inf = cfg.sigma_mode == SIGMA_INF
+    sets = index_sets_for_block(cfg, st.t, k)                       # line 4
+    s2 = st.sigma * st.sigma if abs(st.sigma) < 1e150 else float('inf')
+    sig = 1.0 if sigma_inf else st.sigma
+    d, sum_e2, welsch, n, abs_e = source.pass1(st.cores, k, sets, cfg.ranks, sig, sigma_inf,
+                                               want_abs=cfg.sigma_mode == SIGMA_MAD)   # lines 5-7
+    rec.sum_e2 += sum_e2
+    rec.n_obs += n
+    rec.nnz[k] = n
+    if cfg.sigma_mode == SIGMA_MAD:
+        rec.abs_e.append(abs_e)
+    if not sigma_inf and math.isfinite(s2):
+        rec.welsch += welsch
+    G = gram_fgmc(st.Qs, k, cfg.ranks)                              # line 8
+    h = update_direction(cfg, d, G, st.cores, k, sets)              # line 9
+    num = float(np.sum(d * h))
+    den = source.pass2(st.cores, k, sets, cfg.ranks, sig, sigma_inf, h)
+    rec.num[k], rec.den[k] = num, den
+    if cfg.step > 0.0:
+        eta = cfg.step
+    elif num > 0.0 and den > 0.0:
+        eta = num / den
+    else:
+        eta = 0.0
+    rec.eta[k] = eta
+    if eta == 0.0:
+        rec.skipped[k] = True
+    else:
+        st.cores[k] = st.cores[k] + eta * core_fold2(h, rk, rk1)
+    st.Qs[k] = q_matrix(st.cores[k])                                # line 10
     return G
 
 
