@@ -65,8 +65,8 @@ typedef enum {
   TRD_SIGMA_RMS = 2,    /* reading R9: sigma_{t+1} = max(sigma_min, theta * RMS(e))      */
   TRD_SIGMA_MAD = 3     /* reading R21 (robust rule): sigma_{t+1} = max(sigma_min,
                            theta * 1.4826 * median |e|) over the sweep's pass-1 residuals, the
-                           median from a 512-bin histogram of |e| (16 linear sub-bins per
-                           octave over 2^-20 .. 2^12) with linear interpolation in its bin   */
+                           exact median (mean of the two middle values of an even count) by a
+                           radix select over the fp32 |e| values                             */
 } trd_sigma_mode;
 
 typedef struct {
@@ -147,7 +147,7 @@ typedef struct {
 typedef struct {
   double rel_err_all;               /* ||X_hat - X_ref|| / ||X_ref|| over evaluated entries  */
   double rel_err_observed;          /* same, restricted to observed entries                  */
-  double psnr;                      /* 10 log10(peak^2 / MSE), peak = max |X_ref|    */
+  double psnr;                      /* 10 log10(peak^2 / MSE) over the evaluated entries */
   int64_t n_eval;                   /* entries evaluated                                      */
 } trd_error_stats;
 
@@ -164,7 +164,8 @@ TRD_API trd_status trd_init(const trd_config* cfg, const trd_shard* shard,
  * oldest pending upload (waits for its copy, restages, recomputes the packed rank prefix).
  * At most two uploads may be pending (TRD_ERR_STATE otherwise).  Same layout and sizes as at
  * trd_init (packed: same number of observed entries).  The host buffers (pinned for overlap)
- * must stay unmodified until the trd_sweep that consumes them returns. */
+ * must stay unmodified until the call that consumes the upload (trd_sweep, trd_block_probe or
+ * trd_error) returns; that call waits for the copy before returning. */
 TRD_API trd_status trd_upload(trd_ctx* ctx, const float* values_host, const uint32_t* mask_host);
 
 /* Write the RStS index sets of sweep `sweep`, block k (Alg. 1 line 4; reading R11)
@@ -179,22 +180,27 @@ TRD_API trd_status trd_sketch(trd_ctx* ctx, int32_t sweep, int32_t k, int32_t* i
                       int64_t* sizes_host);
 
 /* Run n_sweeps iterations of Alg. 1 (lines 3-13).  stats: host array of n_sweeps records
- * or NULL.  With stats == NULL the call only enqueues work (no host synchronisation).
- * Returns TRD_ERR_NONFINITE if a non-finite value appeared (checked when stats != NULL
- * and at trd_get_cores). */
+ * or NULL.  With stats == NULL the call only enqueues work (no host synchronisation, except
+ * that a pending upload's copy is waited for).  Returns TRD_ERR_NONFINITE if a non-finite
+ * value appeared, TRD_ERR_NOT_SPD if G + lambda I stayed indefinite through the retries of
+ * reading R23 (both checked when stats != NULL; NONFINITE also at trd_get_cores). */
 TRD_API trd_status trd_sweep(trd_ctx* ctx, int32_t n_sweeps, trd_sweep_stats* stats);
 
 /* Evaluate the TR model (Def. 1) at n global linear indices (device int64) into
  * out_dev (device float).  Enqueued on the context stream; no synchronisation. */
 TRD_API trd_status trd_reconstruct(trd_ctx* ctx, const int64_t* lin_idx_dev, int64_t n, float* out_dev);
 
-/* Relative error of the model against ref_dev (device float, dense local shard layout),
- * over all local entries, or over those whose bit is set in eval_bits (device, may be
- * NULL).  Partial sums are allreduced when world > 1.  Synchronises the stream. */
-TRD_API trd_status trd_error(trd_ctx* ctx, const float* ref_dev, const uint32_t* eval_bits,
+/* Relative error and PSNR of the model against ref_dev (device float, dense local
+ * shard layout), over all local entries, or over those whose bit is set in eval_bits (device,
+ * may be NULL).  peak: the PSNR peak value (0 = 1.0: the paper rescales data to [0, 1],
+ * P:326; < 0 is TRD_ERR_INVALID_ARG).  Partial sums are allreduced when world > 1.
+ * Synchronises the stream. */
+TRD_API trd_status trd_error(trd_ctx* ctx, const float* ref_dev, const uint32_t* eval_bits, double peak,
                      trd_error_stats* out);
 
 /* Copy cores to / from the host (layout as init_cores).  Synchronises the stream.
+ * trd_get_cores copies the cores even in the sticky error state; it returns
+ * TRD_ERR_NONFINITE if a copied value is not finite or a sweep flagged a non-finite step.
  * trd_set_cores rebuilds the FGMC cache. */
 TRD_API trd_status trd_get_cores(trd_ctx* ctx, float* const* cores_host);
 TRD_API trd_status trd_set_cores(trd_ctx* ctx, const float* const* cores_host);

@@ -303,6 +303,7 @@ trd_status block_pass1(Context* c, const BlockPlan& bp) {
   if (bp.use_tc) launch_tc_pass(*c, bp, stg, false, s);
   else launch_pass1(*c, bp, 0, s);
   if (c->prof) c->ev_pass1.push_back({e0, prof_event(c)});
+  if (bp.use_tc && c->eabs) launch_eabs_advance(*c, stg, s);   // R21 |e| slots of this block
   if (bp.use_tc) launch_tc_reduce_d(*c, bp, s);
   else launch_reduce_d(*c, bp, s);
   trd_status st = check_launch(c, "pass 1");
@@ -331,6 +332,20 @@ trd_status block_pass2(Context* c, const BlockPlan& bp) {
   return allreduce(c, c->red_ws, 1);
 }
 
+// R21: exact median of eabs[0, eabs_fill) (all ranks' values: the histograms are allreduced)
+trd_status mad_select(Context* c) {
+  cudaStream_t s = c->stream;
+  for (int level = 0; level < 3; ++level) {
+    launch_mad_hist(*c, level, s);
+    const size_t off = level == 0 ? 0 : level == 1 ? kMadBins0 : kMadBins0 + 2 * kMadBins1;
+    const size_t n = level == 0 ? kMadBins0 : level == 1 ? 2 * kMadBins1 : 2 * kMadBins2;
+    trd_status st = allreduce(c, c->mhist + off, n);
+    if (st) return st;
+    launch_mad_scan(*c, level, s);
+  }
+  return check_launch(c, "mad select");
+}
+
 trd_status ensure_stats(Context* c, int n) {
   if (n <= c->stats_cap) return TRD_OK;
   if (c->stats) cudaFree(c->stats);
@@ -344,7 +359,7 @@ trd_status ensure_stats(Context* c, int n) {
 trd_status sigma0_pass(Context* c) {
   const BlockPlan& bp = c->full_plan;
   cudaStream_t s = c->stream;
-  if (c->hist) CUDA_TRY(c, cudaMemsetAsync(c->hist, 0, kHistBins * sizeof(double), s));
+  if (c->eabs) CUDA_TRY(c, cudaMemsetAsync(&c->sc->eabs_fill, 0, sizeof(unsigned long long), s));
   launch_sampler(*c, bp, s);
   launch_plan(*c, bp, s);
   launch_lft(*c, bp, c->Z + c->zoff[bp.k], 0, c->lft, s);
@@ -360,9 +375,23 @@ trd_status sigma0_pass(Context* c) {
   if (st) return st;
   st = allreduce(c, c->red_ws, 3);
   if (st) return st;
-  if (c->hist && (st = allreduce(c, c->hist, (size_t)kHistBins))) return st;
+  if (c->eabs && (st = mad_select(c))) return st;
   launch_sigma0(*c, s);
   return check_launch(c, "sigma0");
+}
+
+// observed entries of the local mask (dense storage; packed: n_values)
+trd_status count_observed(Context* c, int64_t* out) {
+  unsigned long long* d = nullptr;
+  CUDA_TRY(c, cudaMalloc(&d, sizeof(unsigned long long)));
+  launch_count_bits(*c, d, c->stream);
+  unsigned long long h = 0;
+  cudaError_t e = cudaMemcpyAsync(&h, d, sizeof(h), cudaMemcpyDeviceToHost, c->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+  cudaFree(d);
+  if (e != cudaSuccess) return fail(c, TRD_ERR_CUDA, "count_observed: %s", cudaGetErrorString(e));
+  *out = (int64_t)h;
+  return TRD_OK;
 }
 
 void host_to_dev_core(const Context& c, int k, const float* src, std::vector<float>& tmp) {
@@ -379,7 +408,9 @@ void host_to_dev_core(const Context& c, int k, const float* src, std::vector<flo
 // =======================================================================================
 extern "C" {
 
-const char* trd_version(void) { return "libtrd 0.1 (sm_100a, v1 SIMT pass kernels)"; }
+const char* trd_version(void) {
+  return "libtrd 0.2 (sm_100a: persistent tcgen05 pass kernels, CTA pairs; fp64 FGMC / filtered solve)";
+}
 
 trd_status trd_nccl_unique_id(void* out128) {
   if (!out128) return TRD_ERR_INVALID_ARG;
@@ -473,7 +504,6 @@ trd_status trd_init(const trd_config* cfg, const trd_shard* shard, const float* 
     if (cfg->ranks[m] < 1 || cfg->ranks[m] > TRD_MAX_RANK) return TRD_ERR_SHAPE;
     if (cfg->sketch[m] < 0) return TRD_ERR_SHAPE;
     if (!init_cores[m]) return TRD_ERR_INVALID_ARG;
-    if (cfg->sketch[m] > 0 && cfg->sketch[m] < cfg->dims[m] && cfg->dims[m] > 16384) return TRD_ERR_SHAPE;
   }
   if (cfg->sigma_mode < 0 || cfg->sigma_mode > TRD_SIGMA_MAD) return TRD_ERR_INVALID_ARG;
   if (cfg->sigma_mode == TRD_SIGMA_FIXED && !(cfg->sigma > 0.0)) return TRD_ERR_INVALID_ARG;
@@ -542,7 +572,7 @@ trd_status trd_init(const trd_config* cfg, const trd_shard* shard, const float* 
   // ---- plans and workspace sizes ----
   size_t max_rows = 0, max_cols = 0, max_lft = 0, max_rgt = 0, max_mid = 0, max_dp = 0, max_sp = 0;
   size_t max_dvec = 0, max_h = 0, idx_total = 0;
-  size_t max_lhl = 0, max_rhl = 0, max_contrib = 0;
+  size_t max_lhl = 0, max_rhl = 0, max_contrib = 0, max_rpad = 0;
   int64_t full_s[kMaxN];
   for (int m = 0; m < N; ++m) full_s[m] = 0;
   {
@@ -563,6 +593,7 @@ trd_status trd_init(const trd_config* cfg, const trd_shard* shard, const float* 
       if (bp.explicit_cols) st.invariant = false;          // rows are redrawn every sweep
       st.vcap = bp.n_row_tiles * 128 * bp.n_col_tiles * 64;   // refined after the data is known
       max_lhl = std::max(max_lhl, (size_t)(bp.n_row_tiles * 2 * 128 * bp.KP));
+      max_rpad = std::max(max_rpad, (size_t)(bp.n_row_tiles * 128));
       max_rhl = std::max(max_rhl, (size_t)(bp.n_col_tiles * 2 * 64 * bp.KP));
       max_contrib = std::max(max_contrib, (size_t)bp.tc_nsplit * bp.n_row_tiles * 128 * bp.KP);
       max_sp = std::max(max_sp, (size_t)bp.tc_grid * 3);
@@ -623,12 +654,13 @@ trd_status trd_init(const trd_config* cfg, const trd_shard* shard, const float* 
       (st = dalloc(c, &c->Dcur, (size_t)(In * In))) || (st = dalloc(c, &c->Dprev, (size_t)(In * In))) ||
       (st = dalloc(c, &c->sc, 1)) || (st = dalloc(c, &c->red_ws, 1024)))
     return bail(st);
-  if (cfg->sigma_mode == TRD_SIGMA_MAD && (st = dalloc(c, &c->hist, (size_t)kHistBins))) return bail(st);
+  if (cfg->sigma_mode == TRD_SIGMA_MAD && (st = dalloc(c, &c->mhist, (size_t)kMadHist))) return bail(st);
   if (cfg->scaling == TRD_SCALING_LOCAL &&
       ((st = dalloc(c, &c->Qloc, (size_t)qtot)) || (st = dalloc(c, &c->Gloc, (size_t)kMaxR2 * kMaxR2))))
     return bail(st);
   if (max_lhl > 0) {
     if ((st = dalloc(c, &c->lftHL, max_lhl)) || (st = dalloc(c, &c->lfthHL, max_lhl)) ||
+        (st = dalloc(c, &c->lscl, max_rpad)) || (st = dalloc(c, &c->lsclh, max_rpad)) ||
         (st = dalloc(c, &c->rgtHL, max_rhl)) || (st = dalloc(c, &c->rgtHL2, max_rhl)) ||
         (st = dalloc(c, &c->contrib, max_contrib)))
       return bail(st);
@@ -664,7 +696,10 @@ trd_status trd_init(const trd_config* cfg, const trd_shard* shard, const float* 
       if (!c->plan[k].use_tc) continue;
       TcStage& sg = c->stage[k];
       const int64_t obs_cap = c->packed ? c->n_values : c->n_local;
-      sg.vcap = std::max<int64_t>(1, std::min(sg.vcap, obs_cap)) + 8 * sg.n_tiles;   // + tile padding
+      // (row sampling draws with replacement: a duplicate draw stages an observed entry again,
+      //  so explicit-column plans keep the dense working-set bound)
+      if (!c->plan[k].explicit_cols) sg.vcap = std::min(sg.vcap, obs_cap);
+      sg.vcap = std::max<int64_t>(1, sg.vcap) + 8 * sg.n_tiles;   // + tile padding
       sg.scan_tmp_bytes = tc_scan_tmp_bytes(sg.n_tiles);
       if ((st = dalloc(c, &sg.tbits, (size_t)sg.n_tiles * 128)) ||
           (st = dalloc(c, &sg.troff, (size_t)sg.n_tiles * 128)) ||
@@ -675,6 +710,19 @@ trd_status trd_init(const trd_config* cfg, const trd_shard* shard, const float* 
       max_v = std::max(max_v, sg.vcap);
     }
     if (max_v > 0 && (st = dalloc(c, &c->tw, (size_t)max_v))) return bail(st);
+  }
+  // R21: |e| slots of one sweep (every block's staged slots, or its observed entries) or of the
+  // sigma_0 pass (all local observed entries)
+  if (cfg->sigma_mode == TRD_SIGMA_MAD) {
+    int64_t n_obs = c->n_values;
+    if (!c->packed) {
+      if ((st = count_observed(c, &n_obs))) return bail(st);
+    }
+    int64_t per_sweep = 0;
+    for (int k = 0; k < N; ++k)
+      per_sweep += c->plan[k].use_tc ? c->stage[k].vcap : std::min<int64_t>(c->plan[k].nnz_ws, n_obs);
+    c->eabs_cap = (size_t)std::max<int64_t>(per_sweep, n_obs);
+    if ((st = dalloc(c, &c->eabs, c->eabs_cap))) return bail(st);
   }
   if (shard->host) {
     if ((st = dalloc(c, &c->own_values, (size_t)c->n_values))) return bail(st);
@@ -697,6 +745,7 @@ trd_status trd_init(const trd_config* cfg, const trd_shard* shard, const float* 
   hs.sigma = cfg->sigma_mode == TRD_SIGMA_FIXED ? cfg->sigma : (cfg->sigma_mode == TRD_SIGMA_INF ? INFINITY : 1.0);
   CUDA_TRY(c, cudaMemcpyAsync(c->sc, &hs, sizeof(hs), cudaMemcpyHostToDevice, s));
   CUDA_TRY(c, cudaMemsetAsync(c->Dprev, 0, (size_t)(In * In) * 8, s));
+  launch_amax_obs(*c, s);
   for (int k = 0; k < N; ++k) launch_q(*c, k, s);
   if ((st = check_launch(c, "init Q"))) return bail(st);
 
@@ -754,12 +803,16 @@ static trd_status consume_upload(Context* c) {
   c->up_pend[0] = c->up_pend[1];
   --c->up_npend;
   CUDA_TRY(c, cudaStreamWaitEvent(c->stream, c->ev_up_ready[b], 0));
+  // trd.h: the host buffers of an upload may be reused once the consuming call returns, so
+  // that call returns only after the copy has read them
+  CUDA_TRY(c, cudaEventSynchronize(c->ev_up_ready[b]));
   c->up_active = b;
   c->own_values = c->up_values[b];
   c->own_mask = c->up_mask[b];
   c->values = c->own_values;
   c->mask = c->own_mask;
   if (c->packed) launch_rank_prefix(*c, c->stream);
+  launch_amax_obs(*c, c->stream);
   for (int k = 0; k < c->N; ++k) c->stage[k].valid = false;   // staged sketches are stale
   return check_launch(c, "upload consume");
 }
@@ -770,8 +823,9 @@ trd_status trd_sketch(trd_ctx* ctx, int32_t sweep, int32_t k, int32_t* idx_dev, 
   if (c->sticky) return c->sticky;
   if (k < 0 || k >= c->N || sweep < 0) return TRD_ERR_INVALID_ARG;
   const BlockPlan& bp = c->plan[k];
-  int saved = 0;
-  CUDA_TRY(c, cudaMemcpy(&saved, &c->sc->sweep, 4, cudaMemcpyDeviceToHost));
+  int saved = 0;                             // (read on the context stream: sweeps may be in flight)
+  CUDA_TRY(c, cudaMemcpyAsync(&saved, &c->sc->sweep, 4, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
   CUDA_TRY(c, cudaMemcpyAsync(&c->sc->sweep, &sweep, 4, cudaMemcpyHostToDevice, c->stream));
   launch_sampler(*c, bp, c->stream);
   trd_status st = check_launch(c, "sampler");
@@ -805,7 +859,6 @@ trd_status trd_sweep(trd_ctx* ctx, int32_t n_sweeps, trd_sweep_stats* stats) {
   }
   for (int t = 0; t < n_sweeps; ++t) {
     launch_sweep_begin(*c, t, s);
-    if (c->hist) CUDA_TRY(c, cudaMemsetAsync(c->hist, 0, kHistBins * sizeof(double), s));
     for (int k = 0; k < c->N; ++k) {
       const BlockPlan& bp = c->plan[k];
       if ((st = block_pass1(c, bp))) return st;
@@ -816,7 +869,7 @@ trd_status trd_sweep(trd_ctx* ctx, int32_t n_sweeps, trd_sweep_stats* stats) {
       launch_q(*c, k, s);
       if ((st = check_launch(c, "update"))) return st;
     }
-    if (c->hist && (st = allreduce(c, c->hist, (size_t)kHistBins))) return st;   // (world > 1)
+    if (c->eabs && (st = mad_select(c))) return st;         // R21 (histograms allreduced)
     launch_sweep_end(*c, t, s);
     if ((st = check_launch(c, "sweep end"))) return st;
     if (stats) CUDA_TRY(c, cudaEventRecord(ev[(size_t)t + 1], s));
@@ -856,9 +909,11 @@ trd_status trd_block_probe(trd_ctx* ctx, int32_t sweep, int32_t k, double* d_hos
   if (trd_status su = consume_upload(c)) return su;
   const BlockPlan& bp = c->plan[k];
   cudaStream_t s = c->stream;
-  int saved = 0;
-  CUDA_TRY(c, cudaMemcpy(&saved, &c->sc->sweep, 4, cudaMemcpyDeviceToHost));
+  int saved = 0;                             // (read on the context stream: sweeps may be in flight)
+  CUDA_TRY(c, cudaMemcpyAsync(&saved, &c->sc->sweep, 4, cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(c, cudaStreamSynchronize(s));
   CUDA_TRY(c, cudaMemcpyAsync(&c->sc->sweep, &sweep, 4, cudaMemcpyHostToDevice, s));
+  if (c->eabs) CUDA_TRY(c, cudaMemsetAsync(&c->sc->eabs_fill, 0, sizeof(unsigned long long), s));
   trd_status st;
   if ((st = block_pass1(c, bp))) return st;
   if ((st = block_pass2(c, bp))) return st;
@@ -891,9 +946,11 @@ trd_status trd_reconstruct(trd_ctx* ctx, const int64_t* lin_idx_dev, int64_t n, 
   return check_launch(c, "reconstruct");
 }
 
-trd_status trd_error(trd_ctx* ctx, const float* ref_dev, const uint32_t* eval_bits, trd_error_stats* out) {
+trd_status trd_error(trd_ctx* ctx, const float* ref_dev, const uint32_t* eval_bits, double peak,
+                     trd_error_stats* out) {
   Context* c = reinterpret_cast<Context*>(ctx);
-  if (!c || !ref_dev || !out) return TRD_ERR_INVALID_ARG;
+  if (!c || !ref_dev || !out || !(peak >= 0.0)) return TRD_ERR_INVALID_ARG;
+  if (peak == 0.0) peak = 1.0;                // data rescaled to [0, 1]
   if (c->sticky) return c->sticky;
   if (trd_status su = consume_upload(c)) return su;
   const BlockPlan& bp = c->full_plan;
@@ -915,7 +972,7 @@ trd_status trd_error(trd_ctx* ctx, const float* ref_dev, const uint32_t* eval_bi
   out->rel_err_observed = v[3] > 0 ? sqrt(v[2] / v[3]) : 0.0;
   out->n_eval = (int64_t)v[4];
   const double mse = v[4] > 0 ? v[0] / v[4] : 0.0;
-  out->psnr = mse > 0 ? 10.0 * log10(v[5] * v[5] / mse) : INFINITY;
+  out->psnr = mse > 0 ? 10.0 * log10(peak * peak / mse) : INFINITY;
   return TRD_OK;
 }
 
@@ -923,6 +980,7 @@ trd_status trd_get_cores(trd_ctx* ctx, float* const* cores_host) {
   Context* c = reinterpret_cast<Context*>(ctx);
   if (!c || !cores_host) return TRD_ERR_INVALID_ARG;
   std::vector<float> tmp;
+  bool nonfinite = false;
   cudaStreamSynchronize(c->stream);
   for (int k = 0; k < c->N; ++k) {
     if (!cores_host[k]) return TRD_ERR_INVALID_ARG;
@@ -934,7 +992,14 @@ trd_status trd_get_cores(trd_ctx* ctx, float* const* cores_host) {
     for (int a = 0; a < r0; ++a)
       for (int64_t i = 0; i < I; ++i)
         for (int b = 0; b < r1; ++b) cores_host[k][(a * I + i) * r1 + b] = tmp[(i * r0 + a) * r1 + b];
+    for (const float v : tmp)
+      if (!std::isfinite(v)) nonfinite = true;
   }
+  if (!c->sticky) {
+    DevScalars hs;
+    if (cudaMemcpy(&hs, c->sc, sizeof(hs), cudaMemcpyDeviceToHost) == cudaSuccess && hs.nonfinite) nonfinite = true;
+  }
+  if (nonfinite) return fail(c, TRD_ERR_NONFINITE, "non-finite core values or statistics");
   return TRD_OK;
 }
 
@@ -980,7 +1045,8 @@ void trd_destroy(trd_ctx* ctx) {
                   c->row_off, c->col_off, c->mid, c->lft, c->lfth, c->rgtT, c->dpart, c->spart,
                   c->denpart, c->numpart, c->dvec, c->G, c->G_last, c->Mop, c->chol_ws,
                   c->chain_ws, c->h, c->Dcur, c->Dprev, c->sc, c->stats, c->red_ws,
-                  c->lftHL, c->lfthHL, c->rgtHL, c->rgtHL2, c->contrib, c->Qloc, c->Gloc, c->hist};
+                  c->lftHL, c->lfthHL, c->lscl, c->lsclh, c->rgtHL, c->rgtHL2, c->contrib, c->Qloc, c->Gloc, c->mhist,
+                  c->eabs};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->tw) cudaFree(c->tw);

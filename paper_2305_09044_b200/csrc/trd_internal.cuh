@@ -26,18 +26,25 @@ struct DevStats {
 };
 
 // Scalars shared by the kernels of one block (device memory).
-// |e| histogram of the robust sigma rule (reading R21, TRD_SIGMA_MAD): bin (E - E0) * 16 + m
-// covers [(1 + m/16) 2^E, (1 + (m+1)/16) 2^E), E in [E0, E0 + 32); below -> bin 0, above ->
-// the last bin.  Read off the fp32 exponent and the top 4 mantissa bits.
-constexpr int kHistBins = 512, kHistE0 = -20;
-__device__ __forceinline__ int mad_bin(float ae) {
-  if (!(ae > 0.f)) return 0;
-  const uint32_t b = __float_as_uint(ae);
-  const int E = (int)(b >> 23) - 127;
-  if (E < kHistE0) return 0;
-  if (E >= kHistE0 + 32) return kHistBins - 1;
-  return (E - kHistE0) * 16 + (int)((b >> 19) & 15u);
+// Exact median of the sweep's |e| (robust sigma rule, reading R21, TRD_SIGMA_MAD): pass 1
+// writes the fp32 bit pattern of every observed |e| (tile-staged slots of padding entries get
+// kEabsPad, which the select skips); an exact radix select over the bit patterns (11 + 11 + 10
+// bits, per-CTA shared-memory histograms, integer counts) finds the two middle order
+// statistics.  Histogram regions of c->mhist: level 0 [2048] | level 1 [2][2048] | level 2 [2][1024].
+constexpr uint32_t kEabsPad = 0xFFFFFFFFu;
+
+// Power-of-two scale exponent E of an fp16 hi / lo operand with max |.| = amax: amax 2^E lies
+// in [2^14, 2^15), so every element is below the fp16 maximum (65504) and elements down to
+// 2^-15 of the maximum keep a normal lo part (22 significant bits).  Scaling by 2^E is exact.
+__host__ __device__ __forceinline__ int tc_scale_exp(float amax) {
+  if (!(amax > 0.f) || !(amax < 3.0e38f)) return 0;
+  int e = 0;
+  frexpf(amax, &e);                  // amax = f 2^e, f in [0.5, 1): floor(log2 amax) = e - 1
+  const int E = 15 - e;
+  return E < -100 ? -100 : (E > 100 ? 100 : E);
 }
+constexpr int kMadBins0 = 2048, kMadBins1 = 2048, kMadBins2 = 1024;
+constexpr int kMadHist = kMadBins0 + 2 * kMadBins1 + 2 * kMadBins2;
 
 struct DevScalars {
   double sigma;          // kernel width of the current sweep
@@ -54,6 +61,16 @@ struct DevScalars {
   int have_prev_D;
   int prof_on;           // accumulate local observed entries per block (profiling)
   double prof_nobs[kMaxN];
+  // power-of-two operand scaling of the fp16 hi / lo tensor-core operands:
+  // max |.| as fp32 bit patterns (non-negative floats order like unsigned ints: atomicMax)
+  unsigned int amax_x;            // observed values (init / each upload)
+  unsigned int amax_a;            // pass-1 A operand (Lft) of the current block
+  unsigned int amax_b;            // B operand (Rgt) of the current block
+  unsigned long long eabs_fill;   // R21: |e| slots written in this sweep (or the sigma_0 pass)
+  unsigned int mad_pre[2];        // R21 select: bit prefixes of the two middle order statistics
+  long long mad_rank[2];          //   and their ranks among the values with that prefix
+  double mad_n;                   //   number of |e| values
+  double mad_med;                 //   their median
 };
 
 // GEMM form of block k: the working set WS_k = I_k x prod_{m!=k} s_m is
@@ -153,7 +170,9 @@ struct Context {
   float* Z = nullptr;                  // cores, slice-major: Z_k[i][a][b]
   int64_t zoff[kMaxN + 1];
   double* Q = nullptr;                 // FGMC Q_k (r_k^2 x r_{k+1}^2)
-  double* hist = nullptr;              // TRD_SIGMA_MAD: |e| histogram of the sweep (counts)
+  uint32_t* eabs = nullptr;            // TRD_SIGMA_MAD: fp32 bits of the sweep's |e| (R21)
+  size_t eabs_cap = 0;
+  double* mhist = nullptr;             // TRD_SIGMA_MAD: radix-select histograms (kMadHist)
   double* Qloc = nullptr;              // 'local scaled term' arm: Q_m over the sampled slices
   double* Gloc = nullptr;              //   and its Gram
   int64_t qoff[kMaxN + 1];
@@ -174,6 +193,8 @@ struct Context {
   int want_tc = 1;                     // TRD_PASS=simt disables the tcgen05 pass kernels
   __half* lftHL = nullptr;             // [row][hi KP | lo KP] (A operand, loaded into TMEM)
   __half* lfthHL = nullptr;            // same for the scaled gradient (pass 2)
+  float* lscl = nullptr;               // [row] 2^-E of the row's A scaling (pass 1)
+  float* lsclh = nullptr;              // [row] same for pass 2
   __half* rgtHL = nullptr;             // [col tile][hi | lo][64 x KP] core-matrix layout (L1)
   __half* rgtHL2 = nullptr;            // same tiles, layout L2 ([hi KP | lo KP] per column)
   float* contrib = nullptr;            // [split][row][KP] D rows of pass 1
@@ -227,10 +248,15 @@ void launch_reduce_den(Context& c, const BlockPlan& bp, cudaStream_t s);
 void launch_update(Context& c, const BlockPlan& bp, int sweep_slot, cudaStream_t s);
 void launch_sweep_end(Context& c, int sweep_slot, cudaStream_t s);
 void launch_sigma0(Context& c, cudaStream_t s);
+void launch_eabs_advance(Context& c, const TcStage& st, cudaStream_t s);
+void launch_mad_hist(Context& c, int level, cudaStream_t s);   // R21 select, level 0..2
+void launch_mad_scan(Context& c, int level, cudaStream_t s);
 void launch_reconstruct(Context& c, const int64_t* lin, int64_t n, float* out, cudaStream_t s);
 void launch_error(Context& c, const float* ref, const uint32_t* eval_bits, double* out4,
                   cudaStream_t s);
 void launch_rank_prefix(Context& c, cudaStream_t s);
+void launch_count_bits(Context& c, unsigned long long* out, cudaStream_t s);
+void launch_amax_obs(Context& c, cudaStream_t s);   // sc->amax_x of the observed values
 void launch_reset_block_scalars(Context& c, cudaStream_t s);
 void launch_record_block(Context& c, const BlockPlan& bp, int slot, cudaStream_t s);
 void launch_sweep_begin(Context& c, int slot, cudaStream_t s);

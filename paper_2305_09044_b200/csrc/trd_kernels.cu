@@ -33,7 +33,11 @@ __device__ __forceinline__ void philox10(uint32_t c[4], uint32_t k0, uint32_t k1
 }
 
 // One CTA per mode m: writes the index set I_m of (sweep t, block k) and the data offsets.
-// Selection = the s_m smallest (kappa_i, i), output ascending (rank-based, deterministic).
+// Selection = the s_m smallest (kappa_i, i), output ascending (reading R11).  The key kappa_K
+// of rank s_m - 1 is found by an 8-pass radix select over the 64-bit keys (8 bits per pass,
+// per-CTA shared-memory histograms; the keys are recomputed, nothing of size I is stored), then
+// one ascending pass over i keeps kappa_i < kappa_K and the first (in i) of the keys equal to
+// kappa_K up to rank s_m - 1: O(I) work, no limit on I_m.
 struct SamplerArgs {
   int N, k, shard_mode;
   uint64_t seed;
@@ -44,10 +48,22 @@ struct SamplerArgs {
   int64_t s_samp[kMaxN]; // RStS sample sizes (the draw; s[m] may be a smaller capacity)
 };
 
-__global__ void sampler_kernel(SamplerArgs sa, const DevScalars* __restrict__ sc,
-                               int32_t* __restrict__ idx, int64_t* __restrict__ doff) {
-  extern __shared__ unsigned long long keys[];
-  const int m = blockIdx.x;
+constexpr int kSamplerThreads = 256;
+__device__ __forceinline__ unsigned long long sample_key(uint64_t seed, int64_t i, int m, int k, uint32_t t) {
+  uint32_t c[4] = {(uint32_t)i, (uint32_t)m, (uint32_t)k, t};
+  philox10(c, (uint32_t)(seed & 0xffffffffu), (uint32_t)(seed >> 32));
+  return ((unsigned long long)c[0] << 32) | c[1];
+}
+
+__global__ void __launch_bounds__(kSamplerThreads)
+sampler_kernel(SamplerArgs sa, const DevScalars* __restrict__ sc, int32_t* __restrict__ idx,
+               int64_t* __restrict__ doff) {
+  using Scan = cub::BlockScan<long long, kSamplerThreads>;
+  __shared__ typename Scan::TempStorage scan_tmp;
+  __shared__ unsigned int hist[256];
+  __shared__ int sel_bin;
+  __shared__ long long rank_s;
+  const int m = blockIdx.x, tid = threadIdx.x;
   const int k = sa.k;
   const uint64_t seed = sa.seed;
   const int64_t I = sa.dims[m];
@@ -57,49 +73,65 @@ __global__ void sampler_kernel(SamplerArgs sa, const DevScalars* __restrict__ sc
   int32_t* out = idx + sa.idx_off[m];
   int64_t* dof = doff + sa.idx_off[m];
   const uint32_t t = (uint32_t)sc->sweep;
-  __shared__ int64_t n_local;                                         // (compacted lists)
-  if (threadIdx.x == 0) n_local = s;
+  int64_t n_local = s;                                                // (compacted lists)
   if (m == sa.shard_mode && sa.shard_local) {               // this rank's slice, global indices
-    for (int64_t q = threadIdx.x; q < s; q += blockDim.x) out[q] = (int32_t)(sa.shard_begin + q);
-  } else if (s >= I && !compact) {
-    for (int64_t i = threadIdx.x; i < I; i += blockDim.x) out[i] = (int32_t)i;
+    for (int64_t q = tid; q < s; q += blockDim.x) out[q] = (int32_t)(sa.shard_begin + q);
+  } else if (s_draw >= I && !compact) {
+    for (int64_t i = tid; i < I; i += blockDim.x) out[i] = (int32_t)i;
   } else {
-    for (int64_t i = threadIdx.x; i < I; i += blockDim.x) {
-      uint32_t c[4] = {(uint32_t)i, (uint32_t)m, (uint32_t)k, t};
-      philox10(c, (uint32_t)(seed & 0xffffffffu), (uint32_t)(seed >> 32));
-      keys[i] = ((unsigned long long)c[0] << 32) | c[1];
-    }
-    __syncthreads();
-    // rank of each i; selected if rank < s
-    unsigned char* sel = reinterpret_cast<unsigned char*>(keys + I);
-    for (int64_t i = threadIdx.x; i < I; i += blockDim.x) {
-      const unsigned long long ki = keys[i];
-      int64_t rank = 0;
-      for (int64_t j = 0; j < I; ++j) {
-        const unsigned long long kj = keys[j];
-        rank += (kj < ki) || (kj == ki && j < i);
+    // radix select of the key of rank s_draw - 1
+    unsigned long long prefix = 0ull, pmask = 0ull;
+    if (tid == 0) rank_s = (long long)s_draw - 1;
+    for (int pass = 0; pass < 8; ++pass) {
+      const int shift = 56 - 8 * pass;
+      for (int b = tid; b < 256; b += blockDim.x) hist[b] = 0u;
+      __syncthreads();
+      for (int64_t i = tid; i < I; i += blockDim.x) {
+        const unsigned long long key = sample_key(seed, i, m, k, t);
+        if ((key & pmask) == prefix) atomicAdd(&hist[(key >> shift) & 255u], 1u);
       }
-      // the draw selects s_draw of I; a compacted shard-mode list keeps this rank's ones
-      sel[i] = rank < s_draw && (!compact || (i >= sa.shard_begin && i < sa.shard_end));
+      __syncthreads();
+      if (tid == 0) {
+        long long cum = 0, r = rank_s;
+        int b = 0;
+        for (; b < 255; ++b) {
+          if (cum + (long long)hist[b] > r) break;
+          cum += hist[b];
+        }
+        sel_bin = b;
+        rank_s = r - cum;
+      }
+      __syncthreads();
+      prefix |= (unsigned long long)sel_bin << shift;
+      pmask |= 0xFFull << shift;
     }
+    // keys equal to kappa_K: keep the first rank_s + 1 of them in ascending i
+    const long long take_eq = rank_s + 1;
+    long long eq_seen = 0, n_out = 0;      // running totals over the previous chunks
     __syncthreads();
-    for (int64_t i = threadIdx.x; i < I; i += blockDim.x) {
-      if (!sel[i]) continue;
-      int64_t pos = 0;
-      for (int64_t j = 0; j < i; ++j) pos += sel[j];
-      out[pos] = (int32_t)i;
+    for (int64_t c0 = 0; c0 < I; c0 += blockDim.x) {
+      const int64_t i = c0 + tid;
+      unsigned long long key = ~0ull;
+      if (i < I) key = sample_key(seed, i, m, k, t);
+      const bool eq = i < I && key == prefix;
+      long long eq_ex, eq_tot;
+      Scan(scan_tmp).ExclusiveSum(eq ? 1ll : 0ll, eq_ex, eq_tot);
+      __syncthreads();
+      const bool sel = i < I && (key < prefix || (eq && eq_seen + eq_ex < take_eq));
+      const bool put = sel && (!compact || (i >= sa.shard_begin && i < sa.shard_end));
+      long long pos, put_tot;
+      Scan(scan_tmp).ExclusiveSum(put ? 1ll : 0ll, pos, put_tot);
+      __syncthreads();
+      if (put) out[n_out + pos] = (int32_t)i;
+      eq_seen += eq_tot;
+      n_out += put_tot;
     }
-    if (compact && threadIdx.x == 0) {
-      int64_t nl = 0;
-      for (int64_t j = 0; j < I; ++j) nl += sel[j];
-      n_local = nl;
-    }
-    __syncthreads();
-    for (int64_t q = n_local + threadIdx.x; q < s; q += blockDim.x) out[q] = (int32_t)sa.shard_begin;   // padding
+    n_local = compact ? n_out : s;
+    for (int64_t q = n_local + tid; q < s; q += blockDim.x) out[q] = (int32_t)sa.shard_begin;   // padding
   }
   __syncthreads();
   const int64_t cnt = s >= I ? I : s;
-  for (int64_t q = threadIdx.x; q < cnt; q += blockDim.x) {
+  for (int64_t q = tid; q < cnt; q += blockDim.x) {
     int64_t g = out[q];
     int64_t loc = g;
     if (m == sa.shard_mode) loc = (g >= sa.shard_begin && g < sa.shard_end) ? g - sa.shard_begin : -1;
@@ -206,7 +238,9 @@ __device__ __forceinline__ void right_digits(const PlanArgs& a, int64_t col, int
 }
 
 __global__ void offsets_kernel(PlanArgs a, const int64_t* __restrict__ doff,
-                               int64_t* __restrict__ row_off, int64_t* __restrict__ col_off) {
+                               int64_t* __restrict__ row_off, int64_t* __restrict__ col_off,
+                               DevScalars* __restrict__ sc) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) { sc->amax_a = 0u; sc->amax_b = 0u; }   // (operand scaling)
   const int64_t tot = a.nrows + a.ncols;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tot;
        t += (int64_t)gridDim.x * blockDim.x) {
@@ -283,8 +317,22 @@ __global__ void mid_kernel(PlanArgs a, const int32_t* __restrict__ idx, const fl
 // Rgt(j_R) = Z_{k+p+1}(.) .. Z_{k-1}(.)  (r_s x r_k); stored RgtT[(a + r_k c) * ncols + col]
 // = Rgt[c][a].  One thread per (col, c); the r_s threads of a column are adjacent so that
 // their slice reads coincide (columns of explicit draws hit unrelated slices)
+__device__ __forceinline__ void block_amax(float v, unsigned int* dst) {
+  // max |v| over the CTA -> atomicMax on the fp32 bit pattern (v >= 0)
+  __shared__ float red[32];
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float m = 0.f;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) m = fmaxf(m, red[w]);
+    if (m > 0.f) atomicMax(dst, __float_as_uint(m));
+  }
+}
+
 __global__ void rgt_kernel(PlanArgs a, const int32_t* __restrict__ idx, const float* __restrict__ Z,
-                           float* __restrict__ rgtT) {
+                           float* __restrict__ rgtT, DevScalars* __restrict__ sc) {
+  float amax = 0.f;
   const int64_t tot = a.ncols * a.rs;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tot;
        t += (int64_t)gridDim.x * blockDim.x) {
@@ -303,8 +351,12 @@ __global__ void rgt_kernel(PlanArgs a, const int32_t* __restrict__ idx, const fl
       vecmat(v, Z + a.zoff[m] + i * (int64_t)a.rank_of[m] * rout, rin, rout);
       rin = rout;
     }
-    for (int aa = 0; aa < a.rk; ++aa) rgtT[(int64_t)(aa + a.rk * cc) * a.ncols + col] = v[aa];
+    for (int aa = 0; aa < a.rk; ++aa) {
+      rgtT[(int64_t)(aa + a.rk * cc) * a.ncols + col] = v[aa];
+      amax = fmaxf(amax, fabsf(v[aa]));
+    }
   }
+  block_amax(amax, &sc->amax_b);     // (B operand scaling of the tensor-core passes)
 }
 
 // Lft(row)[a + r_k c] = (X_k(i_k) Mid(j_L))[a][c] where X_k is the core slice (pass 1) or
@@ -363,7 +415,9 @@ struct PassArgs {
   double* dpart;      // [ik][cta][R2]
   double* spart;      // [ik][cta][3]
   double* denpart;    // [ik][cta]
-  double* hist;       // TRD_SIGMA_MAD: |e| histogram (pass 1), else nullptr
+  uint32_t* eabs;     // TRD_SIGMA_MAD: |e| bit patterns of pass 1 (R21), else nullptr
+  unsigned long long* efill;   // its fill counter (warp-aggregated atomics)
+  unsigned long long ecap;
 };
 
 __device__ __forceinline__ float warp_sum_f(float v) {
@@ -399,12 +453,7 @@ pass_kernel(PassArgs a) {
   __shared__ float lfhS[kPassWarps][PASS2 ? KT : 1];
   __shared__ float dS[kPassWarps][KT];
   __shared__ double redS[kPassWarps][kMaxR2 + 3];
-  __shared__ uint32_t histS[PASS2 ? 1 : kHistBins];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (!PASS2 && a.hist) {
-    for (int b = threadIdx.x; b < kHistBins; b += blockDim.x) histS[b] = 0u;
-    __syncthreads();
-  }
   const int64_t ik = blockIdx.y;
   const int64_t jl0 = (int64_t)blockIdx.x * a.jl_per_cta;
   const int jlc = (int)min((int64_t)a.jl_per_cta, a.nL - jl0);
@@ -458,6 +507,14 @@ pass_kernel(PassArgs a) {
       }
       const float e = x - recon;
       const float w = a.sigma_inf ? 1.f : expf(-e * e * inv2s2);
+      if (!PASS2 && a.eabs) {                // R21: |e| of the observed entries, any order
+        const unsigned bal = __ballot_sync(0xffffffffu, obs);
+        unsigned long long base = 0ull;
+        if (lane == 0) base = atomicAdd(a.efill, (unsigned long long)__popc(bal));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        const unsigned long long q = base + __popc(bal & ((1u << lane) - 1u));
+        if (obs && q < a.ecap) a.eabs[q] = __float_as_uint(fabsf(e));
+      }
       if (PASS2) {
         if (obs) st_den += (double)w * (double)tdir * (double)tdir;
       } else {
@@ -465,7 +522,6 @@ pass_kernel(PassArgs a) {
           st_e2 += (double)e * (double)e;
           st_n += 1.0;
           st_w += s2 * (1.0 - (double)w);
-          if (a.hist) atomicAdd(&histS[mad_bin(fabsf(e))], 1u);
         }
         if (!STATS_ONLY) {
           const float cv = obs ? w * e : 0.f;
@@ -520,11 +576,6 @@ pass_kernel(PassArgs a) {
     }
     return;
   }
-  if (a.hist) {                              // (PASS2 returned above)
-    __syncthreads();
-    for (int b = threadIdx.x; b < kHistBins; b += blockDim.x)
-      if (histS[b]) atomicAdd(&a.hist[b], (double)histS[b]);   // integer counts: exact in any order
-  }
   {
     double v0 = warp_sum_d(st_e2), v1 = warp_sum_d(st_w), v2 = warp_sum_d(st_n);
     if (lane == 0) { redS[warp][kMaxR2] = v0; redS[warp][kMaxR2 + 1] = v1; redS[warp][kMaxR2 + 2] = v2; }
@@ -564,7 +615,9 @@ static PassArgs make_pass_args(const Context& c, const BlockPlan& bp) {
   a.values = c.values; a.mask = c.mask; a.rank_prefix = c.rank_prefix;
   a.sc = c.sc;
   a.dpart = c.dpart; a.spart = c.spart; a.denpart = c.denpart;
-  a.hist = c.cfg.sigma_mode == TRD_SIGMA_MAD ? c.hist : nullptr;
+  a.eabs = c.cfg.sigma_mode == TRD_SIGMA_MAD ? c.eabs : nullptr;
+  a.efill = &c.sc->eabs_fill;
+  a.ecap = (unsigned long long)c.eabs_cap;
   return a;
 }
 
@@ -760,7 +813,7 @@ solve_kernel(const double* __restrict__ G, int n, double lambda_rel, double* __r
     }
     __syncthreads();
     if (!fail_s || attempt >= 3) break;
-    lam *= 10.0;
+    lam = lam > 0.0 ? 10.0 * lam : ldexp(tr_s / n, -40);   // R23 retry rule
     __syncthreads();
   }
   if (fail_s) {
@@ -850,7 +903,7 @@ __global__ void __launch_bounds__(1024) gj_solve_kernel(const double* __restrict
     }
     __syncthreads();
     if (!fail_s || attempt >= 3) break;
-    lam *= 10.0;
+    lam = lam > 0.0 ? 10.0 * lam : ldexp(tr_s / n, -40);   // R23 retry rule
     __syncthreads();
   }
   if (fail_s) {
@@ -989,6 +1042,7 @@ __global__ void sweep_begin_kernel(DevScalars* sc, DevStats* stats, int slot) {
   for (int k = 0; k < kMaxN; ++k) { st.eta[k] = 0.0; st.num[k] = 0.0; st.den[k] = 0.0; st.nnz[k] = 0; }
   st.skipped = 0; st.nonfinite = 0;
   sc->acc_e2 = 0.0; sc->acc_n = 0.0;
+  sc->eabs_fill = 0ull;
 }
 
 // ----------------------------------------------------------------------------------------
@@ -1023,28 +1077,91 @@ __global__ void dt_D_kernel(const float* __restrict__ Zn, int64_t In, int rk, in
   }
 }
 
-// R21: 1.4826 x the histogram median of |e| (bin reaching n/2, linear inside it)
-__device__ double hist_median_sigma(const double* __restrict__ hist, double theta, double sigma_min) {
-  double n = 0.0;
-  for (int b = 0; b < kHistBins; ++b) n += hist[b];
-  const double target = 0.5 * n;
-  double cum = 0.0, med = 0.0;
-  for (int b = 0; b < kHistBins; ++b) {
-    const double c = hist[b];
-    if (c > 0.0 && cum + c >= target) {
-      const int E = kHistE0 + b / 16, m = b % 16;
-      const double lo = (1.0 + m / 16.0) * ldexp(1.0, E);
-      med = lo + (target - cum) / c * ldexp(1.0, E) / 16.0;
-      break;
+// ----------------------------------------------------------------------------------------
+// R21: exact median of the |e| bit patterns eabs[0, eabs_fill) by radix select.  Level 0 counts
+// bits 31..21, level 1 bits 20..10 of the values under each target's level-0 prefix, level 2
+// bits 9..0; the two targets are the order statistics floor((n-1)/2) and floor(n/2).  Counts
+// are integers (atomics in any order give the same histogram); scans run in one thread.
+// ----------------------------------------------------------------------------------------
+template <int LEVEL>
+__global__ void __launch_bounds__(512) mad_hist_kernel(const uint32_t* __restrict__ eabs,
+                                                       const DevScalars* __restrict__ sc, double* __restrict__ mh) {
+  constexpr int NB = LEVEL == 2 ? kMadBins2 : kMadBins0;
+  constexpr int NT = LEVEL == 0 ? 1 : 2;
+  __shared__ unsigned int h[NT * NB];
+  for (int i = threadIdx.x; i < NT * NB; i += blockDim.x) h[i] = 0u;
+  __syncthreads();
+  const unsigned long long n = sc->eabs_fill;
+  const uint32_t p0 = sc->mad_pre[0], p1 = sc->mad_pre[1];
+  for (unsigned long long q = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; q < n;
+       q += (unsigned long long)gridDim.x * blockDim.x) {
+    const uint32_t b = __ldg(eabs + q);
+    if (b >= 0x80000000u) continue;                      // padding slot (kEabsPad)
+    if (LEVEL == 0) {
+      atomicAdd(&h[b >> 21], 1u);
+    } else if (LEVEL == 1) {
+      const uint32_t pf = b >> 21, bin = (b >> 10) & 2047u;
+      if (pf == p0) atomicAdd(&h[bin], 1u);
+      if (pf == p1) atomicAdd(&h[NB + bin], 1u);
+    } else {
+      const uint32_t pf = b >> 10, bin = b & 1023u;
+      if (pf == p0) atomicAdd(&h[bin], 1u);
+      if (pf == p1) atomicAdd(&h[NB + bin], 1u);
     }
-    cum += c;
   }
-  return fmax(sigma_min, theta * 1.4826 * med);
+  __syncthreads();
+  double* dst = mh + (LEVEL == 0 ? 0 : LEVEL == 1 ? kMadBins0 : kMadBins0 + 2 * kMadBins1);
+  for (int i = threadIdx.x; i < NT * NB; i += blockDim.x)
+    if (h[i]) atomicAdd(dst + i, (double)h[i]);
+}
+
+template <int LEVEL>
+__global__ void mad_scan_kernel(const double* __restrict__ mh, DevScalars* sc) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  if (LEVEL == 0) {
+    double n = 0.0;
+    for (int b = 0; b < kMadBins0; ++b) n += mh[b];
+    sc->mad_n = n;
+    const long long ni = (long long)n;
+    const long long r[2] = {ni > 0 ? (ni - 1) / 2 : 0, ni / 2};
+    for (int t = 0; t < 2; ++t) {
+      long long cum = 0;
+      int b = 0;
+      for (; b < kMadBins0 - 1; ++b) {
+        if (cum + (long long)mh[b] > r[t]) break;
+        cum += (long long)mh[b];
+      }
+      sc->mad_pre[t] = (uint32_t)b;
+      sc->mad_rank[t] = r[t] - cum;
+    }
+    return;
+  }
+  const int NB = LEVEL == 1 ? kMadBins1 : kMadBins2;
+  const double* h0 = mh + (LEVEL == 1 ? kMadBins0 : kMadBins0 + 2 * kMadBins1);
+  float v[2];
+  for (int t = 0; t < 2; ++t) {
+    const double* h = h0 + t * NB;
+    long long cum = 0;
+    int b = 0;
+    for (; b < NB - 1; ++b) {
+      if (cum + (long long)h[b] > sc->mad_rank[t]) break;
+      cum += (long long)h[b];
+    }
+    sc->mad_rank[t] -= cum;
+    if (LEVEL == 1) sc->mad_pre[t] = (sc->mad_pre[t] << 11) | (uint32_t)b;
+    else v[t] = __uint_as_float((sc->mad_pre[t] << 10) | (uint32_t)b);
+  }
+  if (LEVEL == 2) sc->mad_med = sc->mad_n > 0.0 ? 0.5 * ((double)v[0] + (double)v[1]) : 0.0;
+}
+
+// pass 1 of a staged block wrote its tile slots (padding included) at eabs_fill + [0, total)
+__global__ void eabs_advance_kernel(DevScalars* sc, const uint64_t* __restrict__ tbase_end) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) sc->eabs_fill += *tbase_end;
 }
 
 __global__ void sweep_end_kernel(double* __restrict__ D, double* __restrict__ Dprev, int64_t n2,
                                  DevScalars* sc, DevStats* stats, int slot, int sigma_mode,
-                                 double theta, double sigma_min, const double* __restrict__ hist) {
+                                 double theta, double sigma_min) {
   __shared__ double a1[1024], a2[1024];
   double s1 = 0.0, s2 = 0.0;
   for (int64_t t = threadIdx.x; t < n2; t += blockDim.x) {
@@ -1063,7 +1180,7 @@ __global__ void sweep_end_kernel(double* __restrict__ D, double* __restrict__ Dp
     stats[slot].stop_e = e;
     if (sigma_mode == TRD_SIGMA_RMS && sc->acc_n > 0.0)
       sc->sigma = fmax(sigma_min, theta * sqrt(sc->acc_e2 / sc->acc_n));
-    if (sigma_mode == TRD_SIGMA_MAD && sc->acc_n > 0.0) sc->sigma = hist_median_sigma(hist, theta, sigma_min);
+    if (sigma_mode == TRD_SIGMA_MAD && sc->acc_n > 0.0) sc->sigma = fmax(sigma_min, theta * 1.4826 * sc->mad_med);
     sc->have_prev_D = 1;
     sc->sweep += 1;
   }
@@ -1071,12 +1188,13 @@ __global__ void sweep_end_kernel(double* __restrict__ D, double* __restrict__ Dp
   for (int64_t t = threadIdx.x; t < n2; t += blockDim.x) Dprev[t] = D[t];
 }
 
-// sigma_0 = max(sigma_min, theta * RMS) from [sum_e2, welsch, n] (after allreduce)
+// sigma_0 = max(sigma_min, theta * RMS) from [sum_e2, welsch, n] (after allreduce), or the
+// MAD rule's median (R21)
 __global__ void sigma0_kernel(const double* __restrict__ s3, DevScalars* sc, double theta,
-                              double sigma_min, const double* __restrict__ hist) {
+                              double sigma_min, int mad) {
   if (threadIdx.x == 0 && blockIdx.x == 0)
-    sc->sigma = hist ? hist_median_sigma(hist, theta, sigma_min)
-                     : fmax(sigma_min, theta * sqrt(s3[0] / fmax(s3[2], 1.0)));
+    sc->sigma = mad ? fmax(sigma_min, theta * 1.4826 * sc->mad_med)
+                    : fmax(sigma_min, theta * sqrt(s3[0] / fmax(s3[2], 1.0)));
 }
 
 // ----------------------------------------------------------------------------------------
@@ -1211,39 +1329,33 @@ void launch_sampler(Context& c, const BlockPlan& bp, cudaStream_t s) {
   sa.shard_begin = c.shard_begin; sa.shard_end = c.shard_end;
   sa.shard_local = bp.shard_local;
   sa.shard_sampled = bp.shard_sampled;
-  int64_t maxI = 0;
   for (int m = 0; m < c.N; ++m) {
     sa.dims[m] = c.dims[m];
     sa.s[m] = bp.s[m];
     sa.s_samp[m] = bp.s_samp[m];
     sa.idx_off[m] = c.idx_off[m];
     sa.lstride[m] = c.lstride[m];
-    if (bp.s[m] < c.dims[m] && c.dims[m] > maxI) maxI = c.dims[m];
   }
   sa.idx_off[c.N] = c.idx_off[c.N];
-  static uint64_t attr_set = 0;
-  if (first_on_device(attr_set))
-    cudaFuncSetAttribute(sampler_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
   if (bp.explicit_cols) {
     const int64_t J = bp.ncols;
     row_sampler_kernel<<<grid_for(J + c.dims[bp.k]), 256, 0, s>>>(sa, J, c.sc, c.idx, c.doff);
     c.launches++;
     return;
   }
-  size_t smem = (size_t)maxI * 9 + 16;
-  sampler_kernel<<<c.N, 256, smem, s>>>(sa, c.sc, c.idx, c.doff);
+  sampler_kernel<<<c.N, kSamplerThreads, 0, s>>>(sa, c.sc, c.idx, c.doff);
   c.launches++;
 }
 
 void launch_plan(Context& c, const BlockPlan& bp, cudaStream_t s) {
   PlanArgs a = make_plan_args(c, bp);
-  offsets_kernel<<<grid_for(bp.nrows + bp.ncols), 256, 0, s>>>(a, c.doff, c.row_off, c.col_off);
+  offsets_kernel<<<grid_for(bp.nrows + bp.ncols), 256, 0, s>>>(a, c.doff, c.row_off, c.col_off, c.sc);
   c.launches++;
   if (bp.p > 0) {
     mid_kernel<<<grid_for(bp.nL * bp.rk1), 256, 0, s>>>(a, c.idx, c.Z, c.mid);
     c.launches++;
   }
-  rgt_kernel<<<grid_for(bp.ncols * bp.rs), 256, 0, s>>>(a, c.idx, c.Z, c.rgtT);
+  rgt_kernel<<<grid_for(bp.ncols * bp.rs), 256, 0, s>>>(a, c.idx, c.Z, c.rgtT, c.sc);
   c.launches++;
 }
 
@@ -1413,15 +1525,40 @@ void launch_sweep_end(Context& c, int slot, cudaStream_t s) {
   dt_T_kernel<<<(unsigned)In, 128, 0, s>>>(c.Z + c.zoff[n], In, rk, rk1, c.G_last, T);
   dt_D_kernel<<<grid_for(In * In), 256, 0, s>>>(c.Z + c.zoff[n], In, rk, rk1, T, c.Dcur);
   sweep_end_kernel<<<1, 1024, 0, s>>>(c.Dcur, c.Dprev, In * In, c.sc, c.stats, slot,
-                                      c.cfg.sigma_mode, c.cfg.sigma_theta, c.cfg.sigma_min, c.hist);
+                                      c.cfg.sigma_mode, c.cfg.sigma_theta, c.cfg.sigma_min);
   c.launches += 3;
 }
 
 void launch_sigma0(Context& c, cudaStream_t s) {
   // dvec[Ik*R2 .. +3] of the stats-only full pass hold [sum_e2, welsch, n]; the caller
-  // reduced them into red_ws[0..2]
+  // reduced them into red_ws[0..2] (and ran the R21 select in MAD mode)
   sigma0_kernel<<<1, 32, 0, s>>>(c.red_ws, c.sc, c.cfg.sigma_theta, c.cfg.sigma_min,
-                                 c.cfg.sigma_mode == TRD_SIGMA_MAD ? c.hist : nullptr);
+                                 c.cfg.sigma_mode == TRD_SIGMA_MAD ? 1 : 0);
+  c.launches++;
+}
+
+void launch_eabs_advance(Context& c, const TcStage& st, cudaStream_t s) {
+  eabs_advance_kernel<<<1, 32, 0, s>>>(c.sc, st.tbase + st.n_tiles);
+  c.launches++;
+}
+
+void launch_mad_hist(Context& c, int level, cudaStream_t s) {
+  const int grid = c.num_sm * 4;
+  if (level == 0) {
+    cudaMemsetAsync(c.mhist, 0, kMadHist * sizeof(double), s);
+    mad_hist_kernel<0><<<grid, 512, 0, s>>>(c.eabs, c.sc, c.mhist);
+  } else if (level == 1) {
+    mad_hist_kernel<1><<<grid, 512, 0, s>>>(c.eabs, c.sc, c.mhist);
+  } else {
+    mad_hist_kernel<2><<<grid, 512, 0, s>>>(c.eabs, c.sc, c.mhist);
+  }
+  c.launches++;
+}
+
+void launch_mad_scan(Context& c, int level, cudaStream_t s) {
+  if (level == 0) mad_scan_kernel<0><<<1, 32, 0, s>>>(c.mhist, c.sc);
+  else if (level == 1) mad_scan_kernel<1><<<1, 32, 0, s>>>(c.mhist, c.sc);
+  else mad_scan_kernel<2><<<1, 32, 0, s>>>(c.mhist, c.sc);
   c.launches++;
 }
 
@@ -1442,6 +1579,44 @@ void launch_error(Context& c, const float* ref, const uint32_t* eval_bits, doubl
   error_kernel<<<nb, 256, 0, s>>>(a, ref, eval_bits, c.dpart);
   error_reduce_kernel<<<1, 32, 0, s>>>(c.dpart, nb, out6);
   c.launches += 2;
+}
+
+__global__ void count_bits_kernel(const uint32_t* __restrict__ mask, int64_t nw, int64_t nbits,
+                                  unsigned long long* __restrict__ out) {
+  unsigned long long cnt = 0;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < nw; t += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t w = mask[t];
+    const int64_t tail = nbits - t * 32;
+    if (tail < 32) w &= (1u << tail) - 1u;
+    cnt += __popc(w);
+  }
+  for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+  if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(out, cnt);
+}
+
+void launch_count_bits(Context& c, unsigned long long* out, cudaStream_t s) {
+  cudaMemsetAsync(out, 0, sizeof(unsigned long long), s);
+  count_bits_kernel<<<grid_for(c.n_words), 256, 0, s>>>(c.mask, c.n_words, c.n_local, out);
+  c.launches++;
+}
+
+// max |x| over the observed values (P-operand bound of the tensor-core passes)
+__global__ void amax_obs_kernel(const float* __restrict__ values, const uint32_t* __restrict__ mask, int64_t n,
+                                int packed, DevScalars* __restrict__ sc) {
+  float amax = 0.f;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
+    if (!packed && !((mask[t >> 5] >> (t & 31)) & 1u)) continue;
+    const float v = fabsf(values[t]);
+    if (v == v) amax = fmaxf(amax, v);
+  }
+  block_amax(amax, &sc->amax_x);
+}
+
+void launch_amax_obs(Context& c, cudaStream_t s) {
+  cudaMemsetAsync(&c.sc->amax_x, 0, sizeof(unsigned int), s);
+  const int64_t n = c.packed ? c.n_values : c.n_local;
+  amax_obs_kernel<<<grid_for(n), 256, 0, s>>>(c.values, c.mask, n, c.packed, c.sc);
+  c.launches++;
 }
 
 void launch_rank_prefix(Context& c, cudaStream_t s) {

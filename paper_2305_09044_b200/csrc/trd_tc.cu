@@ -202,6 +202,8 @@ struct LftArgs {
   const float* zk;       // Z_k[i][a][b]
   const double* hk;      // h[i][a + r_k b]
   const float* mid;      // Mid[jl][b][c]
+  float* lscl;           // [row] 2^-E of the row's power-of-two scaling (tc_scale_exp)
+  unsigned int* amax;    // pass 1: max |Lft| over all rows (P-operand bound), else nullptr
 };
 // CTA = one 128-row tile: the rows' X(i_k) and Mid(j_L) are staged in shared memory (row
 // stride padded to an odd word count: conflict-free across rows), then thread (row, half)
@@ -248,20 +250,30 @@ __global__ void __launch_bounds__(256) tc_lft_pack_kernel(LftArgs a, int pass2, 
       const float* X = Xs + r * XP;
       const float* M = Ms + r * MP;
       const int kh = a.KP / 2;
+      auto lft_val = [&](int kap) -> float {
+        float v = 0.f;
+        if (row < a.nrows && kap < a.K) {
+          const int aa = kap % a.rk, c = kap / a.rk;
+          if (a.p == 0) {
+            v = X[aa * a.rk1 + c];
+          } else {
+            for (int b = 0; b < a.rk1; ++b) v = fmaf(X[aa * a.rk1 + b], M[b * a.rs + c], v);
+          }
+        }
+        return v;
+      };
+      // the row's max |Lft| (both halves: partner lane tid ^ 1) -> power-of-two scale
+      float amax = 0.f;
+      for (int kap = hf * kh; kap < (hf + 1) * kh; ++kap) amax = fmaxf(amax, fabsf(lft_val(kap)));
+      amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, 1));
+      const int E = tc_scale_exp(amax);
+      if (hf == 0 && row < nrows_pad) a.lscl[row] = ldexpf(1.f, -E);
+      if (a.amax && amax > 0.f) atomicMax(a.amax, __float_as_uint(amax));
       for (int k0 = hf * kh; k0 < (hf + 1) * kh; k0 += 8) {
         __half hh[8], ll[8];
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
-          const int kap = k0 + e;
-          float v = 0.f;
-          if (row < a.nrows && kap < a.K) {
-            const int aa = kap % a.rk, c = kap / a.rk;
-            if (a.p == 0) {
-              v = X[aa * a.rk1 + c];
-            } else {
-              for (int b = 0; b < a.rk1; ++b) v = fmaf(X[aa * a.rk1 + b], M[b * a.rs + c], v);
-            }
-          }
+          const float v = ldexpf(lft_val(k0 + e), E);
           hh[e] = __float2half_rn(v);
           ll[e] = __float2half_rn(v - __half2float(hh[e]));
         }
@@ -332,13 +344,26 @@ __global__ void __launch_bounds__(128, 4) tc_lft_pack_rb_kernel(LftArgs a, int p
           out[aa + RK * c] = v;
         }
     }
+    // the row's power-of-two scale (tc_scale_exp): exact, keeps the fp16 split in range
+    float amax = 0.f;
+#pragma unroll
+    for (int q = 0; q < KP; ++q) amax = fmaxf(amax, fabsf(out[q]));
+    const int E = tc_scale_exp(amax);
+    const float sc2 = ldexpf(1.f, E);
+    if (row < nrows_pad) a.lscl[row] = ldexpf(1.f, -E);
+    if (a.amax) {
+      float m = amax;
+      for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+      if ((threadIdx.x & 31) == 0 && m > 0.f) atomicMax(a.amax, __float_as_uint(m));
+    }
 #pragma unroll
     for (int k0 = 0; k0 < KP; k0 += 8) {
       __half hh[8], ll[8];
 #pragma unroll
       for (int e = 0; e < 8; ++e) {
-        hh[e] = __float2half_rn(out[k0 + e]);
-        ll[e] = __float2half_rn(out[k0 + e] - __half2float(hh[e]));
+        const float v = out[k0 + e] * sc2;
+        hh[e] = __float2half_rn(v);
+        ll[e] = __float2half_rn(v - __half2float(hh[e]));
       }
       uint4 hv, lv;
       hv.x = pack_half2(hh[0], hh[1]); hv.y = pack_half2(hh[2], hh[3]);
@@ -369,14 +394,16 @@ __device__ __forceinline__ int64_t cm_offset(int r, int kap, int HK) {
 
 // B (Rgt) core-matrix tiles: [col tile][hi | lo][64 x KP]
 __global__ void tc_pack_cols_kernel(const float* __restrict__ rgtT, int64_t ncols, int K, int KP,
-                                    int64_t ntiles, __half* __restrict__ dst, __half* __restrict__ dst2) {
+                                    int64_t ntiles, __half* __restrict__ dst, __half* __restrict__ dst2,
+                                    const DevScalars* __restrict__ sc) {
   const int HK = KP / 8;
+  const float sc2 = ldexpf(1.f, tc_scale_exp(__uint_as_float(sc->amax_b)));   // B scaling
   const int64_t tot = ntiles * TC_NT * KP;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tot;
        t += (int64_t)gridDim.x * blockDim.x) {
     const int64_t col = t % (ntiles * TC_NT);
     const int kap = (int)(t / (ntiles * TC_NT));
-    const float v = (col < ncols && kap < K) ? rgtT[(int64_t)kap * ncols + col] : 0.f;
+    const float v = (col < ncols && kap < K) ? rgtT[(int64_t)kap * ncols + col] * sc2 : 0.f;
     const __half hi = __float2half_rn(v);
     const __half lo = __float2half_rn(v - __half2float(hi));
     const int64_t tile = col / TC_NT;
@@ -709,7 +736,9 @@ struct TcArgs {
   const float* tvals;
   const uint16_t* tidx;    // staged entry lists
   float* tw;               // staged weights (pass 1 writes, pass 2 reads)
-  double* hist;            // TRD_SIGMA_MAD: |e| histogram (pass 1), else nullptr
+  const float* lscl;       // [row] 2^-E of the A rows' scaling (Lft in pass 1, Lft_h in pass 2)
+  uint32_t* eabs;          // TRD_SIGMA_MAD: |e| bit patterns (pass 1, R21), else nullptr
+  unsigned long long ecap;
   const DevScalars* sc;
   float* contrib;          // [split][nrows_pad][KP]  D rows of pass 1
   double* spart;           // [cta][3]
@@ -957,6 +986,8 @@ void launch_tc_lft(Context& c, const BlockPlan& bp, bool pass2, cudaStream_t s) 
   a.zk = c.Z + c.zoff[bp.k];
   a.hk = c.h;
   a.mid = c.mid;
+  a.lscl = pass2 ? c.lsclh : c.lscl;
+  a.amax = pass2 ? nullptr : &c.sc->amax_a;
   const int64_t pad = bp.n_row_tiles * TC_M;
   if (bp.p > 0 && bp.rk == 8 && bp.rk1 == 8 && bp.rs == 8) {
     const int grid = (int)std::min<int64_t>((pad + 127) / 128, (int64_t)c.num_sm * 16);
@@ -973,7 +1004,7 @@ void launch_tc_lft(Context& c, const BlockPlan& bp, bool pass2, cudaStream_t s) 
 
 void launch_tc_pack_cols(Context& c, const BlockPlan& bp, cudaStream_t s) {
   tc_pack_cols_kernel<<<tc_grid(bp.n_col_tiles * TC_NT * bp.KP), 256, 0, s>>>(c.rgtT, bp.ncols, bp.K, bp.KP,
-                                                                                bp.n_col_tiles, c.rgtHL, c.rgtHL2);
+                                                                                bp.n_col_tiles, c.rgtHL, c.rgtHL2, c.sc);
   c.launches++;
 }
 
@@ -1017,12 +1048,14 @@ static TcArgs make_tc_args(const Context& c, const BlockPlan& bp, const TcStage&
   a.mid = c.mid;
   const char* ex = getenv("TRD_TC_EXP");
   a.exp = ex ? atoi(ex) : 0;
-  a.rgtHL = ((!pass2 && !TRD_P1_MERGE) || (pass2 && (a.exp & 32))) ? c.rgtHL : c.rgtHL2;
+  a.rgtHL = ((!pass2 && !TRD_P1_MERGE) || (pass2 && TRD_EXPERIMENTS && (a.exp & 32))) ? c.rgtHL : c.rgtHL2;
   a.tbits = st.tbits; a.troff = st.troff; a.tbase = st.tbase; a.tvals = st.tvals; a.tidx = st.tidx;
   a.tw = c.tw;
+  a.lscl = pass2 ? c.lsclh : c.lscl;
   a.sc = c.sc;
   a.contrib = c.contrib; a.spart = c.spart; a.denpart = c.denpart;
-  a.hist = (!pass2 && c.cfg.sigma_mode == TRD_SIGMA_MAD) ? c.hist : nullptr;
+  a.eabs = (!pass2 && c.cfg.sigma_mode == TRD_SIGMA_MAD) ? c.eabs : nullptr;
+  a.ecap = (unsigned long long)c.eabs_cap;
   return a;
 }
 

@@ -108,7 +108,7 @@ def load_library(path: str = LIB_PATH):
         "trd_sketch": (i32, [P, i32, i32, P, P]),
         "trd_sweep": (i32, [P, i32, P]),
         "trd_reconstruct": (i32, [P, P, i64, P]),
-        "trd_error": (i32, [P, P, P, ctypes.POINTER(trd_error_stats)]),
+        "trd_error": (i32, [P, P, P, d, ctypes.POINTER(trd_error_stats)]),
         "trd_get_cores": (i32, [P, P]),
         "trd_set_cores": (i32, [P, P]),
         "trd_block_probe": (i32, [P, i32, i32, P, P, P, P]),
@@ -263,10 +263,10 @@ class TRD:
                     "trd_reconstruct")
         return out
 
-    def error(self, ref, eval_bits=None):
+    def error(self, ref, eval_bits=None, peak=1.0):
         es = trd_error_stats()
         self._check(self.lib.trd_error(self.ctx, ctypes.c_void_p(_ptr(ref)),
-                                       ctypes.c_void_p(_ptr(eval_bits)), ctypes.byref(es)),
+                                       ctypes.c_void_p(_ptr(eval_bits)), float(peak), ctypes.byref(es)),
                     "trd_error")
         return dict(rel_err_all=es.rel_err_all, rel_err_observed=es.rel_err_observed,
                     psnr=es.psnr, n_eval=es.n_eval)

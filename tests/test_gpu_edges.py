@@ -1,0 +1,255 @@
+"""GPU parity of the method's edge cases and the operand scaling (-m gpu), through the C ABI.
+
+Skipped / degenerate blocks (R14), the lambda retry and NOT_SPD (R23), a rank slice without
+sampled indices, the Welsch monitor (R3), data far from unit scale (the fp16 hi / lo
+tensor-core operands are power-of-two scaled), row-wise d, PSNR and the
+relative errors of trd_error.  Citations are PAPER.md lines (P:L)."""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import trd_oracle as O
+from oracle.philox import sample_indices
+from synth.generate import make_problem, pack_bits
+from tests.helpers import cores_rel_err, gpu_context, oracle_config, oracle_source, rel_fro, small_spec
+
+pytestmark = pytest.mark.gpu
+
+
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+def _rowwise(dg, do):
+    """max over rows i_k of ||d_gpu(i_k) - d_oracle(i_k)|| / ||d_oracle(i_k)|| (rows with a
+    norm below 1e-6 of the largest are compared against that floor)."""
+    n = np.linalg.norm(do, axis=1)
+    floor = 1e-6 * max(float(n.max()), 1e-300)
+    return float(np.max(np.linalg.norm(dg - do, axis=1) / np.maximum(n, floor)))
+
+
+# ---------------------------------------------------------------- R14 skip, R23 retry / NOT_SPD
+def test_zero_core_skips_blocks_gradient_descent_arm():
+    """A zero core m makes S(j) = 0 for every block k != m: d = 0, num = den = 0, so those
+    blocks are skipped (eta = 0, R14) on both sides; block m itself updates."""
+    _cuda()
+    spec = small_spec("C4", [10, 9, 8, 7], [5, 4, 4, 3])
+    prob = make_problem(spec)
+    prob.init[2][:] = 0.0
+    src, _ = oracle_source(prob)
+    over = dict(sigma_mode=O.SIGMA_FIXED, sigma=1.0, scaling=O.SCALING_NONE)
+    st, recs = O.run(oracle_config(spec, **over), prob.init, src, 1)
+    ctx = gpu_context(prob, packed=True, **over)
+    g = ctx.sweep(1)[0]
+    want = sum(1 << k for k in range(4) if recs[0].skipped[k])
+    assert want == (1 << 0) | (1 << 1)     # block 2 updates core 2, so block 3 is not skipped
+    assert g["skipped"] == want
+    for k in range(4):
+        assert (g["eta"][k] == 0.0) == recs[0].skipped[k]
+    assert cores_rel_err(ctx.get_cores(), st.cores) <= 1e-4
+    ctx.close()
+
+
+def test_zero_core_is_not_spd_with_the_fgmc_gram():
+    """With the FGMC Gram a zero core gives G = 0 for k != m: G + lambda I stays singular
+    through the retries of R23 -> TRD_ERR_NOT_SPD, and the oracle raises NotSPD."""
+    _cuda()
+    from paper_2305_09044_b200.trd import TrdError
+    spec = small_spec("C4", [10, 9, 8, 7], [5, 4, 4, 3])
+    prob = make_problem(spec)
+    prob.init[1][:] = 0.0
+    src, _ = oracle_source(prob)
+    over = dict(sigma_mode=O.SIGMA_FIXED, sigma=1.0)
+    with pytest.raises(O.NotSPD):
+        O.run(oracle_config(spec, **over), prob.init, src, 1)
+    ctx = gpu_context(prob, packed=True, **over)
+    with pytest.raises(TrdError) as ei:
+        ctx.sweep(1)
+    assert ei.value.status == 6                       # TRD_ERR_NOT_SPD
+    ctx.close()
+
+
+def test_lambda_retry_on_a_gram_with_zero_rows():
+    """R23: lambda_rel = 0 and a zero rank component (Z_{k+1}[0, :, :] = 0) give G_{!=k} exactly
+    zero rows: the solve fails at lambda = 0 and both sides retry with 2^-40 tr(G)/R^2; h, num
+    and den of block k agree."""
+    _cuda()
+    spec = small_spec("C4", [12, 11, 10, 9], [6, 5, 4, 5])
+    prob = make_problem(spec)
+    k = 1
+    prob.init[k + 1][0, :, :] = 0.0
+    src, _ = oracle_source(prob)
+    cfg = oracle_config(spec, sigma_mode=O.SIGMA_FIXED, sigma=1.0, lambda_rel=0.0)
+    st = O.State(cfg, prob.init, src)
+    ctx = gpu_context(prob, packed=True, sigma_mode=O.SIGMA_FIXED, sigma=1.0, lambda_rel=0.0)
+    g = ctx.block_probe(0, k)
+    ctx.close()
+    sets = O.index_sets_for_block(cfg, 0, k)
+    Xk, Pk = O.working_set(src, k, sets)
+    S = O.subchain(st.cores, k, sets)
+    d, _, W = O.gradient_block(Xk, Pk, O.core_unfold2(st.cores[k]), S, 1.0)
+    G = O.gram_fgmc(st.Qs, k, spec.ranks)
+    zero_rows = np.all(G == 0.0, axis=1)
+    assert zero_rows.sum() == spec.ranks[k]            # rows c + r_k b with b = 0
+    h, lam = O.scaled_gradient(d, G, 0.0)
+    assert lam > 0.0
+    assert rel_fro(g["d"], d) <= 1e-4
+    assert rel_fro(g["h"], h) <= 1e-4
+    assert np.all(g["h"][:, zero_rows] == 0.0)
+    assert abs(g["den"] - O.line_search_den(h, Pk, W, S)) <= 1e-4 * g["den"]
+
+
+def test_rank_slice_without_sampled_indices():
+    """A partial shard whose slice of the (sampled) shard mode holds none of the block's sampled
+    indices contributes nothing: n_obs = 0, d = 0, den = 0 (no hang, no stale data)."""
+    _cuda()
+    from paper_2305_09044_b200 import TRD
+    import bench
+    spec = small_spec("C4", [16, 11, 10, 9], [3, 5, 3, 4])
+    prob = make_problem(spec, keep_mask_bool=True)
+    k = 2
+    s0 = sample_indices(spec.sampler_seed, 0, k, 0, 16, 3)
+    # the longest run of mode-0 indices with no sampled index -> the rank's slice
+    free = [i for i in range(16) if i not in set(s0.tolist())]
+    runs, cur = [], [free[0]]
+    for i in free[1:]:
+        if i == cur[-1] + 1:
+            cur.append(i)
+        else:
+            runs.append(cur)
+            cur = [i]
+    runs.append(cur)
+    run = max(runs, key=len)
+    b, e = run[0], run[-1] + 1
+    shape = list(reversed(spec.dims))
+    Xl = prob.X.view(*shape)[..., b:e].reshape(-1).contiguous()
+    Ml = prob.mask_bool.view(*shape)[..., b:e].reshape(-1).contiguous()
+    ctx = TRD(spec.dims, spec.ranks, Xl[Ml].contiguous().cuda(), pack_bits(Ml).cuda(), prob.init,
+              packed=True, sketch=spec.sketch, seed=spec.sampler_seed, sigma_mode=O.SIGMA_FIXED,
+              sigma=1.0, shard_mode=0, shard_range=(b, e), world=1, rank=0)
+    g = ctx.block_probe(0, k)
+    assert g["n_obs"] == 0 and np.all(g["d"] == 0.0) and g["den"] == 0.0
+    g1 = ctx.block_probe(0, 0)                          # block 0: mode 0 is the full row mode
+    assert g1["n_obs"] > 0
+    ctx.close()
+    _ = bench
+
+
+def test_welsch_monitor_matches_oracle():
+    """R3: the per-sweep Welsch loss sum_blocks sum_obs sigma^2 (1 - w) and sum e^2 (fixed
+    sigma and RMS)."""
+    _cuda()
+    spec = small_spec("C1", [24, 22, 20])
+    prob = make_problem(spec)
+    src, _ = oracle_source(prob)
+    for over in [dict(sigma_mode=O.SIGMA_FIXED, sigma=0.8), dict()]:
+        st, recs = O.run(oracle_config(spec, **over), prob.init, src, 2)
+        ctx = gpu_context(prob, packed=True, **over)
+        g = ctx.sweep(2)
+        for t in range(2):
+            assert abs(g[t]["welsch"] - recs[t].welsch) <= 1e-5 * recs[t].welsch, (over, t)
+            assert abs(g[t]["sum_e2"] - recs[t].sum_e2) <= 1e-5 * recs[t].sum_e2, (over, t)
+        ctx.close()
+
+
+# ---------------------------------------------------------------- data scale (operand scaling)
+@pytest.mark.parametrize("alpha", [1e-3, 1e-5, 1e5])
+@pytest.mark.parametrize("spread", ["balanced", "one_core"])
+@pytest.mark.parametrize("name,dims,sketch", [("C4", [16, 16, 16, 16], [8, 8, 8, 8]),
+                                               ("C5a", [8, 8, 8, 8, 8], [5, 5, 5, 5, 5])])
+def test_data_far_from_unit_scale(name, dims, sketch, alpha, spread):
+    """X and the initial cores scaled so that X is alpha times the BASELINE recipe (the cores
+    either all by alpha^(1/N), or one core by alpha): cores after one sweep and the block
+    quantities stay within the north-star tolerances (power-of-two scaled fp16 hi / lo
+    operands; an unscaled split loses 1e-4 at alpha = 1e-4 and overflows above 6.5e4)."""
+    _cuda()
+    spec = small_spec(name, dims, sketch)
+    prob = make_problem(spec)
+    N = len(dims)
+    prob.X.mul_(alpha)
+    prob.X_clean.mul_(alpha)
+    if spread == "balanced":
+        f = alpha ** (1.0 / N)
+        prob.init = [(c * f).astype(np.float32) for c in prob.init]
+    else:
+        prob.init[1] = (prob.init[1] * alpha).astype(np.float32)
+    src, _ = oracle_source(prob)
+    cfg = oracle_config(spec)
+    st0 = O.State(cfg, prob.init, src)
+    ctx = gpu_context(prob, packed=True)
+    for k in (0, N - 1):
+        g = ctx.block_probe(0, k)
+        sets = O.index_sets_for_block(cfg, 0, k)
+        Xk, Pk = O.working_set(src, k, sets)
+        S = O.subchain(st0.cores, k, sets)
+        d, _, W = O.gradient_block(Xk, Pk, O.core_unfold2(st0.cores[k]), S, st0.sigma)
+        h, _ = O.scaled_gradient(d, O.gram_fgmc(st0.Qs, k, spec.ranks), cfg.lambda_rel)
+        assert _rowwise(g["d"], d) <= 1e-4, (k, _rowwise(g["d"], d))
+        assert abs(g["den"] - O.line_search_den(h, Pk, W, S)) <= 1e-4 * g["den"], k
+    ctx.close()
+    st, _ = O.run(cfg, prob.init, src, 1)
+    ctx = gpu_context(prob, packed=True)
+    ctx.sweep(1)
+    assert cores_rel_err(ctx.get_cores(), st.cores) <= 1e-4
+    ctx.close()
+
+
+# ---------------------------------------------------------------- row-wise d
+@pytest.mark.parametrize("name,dims,sketch", [("C2", [64, 48, 3], None), ("C3", [48, 64, 3, 20], [10, 13, 1, 4]),
+                                               ("C5b", [12, 9, 8, 7, 6], None)])
+def test_gradient_rows_elementwise(name, dims, sketch):
+    """Eq. 9/15 row by row: every row i_k of d within 1e-4 of its own norm (a single bad row
+    cannot hide in a Frobenius norm over I_k x R^2)."""
+    _cuda()
+    spec = small_spec(name, dims, sketch)
+    prob = make_problem(spec)
+    src, _ = oracle_source(prob)
+    cfg = oracle_config(spec)
+    st = O.State(cfg, prob.init, src)
+    ctx = gpu_context(prob, packed=True)
+    for k in range(len(dims)):
+        g = ctx.block_probe(0, k)
+        sets = O.index_sets_for_block(cfg, 0, k)
+        Xk, Pk = O.working_set(src, k, sets)
+        S = O.subchain(st.cores, k, sets)
+        d, _, _ = O.gradient_block(Xk, Pk, O.core_unfold2(st.cores[k]), S, st.sigma)
+        assert _rowwise(g["d"], d) <= 1e-4, (k, _rowwise(g["d"], d))
+        h, _ = O.scaled_gradient(d, O.gram_fgmc(st.Qs, k, spec.ranks), cfg.lambda_rel)
+        assert _rowwise(g["h"], h) <= 1e-4, k
+    ctx.close()
+
+
+# ---------------------------------------------------------------- trd_error: PSNR
+def test_error_psnr_and_observed_error_match_oracle():
+    """trd_error against the oracle formulas: relative error over all entries and over the
+    observed entries, and PSNR = 10 log10(peak^2 / MSE) (peak 1 for data in [0, 1] as
+    in the paper, and an explicit peak), over all entries and over an evaluation subset."""
+    _cuda()
+    spec = small_spec("C2", [48, 40, 3])
+    prob = make_problem(spec)
+    src, Xc = oracle_source(prob)
+    st, _ = O.run(oracle_config(spec), prob.init, src, 3)
+    ctx = gpu_context(prob, packed=True)
+    ctx.sweep(3, stats=False)
+    cores = ctx.get_cores()
+    Xhat = O.tr_reconstruct([c.astype(np.float64) for c in cores])
+    P = src.P
+    rng = np.random.default_rng(5)
+    ev = rng.random(Xc.shape) < 0.3
+    ev_words = pack_bits(torch.from_numpy(ev.transpose().reshape(-1).copy())).cuda()
+    for peak in (1.0, 2.5):
+        for bits, sel in ((None, np.ones(Xc.shape, dtype=bool)), (ev_words, ev)):
+            g = ctx.error(prob.X_clean.cuda(), bits, peak=peak)
+            diff = (Xhat - Xc)
+            want_all = math.sqrt(float(np.sum(diff[sel] ** 2)) / float(np.sum(Xc[sel] ** 2)))
+            obs = sel & P
+            want_obs = math.sqrt(float(np.sum(diff[obs] ** 2)) / float(np.sum(Xc[obs] ** 2)))
+            want_psnr = O.psnr(Xc[sel], Xhat[sel], peak=peak)
+            assert g["n_eval"] == int(sel.sum())
+            assert abs(g["rel_err_all"] - want_all) <= 1e-5 * want_all
+            assert abs(g["rel_err_observed"] - want_obs) <= 1e-5 * want_obs
+            assert abs(g["psnr"] - want_psnr) <= 1e-4, (peak, g["psnr"], want_psnr)
+    ctx.close()

@@ -261,8 +261,9 @@ def test_ablation_arms_match_oracle(scaling):
 
 @pytest.mark.parametrize("name,dims,sketch", [("C1", [32, 32, 32], None), ("C4", [16, 16, 16, 16], [8, 8, 8, 8])])
 def test_robust_sigma_rule_matches_oracle(name, dims, sketch):
-    """Reading R21 (TRD_SIGMA_MAD): sigma_0 and each sweep's sigma from the |e| histogram
-    median (same bins on both sides), and the cores after two sweeps."""
+    """Reading R21 (TRD_SIGMA_MAD): sigma_0 and each sweep's sigma from the exact median of |e|
+    (GPU: radix select over the fp32 |e|; oracle: np.median of the float64 |e|), and the cores
+    after two sweeps."""
     _cuda()
     spec = small_spec(name, dims, sketch)
     prob = make_problem(spec)
