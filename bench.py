@@ -39,7 +39,7 @@ def parse():
     ap.add_argument("--impl", default="mine", choices=["mine", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-budget-s", type=float, default=15.0)
+    ap.add_argument("--cpu-budget-s", type=float, default=10.0)
     # variants of the method (defaults: the config's sigma rule, the paper's scaled gradient)
     ap.add_argument("--sigma-mode", default=None, choices=["fixed", "inf", "rms", "mad"],
                     help="sigma rule (mad: robust rule R21)")
@@ -125,43 +125,21 @@ def local_shard(prob, rank, world):
     return (b, e), vals, words, Ml
 
 
-class GpuGatherSource:
-    """Oracle data source reading the sketch entries of the resident tensor (plumbing for the
-    cpu_baseline leg: the oracle gets float64 copies of the same fp32 bytes)."""
-
-    def __init__(self, prob):
-        self.prob = prob
-        self.dims = prob.spec.dims
-
-    def subtensor(self, index_sets):
-        import torch
-        dev = self.prob.X.device
-        lin = torch.zeros(1, dtype=torch.int64, device=dev)
-        stride = 1
-        shape = []
-        for m, idx in enumerate(index_sets):
-            t = torch.as_tensor(np.asarray(idx), dtype=torch.int64, device=dev) * stride
-            lin = (lin.view(-1, 1) + t.view(1, -1)).view(-1)   # mode m slower than previous
-            stride *= self.dims[m]
-            shape.append(len(idx))
-        x = self.prob.X[lin].double().cpu().numpy()
-        p = self.prob.mask_bool[lin].cpu().numpy()
-        # lin enumerates mode 0 fastest -> numpy order reversed then transposed
-        x = x.reshape(shape[::-1]).transpose()
-        p = p.reshape(shape[::-1]).transpose()
-        return x, p
-
-
-def oracle_sample(prob, budget_s, sample_s=12, max_blocks=None):
-    """Time the oracle (oracle/trd_oracle.py, as it stands) on bounded samples of the
-    workload: block updates of Alg. 1 on a sub-sketch with s_m = sample_s for m != k."""
+def oracle_sample(prob, budget_s, max_blocks=None):
+    """Time the oracle (oracle/, as it stands) on bounded samples of the same workload: whole
+    block updates of Alg. 1 (lines 4-10: sampler, both per-entry passes over every observed
+    entry of the block's working set, FGMC Gram, filtered solve, step), one after another in
+    the cyclic block order, at the workload's full size -- the per-entry passes through the
+    oracle's entry-wise C source (float64, OpenMP over the host cores), the rest in numpy.
+    Runs at least one block and stops after the block that crosses budget_s."""
     from oracle import trd_oracle as O
+    from oracle.entries import EntrySource
     spec = prob.spec
     N = spec.order
-    sk = [min(sample_s, spec.dims[m]) for m in range(N)]
-    cfg = O.Config(spec.dims, spec.ranks, sigma_mode=O.SIGMA_FIXED, sigma=1.0, sketch=sk,
+    src = EntrySource(spec.dims, prob.mask.cpu().numpy().view(np.uint32),
+                      prob.X[prob.mask_bool].cpu().numpy(), True)
+    cfg = O.Config(spec.dims, spec.ranks, sigma_mode=O.SIGMA_FIXED, sigma=1.0, sketch=spec.sketch,
                    seed=spec.sampler_seed)
-    src = GpuGatherSource(prob)
 
     class _St:
         pass
@@ -171,7 +149,6 @@ def oracle_sample(prob, budget_s, sample_s=12, max_blocks=None):
     st.sigma = 1.0
     st.t = 0
     nnz, secs, blocks = 0, 0.0, 0
-    t_start = time.perf_counter()
     while True:
         k = blocks % N
         rec = O.SweepRecord(N)
@@ -182,18 +159,18 @@ def oracle_sample(prob, budget_s, sample_s=12, max_blocks=None):
         blocks += 1
         if k == N - 1:
             st.t += 1
-        if time.perf_counter() - t_start > budget_s or (max_blocks and blocks >= max_blocks):
+        if secs > budget_s or (max_blocks and blocks >= max_blocks):
             break
+    cores = os.cpu_count()
     try:
-        from threadpoolctl import threadpool_info
-        cores = max([i.get("num_threads", 1) for i in threadpool_info()] + [1])
+        cores = len(os.sched_getaffinity(0))
     except Exception:
-        cores = os.cpu_count()
-    return dict(value=nnz / secs, unit="observed-entry updates/s", cores=int(cores),
-                kind="oracle",
-                sample=f"{blocks} oracle block updates (Alg. 1 lines 4-10) of {spec.name} on a "
-                       f"sub-sketch s_m={sample_s} (m != k): {nnz} observed-entry updates in "
-                       f"{secs:.2f} s, float64 numpy")
+        pass
+    threads = int(os.environ.get("OMP_NUM_THREADS", cores))
+    return dict(value=nnz / secs, unit="observed-entry updates/s", cores=threads, kind="oracle",
+                sample=f"{blocks} oracle block update(s) (Alg. 1 lines 4-10) of {spec.name} at full size "
+                       f"(sigma fixed at 1): {nnz} observed-entry updates in {secs:.2f} s; per-entry passes "
+                       f"float64 C + OpenMP ({threads} threads), Gram / solve numpy float64")
 
 
 def make_workload(spec, device):
@@ -214,12 +191,11 @@ def run_reference(args):
     spec = CONFIGS[args.config]
     dev = "cuda" if torch.cuda.is_available() else "cpu"
     prob = make_workload(spec, dev)
-    budget = max(2.0, min(args.cpu_budget_s, 60.0) / max(1, args.steps + args.warmup))
-    for _ in range(args.warmup):
-        oracle_sample(prob, budget, max_blocks=1)
+    for _ in range(min(args.warmup, 1)):                  # (warm-up: build the C oracle, page in)
+        oracle_sample(prob, 0.0, max_blocks=1)
     vals, last = [], None
-    for _ in range(args.steps):
-        last = oracle_sample(prob, budget)
+    for _ in range(args.steps):                           # one full-size block update per step
+        last = oracle_sample(prob, 0.0, max_blocks=1)
         vals.append(last["value"])
     value = float(np.median(vals))
     cb = dict(last)
@@ -229,7 +205,8 @@ def run_reference(args):
             "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": spec.name, "dims": spec.dims, "ranks": spec.ranks,
-                       "observed": spec.observed, "sketch": spec.sketch},
+                       "observed": spec.observed, "sketch": spec.sketch, "same_config": True,
+                       "sample": "each step: one block update of the full-size workload"},
             "cpu_baseline": cb,
             "e2e": {"value": value, "unit": "observed-entry updates/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
@@ -276,7 +253,8 @@ def run_mine(args):
     torch.cuda.synchronize()
 
     # ---------------- device-timed region: K sweeps, inputs resident in HBM ----------------
-    ctx.set_profiling(True)
+    prof_on = not os.environ.get("TRD_BENCH_NOPROF")          # (A/B: timed region without events)
+    ctx.set_profiling(prof_on)
     l0 = ctx.launch_count
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local_rank) as clk:
@@ -317,7 +295,8 @@ def run_mine(args):
                 if i + 1 < n:
                     ctx2.upload(vals_h, words_h)             # H2D of step i + 1's inputs
                 marks.append(time.perf_counter())
-                r = ctx2.sweep(1, stats=True)                # step i, D2H of its result
+                r = ctx2.sweep(1, stats=True)                # step i, D2H of its statistics
+                ctx2.get_cores()                             # D2H of the step's result: the cores
                 done += r[0]["n_obs"]
                 marks.append(time.perf_counter())
             return done, marks
@@ -342,20 +321,32 @@ def run_mine(args):
             ms2 = float(t.item())
         from paper_2305_09044_b200.trd import trd_sweep_stats
         import ctypes
+        core_bytes = sum(int(np.prod(c.shape)) * 4 for c in prob.init)
         e2e = {"value": upd2 / (ms2 / 1e3), "unit": "observed-entry updates/s",
                "h2d_bytes_per_step": int(vals_h.numel() * 4 + words_h.numel() * 4),
-               "d2h_bytes_per_step": int(ctypes.sizeof(trd_sweep_stats))}
+               "d2h_bytes_per_step": int(ctypes.sizeof(trd_sweep_stats)) + core_bytes,
+               "d2h": "sweep record + all N cores (trd_get_cores) every step"}
         ctx2.close()
 
     # ---------------- roofline of the dominant kernel ----------------
     peaks, src = measured_peaks()
     sm_max = float(peaks.get("sm_max_mhz", 1965.0))
     p_fp32 = SM_COUNT * FP32_LANES_PER_SM * 2 * sm_max * 1e6 / 1e12      # TFLOP/s
+    fp32_src = f"FP32 FMA: {SM_COUNT} SM x {FP32_LANES_PER_SM} lanes x 2 x {sm_max:.0f} MHz ({src} sm_max_mhz)"
+    fp = os.path.join(ROOT, "profiles", "fp32_peak.json")
+    if os.path.exists(fp):                       # measured FMA peak (scripts/microbench/fma_peak.cu)
+        try:
+            m = json.load(open(fp))
+            p_fp32 = float(m["fp32_fma_tflops"])
+            fp32_src = f"measured FP32 FMA peak (profiles/fp32_peak.json: {m.get('how', '')})"
+        except Exception:
+            pass
     dom = "pass1" if prof["pass1_ms"] >= prof["pass2_ms"] else "pass2"
     n_l = max(1, prof[dom + "_launches"])
     avg_ms = prof[dom + "_ms"] / n_l
     flops_per_launch = prof[dom + "_flops"] / n_l
     bytes_per_launch = prof[dom + "_bytes"] / n_l
+    avg_ms = max(avg_ms, 1e-9)                 # (profiling off: no kernel times)
     achieved = flops_per_launch / (avg_ms / 1e3) / 1e12
     traffic = None
     tp = os.path.join(ROOT, "profiles", "traffic.json")
@@ -367,8 +358,7 @@ def run_mine(args):
     kname = {"pass1": "tc_pass1_kernel", "pass2": "tc_pass2_kernel"}[dom]
     roof = {"bound": "alu", "kernel": f"{dom} ({kname}, libtrd)", "achieved": achieved,
             "peak": p_fp32, "unit": "TFLOP/s", "frac": achieved / p_fp32, "traffic": traffic,
-            "peak_source": f"FP32 FMA: {SM_COUNT} SM x {FP32_LANES_PER_SM} lanes x 2 x "
-                           f"{sm_max:.0f} MHz ({src} sm_max_mhz)",
+            "peak_source": fp32_src,
             "algorithmic_bytes_per_launch": bytes_per_launch,
             "hbm_frac": bytes_per_launch / (avg_ms / 1e3) / (float(peaks.get("hbm_gbs", 6545.6)) * 1e9),
             "avg_launch_ms": avg_ms,

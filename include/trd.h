@@ -19,8 +19,8 @@
  *   - Zk2 column a + r_k*b (classical mode-2 unfolding, Thm 1); d and h use it too.
  *
  * Errors: every call returns trd_status and never throws across the ABI.  Arguments are
- * validated before anything is enqueued.  A CUDA or NCCL failure puts the context into a
- * sticky error state in which only trd_get_cores / trd_last_error / trd_destroy are valid.
+ * validated before anything is enqueued.  A CUDA or exchange (NCCL) failure puts the context
+ * into a sticky error state in which only trd_get_cores / trd_last_error / trd_destroy are valid.
  *
  * Threading: a context is used by one host thread at a time.  All device work is enqueued
  * on the stream given to trd_init (trd_upload's copies: on a library copy stream ordered
@@ -43,7 +43,7 @@ extern "C" {
 #endif
 
 #define TRD_MAX_ORDER 8
-#define TRD_MAX_RANK 16
+#define TRD_MAX_RANK 32
 
 typedef struct trd_ctx trd_ctx;
 
@@ -72,7 +72,9 @@ typedef enum {
 typedef struct {
   int32_t order;                    /* N, 3..TRD_MAX_ORDER                                  */
   int64_t dims[TRD_MAX_ORDER];      /* global I_0..I_{N-1}                                  */
-  int32_t ranks[TRD_MAX_ORDER];     /* r_0..r_{N-1}, 1..TRD_MAX_RANK, ring r_N = r_0   */
+  int32_t ranks[TRD_MAX_ORDER];     /* r_0..r_{N-1}, 1..TRD_MAX_RANK, ring r_N = r_0;
+                                       r_k r_{k+1} <= 1024, and every block must have a split
+                                       with r_k r_s <= 256 (else TRD_ERR_SHAPE)               */
   int32_t sigma_mode;               /* trd_sigma_mode                                       */
   double sigma;                     /* FIXED: the kernel width; RMS: ignored (sigma_0 from
                                        an initial residual pass); INF: ignored              */
@@ -129,6 +131,24 @@ typedef struct {
                                        device buffers and copies them (trd_upload re-copies) */
 } trd_shard;
 
+/* Data-parallel exchange (world > 1), the one collective of the path: an in-place allreduce
+ * of n doubles in device memory across the ranks (op TRD_OP_SUM or TRD_OP_MAX), ordered on
+ * `stream`: it must include all work enqueued on the stream before the call, and work enqueued
+ * after it must see the result (a host-synchronous implementation -- synchronise the stream,
+ * exchange, copy back -- qualifies).  Returns 0 on success.  With trd_init the library uses
+ * NCCL (ncclAllReduce on the context stream, bootstrapped from cfg.nccl_unique_id); with
+ * trd_init_ex a caller-supplied exchange replaces it (for example torch.distributed, or a
+ * test harness driving several contexts).  The call sites, per block (Alg. 1): the
+ * gradient partials and residual statistics [d | sum e^2 | welsch | n] after pass 1, the
+ * line-search denominator after pass 2; per sweep: the R21 select histograms (MAD) and the
+ * replica-consistency check; at init: sigma_0's statistics; trd_error's sums. */
+typedef enum { TRD_OP_SUM = 0, TRD_OP_MAX = 1 } trd_reduce_op;
+typedef int (*trd_allreduce_fn)(void* user, double* buf_dev, uint64_t n, int32_t op, void* stream);
+typedef struct {
+  trd_allreduce_fn allreduce;
+  void* user;
+} trd_exchange;
+
 /* One record per sweep.  ms is the device time of the sweep (CUDA events). */
 typedef struct {
   double sigma;                     /* kernel width used in this sweep                      */
@@ -142,6 +162,9 @@ typedef struct {
   double den[TRD_MAX_ORDER];        /* ||sqrt(W) o P o (h S^T)||^2 per block                  */
   int64_t nnz[TRD_MAX_ORDER];       /* observed entries in block k's working set             */
   uint32_t skipped_mask;            /* bit k set: block k skipped (num <= 0 or den == 0, R14) */
+  uint32_t replica_mismatch;        /* world > 1: 1 if the ranks' cores differed after the
+                                       sweep (a 64-bit checksum compared across ranks; the
+                                       replicated update must be bitwise identical) */
 } trd_sweep_stats;
 
 typedef struct {
@@ -157,6 +180,12 @@ typedef struct {
  * (allreduced).  Synchronises the stream once.  *out is NULL on failure. */
 TRD_API trd_status trd_init(const trd_config* cfg, const trd_shard* shard,
                     const float* const* init_cores, void* stream, trd_ctx** out);
+
+/* trd_init with a caller-supplied exchange (world > 1; cfg.nccl_unique_id is then ignored and
+ * NCCL is not loaded).  `ex` is copied; ex->user must stay valid until trd_destroy. */
+TRD_API trd_status trd_init_ex(const trd_config* cfg, const trd_shard* shard,
+                       const float* const* init_cores, void* stream, const trd_exchange* ex,
+                       trd_ctx** out);
 
 /* Copy host-resident X / P (shard.host == 1 only) for a later sweep: the host->device leg of
  * an end-to-end step.  The copy runs on the library's copy stream into one of two device

@@ -145,7 +145,8 @@ void build_plan(const Context& c, int k, const int64_t* s_in, BlockPlan& bp, boo
     const int64_t K = (int64_t)c.ranks[k] * rs;
     int64_t ncols = 1;
     for (int q = p + 1; q <= N - 1; ++q) ncols *= bp.s[(k + q) % N];
-    const double cost = want_tc ? plan_cost_tc(K, ncols) : plan_cost(K, ncols);
+    double cost = want_tc ? plan_cost_tc(K, ncols) : plan_cost(K, ncols);
+    if (K > 256) cost += 1e200;            // the pass kernels need K = r_k r_s <= 256
     if (cost < best - 1e-12) { best = cost; best_p = p; }
   }
   const int p = best_p;
@@ -249,23 +250,46 @@ void build_plan(const Context& c, int k, const int64_t* s_in, BlockPlan& bp, boo
 
 size_t ncta_of(const BlockPlan& bp) { return (size_t)(bp.grid_x * bp.nsplit); }
 
-trd_status allreduce(Context* c, double* buf, size_t n, int op = kNcclSum) {
+// the data-parallel exchange: NCCL on the context stream, or the caller's allreduce (trd_init_ex)
+trd_status allreduce(Context* c, double* buf, size_t n, int op = TRD_OP_SUM) {
   if (c->cfg.world <= 1) return TRD_OK;
-  int r = g_nccl.all_reduce(buf, buf, n, kNcclFloat64, op, c->nccl_comm, c->stream);
+  if (c->ex.allreduce) {
+    const int r = c->ex.allreduce(c->ex.user, buf, (uint64_t)n, op, (void*)c->stream);
+    if (r != 0) return fail(c, TRD_ERR_NCCL, "exchange allreduce failed (%d)", r);
+    return TRD_OK;
+  }
+  int r = g_nccl.all_reduce(buf, buf, n, kNcclFloat64, op == TRD_OP_MAX ? kNcclMax : kNcclSum, c->nccl_comm,
+                            c->stream);
   if (r != 0) return fail(c, TRD_ERR_NCCL, "ncclAllReduce: %s", g_nccl.err_str ? g_nccl.err_str(r) : "?");
   return TRD_OK;
 }
 
 // profiling events around a pass kernel (pool reused across sweeps)
-int prof_event(Context* c) {
+int prof_event_slot(Context* c) {
   if (c->ev_used == c->ev_pool.size()) {
     cudaEvent_t e;
     if (cudaEventCreate(&e) != cudaSuccess) return -1;
     c->ev_pool.push_back(e);
   }
-  const int i = (int)c->ev_used++;
-  cudaEventRecord(c->ev_pool[(size_t)i], c->stream);
+  return (int)c->ev_used++;
+}
+// During a sweep capture the event becomes a graph node: its own capture event, re-pointed at
+// a pool event on every replay (launch_graph)
+int prof_event(Context* c) {
+  if (c->capturing) {
+    cudaEvent_t e;
+    if (cudaEventCreate(&e) != cudaSuccess) return -1;
+    c->capturing->cap_ev.push_back(e);
+    cudaEventRecordWithFlags(e, c->stream, cudaEventRecordExternal);   // -> an event-record node
+    return (int)c->capturing->cap_ev.size() - 1;
+  }
+  const int i = prof_event_slot(c);
+  if (i >= 0) cudaEventRecord(c->ev_pool[(size_t)i], c->stream);
   return i;
+}
+void prof_pair(Context* c, int pass, int e0, int e1) {
+  if (c->capturing) (pass == 1 ? c->capturing->pairs1 : c->capturing->pairs2).push_back({e0, e1});
+  else (pass == 1 ? c->ev_pass1 : c->ev_pass2).push_back({e0, e1});
 }
 
 // a1-a6 + a7 (pass 1 and the d/stat exchange) of block k
@@ -299,10 +323,11 @@ trd_status block_pass1(Context* c, const BlockPlan& bp) {
       stg.valid = stg.invariant;
     }
   }
-  const int e0 = c->prof ? prof_event(c) : -1;
+  const bool pe = c->prof || c->capturing;
+  const int e0 = pe ? prof_event(c) : -1;
   if (bp.use_tc) launch_tc_pass(*c, bp, stg, false, s);
   else launch_pass1(*c, bp, 0, s);
-  if (c->prof) c->ev_pass1.push_back({e0, prof_event(c)});
+  if (pe) prof_pair(c, 1, e0, prof_event(c));
   if (bp.use_tc && c->eabs) launch_eabs_advance(*c, stg, s);   // R21 |e| slots of this block
   if (bp.use_tc) launch_tc_reduce_d(*c, bp, s);
   else launch_reduce_d(*c, bp, s);
@@ -322,10 +347,11 @@ trd_status block_pass2(Context* c, const BlockPlan& bp) {
   launch_h(*c, bp, s);
   if (!bp.use_tc) launch_lft(*c, bp, nullptr, 1, c->lfth, s);
   else launch_tc_lft(*c, bp, true, s);
-  const int e0 = c->prof ? prof_event(c) : -1;
+  const bool pe = c->prof || c->capturing;
+  const int e0 = pe ? prof_event(c) : -1;
   if (bp.use_tc) launch_tc_pass(*c, bp, c->stage[bp.k], true, s);
   else launch_pass2(*c, bp, s);
-  if (c->prof) c->ev_pass2.push_back({e0, prof_event(c)});
+  if (pe) prof_pair(c, 2, e0, prof_event(c));
   launch_reduce_den(*c, bp, s);
   trd_status st = check_launch(c, "pass 2");
   if (st) return st;
@@ -494,6 +520,11 @@ trd_status trd_get_profile(trd_ctx* ctx, trd_profile* out) {
 
 trd_status trd_init(const trd_config* cfg, const trd_shard* shard, const float* const* init_cores,
                     void* stream, trd_ctx** out) {
+  return trd_init_ex(cfg, shard, init_cores, stream, nullptr, out);
+}
+
+trd_status trd_init_ex(const trd_config* cfg, const trd_shard* shard, const float* const* init_cores,
+                       void* stream, const trd_exchange* ex, trd_ctx** out) {
   if (!out) return TRD_ERR_INVALID_ARG;
   *out = nullptr;
   if (!cfg || !shard || !init_cores) return TRD_ERR_INVALID_ARG;
@@ -516,7 +547,8 @@ trd_status trd_init(const trd_config* cfg, const trd_shard* shard, const float* 
   if (cfg->sampling == TRD_SAMPLING_ROWS && cfg->scaling == TRD_SCALING_LOCAL) return TRD_ERR_INVALID_ARG;
   if (cfg->world < 1 || cfg->rank < 0 || cfg->rank >= cfg->world) return TRD_ERR_INVALID_ARG;
   if (cfg->shard_mode < 0 || cfg->shard_mode >= N) return TRD_ERR_SHAPE;
-  if (cfg->world > 1 && !cfg->nccl_unique_id) return TRD_ERR_INVALID_ARG;
+  if (ex && !ex->allreduce) return TRD_ERR_INVALID_ARG;
+  if (cfg->world > 1 && !cfg->nccl_unique_id && !ex) return TRD_ERR_INVALID_ARG;
   if (!shard->values || !shard->mask_bits) return TRD_ERR_INVALID_ARG;
   const int sm = cfg->shard_mode;
   const int64_t sb = shard->shard_begin, se = shard->shard_end;
@@ -529,6 +561,7 @@ trd_status trd_init(const trd_config* cfg, const trd_shard* shard, const float* 
   if (!c) return TRD_ERR_OOM;
   c->cfg = *cfg;
   c->cfg.nccl_unique_id = nullptr;
+  if (ex && cfg->world > 1) c->ex = *ex;
   c->N = N;
   c->stream = (cudaStream_t)stream;
   {
@@ -563,8 +596,17 @@ trd_status trd_init(const trd_config* cfg, const trd_shard* shard, const float* 
   }
   c->n_local = stride;
   c->n_words = (c->n_local + 31) / 32;
-  for (int k = 0; k < N; ++k)
-    if (c->ranks[k] * c->ranks[(k + 1) % N] > kMaxR2) { delete c; return TRD_ERR_SHAPE; }
+  int64_t r2max = 1, chain_max = 1;
+  for (int k = 0; k < N; ++k) {
+    const int64_t r2 = (int64_t)c->ranks[k] * c->ranks[(k + 1) % N];
+    if (r2 > kMaxR2) { delete c; return TRD_ERR_SHAPE; }
+    r2max = std::max(r2max, r2);
+    c->rbucket = std::max(c->rbucket, c->ranks[k] <= 16 ? 16 : 32);
+    // FGMC chain products r_{k+1}^2 x r_m^2 (Eq. 13): the largest intermediate
+    for (int m = 0; m < N; ++m)
+      chain_max = std::max(chain_max, (int64_t)c->ranks[(k + 1) % N] * c->ranks[(k + 1) % N] * c->ranks[m] * c->ranks[m]);
+  }
+  c->chain_half = (size_t)chain_max;
 
   trd_status st = TRD_OK;
   auto bail = [&](trd_status s2) { trd_destroy(reinterpret_cast<trd_ctx*>(c)); return s2; };
@@ -584,6 +626,7 @@ trd_status trd_init(const trd_config* cfg, const trd_shard* shard, const float* 
     if (k < N) build_plan(*c, k, cfg->sketch, bp, c->want_tc != 0, cfg->sampling == TRD_SAMPLING_ROWS);
     else build_plan(*c, 0, full_s, bp, false);
     if (bp.use_tc && !tc_supported_kp(bp.KP)) bp.use_tc = 0;
+    if (bp.K > 256) return bail(fail(c, TRD_ERR_SHAPE, "block %d: no split with r_k r_s <= 256", k));
     if (bp.use_tc) {
       TcStage& st = c->stage[k];
       st.n_tiles = bp.n_row_tiles * bp.n_col_tiles;
@@ -638,7 +681,8 @@ trd_status trd_init(const trd_config* cfg, const trd_shard* shard, const float* 
   c->zoff[N] = ztot;
   c->qoff[N] = qtot;
   const int64_t In = c->dims[N - 1];
-  const size_t chain_cap = std::max((size_t)2 * kMaxR2 * kMaxR2, (size_t)In * kMaxR2);
+  const size_t chain_cap = std::max((size_t)2 * chain_max, (size_t)(In * r2max));   // (+ D^t's T)
+  const size_t g2 = (size_t)(r2max * r2max);
   if ((st = dalloc(c, &c->Z, (size_t)ztot)) || (st = dalloc(c, &c->Q, (size_t)qtot)) ||
       (st = dalloc(c, &c->idx, idx_total)) || (st = dalloc(c, &c->doff, idx_total)) ||
       (st = dalloc(c, &c->row_off, max_rows)) || (st = dalloc(c, &c->col_off, max_cols)) ||
@@ -646,17 +690,16 @@ trd_status trd_init(const trd_config* cfg, const trd_shard* shard, const float* 
       (st = dalloc(c, &c->lfth, max_lft)) || (st = dalloc(c, &c->rgtT, max_rgt)) ||
       (st = dalloc(c, &c->dpart, max_dp)) || (st = dalloc(c, &c->spart, max_sp)) ||
       (st = dalloc(c, &c->denpart, max_sp)) || (st = dalloc(c, &c->numpart, max_h)) ||
-      (st = dalloc(c, &c->dvec, max_dvec)) || (st = dalloc(c, &c->G, (size_t)kMaxR2 * kMaxR2)) ||
-      (st = dalloc(c, &c->G_last, (size_t)kMaxR2 * kMaxR2)) ||
-      (st = dalloc(c, &c->Mop, (size_t)kMaxR2 * kMaxR2)) ||
-      (st = dalloc(c, &c->chol_ws, (size_t)2 * kMaxR2 * kMaxR2)) ||
+      (st = dalloc(c, &c->dvec, max_dvec)) || (st = dalloc(c, &c->G, g2)) ||
+      (st = dalloc(c, &c->G_last, g2)) || (st = dalloc(c, &c->Mop, g2)) ||
+      (st = dalloc(c, &c->chol_ws, 2 * g2)) ||
       (st = dalloc(c, &c->chain_ws, chain_cap)) || (st = dalloc(c, &c->h, max_h)) ||
       (st = dalloc(c, &c->Dcur, (size_t)(In * In))) || (st = dalloc(c, &c->Dprev, (size_t)(In * In))) ||
       (st = dalloc(c, &c->sc, 1)) || (st = dalloc(c, &c->red_ws, 1024)))
     return bail(st);
   if (cfg->sigma_mode == TRD_SIGMA_MAD && (st = dalloc(c, &c->mhist, (size_t)kMadHist))) return bail(st);
   if (cfg->scaling == TRD_SCALING_LOCAL &&
-      ((st = dalloc(c, &c->Qloc, (size_t)qtot)) || (st = dalloc(c, &c->Gloc, (size_t)kMaxR2 * kMaxR2))))
+      ((st = dalloc(c, &c->Qloc, (size_t)qtot)) || (st = dalloc(c, &c->Gloc, g2))))
     return bail(st);
   if (max_lhl > 0) {
     if ((st = dalloc(c, &c->lftHL, max_lhl)) || (st = dalloc(c, &c->lfthHL, max_lhl)) ||
@@ -749,8 +792,11 @@ trd_status trd_init(const trd_config* cfg, const trd_shard* shard, const float* 
   for (int k = 0; k < N; ++k) launch_q(*c, k, s);
   if ((st = check_launch(c, "init Q"))) return bail(st);
 
-  // ---- NCCL ----
-  if (cfg->world > 1) {
+  if (cfg->world > 1 &&
+      ((st = dalloc(c, &c->chk, 4)) || (st = dalloc(c, &c->chk_acc, 1))))
+    return bail(st);
+  // ---- NCCL (unless the caller supplied the exchange) ----
+  if (cfg->world > 1 && !c->ex.allreduce) {
     if (!load_nccl()) return bail(fail(c, TRD_ERR_NCCL, "libnccl.so.2 could not be loaded"));
     NcclId id;
     memcpy(id.internal, cfg->nccl_unique_id, 128);
@@ -842,6 +888,110 @@ trd_status trd_sketch(trd_ctx* ctx, int32_t sweep, int32_t k, int32_t* idx_dev, 
   return TRD_OK;
 }
 
+// One sweep of Alg. 1 (lines 3-13) enqueued on the context stream (eagerly or under capture).
+static trd_status enqueue_sweep(Context* c) {
+  cudaStream_t s = c->stream;
+  trd_status st;
+  launch_sweep_begin(*c, s);
+  for (int k = 0; k < c->N; ++k) {
+    const BlockPlan& bp = c->plan[k];
+    if ((st = block_pass1(c, bp))) return st;
+    if ((st = block_pass2(c, bp))) return st;
+    if (k == c->N - 1)
+      CUDA_TRY(c, cudaMemcpyAsync(c->G_last, c->G, (size_t)bp.R2 * bp.R2 * 8, cudaMemcpyDeviceToDevice, s));
+    launch_update(*c, bp, s);
+    launch_q(*c, k, s);
+    if ((st = check_launch(c, "update"))) return st;
+  }
+  if (c->eabs && (st = mad_select(c))) return st;         // R21 (histograms allreduced)
+  launch_sweep_end(*c, s);
+  if (c->cfg.world > 1) {                 // replica consistency of the replicated cores
+    launch_core_checksum(*c, s);
+    if ((st = allreduce(c, c->chk, 4, TRD_OP_MAX))) return st;
+    launch_replica_check(*c, s);
+  }
+  return check_launch(c, "sweep end");
+}
+
+static void destroy_graph(SweepGraph& g) {
+  if (g.exec) cudaGraphExecDestroy(g.exec);
+  if (g.graph) cudaGraphDestroy(g.graph);
+  for (cudaEvent_t e : g.cap_ev) cudaEventDestroy(e);
+  g = SweepGraph();
+}
+
+// A sweep can be replayed from a captured CUDA graph when nothing in it synchronises the host
+// (the caller-supplied exchange does) and the invariant staged sketches are current (the
+// graph then holds no staging); TRD_GRAPH=0 disables graphs.
+static bool graph_usable(const Context* c) {
+  const char* ge = getenv("TRD_GRAPH");
+  const bool off = ge && atoi(ge) == 0;
+  if (off || c->ex.allreduce) return false;
+  for (int k = 0; k < c->N; ++k)
+    if (c->plan[k].use_tc && c->stage[k].invariant && !c->stage[k].valid) return false;
+  return true;
+}
+
+static trd_status capture_sweep(Context* c, SweepGraph& g) {
+  destroy_graph(g);
+  const long long l0 = c->launches;
+  // capture on a library stream (the caller's may be the legacy default stream, which cannot
+  // be captured); the graph is launched on the caller's stream
+  if (!c->cap_stream) CUDA_TRY(c, cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking));
+  cudaStream_t user = c->stream;
+  c->stream = c->cap_stream;
+  c->capturing = &g;
+  cudaError_t e = cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeRelaxed);
+  trd_status st = e == cudaSuccess ? enqueue_sweep(c) : TRD_OK;
+  cudaGraph_t graph = nullptr;
+  if (e == cudaSuccess) e = cudaStreamEndCapture(c->stream, &graph);
+  c->capturing = nullptr;
+  c->stream = user;
+  if (st) { if (graph) cudaGraphDestroy(graph); return st; }
+  if (e != cudaSuccess) return fail(c, TRD_ERR_CUDA, "sweep capture: %s", cudaGetErrorString(e));
+  g.graph = graph;
+  CUDA_TRY(c, cudaGraphInstantiate(&g.exec, graph, 0));
+  g.launches = c->launches - l0;
+  c->launches = l0;
+  // the event-record nodes of the profiling events, in capture order
+  size_t nn = 0;
+  CUDA_TRY(c, cudaGraphGetNodes(graph, nullptr, &nn));
+  std::vector<cudaGraphNode_t> nodes(nn);
+  CUDA_TRY(c, cudaGraphGetNodes(graph, nodes.data(), &nn));
+  g.ev_nodes.assign(g.cap_ev.size(), nullptr);
+  for (cudaGraphNode_t nd : nodes) {
+    cudaGraphNodeType ty;
+    CUDA_TRY(c, cudaGraphNodeGetType(nd, &ty));
+    if (ty != cudaGraphNodeTypeEventRecord) continue;
+    cudaEvent_t ev;
+    CUDA_TRY(c, cudaGraphEventRecordNodeGetEvent(nd, &ev));
+    for (size_t i = 0; i < g.cap_ev.size(); ++i)
+      if (g.cap_ev[i] == ev) g.ev_nodes[i] = nd;
+  }
+  for (cudaGraphNode_t nd : g.ev_nodes)
+    if (!nd) return fail(c, TRD_ERR_CUDA, "sweep capture: profiling event node not found");
+  g.stats_ptr = c->stats;
+  return TRD_OK;
+}
+
+// replay: point the profiling events of this launch at fresh pool events, then launch
+static trd_status launch_graph(Context* c, SweepGraph& g) {
+  if (c->prof) {
+    std::vector<int> map(g.cap_ev.size());
+    for (size_t i = 0; i < g.cap_ev.size(); ++i) {
+      const int idx = prof_event_slot(c);
+      if (idx < 0) return fail(c, TRD_ERR_CUDA, "profiling event");
+      map[i] = idx;
+      CUDA_TRY(c, cudaGraphExecEventRecordNodeSetEvent(g.exec, g.ev_nodes[i], c->ev_pool[(size_t)idx]));
+    }
+    for (auto& pr : g.pairs1) c->ev_pass1.push_back({map[(size_t)pr.first], map[(size_t)pr.second]});
+    for (auto& pr : g.pairs2) c->ev_pass2.push_back({map[(size_t)pr.first], map[(size_t)pr.second]});
+  }
+  CUDA_TRY(c, cudaGraphLaunch(g.exec, c->stream));
+  c->launches += g.launches;
+  return TRD_OK;
+}
+
 trd_status trd_sweep(trd_ctx* ctx, int32_t n_sweeps, trd_sweep_stats* stats) {
   Context* c = reinterpret_cast<Context*>(ctx);
   if (!c || n_sweeps < 0) return TRD_ERR_INVALID_ARG;
@@ -851,6 +1001,7 @@ trd_status trd_sweep(trd_ctx* ctx, int32_t n_sweeps, trd_sweep_stats* stats) {
   if (st) return st;
   if ((st = consume_upload(c))) return st;
   cudaStream_t s = c->stream;
+  CUDA_TRY(c, cudaMemsetAsync(&c->sc->slot_next, 0, sizeof(int), s));
   std::vector<cudaEvent_t> ev;
   if (stats) {
     ev.resize((size_t)n_sweeps + 1);
@@ -858,20 +1009,15 @@ trd_status trd_sweep(trd_ctx* ctx, int32_t n_sweeps, trd_sweep_stats* stats) {
     CUDA_TRY(c, cudaEventRecord(ev[0], s));
   }
   for (int t = 0; t < n_sweeps; ++t) {
-    launch_sweep_begin(*c, t, s);
-    for (int k = 0; k < c->N; ++k) {
-      const BlockPlan& bp = c->plan[k];
-      if ((st = block_pass1(c, bp))) return st;
-      if ((st = block_pass2(c, bp))) return st;
-      if (k == c->N - 1)
-        CUDA_TRY(c, cudaMemcpyAsync(c->G_last, c->G, (size_t)bp.R2 * bp.R2 * 8, cudaMemcpyDeviceToDevice, s));
-      launch_update(*c, bp, t, s);
-      launch_q(*c, k, s);
-      if ((st = check_launch(c, "update"))) return st;
+    if (graph_usable(c)) {
+      SweepGraph& g = c->graphs[c->up_active];
+      if (!g.exec || g.stats_ptr != c->stats) {
+        if ((st = capture_sweep(c, g))) return st;
+      }
+      if ((st = launch_graph(c, g))) return st;
+    } else {
+      if ((st = enqueue_sweep(c))) return st;
     }
-    if (c->eabs && (st = mad_select(c))) return st;         // R21 (histograms allreduced)
-    launch_sweep_end(*c, t, s);
-    if ((st = check_launch(c, "sweep end"))) return st;
     if (stats) CUDA_TRY(c, cudaEventRecord(ev[(size_t)t + 1], s));
   }
   if (!stats) return TRD_OK;
@@ -889,6 +1035,7 @@ trd_status trd_sweep(trd_ctx* ctx, int32_t n_sweeps, trd_sweep_stats* stats) {
     o.n_obs = d.n_obs;
     for (int k = 0; k < c->N; ++k) { o.eta[k] = d.eta[k]; o.num[k] = d.num[k]; o.den[k] = d.den[k]; o.nnz[k] = d.nnz[k]; }
     o.skipped_mask = d.skipped;
+    o.replica_mismatch = d.replica_mismatch;
     float ms = 0.f;
     cudaEventElapsedTime(&ms, ev[(size_t)t], ev[(size_t)t + 1]);
     o.ms = ms;
@@ -897,6 +1044,7 @@ trd_status trd_sweep(trd_ctx* ctx, int32_t n_sweeps, trd_sweep_stats* stats) {
   for (auto& e : ev) cudaEventDestroy(e);
   if (sc.not_spd) return fail(c, TRD_ERR_NOT_SPD, "G + lambda I not positive definite after retries");
   if (nonfinite || sc.nonfinite) return fail(c, TRD_ERR_NONFINITE, "non-finite step or statistics");
+  if (sc.replica_bad) return fail(c, TRD_ERR_STATE, "replicas diverged: the ranks' cores differ");
   return TRD_OK;
 }
 
@@ -914,6 +1062,7 @@ trd_status trd_block_probe(trd_ctx* ctx, int32_t sweep, int32_t k, double* d_hos
   CUDA_TRY(c, cudaStreamSynchronize(s));
   CUDA_TRY(c, cudaMemcpyAsync(&c->sc->sweep, &sweep, 4, cudaMemcpyHostToDevice, s));
   if (c->eabs) CUDA_TRY(c, cudaMemsetAsync(&c->sc->eabs_fill, 0, sizeof(unsigned long long), s));
+  CUDA_TRY(c, cudaMemsetAsync(&c->sc->slot, 0, sizeof(int), s));
   trd_status st;
   if ((st = block_pass1(c, bp))) return st;
   if ((st = block_pass2(c, bp))) return st;
@@ -964,7 +1113,7 @@ trd_status trd_error(trd_ctx* ctx, const float* ref_dev, const uint32_t* eval_bi
   double v[6];
   if (c->cfg.world > 1) {
     if ((st = allreduce(c, c->red_ws, 5))) return st;                 // sums
-    if ((st = allreduce(c, c->red_ws + 5, 1, kNcclMax))) return st;   // max |ref|
+    if ((st = allreduce(c, c->red_ws + 5, 1, TRD_OP_MAX))) return st;   // max |ref|
   }
   CUDA_TRY(c, cudaMemcpyAsync(v, c->red_ws, sizeof(v), cudaMemcpyDeviceToHost, s));
   CUDA_TRY(c, cudaStreamSynchronize(s));
@@ -1023,6 +1172,8 @@ void trd_destroy(trd_ctx* ctx) {
   Context* c = reinterpret_cast<Context*>(ctx);
   if (!c) return;
   if (c->stream) cudaStreamSynchronize(c->stream);
+  for (auto& g : c->graphs) destroy_graph(g);
+  if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
   if (c->nccl_comm && g_nccl.comm_destroy) g_nccl.comm_destroy(c->nccl_comm);
   for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
   if (c->side) { cudaStreamSynchronize(c->side); cudaStreamDestroy(c->side); }
@@ -1046,7 +1197,7 @@ void trd_destroy(trd_ctx* ctx) {
                   c->denpart, c->numpart, c->dvec, c->G, c->G_last, c->Mop, c->chol_ws,
                   c->chain_ws, c->h, c->Dcur, c->Dprev, c->sc, c->stats, c->red_ws,
                   c->lftHL, c->lfthHL, c->lscl, c->lsclh, c->rgtHL, c->rgtHL2, c->contrib, c->Qloc, c->Gloc, c->mhist,
-                  c->eabs};
+                  c->eabs, c->chk, c->chk_acc};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->tw) cudaFree(c->tw);

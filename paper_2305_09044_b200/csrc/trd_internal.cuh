@@ -23,6 +23,7 @@ struct DevStats {
   long long nnz[kMaxN];
   unsigned int skipped;
   int nonfinite;
+  unsigned int replica_mismatch;   // world > 1: the ranks' core checksums differed
 };
 
 // Scalars shared by the kernels of one block (device memory).
@@ -53,9 +54,12 @@ struct DevScalars {
   double n_obs;          // observed entries of the block (double so it rides the allreduce)
   double eta;            // step of the current block
   double lambda;         // lambda used by the solve
+  double h_lam;          // h = u - h_lam u Mop, u = d Mop (lambda when Mop = (G + lambda I)^-1)
   int sweep;             // sweep counter t (read by the sampler: graph-replayable)
+  int slot, slot_next;   // record slot of the current sweep in the DevStats array of the call
   int not_spd;           // Cholesky failed after retries
   int nonfinite;         // non-finite value detected
+  int replica_bad;       // world > 1: a sweep ended with differing replicas
   double acc_e2, acc_n;  // sweep accumulators for the RMS sigma rule (R9)
   double stop_e;         // relative change of D^t
   int have_prev_D;
@@ -131,6 +135,17 @@ struct TcStage {
   bool valid = false;            // staged data current
 };
 
+// One sweep captured as a CUDA graph (trd_sweep replays it; one per upload buffer set)
+struct SweepGraph {
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  long long launches = 0;              // kernels per replay (launch counter)
+  const void* stats_ptr = nullptr;     // the stats array the graph writes
+  std::vector<cudaEvent_t> cap_ev;     // profiling events recorded during the capture
+  std::vector<cudaGraphNode_t> ev_nodes;   // their event-record nodes (same order)
+  std::vector<std::pair<int, int>> pairs1, pairs2;   // pass-1 / pass-2 (begin, end) in cap_ev
+};
+
 struct Context {
   trd_config cfg;
   int N;
@@ -145,6 +160,8 @@ struct Context {
                                        // concurrently with pass 1 (they need only cores != k)
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   int num_sm = 148;                    // SMs of the current device (persistent grids)
+  int rbucket = 16;                    // 16 or 32: >= every rank (register arrays of the plan kernels)
+  size_t chain_half = 0;               // doubles per FGMC chain buffer (chain_ws holds two)
   std::string err;
   trd_status sticky = TRD_OK;
   long long launches = 0;
@@ -219,14 +236,22 @@ struct Context {
   double* red_ws = nullptr;            // small reductions
   size_t max_dpart = 0, max_spart = 0;
 
-  // NCCL (world > 1)
+  // data-parallel exchange (world > 1): NCCL, or a caller-supplied allreduce (trd_init_ex)
   void* nccl_comm = nullptr;
+  trd_exchange ex = {nullptr, nullptr};
+  double* chk = nullptr;               // replica check: [h_lo, h_hi, -h_lo, -h_hi] of the cores
+  unsigned long long* chk_acc = nullptr;
 
   // profiling (trd_set_profiling / trd_get_profile)
   bool prof = false;
   std::vector<cudaEvent_t> ev_pool;
   std::vector<std::pair<int, int>> ev_pass1, ev_pass2;   // indices into ev_pool
   size_t ev_used = 0;
+
+  // CUDA graphs of one sweep (world 1 or NCCL): per upload buffer set
+  SweepGraph graphs[2];
+  SweepGraph* capturing = nullptr;     // set while a sweep is being captured
+  cudaStream_t cap_stream = nullptr;   // capture stream (the caller's may be the legacy stream)
 };
 
 // ---- kernels (trd_kernels.cu) --------------------------------------------------------
@@ -245,8 +270,10 @@ void launch_identity_op(Context& c, const BlockPlan& bp, cudaStream_t s);
 void launch_h(Context& c, const BlockPlan& bp, cudaStream_t s);
 void launch_pass2(Context& c, const BlockPlan& bp, cudaStream_t s);
 void launch_reduce_den(Context& c, const BlockPlan& bp, cudaStream_t s);
-void launch_update(Context& c, const BlockPlan& bp, int sweep_slot, cudaStream_t s);
-void launch_sweep_end(Context& c, int sweep_slot, cudaStream_t s);
+void launch_update(Context& c, const BlockPlan& bp, cudaStream_t s);
+void launch_sweep_end(Context& c, cudaStream_t s);
+void launch_core_checksum(Context& c, cudaStream_t s);   // -> c.chk (world > 1)
+void launch_replica_check(Context& c, cudaStream_t s);
 void launch_sigma0(Context& c, cudaStream_t s);
 void launch_eabs_advance(Context& c, const TcStage& st, cudaStream_t s);
 void launch_mad_hist(Context& c, int level, cudaStream_t s);   // R21 select, level 0..2
@@ -257,10 +284,7 @@ void launch_error(Context& c, const float* ref, const uint32_t* eval_bits, doubl
 void launch_rank_prefix(Context& c, cudaStream_t s);
 void launch_count_bits(Context& c, unsigned long long* out, cudaStream_t s);
 void launch_amax_obs(Context& c, cudaStream_t s);   // sc->amax_x of the observed values
-void launch_reset_block_scalars(Context& c, cudaStream_t s);
-void launch_record_block(Context& c, const BlockPlan& bp, int slot, cudaStream_t s);
-void launch_sweep_begin(Context& c, int slot, cudaStream_t s);
-void launch_fill_full_sets(Context& c, const BlockPlan& bp, cudaStream_t s);
+void launch_sweep_begin(Context& c, cudaStream_t s);
 
 // ---- tensor-core pass kernels (trd_tc.cu) ---------------------------------------------
 bool tc_supported_kp(int KP);

@@ -49,6 +49,7 @@ struct SamplerArgs {
 };
 
 constexpr int kSamplerThreads = 256;
+constexpr int kSamplerSmall = 1024;      // index sets up to this size: comparison ranks
 __device__ __forceinline__ unsigned long long sample_key(uint64_t seed, int64_t i, int m, int k, uint32_t t) {
   uint32_t c[4] = {(uint32_t)i, (uint32_t)m, (uint32_t)k, t};
   philox10(c, (uint32_t)(seed & 0xffffffffu), (uint32_t)(seed >> 32));
@@ -78,6 +79,34 @@ sampler_kernel(SamplerArgs sa, const DevScalars* __restrict__ sc, int32_t* __res
     for (int64_t q = tid; q < s; q += blockDim.x) out[q] = (int32_t)(sa.shard_begin + q);
   } else if (s_draw >= I && !compact) {
     for (int64_t i = tid; i < I; i += blockDim.x) out[i] = (int32_t)i;
+  } else if (I <= kSamplerSmall) {
+    // small sets: keys in shared memory, rank of each key by counting (ties broken by i)
+    __shared__ unsigned long long keys[kSamplerSmall];
+    __shared__ unsigned char sel[kSamplerSmall];
+    for (int64_t i = tid; i < I; i += blockDim.x) keys[i] = sample_key(seed, i, m, k, t);
+    __syncthreads();
+    for (int64_t i = tid; i < I; i += blockDim.x) {
+      const unsigned long long ki = keys[i];
+      int64_t rank = 0;
+      for (int64_t j = 0; j < I; ++j) {
+        const unsigned long long kj = keys[j];
+        rank += (kj < ki) || (kj == ki && j < i);
+      }
+      sel[i] = rank < s_draw && (!compact || (i >= sa.shard_begin && i < sa.shard_end));
+    }
+    __syncthreads();
+    long long n_out = 0;
+    for (int64_t c0 = 0; c0 < I; c0 += blockDim.x) {       // ascending compaction
+      const int64_t i = c0 + tid;
+      const bool put = i < I && sel[i];
+      long long pos, put_tot;
+      Scan(scan_tmp).ExclusiveSum(put ? 1ll : 0ll, pos, put_tot);
+      __syncthreads();
+      if (put) out[n_out + pos] = (int32_t)i;
+      n_out += put_tot;
+    }
+    n_local = compact ? n_out : s;
+    for (int64_t q = n_local + tid; q < s; q += blockDim.x) out[q] = (int32_t)sa.shard_begin;   // padding
   } else {
     // radix select of the key of rank s_draw - 1
     unsigned long long prefix = 0ull, pmask = 0ull;
@@ -272,23 +301,26 @@ __global__ void offsets_kernel(PlanArgs a, const int64_t* __restrict__ doff,
   }
 }
 
-// v (row vector, length r_in) <- v * Z_m(i)  (r_in x r_out slice)
+// v (row vector, length r_in) <- v * Z_m(i)  (r_in x r_out slice); RM = the rank bucket
+// (16 or 32, >= every rank of the context: register arrays of compile-time size)
+template <int RM>
 __device__ __forceinline__ void vecmat(float* v, const float* __restrict__ Zs, int rin, int rout) {
-  float nv[kMaxR];
+  float nv[RM];
 #pragma unroll
-  for (int c = 0; c < kMaxR; ++c) nv[c] = 0.f;
+  for (int c = 0; c < RM; ++c) nv[c] = 0.f;
   for (int a = 0; a < rin; ++a) {
     const float va = v[a];
     const float* row = Zs + a * rout;
 #pragma unroll
-    for (int c = 0; c < kMaxR; ++c)
+    for (int c = 0; c < RM; ++c)
       if (c < rout) nv[c] = fmaf(va, __ldg(row + c), nv[c]);
   }
 #pragma unroll
-  for (int c = 0; c < kMaxR; ++c) v[c] = nv[c];
+  for (int c = 0; c < RM; ++c) v[c] = nv[c];
 }
 
 // Mid(j_L)[b][c] = (Z_{k+1}(.) .. Z_{k+p}(.))[b][c]   (r_{k+1} x r_s), one thread per (jl, b)
+template <int RM>
 __global__ void mid_kernel(PlanArgs a, const int32_t* __restrict__ idx, const float* __restrict__ Z,
                            float* __restrict__ mid) {
   const int64_t tot = a.nL * a.rk1;
@@ -298,15 +330,15 @@ __global__ void mid_kernel(PlanArgs a, const int32_t* __restrict__ idx, const fl
     int64_t jl = t / a.rk1;
     int64_t dq[kMaxN];
     left_digits(a, jl, dq);
-    float v[kMaxR];
+    float v[RM];
 #pragma unroll
-    for (int c = 0; c < kMaxR; ++c) v[c] = (c == b) ? 1.f : 0.f;
+    for (int c = 0; c < RM; ++c) v[c] = (c == b) ? 1.f : 0.f;
     int rin = a.rk1;
     for (int q = 0; q < a.nleft; ++q) {
       int m = a.left[q];
       int64_t i = idx[a.offL[q] + dq[q]];
       int rout = a.rank_of[m + 1];
-      vecmat(v, Z + a.zoff[m] + i * (int64_t)a.rank_of[m] * rout, rin, rout);
+      vecmat<RM>(v, Z + a.zoff[m] + i * (int64_t)a.rank_of[m] * rout, rin, rout);
       rin = rout;
     }
     float* o = mid + (jl * a.rk1 + b) * a.rs;
@@ -330,6 +362,7 @@ __device__ __forceinline__ void block_amax(float v, unsigned int* dst) {
   }
 }
 
+template <int RM>
 __global__ void rgt_kernel(PlanArgs a, const int32_t* __restrict__ idx, const float* __restrict__ Z,
                            float* __restrict__ rgtT, DevScalars* __restrict__ sc) {
   float amax = 0.f;
@@ -340,15 +373,15 @@ __global__ void rgt_kernel(PlanArgs a, const int32_t* __restrict__ idx, const fl
     int cc = (int)(t % a.rs);
     int64_t dq[kMaxN];
     right_digits(a, col, dq);
-    float v[kMaxR];
+    float v[RM];
 #pragma unroll
-    for (int c = 0; c < kMaxR; ++c) v[c] = (c == cc) ? 1.f : 0.f;
+    for (int c = 0; c < RM; ++c) v[c] = (c == cc) ? 1.f : 0.f;
     int rin = a.rs;
     for (int q = 0; q < a.nright; ++q) {
       int m = a.right[q];
       int64_t i = idx[a.offR[q] + dq[q]];
       int rout = a.rank_of[m + 1];
-      vecmat(v, Z + a.zoff[m] + i * (int64_t)a.rank_of[m] * rout, rin, rout);
+      vecmat<RM>(v, Z + a.zoff[m] + i * (int64_t)a.rank_of[m] * rout, rin, rout);
       rin = rout;
     }
     for (int aa = 0; aa < a.rk; ++aa) {
@@ -361,6 +394,7 @@ __global__ void rgt_kernel(PlanArgs a, const int32_t* __restrict__ idx, const fl
 
 // Lft(row)[a + r_k c] = (X_k(i_k) Mid(j_L))[a][c] where X_k is the core slice (pass 1) or
 // the folded scaled gradient H(i_k)[a][b] = h[i_k][a + r_k b] (pass 2).  Thread per (row, a).
+template <int RM>
 __global__ void lft_kernel(PlanArgs a, const float* __restrict__ Zk, const double* __restrict__ h,
                            const float* __restrict__ mid, float* __restrict__ lft) {
   const int64_t tot = a.nrows * a.rk;
@@ -370,9 +404,9 @@ __global__ void lft_kernel(PlanArgs a, const float* __restrict__ Zk, const doubl
     int64_t row = t / a.rk;
     int64_t jl, ik;
     row_split(a, row, ik, jl);
-    float v[kMaxR];
+    float v[RM];
 #pragma unroll
-    for (int b = 0; b < kMaxR; ++b) {
+    for (int b = 0; b < RM; ++b) {
       if (b < a.rk1) {
         v[b] = h ? (float)h[(a.ik0 + ik) * a.rk * a.rk1 + aa + a.rk * b]
                  : __ldg(Zk + ((a.ik0 + ik) * a.rk + aa) * a.rk1 + b);
@@ -384,7 +418,7 @@ __global__ void lft_kernel(PlanArgs a, const float* __restrict__ Zk, const doubl
     if (a.p == 0) {
       for (int c = 0; c < a.rk1; ++c) o[aa + a.rk * c] = v[c];
     } else {
-      vecmat(v, mid + jl * a.rk1 * a.rs, a.rk1, a.rs);
+      vecmat<RM>(v, mid + jl * a.rk1 * a.rs, a.rk1, a.rs);
       for (int c = 0; c < a.rs; ++c) o[aa + a.rk * c] = v[c];
     }
   }
@@ -446,13 +480,14 @@ __device__ __forceinline__ bool load_entry(const PassArgs& a, int64_t ro, int64_
 constexpr int kPassThreads = 256;
 constexpr int kPassWarps = kPassThreads / 32;
 
-template <int KT, bool PASS2, bool STATS_ONLY>
+template <int KT, int R2M, bool PASS2, bool STATS_ONLY>
 __global__ void __launch_bounds__(kPassThreads)
 pass_kernel(PassArgs a) {
   __shared__ float lftS[kPassWarps][KT];
   __shared__ float lfhS[kPassWarps][PASS2 ? KT : 1];
   __shared__ float dS[kPassWarps][KT];
-  __shared__ double redS[kPassWarps][kMaxR2 + 3];
+  constexpr int RCH = 256;                 // R^2 chunk of the CTA reduction
+  __shared__ double redS[kPassWarps][RCH + 3];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t ik = blockIdx.y;
   const int64_t jl0 = (int64_t)blockIdx.x * a.jl_per_cta;
@@ -469,7 +504,7 @@ pass_kernel(PassArgs a) {
   const double s2 = sigma * sigma;
 
   double st_e2 = 0.0, st_w = 0.0, st_n = 0.0, st_den = 0.0;
-  constexpr int OUTS = kMaxR2 / 32;
+  constexpr int OUTS = R2M / 32;
   double outacc[OUTS];
 #pragma unroll
   for (int q = 0; q < OUTS; ++q) outacc[q] = 0.0;
@@ -578,27 +613,32 @@ pass_kernel(PassArgs a) {
   }
   {
     double v0 = warp_sum_d(st_e2), v1 = warp_sum_d(st_w), v2 = warp_sum_d(st_n);
-    if (lane == 0) { redS[warp][kMaxR2] = v0; redS[warp][kMaxR2 + 1] = v1; redS[warp][kMaxR2 + 2] = v2; }
-  }
-  if (!STATS_ONLY) {
-#pragma unroll
-    for (int q = 0; q < OUTS; ++q) {
-      const int o = lane + 32 * q;
-      if (o < a.R2) redS[warp][o] = outacc[q];
-    }
+    if (lane == 0) { redS[warp][RCH] = v0; redS[warp][RCH + 1] = v1; redS[warp][RCH + 2] = v2; }
   }
   __syncthreads();
-  if (!STATS_ONLY) {
-    for (int o = threadIdx.x; o < a.R2; o += blockDim.x) {
-      double tot = 0.0;
-      for (int w = 0; w < kPassWarps; ++w) tot += redS[w][o];
-      a.dpart[(ik * ncta + cta) * a.R2 + o] = tot;
-    }
-  }
   if (threadIdx.x < 3) {
     double tot = 0.0;
-    for (int w = 0; w < kPassWarps; ++w) tot += redS[w][kMaxR2 + threadIdx.x];
+    for (int w = 0; w < kPassWarps; ++w) tot += redS[w][RCH + threadIdx.x];
     a.spart[(ik * ncta + cta) * 3 + threadIdx.x] = tot;
+  }
+  if (!STATS_ONLY) {
+    // d partials over the warps in chunks of RCH columns (fixed order)
+#pragma unroll
+    for (int c0 = 0; c0 < R2M; c0 += RCH) {
+      if (c0 >= a.R2) break;
+#pragma unroll
+      for (int q = c0 / 32; q < (c0 + RCH) / 32 && q < OUTS; ++q) {
+        const int o = lane + 32 * q;
+        if (o < a.R2) redS[warp][o - c0] = outacc[q];
+      }
+      __syncthreads();
+      for (int o = c0 + threadIdx.x; o < min(a.R2, c0 + RCH); o += blockDim.x) {
+        double tot = 0.0;
+        for (int w = 0; w < kPassWarps; ++w) tot += redS[w][o - c0];
+        a.dpart[(ik * ncta + cta) * a.R2 + o] = tot;
+      }
+      __syncthreads();
+    }
   }
 }
 
@@ -625,10 +665,17 @@ template <bool PASS2, bool STATS_ONLY>
 static void launch_pass_t(Context& c, const BlockPlan& bp, cudaStream_t s) {
   PassArgs a = make_pass_args(c, bp);
   dim3 grid((unsigned)bp.grid_x, (unsigned)(bp.nrows / bp.nL), (unsigned)bp.nsplit);
-  if (bp.K <= 32) pass_kernel<32, PASS2, STATS_ONLY><<<grid, kPassThreads, 0, s>>>(a);
-  else if (bp.K <= 64) pass_kernel<64, PASS2, STATS_ONLY><<<grid, kPassThreads, 0, s>>>(a);
-  else if (bp.K <= 128) pass_kernel<128, PASS2, STATS_ONLY><<<grid, kPassThreads, 0, s>>>(a);
-  else pass_kernel<256, PASS2, STATS_ONLY><<<grid, kPassThreads, 0, s>>>(a);
+  // (K <= 256 and R^2 <= 1024 are checked at trd_init)
+  if (bp.R2 <= 256) {
+    if (bp.K <= 32) pass_kernel<32, 256, PASS2, STATS_ONLY><<<grid, kPassThreads, 0, s>>>(a);
+    else if (bp.K <= 64) pass_kernel<64, 256, PASS2, STATS_ONLY><<<grid, kPassThreads, 0, s>>>(a);
+    else if (bp.K <= 128) pass_kernel<128, 256, PASS2, STATS_ONLY><<<grid, kPassThreads, 0, s>>>(a);
+    else pass_kernel<256, 256, PASS2, STATS_ONLY><<<grid, kPassThreads, 0, s>>>(a);
+  } else {
+    if (bp.K <= 64) pass_kernel<64, 1024, PASS2, STATS_ONLY><<<grid, kPassThreads, 0, s>>>(a);
+    else if (bp.K <= 128) pass_kernel<128, 1024, PASS2, STATS_ONLY><<<grid, kPassThreads, 0, s>>>(a);
+    else pass_kernel<256, 1024, PASS2, STATS_ONLY><<<grid, kPassThreads, 0, s>>>(a);
+  }
   c.launches++;
 }
 
@@ -685,17 +732,21 @@ __global__ void reduce_den_kernel(const double* __restrict__ denpart, int64_t n,
 // ----------------------------------------------------------------------------------------
 // FGMC (Eq. 13; reading R6).  Q_k[(a r + a'), (b r' + b')] = sum_i Z(i)[a][b] Z(i)[a'][b']
 // ----------------------------------------------------------------------------------------
+// one warp per entry of Q_k: lane l sums the slices i = l, l + 32, .. in order, then a fixed
+// butterfly over the lanes (deterministic; Z_k stays in L1 / L2)
 __global__ void q_kernel(const float* __restrict__ Zk, int64_t Ik, int r0, int r1, double* __restrict__ Qk) {
-  const int n0 = r0 * r0, n1 = r1 * r1;
-  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n0 * n1; t += gridDim.x * blockDim.x) {
-    const int row = t / n1, col = t % n1;
+  const int n0 = r0 * r0, n1 = r1 * r1, lane = threadIdx.x & 31;
+  const int64_t stride = (int64_t)r0 * r1;
+  for (int64_t t = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; t < (int64_t)n0 * n1;
+       t += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int row = (int)(t / n1), col = (int)(t % n1);
     const int a = row / r0, ap = row % r0, b = col / r1, bp = col % r1;
+    const float* P = Zk + a * r1 + b;
+    const float* R = Zk + ap * r1 + bp;
     double acc = 0.0;
-    for (int64_t i = 0; i < Ik; ++i) {
-      const float* S = Zk + i * r0 * r1;
-      acc += (double)S[a * r1 + b] * (double)S[ap * r1 + bp];
-    }
-    Qk[t] = acc;
+    for (int64_t i = lane; i < Ik; i += 32) acc += (double)__ldg(P + i * stride) * (double)__ldg(R + i * stride);
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) Qk[t] = acc;
   }
 }
 
@@ -817,7 +868,7 @@ solve_kernel(const double* __restrict__ G, int n, double lambda_rel, double* __r
     __syncthreads();
   }
   if (fail_s) {
-    if (threadIdx.x == 0) { sc->not_spd = 1; sc->lambda = lam; }
+    if (threadIdx.x == 0) { sc->not_spd = 1; sc->lambda = lam; sc->h_lam = 0.0; }
     for (int t = threadIdx.x; t < n * n; t += blockDim.x) Mout[t] = 0.0;
     return;
   }
@@ -838,7 +889,7 @@ solve_kernel(const double* __restrict__ G, int n, double lambda_rel, double* __r
   chol_solve_inplace(L, B, n);              // B = A^-1 (A^-1 G)^T = A^-1 G A^-1
   __syncthreads();
   for (int t = threadIdx.x; t < n * n; t += blockDim.x) Mout[t] = B[t];
-  if (threadIdx.x == 0) sc->lambda = lam;
+  if (threadIdx.x == 0) { sc->lambda = lam; sc->h_lam = 0.0; }
 }
 
 // Small-n path of a9 (R_k^2 <= kGjMaxN): the same filtered operator M = A^-1 G A^-1 with
@@ -907,7 +958,7 @@ __global__ void __launch_bounds__(1024) gj_solve_kernel(const double* __restrict
     __syncthreads();
   }
   if (fail_s) {
-    if (threadIdx.x == 0) { sc->not_spd = 1; sc->lambda = lam; }
+    if (threadIdx.x == 0) { sc->not_spd = 1; sc->lambda = lam; sc->h_lam = 0.0; }
     for (int t = threadIdx.x; t < n * n; t += blockDim.x) Mout[t] = 0.0;
     return;
   }
@@ -952,23 +1003,126 @@ __global__ void __launch_bounds__(1024) gj_solve_kernel(const double* __restrict
         if (i < n && j < n) Mout[i * n + j] = fma(-lam, acc[u][v], Ainv[i * n + j]);
       }
   }
-  if (threadIdx.x == 0) sc->lambda = lam;
+  if (threadIdx.x == 0) { sc->lambda = lam; sc->h_lam = 0.0; }
 }
 
-// h = d M (row-wise), num partial per row = <d(i), h(i)>
+// Register Gauss-Jordan inverse for R^2 <= 128 (the a9 solve of the configs' blocks): X = A^-1,
+// A = G + lambda I, two threads per row, each holding NP/2 columns of its row in registers for
+// the whole elimination (NP = R^2 padded to a multiple of 16 with an identity block).  Step k:
+// the owners of row k publish it to a double-buffered shared row, every thread updates
+// a_ij -= (a_ik / p) a_kj over its columns (independent FMAs), the pivot row and column get
+// their Gauss-Jordan values; one barrier per step.  A is SPD, so no pivoting; a non-positive
+// pivot means "not SPD" and triggers the lambda retry of R23.  The filtered operator
+// M = A^-1 G A^-1 = X - lambda X^2 (G = A - lambda I) is applied in h_kernel as
+// h = d X - lambda (d X) X, so no X^2 product sits on this (side-stream) chain.
+template <int NP>
+__global__ void __launch_bounds__(256) gj2_solve_kernel(const double* __restrict__ G, int n, double lambda_rel,
+                                                        double* __restrict__ Xout, DevScalars* __restrict__ sc) {
+  constexpr int HC = NP / 2;
+  static_assert(2 * NP <= 256 && NP % 16 == 0, "two threads per row");
+  __shared__ __align__(16) double rowk[2][NP];
+  __shared__ int fail_s;
+  __shared__ double tr_s;
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int row = tid >> 1, half = tid & 1;
+  const bool act = row < NP;
+  if (tid == 0) {
+    double tr = 0.0;
+    for (int i = 0; i < n; ++i) tr += G[i * n + i];
+    tr_s = tr;
+  }
+  __syncthreads();
+  double lam = lambda_rel * tr_s / n;
+  double a[HC];
+  for (int attempt = 0;; ++attempt) {
+#pragma unroll
+    for (int j = 0; j < HC; ++j) {
+      const int col = half * HC + j;
+      a[j] = (act && row < n && col < n) ? G[row * n + col] + (row == col ? lam : 0.0) : (row == col ? 1.0 : 0.0);
+    }
+    if (tid == 0) fail_s = 0;
+    if (row == 0) {
+#pragma unroll
+      for (int j = 0; j < HC; ++j) rowk[0][half * HC + j] = a[j];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < NP; ++k) {
+      const int b = k & 1;
+      const double p = rowk[b][k];
+      if (!(p > 0.0)) {                      // (uniform: every thread reads the same pivot)
+        if (tid == 0) fail_s = 1;
+        break;
+      }
+      const double ip = 1.0 / p;
+      constexpr int dummy = 0;
+      (void)dummy;
+      const int kh = k / HC, kl = k % HC;    // compile-time after unrolling
+      const double aik = __shfl_sync(0xffffffffu, a[kl], (lane & ~1) | kh);
+      if (row == k) {
+#pragma unroll
+        for (int j = 0; j < HC; ++j) a[j] *= ip;
+        if (half == kh) a[kl] = ip;
+      } else {
+        const double f = aik * ip;
+#pragma unroll
+        for (int j = 0; j < HC; ++j) a[j] = fma(-f, rowk[b][half * HC + j], a[j]);
+        if (half == kh) a[kl] = -f;
+      }
+      if (k + 1 < NP && row == k + 1) {
+#pragma unroll
+        for (int j = 0; j < HC; ++j) rowk[b ^ 1][half * HC + j] = a[j];
+      }
+      __syncthreads();
+    }
+    __syncthreads();
+    if (!fail_s || attempt >= 3) break;
+    lam = lam > 0.0 ? 10.0 * lam : ldexp(tr_s / n, -40);   // R23 retry rule
+    __syncthreads();
+  }
+  if (fail_s) {
+    if (tid == 0) { sc->not_spd = 1; sc->lambda = lam; sc->h_lam = 0.0; }
+    for (int t = tid; t < n * n; t += blockDim.x) Xout[t] = 0.0;
+    return;
+  }
+  if (act && row < n) {
+#pragma unroll
+    for (int j = 0; j < HC; ++j) {
+      const int col = half * HC + j;
+      if (col < n) Xout[row * n + col] = a[j];
+    }
+  }
+  if (tid == 0) { sc->lambda = lam; sc->h_lam = lam; }
+}
+
+// h = d M (row-wise) with M = Mop - h_lam Mop^2 (h_lam = lambda when Mop = (G + lambda I)^-1 from
+// gj2_solve_kernel, 0 when Mop is M itself), computed as u = d Mop, h = u - h_lam u Mop;
+// num partial per row = <d(i), h(i)>
 __global__ void h_kernel(const double* __restrict__ dvec, const double* __restrict__ M, int R2,
-                         double* __restrict__ h, double* __restrict__ numpart) {
+                         double* __restrict__ h, double* __restrict__ numpart, const DevScalars* __restrict__ sc) {
   __shared__ double drow[kMaxR2];
+  __shared__ double urow[kMaxR2];
   __shared__ double red[256];
   const int64_t ik = blockIdx.x;
+  const double hl = sc->h_lam;
   for (int o = threadIdx.x; o < R2; o += blockDim.x) drow[o] = dvec[ik * R2 + o];
   __syncthreads();
-  double part = 0.0;
   for (int o = threadIdx.x; o < R2; o += blockDim.x) {
     double acc = 0.0;
     for (int q = 0; q < R2; ++q) acc = fma(drow[q], M[q * R2 + o], acc);
-    h[ik * R2 + o] = acc;
-    part += acc * drow[o];
+    urow[o] = acc;
+  }
+  __syncthreads();
+  double part = 0.0;
+  for (int o = threadIdx.x; o < R2; o += blockDim.x) {
+    double v = urow[o];
+    if (hl != 0.0) {
+      double acc = 0.0;
+      for (int q = 0; q < R2; ++q) acc = fma(urow[q], M[q * R2 + o], acc);
+      v = fma(-hl, acc, v);
+    }
+    h[ik * R2 + o] = v;
+    part += v * drow[o];
   }
   red[threadIdx.x] = part;
   __syncthreads();
@@ -1008,7 +1162,7 @@ __global__ void update2_kernel(float* __restrict__ Zk, const double* __restrict_
 // scalars after the pass-1 allreduce and after the pass-2 allreduce
 __global__ void block_scalars_kernel(const double* __restrict__ dvec, int64_t Ik, int R2,
                                      const double* __restrict__ numden, DevScalars* sc,
-                                     DevStats* stats, int slot, int k, double step, int phase) {
+                                     DevStats* stats, int k, double step, int phase) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   if (phase == 0) {
     sc->sum_e2 = dvec[Ik * R2 + 0];
@@ -1020,7 +1174,7 @@ __global__ void block_scalars_kernel(const double* __restrict__ dvec, int64_t Ik
   sc->num = numden[1];
   const double eta = block_eta(sc, step);
   sc->eta = eta;
-  DevStats& st = stats[slot];
+  DevStats& st = stats[sc->slot];
   st.eta[k] = eta;
   st.num[k] = sc->num;
   st.den[k] = sc->den;
@@ -1034,13 +1188,16 @@ __global__ void block_scalars_kernel(const double* __restrict__ dvec, int64_t Ik
   sc->acc_n += sc->n_obs;
 }
 
-__global__ void sweep_begin_kernel(DevScalars* sc, DevStats* stats, int slot) {
+// the sweep's record slot comes from device memory (sc->slot_next, reset by trd_sweep), so a
+// captured sweep replays into successive records
+__global__ void sweep_begin_kernel(DevScalars* sc, DevStats* stats) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  DevStats& st = stats[slot];
+  sc->slot = sc->slot_next++;
+  DevStats& st = stats[sc->slot];
   st.sigma = sc->sigma;
   st.sum_e2 = 0.0; st.welsch = 0.0; st.stop_e = 0.0; st.n_obs = 0;
   for (int k = 0; k < kMaxN; ++k) { st.eta[k] = 0.0; st.num[k] = 0.0; st.den[k] = 0.0; st.nnz[k] = 0; }
-  st.skipped = 0; st.nonfinite = 0;
+  st.skipped = 0; st.nonfinite = 0; st.replica_mismatch = 0;
   sc->acc_e2 = 0.0; sc->acc_n = 0.0;
   sc->eabs_fill = 0ull;
 }
@@ -1093,13 +1250,19 @@ __global__ void __launch_bounds__(512) mad_hist_kernel(const uint32_t* __restric
   __syncthreads();
   const unsigned long long n = sc->eabs_fill;
   const uint32_t p0 = sc->mad_pre[0], p1 = sc->mad_pre[1];
+  const int lane = threadIdx.x & 31;
   for (unsigned long long q = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; q < n;
        q += (unsigned long long)gridDim.x * blockDim.x) {
     const uint32_t b = __ldg(eabs + q);
-    if (b >= 0x80000000u) continue;                      // padding slot (kEabsPad)
     if (LEVEL == 0) {
-      atomicAdd(&h[b >> 21], 1u);
-    } else if (LEVEL == 1) {
+      // |e| concentrates in few top-11-bit bins: lanes with the same bin add once (match_any)
+      const uint32_t bin = b >= 0x80000000u ? 0xFFFFFFFFu : (b >> 21);
+      const unsigned peers = __match_any_sync(__activemask(), bin);
+      if (bin != 0xFFFFFFFFu && lane == __ffs(peers) - 1) atomicAdd(&h[bin], (unsigned)__popc(peers));
+      continue;
+    }
+    if (b >= 0x80000000u) continue;                      // padding slot (kEabsPad)
+    if (LEVEL == 1) {
       const uint32_t pf = b >> 21, bin = (b >> 10) & 2047u;
       if (pf == p0) atomicAdd(&h[bin], 1u);
       if (pf == p1) atomicAdd(&h[NB + bin], 1u);
@@ -1160,7 +1323,7 @@ __global__ void eabs_advance_kernel(DevScalars* sc, const uint64_t* __restrict__
 }
 
 __global__ void sweep_end_kernel(double* __restrict__ D, double* __restrict__ Dprev, int64_t n2,
-                                 DevScalars* sc, DevStats* stats, int slot, int sigma_mode,
+                                 DevScalars* sc, DevStats* stats, int sigma_mode,
                                  double theta, double sigma_min) {
   __shared__ double a1[1024], a2[1024];
   double s1 = 0.0, s2 = 0.0;
@@ -1177,7 +1340,7 @@ __global__ void sweep_end_kernel(double* __restrict__ D, double* __restrict__ Dp
     for (int t = 0; t < (int)blockDim.x; ++t) { t1 += a1[t]; t2 += a2[t]; }
     const double e = sc->have_prev_D ? sqrt(t1) / sqrt(t2) : __longlong_as_double(0x7ff8000000000000LL);
     sc->stop_e = e;
-    stats[slot].stop_e = e;
+    stats[sc->slot].stop_e = e;
     if (sigma_mode == TRD_SIGMA_RMS && sc->acc_n > 0.0)
       sc->sigma = fmax(sigma_min, theta * sqrt(sc->acc_e2 / sc->acc_n));
     if (sigma_mode == TRD_SIGMA_MAD && sc->acc_n > 0.0) sc->sigma = fmax(sigma_min, theta * 1.4826 * sc->mad_med);
@@ -1207,17 +1370,18 @@ struct ReconArgs {
   int64_t zoff[kMaxN + 1];
 };
 
+template <int RM>
 __device__ float tr_value(const ReconArgs& a, const float* __restrict__ Z, const int64_t* ix) {
   // Tr(prod_k Z_k(i_k)) = sum_a e_a^T Z_0(i_0) ... Z_{N-1}(i_{N-1}) e_a
   float tot = 0.f;
   for (int a0 = 0; a0 < a.ranks[0]; ++a0) {
-    float v[kMaxR];
+    float v[RM];
 #pragma unroll
-    for (int c = 0; c < kMaxR; ++c) v[c] = (c == a0) ? 1.f : 0.f;
+    for (int c = 0; c < RM; ++c) v[c] = (c == a0) ? 1.f : 0.f;
     int rin = a.ranks[0];
     for (int m = 0; m < a.N; ++m) {
       const int rout = a.ranks[m + 1];
-      vecmat(v, Z + a.zoff[m] + ix[m] * (int64_t)a.ranks[m] * rout, rin, rout);
+      vecmat<RM>(v, Z + a.zoff[m] + ix[m] * (int64_t)a.ranks[m] * rout, rin, rout);
       rin = rout;
     }
     tot += v[a0];
@@ -1225,13 +1389,14 @@ __device__ float tr_value(const ReconArgs& a, const float* __restrict__ Z, const
   return tot;
 }
 
+template <int RM>
 __global__ void recon_kernel(ReconArgs a, const float* __restrict__ Z, const int64_t* __restrict__ lin,
                              int64_t n, float* __restrict__ out) {
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
        t += (int64_t)gridDim.x * blockDim.x) {
     int64_t l = lin[t], ix[kMaxN];
     for (int m = 0; m < a.N; ++m) { ix[m] = l % a.dims[m]; l /= a.dims[m]; }
-    out[t] = tr_value(a, Z, ix);
+    out[t] = tr_value<RM>(a, Z, ix);
   }
 }
 
@@ -1352,18 +1517,24 @@ void launch_plan(Context& c, const BlockPlan& bp, cudaStream_t s) {
   offsets_kernel<<<grid_for(bp.nrows + bp.ncols), 256, 0, s>>>(a, c.doff, c.row_off, c.col_off, c.sc);
   c.launches++;
   if (bp.p > 0) {
-    mid_kernel<<<grid_for(bp.nL * bp.rk1), 256, 0, s>>>(a, c.idx, c.Z, c.mid);
+    if (c.rbucket <= 16) mid_kernel<16><<<grid_for(bp.nL * bp.rk1), 256, 0, s>>>(a, c.idx, c.Z, c.mid);
+    else mid_kernel<32><<<grid_for(bp.nL * bp.rk1), 256, 0, s>>>(a, c.idx, c.Z, c.mid);
     c.launches++;
   }
-  rgt_kernel<<<grid_for(bp.ncols * bp.rs), 256, 0, s>>>(a, c.idx, c.Z, c.rgtT, c.sc);
+  if (c.rbucket <= 16) rgt_kernel<16><<<grid_for(bp.ncols * bp.rs), 256, 0, s>>>(a, c.idx, c.Z, c.rgtT, c.sc);
+  else rgt_kernel<32><<<grid_for(bp.ncols * bp.rs), 256, 0, s>>>(a, c.idx, c.Z, c.rgtT, c.sc);
   c.launches++;
 }
 
 void launch_lft(Context& c, const BlockPlan& bp, const float* Zsrc_k, int src_is_h, float* out,
                 cudaStream_t s) {
   PlanArgs a = make_plan_args(c, bp);
-  lft_kernel<<<grid_for(bp.nrows * bp.rk), 256, 0, s>>>(a, src_is_h ? nullptr : Zsrc_k,
-                                                        src_is_h ? c.h : nullptr, c.mid, out);
+  if (c.rbucket <= 16)
+    lft_kernel<16><<<grid_for(bp.nrows * bp.rk), 256, 0, s>>>(a, src_is_h ? nullptr : Zsrc_k,
+                                                              src_is_h ? c.h : nullptr, c.mid, out);
+  else
+    lft_kernel<32><<<grid_for(bp.nrows * bp.rk), 256, 0, s>>>(a, src_is_h ? nullptr : Zsrc_k,
+                                                              src_is_h ? c.h : nullptr, c.mid, out);
   c.launches++;
 }
 
@@ -1388,7 +1559,7 @@ void launch_reduce_d(Context& c, const BlockPlan& bp, cudaStream_t s) {
 // block statistics from the (allreduced) dvec tail
 void launch_block_stats(Context& c, const BlockPlan& bp, cudaStream_t s) {
   const int64_t Ik = c.dims[bp.k];                     // dvec rows: all of I_k
-  block_scalars_kernel<<<1, 32, 0, s>>>(c.dvec, Ik, bp.R2, nullptr, c.sc, c.stats, 0, bp.k, 0.0, 0);
+  block_scalars_kernel<<<1, 32, 0, s>>>(c.dvec, Ik, bp.R2, nullptr, c.sc, c.stats, bp.k, 0.0, 0);
   c.launches++;
 }
 
@@ -1402,8 +1573,8 @@ void launch_reduce_den(Context& c, const BlockPlan& bp, cudaStream_t s) {
 
 void launch_q(Context& c, int k, cudaStream_t s) {
   const int r0 = c.ranks[k], r1 = c.ranks[(k + 1) % c.N];
-  q_kernel<<<grid_for((int64_t)r0 * r0 * r1 * r1), 256, 0, s>>>(c.Z + c.zoff[k], c.dims[k], r0, r1,
-                                                                 c.Q + c.qoff[k]);
+  q_kernel<<<grid_for((int64_t)r0 * r0 * r1 * r1 * 32), 256, 0, s>>>(c.Z + c.zoff[k], c.dims[k], r0, r1,
+                                                                      c.Q + c.qoff[k]);
   c.launches++;
 }
 
@@ -1434,14 +1605,15 @@ void launch_q_sampled(Context& c, const BlockPlan& bp, cudaStream_t s) {
   }
 }
 
-__global__ void identity_kernel(double* __restrict__ M, int n) {
+__global__ void identity_kernel(double* __restrict__ M, int n, DevScalars* __restrict__ sc) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) sc->h_lam = 0.0;
   for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n * n; t += gridDim.x * blockDim.x)
     M[t] = (t / n == t % n) ? 1.0 : 0.0;
 }
 
 // M = I: h = d M = d (the 'gradient descent' ablation arm)
 void launch_identity_op(Context& c, const BlockPlan& bp, cudaStream_t s) {
-  identity_kernel<<<grid_for((int64_t)bp.R2 * bp.R2), 256, 0, s>>>(c.Mop, bp.R2);
+  identity_kernel<<<grid_for((int64_t)bp.R2 * bp.R2), 256, 0, s>>>(c.Mop, bp.R2, c.sc);
   c.launches++;
 }
 
@@ -1450,7 +1622,7 @@ void launch_gram(Context& c, const BlockPlan& bp, cudaStream_t s, const double* 
   // C = Q_{k+1} Q_{k+2} ... Q_{k-1}
   const double* cur = Qsrc + c.qoff[(k + 1) % N];
   int m_rows = bp.rk1 * bp.rk1;
-  double* bufs[2] = {c.chain_ws, c.chain_ws + kMaxR2 * kMaxR2};
+  double* bufs[2] = {c.chain_ws, c.chain_ws + c.chain_half};
   int which = 0;
   for (int q = 2; q < N; ++q) {
     const int mm = (k + q) % N;
@@ -1468,7 +1640,22 @@ void launch_gram(Context& c, const BlockPlan& bp, cudaStream_t s, const double* 
 
 void launch_solve(Context& c, const BlockPlan& bp, cudaStream_t s, const double* G) {
   const int n = bp.R2;
-  if (n <= kGjMaxN) {
+  if (n <= 128 && !(getenv("TRD_SOLVE") && atoi(getenv("TRD_SOLVE")) == 1)) {
+    const int np = (n + 15) / 16 * 16;
+    switch (np) {
+      case 16: gj2_solve_kernel<16><<<1, 256, 0, s>>>(G, n, c.cfg.lambda_rel, c.Mop, c.sc); break;
+      case 32: gj2_solve_kernel<32><<<1, 256, 0, s>>>(G, n, c.cfg.lambda_rel, c.Mop, c.sc); break;
+      case 48: gj2_solve_kernel<48><<<1, 256, 0, s>>>(G, n, c.cfg.lambda_rel, c.Mop, c.sc); break;
+      case 64: gj2_solve_kernel<64><<<1, 256, 0, s>>>(G, n, c.cfg.lambda_rel, c.Mop, c.sc); break;
+      case 80: gj2_solve_kernel<80><<<1, 256, 0, s>>>(G, n, c.cfg.lambda_rel, c.Mop, c.sc); break;
+      case 96: gj2_solve_kernel<96><<<1, 256, 0, s>>>(G, n, c.cfg.lambda_rel, c.Mop, c.sc); break;
+      case 112: gj2_solve_kernel<112><<<1, 256, 0, s>>>(G, n, c.cfg.lambda_rel, c.Mop, c.sc); break;
+      default: gj2_solve_kernel<128><<<1, 256, 0, s>>>(G, n, c.cfg.lambda_rel, c.Mop, c.sc); break;
+    }
+    c.launches++;
+    return;
+  }
+  if (n <= kGjMaxN) {                  // (TRD_SOLVE=1: the round-1 Gauss-Jordan kernel, A/B runs)
     const size_t gneed = (size_t)2 * n * n * sizeof(double);
     static uint64_t gj_attr = 0;
     const int maxs = (int)((size_t)2 * kGjMaxN * kGjMaxN * sizeof(double));
@@ -1498,13 +1685,13 @@ void launch_solve(Context& c, const BlockPlan& bp, cudaStream_t s, const double*
 
 void launch_h(Context& c, const BlockPlan& bp, cudaStream_t s) {
   const int64_t Ik = c.dims[bp.k];                     // h of every i_k (replicated update)
-  h_kernel<<<(unsigned)Ik, 256, 0, s>>>(c.dvec, c.Mop, bp.R2, c.h, c.numpart);
+  h_kernel<<<(unsigned)Ik, 256, 0, s>>>(c.dvec, c.Mop, bp.R2, c.h, c.numpart, c.sc);
   c.launches++;
 }
 
-void launch_update(Context& c, const BlockPlan& bp, int slot, cudaStream_t s) {
+void launch_update(Context& c, const BlockPlan& bp, cudaStream_t s) {
   const int64_t Ik = c.dims[bp.k];
-  block_scalars_kernel<<<1, 32, 0, s>>>(c.dvec, Ik, bp.R2, c.red_ws, c.sc, c.stats, slot, bp.k,
+  block_scalars_kernel<<<1, 32, 0, s>>>(c.dvec, Ik, bp.R2, c.red_ws, c.sc, c.stats, bp.k,
                                         c.cfg.step, 1);
   c.launches++;
   update2_kernel<<<grid_for(Ik * bp.R2), 256, 0, s>>>(c.Z + c.zoff[bp.k], c.h, Ik, bp.rk, bp.rk1,
@@ -1512,19 +1699,62 @@ void launch_update(Context& c, const BlockPlan& bp, int slot, cudaStream_t s) {
   c.launches++;
 }
 
-void launch_sweep_begin(Context& c, int slot, cudaStream_t s) {
-  sweep_begin_kernel<<<1, 32, 0, s>>>(c.sc, c.stats, slot);
+// Replica consistency (world > 1): a 64-bit checksum of the cores' bit patterns
+// (order-independent: a modular sum of hashed (position, bits) words), split into 32-bit halves
+// h and stored as [h_lo, h_hi, -h_lo, -h_hi]; after an allreduce-MAX the ranks agree iff
+// max(h) == -max(-h) for both halves.
+__device__ __forceinline__ unsigned long long mix64(unsigned long long x) {
+  x ^= x >> 33; x *= 0xff51afd7ed558ccdull; x ^= x >> 33; x *= 0xc4ceb9fe1a85ec53ull; x ^= x >> 33;
+  return x;
+}
+__global__ void core_checksum_kernel(const float* __restrict__ Z, int64_t n, unsigned long long* __restrict__ acc) {
+  unsigned long long h = 0ull;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x)
+    h += mix64(((unsigned long long)t << 32) ^ __float_as_uint(Z[t]));
+  for (int o = 16; o > 0; o >>= 1) h += __shfl_xor_sync(0xffffffffu, h, o);
+  if ((threadIdx.x & 31) == 0) atomicAdd(acc, h);
+}
+__global__ void checksum_split_kernel(const unsigned long long* __restrict__ acc, double* __restrict__ chk) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  const unsigned long long h = *acc;
+  chk[0] = (double)(h & 0xffffffffull);
+  chk[1] = (double)(h >> 32);
+  chk[2] = -chk[0];
+  chk[3] = -chk[1];
+}
+__global__ void replica_check_kernel(const double* __restrict__ chk, DevScalars* sc, DevStats* stats) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  const unsigned int bad = (chk[0] != -chk[2]) || (chk[1] != -chk[3]);
+  stats[sc->slot].replica_mismatch = bad;
+  if (bad) sc->replica_bad = 1;
+}
+
+void launch_core_checksum(Context& c, cudaStream_t s) {
+  cudaMemsetAsync(c.chk_acc, 0, sizeof(unsigned long long), s);
+  const int64_t n = c.zoff[c.N];
+  core_checksum_kernel<<<grid_for(n), 256, 0, s>>>(c.Z, n, c.chk_acc);
+  checksum_split_kernel<<<1, 32, 0, s>>>(c.chk_acc, c.chk);
+  c.launches += 2;
+}
+
+void launch_replica_check(Context& c, cudaStream_t s) {
+  replica_check_kernel<<<1, 32, 0, s>>>(c.chk, c.sc, c.stats);
   c.launches++;
 }
 
-void launch_sweep_end(Context& c, int slot, cudaStream_t s) {
+void launch_sweep_begin(Context& c, cudaStream_t s) {
+  sweep_begin_kernel<<<1, 32, 0, s>>>(c.sc, c.stats);
+  c.launches++;
+}
+
+void launch_sweep_end(Context& c, cudaStream_t s) {
   const int n = c.N - 1;
   const int rk = c.ranks[n], rk1 = c.ranks[0];
   const int64_t In = c.dims[n];
   double* T = c.chain_ws;     // In x R2 (<= chain_ws capacity, checked at init)
   dt_T_kernel<<<(unsigned)In, 128, 0, s>>>(c.Z + c.zoff[n], In, rk, rk1, c.G_last, T);
   dt_D_kernel<<<grid_for(In * In), 256, 0, s>>>(c.Z + c.zoff[n], In, rk, rk1, T, c.Dcur);
-  sweep_end_kernel<<<1, 1024, 0, s>>>(c.Dcur, c.Dprev, In * In, c.sc, c.stats, slot,
+  sweep_end_kernel<<<1, 1024, 0, s>>>(c.Dcur, c.Dprev, In * In, c.sc, c.stats,
                                       c.cfg.sigma_mode, c.cfg.sigma_theta, c.cfg.sigma_min);
   c.launches += 3;
 }
@@ -1567,7 +1797,8 @@ void launch_reconstruct(Context& c, const int64_t* lin, int64_t n, float* out, c
   a.N = c.N;
   for (int m = 0; m < c.N; ++m) a.dims[m] = c.dims[m];
   for (int m = 0; m <= c.N; ++m) { a.ranks[m] = c.ranks[m % c.N]; a.zoff[m] = c.zoff[m]; }
-  recon_kernel<<<grid_for(n), 256, 0, s>>>(a, c.Z, lin, n, out);
+  if (c.rbucket <= 16) recon_kernel<16><<<grid_for(n), 256, 0, s>>>(a, c.Z, lin, n, out);
+  else recon_kernel<32><<<grid_for(n), 256, 0, s>>>(a, c.Z, lin, n, out);
   c.launches++;
 }
 
@@ -1634,8 +1865,5 @@ void launch_rank_prefix(Context& c, cudaStream_t s) {
   c.launches += 1;
 }
 
-void launch_record_block(Context& c, const BlockPlan& bp, int slot, cudaStream_t s) { (void)c; (void)bp; (void)slot; (void)s; }
-void launch_reset_block_scalars(Context& c, cudaStream_t s) { (void)c; (void)s; }
-void launch_fill_full_sets(Context& c, const BlockPlan& bp, cudaStream_t s) { launch_sampler(c, bp, s); }
 
 }  // namespace trd

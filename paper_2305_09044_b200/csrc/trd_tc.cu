@@ -208,8 +208,9 @@ struct LftArgs {
 // CTA = one 128-row tile: the rows' X(i_k) and Mid(j_L) are staged in shared memory (row
 // stride padded to an odd word count: conflict-free across rows), then thread (row, half)
 // produces KP/2 consecutive kappa and stores them as 16-byte hi / lo vectors.
+// (gmem = 1: ranks too large for the shared-memory stage; X and Mid are read from global memory)
 __global__ void __launch_bounds__(256) tc_lft_pack_kernel(LftArgs a, int pass2, int64_t nrows_pad,
-                                                          __half* __restrict__ dst) {
+                                                          __half* __restrict__ dst, int gmem) {
   extern __shared__ float lsm[];
   const int XS = a.rk * a.rk1, MS = a.rk1 * a.rs;
   const int XP = XS | 1, MP = MS | 1;                       // odd strides
@@ -218,7 +219,7 @@ __global__ void __launch_bounds__(256) tc_lft_pack_kernel(LftArgs a, int pass2, 
   const int tid = threadIdx.x;
   for (int64_t rt = blockIdx.x; rt * TC_M < nrows_pad; rt += gridDim.x) {
     // stage: threads 0-127 copy row r's X(i_k), threads 128-255 its Mid(j_L)
-    {
+    if (!gmem) {
       const int r = tid & (TC_M - 1);
       const int64_t row = rt * TC_M + r;
       int64_t ik = 0, jl = 0;
@@ -250,14 +251,25 @@ __global__ void __launch_bounds__(256) tc_lft_pack_kernel(LftArgs a, int pass2, 
       const float* X = Xs + r * XP;
       const float* M = Ms + r * MP;
       const int kh = a.KP / 2;
+      int64_t gik = 0, gjl = 0;                             // (gmem) this row's i_k, j_L
+      if (gmem && row < a.nrows) {
+        if (a.rowmode == 0) { gik = row / a.nL; gjl = row - gik * a.nL; }
+        else { gjl = row / a.Ik; gik = row - gjl * a.Ik; }
+      }
+      auto xval = [&](int aa, int b) -> float {
+        if (!gmem) return X[aa * a.rk1 + b];
+        const int64_t base = (a.ik0 + gik) * XS;
+        return pass2 ? (float)__ldg(a.hk + base + aa + a.rk * b) : __ldg(a.zk + base + aa * a.rk1 + b);
+      };
+      auto mval = [&](int b, int c) -> float { return gmem ? __ldg(a.mid + gjl * MS + b * a.rs + c) : M[b * a.rs + c]; };
       auto lft_val = [&](int kap) -> float {
         float v = 0.f;
         if (row < a.nrows && kap < a.K) {
           const int aa = kap % a.rk, c = kap / a.rk;
           if (a.p == 0) {
-            v = X[aa * a.rk1 + c];
+            v = xval(aa, c);
           } else {
-            for (int b = 0; b < a.rk1; ++b) v = fmaf(X[aa * a.rk1 + b], M[b * a.rs + c], v);
+            for (int b = 0; b < a.rk1; ++b) v = fmaf(xval(aa, b), mval(b, c), v);
           }
         }
         return v;
@@ -287,6 +299,69 @@ __global__ void __launch_bounds__(256) tc_lft_pack_kernel(LftArgs a, int pass2, 
       }
     }
     __syncthreads();
+  }
+}
+
+// Generic ranks: a half-warp per row (16 lanes x 8 consecutive kappa cover KP <= 128), X(i_k)
+// and Mid(j_L) read through L1 (no staging: every row is independent, so the grid is as
+// large as the row count).  The row's max |Lft| (16-lane butterfly) gives its power-of-two
+// scale; each lane stores its 8 kappa as 16-byte hi / lo vectors.  Same fp32 arithmetic order as
+// lft_kernel (fmaf over b ascending).
+__global__ void __launch_bounds__(256) tc_lft_pack_hw_kernel(LftArgs a, int pass2, int64_t nrows_pad,
+                                                             __half* __restrict__ dst) {
+  const int lane = threadIdx.x & 31, sub = lane & 15;
+  const unsigned hmask = 0xFFFFu << (lane & 16);
+  const int XS = a.rk * a.rk1, MS = a.rk1 * a.rs;
+  const int64_t nhw = ((int64_t)gridDim.x * blockDim.x) >> 4;
+  for (int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 4; row < nrows_pad; row += nhw) {
+    int64_t ik = 0, jl = 0;
+    const bool ok = row < a.nrows;
+    if (ok) {
+      if (a.rowmode == 0) { ik = row / a.nL; jl = row - ik * a.nL; }
+      else { jl = row / a.Ik; ik = row - jl * a.Ik; }
+    }
+    const int64_t xb = (a.ik0 + ik) * XS;
+    const float* M = a.mid + jl * MS;
+    float v[8];
+    float amax = 0.f;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const int kap = sub * 8 + e;
+      float x = 0.f;
+      if (ok && kap < a.K) {
+        const int aa = kap % a.rk, c = kap / a.rk;
+        if (a.p == 0) {
+          x = pass2 ? (float)__ldg(a.hk + xb + aa + a.rk * c) : __ldg(a.zk + xb + aa * a.rk1 + c);
+        } else {
+          for (int b = 0; b < a.rk1; ++b) {
+            const float xv = pass2 ? (float)__ldg(a.hk + xb + aa + a.rk * b) : __ldg(a.zk + xb + aa * a.rk1 + b);
+            x = fmaf(xv, __ldg(M + b * a.rs + c), x);
+          }
+        }
+      }
+      v[e] = x;
+      amax = fmaxf(amax, fabsf(x));
+    }
+    for (int o = 8; o > 0; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(hmask, amax, o));
+    const int E = tc_scale_exp(amax);
+    if (sub == 0 && row < nrows_pad) a.lscl[row] = ldexpf(1.f, -E);
+    if (a.amax && sub == 0 && amax > 0.f) atomicMax(a.amax, __float_as_uint(amax));
+    if (sub * 8 < a.KP) {
+      __half hh[8], ll[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const float x = ldexpf(v[e], E);
+        hh[e] = __float2half_rn(x);
+        ll[e] = __float2half_rn(x - __half2float(hh[e]));
+      }
+      uint4 hv, lv;
+      hv.x = pack_half2(hh[0], hh[1]); hv.y = pack_half2(hh[2], hh[3]);
+      hv.z = pack_half2(hh[4], hh[5]); hv.w = pack_half2(hh[6], hh[7]);
+      lv.x = pack_half2(ll[0], ll[1]); lv.y = pack_half2(ll[2], ll[3]);
+      lv.z = pack_half2(ll[4], ll[5]); lv.w = pack_half2(ll[6], ll[7]);
+      *reinterpret_cast<uint4*>(dst + row * 2 * a.KP + sub * 8) = hv;
+      *reinterpret_cast<uint4*>(dst + row * 2 * a.KP + a.KP + sub * 8) = lv;
+    }
   }
 }
 
@@ -832,14 +907,15 @@ __device__ __forceinline__ void load_a_to_tmem(const TcArgs& a, int64_t row, uin
 // CTA (ik, jc) sums the jl chunk jc into dpart[jc][ik][R2].
 // ---------------------------------------------------------------------------------------
 constexpr int RD_ROWS = 64;   // jl rows staged per step
-__global__ void __launch_bounds__(256) tc_reduce_d_kernel(
+__global__ void __launch_bounds__(1024) tc_reduce_d_kernel(
     const float* __restrict__ contrib, const float* __restrict__ mid, int nsplit, int64_t nrows_pad, int64_t nL,
-    int64_t Ik, int rowmode, int KP, int R2, int rk, int rs, int p, int64_t jl_chunk, double* __restrict__ dpart) {
+    int64_t Ik, int rowmode, int KP, int R2, int rk, int rs, int p, int64_t jl_chunk, double* __restrict__ dpart,
+    int rd_rows) {
   extern __shared__ float rsm[];
   const int KPp = KP + 4, MS = (R2 / rk) * rs;               // Mid(jl) is r_{k+1} x r_s
-  float* Dt = rsm;                                           // [RD_ROWS][KP + 4] (16-B rows)
-  float* Mt = rsm + RD_ROWS * KPp;                           // [RD_ROWS][MS]
-  __shared__ double acc[256];
+  float* Dt = rsm;                                           // [rd_rows][KP + 4] (16-B rows)
+  float* Mt = rsm + rd_rows * KPp;                           // [rd_rows][MS]
+  __shared__ double acc[1024];
   const int64_t ik = blockIdx.x, jc = blockIdx.y;
   const int tid = threadIdx.x;
   const int G = max(1, (int)blockDim.x / R2);
@@ -848,8 +924,8 @@ __global__ void __launch_bounds__(256) tc_reduce_d_kernel(
   const int q4 = KP / 4;                                     // float4 per D row
   const int64_t j0 = jc * jl_chunk, j1 = min(nL, j0 + jl_chunk);
   double s = 0.0;
-  for (int64_t jb = j0; jb < j1; jb += RD_ROWS) {
-    const int nr = (int)min((int64_t)RD_ROWS, j1 - jb);
+  for (int64_t jb = j0; jb < j1; jb += rd_rows) {
+    const int nr = (int)min((int64_t)rd_rows, j1 - jb);
     if (p > 0) {                                             // Mid rows jb.. are contiguous
       const float* src = mid + jb * MS;
       for (int idx = tid; idx < nr * MS; idx += blockDim.x) Mt[idx] = __ldg(src + idx);
@@ -995,10 +1071,18 @@ void launch_tc_lft(Context& c, const BlockPlan& bp, bool pass2, cudaStream_t s) 
     c.launches++;
     return;
   }
-  const size_t smem = (size_t)TC_M * (((bp.rk * bp.rk1) | 1) + ((bp.rk1 * bp.rs) | 1)) * sizeof(float);
-  cudaFuncSetAttribute(tc_lft_pack_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (getenv("TRD_LFT_TILE") == nullptr) {        // half-warp per row (TRD_LFT_TILE: the tile kernel, A/B)
+    const int grid = (int)std::min<int64_t>((pad * 16 + 255) / 256, (int64_t)c.num_sm * 16);
+    tc_lft_pack_hw_kernel<<<grid, 256, 0, s>>>(a, pass2 ? 1 : 0, pad, pass2 ? c.lfthHL : c.lftHL);
+    c.launches++;
+    return;
+  }
+  size_t smem = (size_t)TC_M * (((bp.rk * bp.rk1) | 1) + ((bp.rk1 * bp.rs) | 1)) * sizeof(float);
+  const int gmem = smem > 200 * 1024 ? 1 : 0;      // large ranks: read X / Mid from global memory
+  if (gmem) smem = 0;
+  else cudaFuncSetAttribute(tc_lft_pack_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int grid = (int)std::min<int64_t>(bp.n_row_tiles, (int64_t)c.num_sm * 8);
-  tc_lft_pack_kernel<<<grid, 256, smem, s>>>(a, pass2 ? 1 : 0, pad, pass2 ? c.lfthHL : c.lftHL);
+  tc_lft_pack_kernel<<<grid, 256, smem, s>>>(a, pass2 ? 1 : 0, pad, pass2 ? c.lfthHL : c.lftHL, gmem);
   c.launches++;
 }
 
@@ -1168,11 +1252,13 @@ void launch_tc_reduce_d(Context& c, const BlockPlan& bp, cudaStream_t s) {
     return;
   }
   const int threads = bp.R2 * std::max(1, 256 / std::max(1, bp.R2));
-  const size_t smem = (size_t)RD_ROWS * ((bp.KP + 4) + (bp.R2 / bp.rk) * bp.rs) * sizeof(float);
+  const size_t per_row = (size_t)((bp.KP + 4) + (bp.R2 / bp.rk) * bp.rs) * sizeof(float);
+  const int rd_rows = (int)std::max<size_t>(1, std::min<size_t>(RD_ROWS, (200 * 1024) / per_row));
+  const size_t smem = (size_t)rd_rows * per_row;
   cudaFuncSetAttribute(tc_reduce_d_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   tc_reduce_d_kernel<<<dim3((unsigned)Ik, (unsigned)bp.tc_jc), threads, smem, s>>>(
       c.contrib, c.mid, bp.tc_nsplit, bp.n_row_tiles * TC_M, bp.nL, Ik, bp.rowmode, bp.KP, bp.R2, bp.rk,
-      bp.rs, bp.p, bp.tc_jl_chunk, c.dpart);
+      bp.rs, bp.p, bp.tc_jl_chunk, c.dpart, rd_rows);
   tc_reduce_final_kernel<<<(unsigned)(Ik + 1), 128, 0, s>>>(c.dpart, bp.tc_jc, Ik, bp.R2, c.spart, bp.tc_grid1,
                                                             c.dvec, c.sc, bp.k, bp.ik0, c.dims[bp.k]);
   c.launches += 2;

@@ -71,7 +71,18 @@ class trd_sweep_stats(ctypes.Structure):
                 ("num", ctypes.c_double * TRD_MAX_ORDER),
                 ("den", ctypes.c_double * TRD_MAX_ORDER),
                 ("nnz", ctypes.c_int64 * TRD_MAX_ORDER),
-                ("skipped_mask", ctypes.c_uint32)]
+                ("skipped_mask", ctypes.c_uint32),
+                ("replica_mismatch", ctypes.c_uint32)]
+
+
+# int allreduce(void* user, double* buf_dev, uint64_t n, int32_t op, void* stream)
+TRD_OP_SUM, TRD_OP_MAX = 0, 1
+ALLREDUCE_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint64,
+                                ctypes.c_int32, ctypes.c_void_p)
+
+
+class trd_exchange(ctypes.Structure):
+    _fields_ = [("allreduce", ALLREDUCE_FN), ("user", ctypes.c_void_p)]
 
 
 class trd_error_stats(ctypes.Structure):
@@ -104,6 +115,8 @@ def load_library(path: str = LIB_PATH):
     P, i32, i64, d = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_double
     sig = {
         "trd_init": (i32, [ctypes.POINTER(trd_config), ctypes.POINTER(trd_shard), P, P, P]),
+        "trd_init_ex": (i32, [ctypes.POINTER(trd_config), ctypes.POINTER(trd_shard), P, P,
+                              ctypes.POINTER(trd_exchange), P]),
         "trd_upload": (i32, [P, P, P]),
         "trd_sketch": (i32, [P, i32, i32, P, P]),
         "trd_sweep": (i32, [P, i32, P]),
@@ -164,7 +177,7 @@ class TRD:
                  sigma=1.0, sigma_theta=1.0, sigma_min=1e-3, lambda_rel=1e-6, step=0.0,
                  sketch=None, seed=0, shard_mode=0, shard_range=None, world=1, rank=0,
                  nccl_id: Optional[bytes] = None, packed=False, host=False, stream=None,
-                 scaling=0, sampling=0):
+                 scaling=0, sampling=0, exchange=None):
         import torch
         self.lib = load_library()
         N = len(dims)
@@ -210,8 +223,23 @@ class TRD:
             stream = torch.cuda.current_stream().cuda_stream
         self.stream = stream
         self.ctx = ctypes.c_void_p()
-        st = self.lib.trd_init(ctypes.byref(cfg), ctypes.byref(sh), arr, ctypes.c_void_p(stream),
-                               ctypes.byref(self.ctx))
+        if exchange is not None:
+            # exchange(buf_dev_ptr, n, op, stream) -> None: an in-place allreduce of n doubles
+            def _cb(user, buf, n, op, strm):
+                try:
+                    exchange(int(buf or 0), int(n), int(op), int(strm or 0))
+                    return 0
+                except Exception:                                  # reported as TRD_ERR_NCCL
+                    import traceback
+                    traceback.print_exc()
+                    return 1
+            self._ex_cb = ALLREDUCE_FN(_cb)
+            self._ex = trd_exchange(self._ex_cb, None)
+            st = self.lib.trd_init_ex(ctypes.byref(cfg), ctypes.byref(sh), arr, ctypes.c_void_p(stream),
+                                      ctypes.byref(self._ex), ctypes.byref(self.ctx))
+        else:
+            st = self.lib.trd_init(ctypes.byref(cfg), ctypes.byref(sh), arr, ctypes.c_void_p(stream),
+                                   ctypes.byref(self.ctx))
         if st != 0:
             raise TrdError(st, "trd_init")
 
@@ -231,7 +259,7 @@ class TRD:
             out.append(dict(sigma=r.sigma, sum_e2=r.sum_e2, welsch=r.welsch_loss, stop_e=r.stop_e,
                             ms=r.ms, n_obs=r.n_obs, eta=list(r.eta)[:self.N], num=list(r.num)[:self.N],
                             den=list(r.den)[:self.N], nnz=list(r.nnz)[:self.N],
-                            skipped=r.skipped_mask))
+                            skipped=r.skipped_mask, replica_mismatch=r.replica_mismatch))
         return out
 
     def sketch(self, t: int, k: int):

@@ -253,3 +253,70 @@ def test_error_psnr_and_observed_error_match_oracle():
             assert abs(g["rel_err_observed"] - want_obs) <= 1e-5 * want_obs
             assert abs(g["psnr"] - want_psnr) <= 1e-4, (peak, g["psnr"], want_psnr)
     ctx.close()
+
+
+# ---------------------------------------------------------------- CUDA-graph sweeps
+@pytest.mark.parametrize("name,dims,sketch", [("C4", [16, 16, 16, 16], [8, 8, 8, 8]),
+                                               ("C5b", [12, 9, 8, 7, 6], None)])
+def test_graph_replay_equals_eager_sweeps(name, dims, sketch, monkeypatch):
+    """Sweeps replayed from a captured CUDA graph (the default after the first sweep) give the
+    same cores, records and launch counts, bit for bit, as eagerly launched sweeps
+    (TRD_GRAPH=0); the profiling events of the replays time every pass-kernel launch."""
+    _cuda()
+    spec = small_spec(name, dims, sketch)
+    prob = make_problem(spec)
+    out = []
+    for graph in ("0", "1"):
+        monkeypatch.setenv("TRD_GRAPH", graph)
+        ctx = gpu_context(prob, packed=True, sigma_mode=O.SIGMA_MAD)
+        ctx.set_profiling(True)
+        l0 = ctx.launch_count
+        recs = ctx.sweep(4)
+        prof = ctx.get_profile()
+        out.append((ctx.get_cores(), recs, ctx.launch_count - l0, prof))
+        ctx.close()
+    (ca, ra, la, pa), (cb, rb, lb, pb) = out
+    for x, y in zip(ca, cb):
+        assert np.array_equal(x, y)
+    for x, y in zip(ra, rb):
+        assert x["sigma"] == y["sigma"] and x["eta"] == y["eta"] and x["n_obs"] == y["n_obs"]
+    assert la == lb
+    assert pa["pass1_launches"] == pb["pass1_launches"] == 4 * len(dims)
+    assert pb["pass1_ms"] > 0.0 and pb["pass2_ms"] > 0.0
+
+
+# ---------------------------------------------------------------- large ranks (SURVEY 8f rank 3)
+@pytest.mark.parametrize("name,dims,ranks,sketch", [
+    ("C2", [256, 256, 3], [20, 20, 3], None),            # the paper's image ranks (P:362)
+    ("C3", [40, 36, 3, 16], [12, 12, 3, 8], [24, 20, 0, 10]),
+])
+def test_large_ranks_match_oracle(name, dims, ranks, sketch):
+    """The large-rank regime: R_k^2 = 400 / 144 blocks (Cholesky solve,
+    generic Lft pack from global memory), tensor-core splits with K = r_k r_s <= 128; block
+    quantities row by row and the cores after one sweep."""
+    _cuda()
+    spec = small_spec(name, dims, sketch)
+    spec.ranks = list(ranks)
+    prob = make_problem(spec)
+    src, _ = oracle_source(prob)
+    cfg = oracle_config(spec)
+    st0 = O.State(cfg, prob.init, src)
+    ctx = gpu_context(prob, packed=True)
+    for k in range(len(dims)):
+        g = ctx.block_probe(0, k)
+        sets = O.index_sets_for_block(cfg, 0, k)
+        Xk, Pk = O.working_set(src, k, sets)
+        S = O.subchain(st0.cores, k, sets)
+        d, _, W = O.gradient_block(Xk, Pk, O.core_unfold2(st0.cores[k]), S, st0.sigma)
+        G = O.gram_fgmc(st0.Qs, k, spec.ranks)
+        h, _ = O.scaled_gradient(d, G, cfg.lambda_rel)
+        assert rel_fro(g["G"], G) <= 1e-6, k
+        assert _rowwise(g["d"], d) <= 1e-4, (k, _rowwise(g["d"], d))
+        assert rel_fro(g["h"], h) <= 1e-4, k
+        assert abs(g["den"] - O.line_search_den(h, Pk, W, S)) <= 1e-4 * g["den"], k
+    ctx.close()
+    st, _ = O.run(cfg, prob.init, src, 1)
+    ctx = gpu_context(prob, packed=True)
+    ctx.sweep(1)
+    assert cores_rel_err(ctx.get_cores(), st.cores) <= 1e-4
+    ctx.close()
