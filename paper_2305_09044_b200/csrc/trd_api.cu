@@ -292,35 +292,57 @@ void prof_pair(Context* c, int pass, int e0, int e1) {
   else (pass == 1 ? c->ev_pass1 : c->ev_pass2).push_back({e0, e1});
 }
 
+// TRD_TIMELINE=1 (diagnostic, eager sweeps only): events at the stage boundaries of every
+// block on both streams; trd_destroy prints the mean time between consecutive marks
+void tl_mark(Context* c, cudaStream_t s, const char* label) {
+  if (!c->tl_on || c->capturing) return;
+  cudaEvent_t e;
+  if (cudaEventCreate(&e) != cudaSuccess) return;
+  cudaEventRecord(e, s);
+  c->tl.push_back({label, (void*)e, (s == c->side || strncmp(label, "side", 4) == 0) ? 1 : 0});
+}
+
 // a1-a6 + a7 (pass 1 and the d/stat exchange) of block k
 trd_status block_pass1(Context* c, const BlockPlan& bp) {
   cudaStream_t s = c->stream;
   // a8 + a9 (FGMC Gram, filtered operator M) depend only on the cores != k: run them on the
   // side stream, overlapping the sampler / staging / pass 1 (which leaves one SM free)
   // (the sampler first: the local-scaled-term arm builds its Gram from the sampled slices)
+  tl_mark(c, s, "block start");
   launch_sampler(*c, bp, s);
+  tl_mark(c, s, "sampler");
+  // (TRD_NO_SIDE=1, diagnostic: the Gram and the solve in line on the main stream)
+  const bool inl = getenv("TRD_NO_SIDE") && atoi(getenv("TRD_NO_SIDE")) != 0;
+  cudaStream_t side = inl ? s : c->side;
   CUDA_TRY(c, cudaEventRecord(c->ev_fork, s));
-  CUDA_TRY(c, cudaStreamWaitEvent(c->side, c->ev_fork, 0));
-  launch_gram(*c, bp, c->side, c->Q, c->G);             // FGMC Gram (also the stop metric's)
+  CUDA_TRY(c, cudaStreamWaitEvent(side, c->ev_fork, 0));
+  tl_mark(c, side, "side: fork");
+  launch_gram(*c, bp, side, c->Q, c->G);                // FGMC Gram (also the stop metric's)
+  tl_mark(c, side, "side: gram");
   if (c->cfg.scaling == TRD_SCALING_GLOBAL) {
-    launch_solve(*c, bp, c->side, c->G);
+    launch_solve(*c, bp, side, c->G);
   } else if (c->cfg.scaling == TRD_SCALING_NONE) {
-    launch_identity_op(*c, bp, c->side);                 // h = d ('gradient descent' arm)
+    launch_identity_op(*c, bp, side);                    // h = d ('gradient descent' arm)
   } else {                                               // 'local scaled term' arm
-    launch_q_sampled(*c, bp, c->side);
-    launch_gram(*c, bp, c->side, c->Qloc, c->Gloc);
-    launch_solve(*c, bp, c->side, c->Gloc);
+    launch_q_sampled(*c, bp, side);
+    launch_gram(*c, bp, side, c->Qloc, c->Gloc);
+    launch_solve(*c, bp, side, c->Gloc);
   }
-  CUDA_TRY(c, cudaEventRecord(c->ev_join, c->side));
+  tl_mark(c, side, "side: solve");
+  CUDA_TRY(c, cudaEventRecord(c->ev_join, side));
   launch_plan(*c, bp, s);
+  tl_mark(c, s, "plan (offsets, mid, rgt)");
   if (!bp.use_tc) launch_lft(*c, bp, c->Z + c->zoff[bp.k], 0, c->lft, s);
   TcStage& stg = c->stage[bp.k];
   if (bp.use_tc) {                          // Lft built directly as the fp16 hi / lo A operand
     launch_tc_lft(*c, bp, false, s);
+    tl_mark(c, s, "lft pack 1");
     launch_tc_pack_cols(*c, bp, s);
+    tl_mark(c, s, "pack cols");
     if (!stg.valid) {                       // a2: stage the sketch in tile order
       launch_tc_stage(*c, bp, stg, s);
       stg.valid = stg.invariant;
+      tl_mark(c, s, "stage");
     }
   }
   const bool pe = c->prof || c->capturing;
@@ -328,15 +350,18 @@ trd_status block_pass1(Context* c, const BlockPlan& bp) {
   if (bp.use_tc) launch_tc_pass(*c, bp, stg, false, s);
   else launch_pass1(*c, bp, 0, s);
   if (pe) prof_pair(c, 1, e0, prof_event(c));
+  tl_mark(c, s, "pass 1");
   if (bp.use_tc && c->eabs) launch_eabs_advance(*c, stg, s);   // R21 |e| slots of this block
   if (bp.use_tc) launch_tc_reduce_d(*c, bp, s);
   else launch_reduce_d(*c, bp, s);
   trd_status st = check_launch(c, "pass 1");
   if (st) return st;
   const int64_t Ik = c->dims[bp.k];
+  tl_mark(c, s, "reduce d");
   st = allreduce(c, c->dvec, (size_t)(Ik * bp.R2 + 3));
   if (st) return st;
   launch_block_stats(*c, bp, s);
+  tl_mark(c, s, "exchange + stats");
   return TRD_OK;
 }
 
@@ -344,15 +369,20 @@ trd_status block_pass1(Context* c, const BlockPlan& bp) {
 trd_status block_pass2(Context* c, const BlockPlan& bp) {
   cudaStream_t s = c->stream;
   CUDA_TRY(c, cudaStreamWaitEvent(s, c->ev_join, 0));       // M of this block (side stream)
+  tl_mark(c, s, "join (wait for the solve)");
   launch_h(*c, bp, s);
+  tl_mark(c, s, "h = d M");
   if (!bp.use_tc) launch_lft(*c, bp, nullptr, 1, c->lfth, s);
   else launch_tc_lft(*c, bp, true, s);
+  tl_mark(c, s, "lft pack 2");
   const bool pe = c->prof || c->capturing;
   const int e0 = pe ? prof_event(c) : -1;
   if (bp.use_tc) launch_tc_pass(*c, bp, c->stage[bp.k], true, s);
   else launch_pass2(*c, bp, s);
   if (pe) prof_pair(c, 2, e0, prof_event(c));
+  tl_mark(c, s, "pass 2");
   launch_reduce_den(*c, bp, s);
+  tl_mark(c, s, "reduce den");
   trd_status st = check_launch(c, "pass 2");
   if (st) return st;
   return allreduce(c, c->red_ws, 1);
@@ -561,6 +591,7 @@ trd_status trd_init_ex(const trd_config* cfg, const trd_shard* shard, const floa
   if (!c) return TRD_ERR_OOM;
   c->cfg = *cfg;
   c->cfg.nccl_unique_id = nullptr;
+  c->tl_on = getenv("TRD_TIMELINE") && atoi(getenv("TRD_TIMELINE")) != 0;
   if (ex && cfg->world > 1) c->ex = *ex;
   c->N = N;
   c->stream = (cudaStream_t)stream;
@@ -900,11 +931,14 @@ static trd_status enqueue_sweep(Context* c) {
     if (k == c->N - 1)
       CUDA_TRY(c, cudaMemcpyAsync(c->G_last, c->G, (size_t)bp.R2 * bp.R2 * 8, cudaMemcpyDeviceToDevice, s));
     launch_update(*c, bp, s);
+    tl_mark(c, s, "step + update");
     launch_q(*c, k, s);
+    tl_mark(c, s, "Q refresh");
     if ((st = check_launch(c, "update"))) return st;
   }
   if (c->eabs && (st = mad_select(c))) return st;         // R21 (histograms allreduced)
   launch_sweep_end(*c, s);
+  tl_mark(c, s, "sweep end (D^t, sigma)");
   if (c->cfg.world > 1) {                 // replica consistency of the replicated cores
     launch_core_checksum(*c, s);
     if ((st = allreduce(c, c->chk, 4, TRD_OP_MAX))) return st;
@@ -925,7 +959,7 @@ static void destroy_graph(SweepGraph& g) {
 // graph then holds no staging); TRD_GRAPH=0 disables graphs.
 static bool graph_usable(const Context* c) {
   const char* ge = getenv("TRD_GRAPH");
-  const bool off = ge && atoi(ge) == 0;
+  const bool off = (ge && atoi(ge) == 0) || c->tl_on;
   if (off || c->ex.allreduce) return false;
   for (int k = 0; k < c->N; ++k)
     if (c->plan[k].use_tc && c->stage[k].invariant && !c->stage[k].valid) return false;
@@ -1172,6 +1206,33 @@ void trd_destroy(trd_ctx* ctx) {
   Context* c = reinterpret_cast<Context*>(ctx);
   if (!c) return;
   if (c->stream) cudaStreamSynchronize(c->stream);
+  if (c->tl_on && !c->tl.empty()) {          // TRD_TIMELINE report: mean us between marks, per stream
+    cudaStreamSynchronize(c->stream);
+    cudaStreamSynchronize(c->side);
+    std::vector<std::string> names;
+    std::vector<double> sum;
+    std::vector<int> cnt;
+    for (int strm = 0; strm < 2; ++strm) {
+      int prev = -1;
+      for (size_t i = 0; i < c->tl.size(); ++i) {
+        if (c->tl[i].side != strm) continue;
+        if (prev >= 0 && strcmp(c->tl[i].label, "block start") != 0 && strcmp(c->tl[i].label, "side: fork") != 0) {
+          float ms = 0.f;
+          cudaEventElapsedTime(&ms, (cudaEvent_t)c->tl[(size_t)prev].ev, (cudaEvent_t)c->tl[i].ev);
+          size_t j = 0;
+          for (; j < names.size(); ++j) if (names[j] == c->tl[i].label) break;
+          if (j == names.size()) { names.push_back(c->tl[i].label); sum.push_back(0.0); cnt.push_back(0); }
+          sum[j] += ms * 1e3;
+          cnt[j] += 1;
+        }
+        prev = (int)i;
+      }
+    }
+    fprintf(stderr, "[trd timeline] mean us per occurrence (main stream, then side stream)\n");
+    for (size_t j = 0; j < names.size(); ++j)
+      fprintf(stderr, "  %-28s %9.1f  (x%d)\n", names[j].c_str(), sum[j] / cnt[j], cnt[j]);
+    for (auto& t : c->tl) cudaEventDestroy((cudaEvent_t)t.ev);
+  }
   for (auto& g : c->graphs) destroy_graph(g);
   if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
   if (c->nccl_comm && g_nccl.comm_destroy) g_nccl.comm_destroy(c->nccl_comm);

@@ -37,6 +37,12 @@ constexpr uint32_t kEabsPad = 0xFFFFFFFFu;
 // Power-of-two scale exponent E of an fp16 hi / lo operand with max |.| = amax: amax 2^E lies
 // in [2^14, 2^15), so every element is below the fp16 maximum (65504) and elements down to
 // 2^-15 of the maximum keep a normal lo part (22 significant bits).  Scaling by 2^E is exact.
+// max into a shared fp32-bits scalar: the atomic only when the value can raise it (same-address
+// atomics serialise at L2: thousands of CTAs / rows would cost ~100 us per kernel)
+__device__ __forceinline__ void amax_update(unsigned int* dst, float v) {
+  if (v > 0.f && __float_as_uint(v) > *reinterpret_cast<volatile unsigned int*>(dst)) atomicMax(dst, __float_as_uint(v));
+}
+
 __host__ __device__ __forceinline__ int tc_scale_exp(float amax) {
   if (!(amax > 0.f) || !(amax < 3.0e38f)) return 0;
   int e = 0;
@@ -251,6 +257,10 @@ struct Context {
   // CUDA graphs of one sweep (world 1 or NCCL): per upload buffer set
   SweepGraph graphs[2];
   SweepGraph* capturing = nullptr;     // set while a sweep is being captured
+  // TRD_TIMELINE diagnostic: (label, event, stream) marks of eager sweeps
+  struct TlMark { const char* label; void* ev; int side; };
+  bool tl_on = false;
+  std::vector<TlMark> tl;
   cudaStream_t cap_stream = nullptr;   // capture stream (the caller's may be the legacy stream)
 };
 

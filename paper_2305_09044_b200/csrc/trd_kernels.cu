@@ -358,7 +358,7 @@ __device__ __forceinline__ void block_amax(float v, unsigned int* dst) {
   if (threadIdx.x == 0) {
     float m = 0.f;
     for (int w = 0; w < (int)(blockDim.x >> 5); ++w) m = fmaxf(m, red[w]);
-    if (m > 0.f) atomicMax(dst, __float_as_uint(m));
+    amax_update(dst, m);
   }
 }
 

@@ -280,7 +280,7 @@ __global__ void __launch_bounds__(256) tc_lft_pack_kernel(LftArgs a, int pass2, 
       amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, 1));
       const int E = tc_scale_exp(amax);
       if (hf == 0 && row < nrows_pad) a.lscl[row] = ldexpf(1.f, -E);
-      if (a.amax && amax > 0.f) atomicMax(a.amax, __float_as_uint(amax));
+      if (a.amax && hf == 0) amax_update(a.amax, amax);
       for (int k0 = hf * kh; k0 < (hf + 1) * kh; k0 += 8) {
         __half hh[8], ll[8];
 #pragma unroll
@@ -345,7 +345,10 @@ __global__ void __launch_bounds__(256) tc_lft_pack_hw_kernel(LftArgs a, int pass
     for (int o = 8; o > 0; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(hmask, amax, o));
     const int E = tc_scale_exp(amax);
     if (sub == 0 && row < nrows_pad) a.lscl[row] = ldexpf(1.f, -E);
-    if (a.amax && sub == 0 && amax > 0.f) atomicMax(a.amax, __float_as_uint(amax));
+    if (a.amax) {                                   // max over the warp's two rows, then one update
+      const float m2 = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, 16));
+      if (lane == 0) amax_update(a.amax, m2);
+    }
     if (sub * 8 < a.KP) {
       __half hh[8], ll[8];
 #pragma unroll
@@ -429,7 +432,7 @@ __global__ void __launch_bounds__(128, 4) tc_lft_pack_rb_kernel(LftArgs a, int p
     if (a.amax) {
       float m = amax;
       for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-      if ((threadIdx.x & 31) == 0 && m > 0.f) atomicMax(a.amax, __float_as_uint(m));
+      if ((threadIdx.x & 31) == 0) amax_update(a.amax, m);
     }
 #pragma unroll
     for (int k0 = 0; k0 < KP; k0 += 8) {
@@ -510,7 +513,25 @@ struct StageArgs {
   uint64_t* tcount;       // [tile]  (counts, then exclusive prefix)
   float* tvals;           // compacted values (tile blocks padded to 8 entries)
   uint16_t* tidx;         // entry list: (row in tile) * 64 + column, 0xFFFF = padding
+  // fibre windows (sampled mode 0 as the fastest column digit, 16 <= s0, I0 <= 128): columns
+  // f s0 .. f s0 + s0 - 1 lie in one mode-0 fibre at base col_off[f s0] - idx0[0], at the
+  // positions idx0[0..s0-1]; 0 = off
+  int fib;
+  int fib_s0;
+  const int32_t* idx0;
 };
+
+// ---- fibre windows: the I0 <= 128 observation bits of a mode-0 fibre starting at linear
+// position lin0 as four aligned words (a0: bits 0-31 of the fibre, ...), from five raw words ----
+struct FibWin {
+  uint32_t a0, a1, a2, a3;   // aligned window (I0 <= 128 bits)
+  uint32_t w0;           // first raw word (index lin0 >> 5) and the shift sh = lin0 & 31
+  uint32_t sh;
+};
+__device__ __forceinline__ FibWin fib_window(const StageArgs& s, int64_t lin0);
+__device__ __forceinline__ uint32_t fib_word(const FibWin& f, uint32_t q) {
+  return q < 2 ? (q == 0 ? f.a0 : f.a1) : (q == 2 ? f.a2 : f.a3);
+}
 
 // The working-set tile (128 GEMM rows x 64 columns) reads the observation bits at linear
 // positions row_off[row] + col_off[col].  Two structures make this cheap:
@@ -547,6 +568,20 @@ __device__ __forceinline__ int64_t mask_rank(const StageArgs& s, int64_t lin) {
   const int64_t w = lin >> 5;
   return (int64_t)__ldg(s.rank_prefix + w) + __popc(__ldg(s.mask + w) & ((1u << (lin & 31)) - 1u));
 }
+__device__ __forceinline__ FibWin fib_window(const StageArgs& s, int64_t lin0) {
+  const int64_t w = lin0 >> 5;
+  FibWin f;
+  f.sh = (uint32_t)(lin0 & 31);
+  const uint32_t r0 = mask_word(s, w), r1 = mask_word(s, w + 1), r2 = mask_word(s, w + 2), r3 = mask_word(s, w + 3),
+                 r4 = mask_word(s, w + 4);
+  f.w0 = r0;
+  f.a0 = __funnelshift_r(r0, r1, f.sh);
+  f.a1 = __funnelshift_r(r1, r2, f.sh);
+  f.a2 = __funnelshift_r(r2, r3, f.sh);
+  f.a3 = __funnelshift_r(r3, r4, f.sh);
+  return f;
+}
+
 // 32 x 32 bit-matrix transpose across a warp: in, lane i holds row i (bit j = element (i, j));
 // out, lane i holds column i (bit j = element (j, i))
 __device__ __forceinline__ uint32_t warp_transpose32(uint32_t x, int lane) {
@@ -616,6 +651,27 @@ __global__ void __launch_bounds__(128) stage_bits_kernel(StageArgs s) {
       const uint32_t w0 = c0 >= 0 ? warp_col_bits(s, wr, c0) : 0u;
       const uint32_t w1 = c1 >= 0 ? warp_col_bits(s, wr, c1) : 0u;
       bits = (uint64_t)warp_transpose32(w0, lane) | ((uint64_t)warp_transpose32(w1, lane) << 32);
+    } else if (s.fib) {
+      // sampled mode 0 as the fastest column digit: the tile's columns lie in a few mode-0
+      // fibres; one aligned window (4 words) per fibre and row, the sampled positions from it
+      if (ro >= 0) {
+        const int64_t c0 = ct * TC_NT;
+        for (int j = 0; j < TC_NT;) {
+          const int64_t col = c0 + j;
+          if (col >= s.ncols) break;
+          const int q0 = (int)(col % s.fib_s0);              // position of column j in its fibre
+          const int nj = min(TC_NT - j, s.fib_s0 - q0);       // columns of this fibre in the tile
+          const int64_t co = sco[j];
+          if (co >= 0) {
+            const FibWin fw = fib_window(s, ro + co - s.idx0[q0]);
+            for (int u = 0; u < nj; ++u) {
+              const uint32_t p = (uint32_t)s.idx0[q0 + u];
+              bits |= (uint64_t)((fib_word(fw, p >> 5) >> (p & 31)) & 1u) << (j + u);
+            }
+          }
+          j += nj;
+        }
+      }
     } else if (__popcll((uint64_t)sstart[0] | ((uint64_t)sstart[1] << 32)) > 16) {
       // scattered columns (sampled index sets): one bit per column, 8 loads in flight per step
       if (ro >= 0) {
@@ -724,6 +780,47 @@ __global__ void __launch_bounds__(128) stage_vals_kernel(StageArgs s) {
           ov[pos] = __ldg(s.values + vi);
           oi[pos] = (uint16_t)(rr * TC_NT + j);
         }
+      }
+    } else if (bits && s.fib) {
+      // fibre windows (see stage_bits): ranks from the window's cumulative popcounts
+      float* out = ov + roff;
+      uint16_t* oidx = oi + roff;
+      int q = 0;
+      const int64_t c0 = ct * TC_NT;
+      for (int j = 0; j < TC_NT;) {
+        const int64_t col = c0 + j;
+        if (col >= s.ncols) break;
+        const int q0 = (int)(col % s.fib_s0);
+        const int nj = min(TC_NT - j, s.fib_s0 - q0);
+        uint64_t fb = (bits >> j) & (nj >= 64 ? ~0ull : ((1ull << nj) - 1ull));
+        if (fb) {
+          const int64_t lin0 = ro + sco[j] - s.idx0[q0];
+          const FibWin fw = fib_window(s, lin0);
+          int64_t base = lin0;                               // dense: value index = linear position
+          uint32_t c1 = 0, c2 = 0, c3 = 0;
+          if (s.packed) {
+            base = (int64_t)__ldg(s.rank_prefix + (lin0 >> 5)) + __popc(fw.w0 & ((1u << fw.sh) - 1u));
+            c1 = __popc(fw.a0);
+            c2 = c1 + __popc(fw.a1);
+            c3 = c2 + __popc(fw.a2);
+          }
+          while (fb) {
+            const int u = __ffsll((long long)fb) - 1;
+            fb &= fb - 1;
+            const uint32_t p = (uint32_t)s.idx0[q0 + u];
+            int64_t vi;
+            if (s.packed) {
+              const uint32_t wq = p >> 5;
+              vi = base + (wq < 2 ? (wq == 0 ? 0u : c1) : (wq == 2 ? c2 : c3)) +
+                   __popc(fib_word(fw, wq) & ((1u << (p & 31)) - 1u));
+            } else {
+              vi = base + p;
+            }
+            oidx[q] = (uint16_t)(tid * TC_NT + j + u);
+            out[q++] = __ldg(s.values + vi);
+          }
+        }
+        j += nj;
       }
     } else if (bits && __popcll((uint64_t)sstart[0] | ((uint64_t)sstart[1] << 32)) > 16) {
       // scattered columns: per entry, the rank from its mask word (cached across entries)
@@ -930,14 +1027,18 @@ __global__ void __launch_bounds__(1024) tc_reduce_d_kernel(
       const float* src = mid + jb * MS;
       for (int idx = tid; idx < nr * MS; idx += blockDim.x) Mt[idx] = __ldg(src + idx);
     }
-    for (int sp = 0; sp < nsplit; ++sp) {
-      const float* base = contrib + (int64_t)sp * nrows_pad * KP;
+    {
+      // the column splits' D rows summed while staging (fixed split order): one barrier per chunk
       for (int f = tid; f < nr * q4; f += blockDim.x) {
         const int rr = f / q4, c4 = f - rr * q4;
         const int64_t jl = jb + rr;
         const int64_t row = rowmode == 0 ? jl + nL * ik : ik + Ik * jl;
-        *reinterpret_cast<float4*>(Dt + rr * KPp + 4 * c4) =
-            __ldg(reinterpret_cast<const float4*>(base + row * KP) + c4);
+        float4 v = __ldg(reinterpret_cast<const float4*>(contrib + row * KP) + c4);
+        for (int sp = 1; sp < nsplit; ++sp) {
+          const float4 w = __ldg(reinterpret_cast<const float4*>(contrib + ((int64_t)sp * nrows_pad + row) * KP) + c4);
+          v.x += w.x; v.y += w.y; v.z += w.z; v.w += w.w;
+        }
+        *reinterpret_cast<float4*>(Dt + rr * KPp + 4 * c4) = v;
       }
       __syncthreads();
       if (g < G) {
@@ -1064,6 +1165,7 @@ void launch_tc_lft(Context& c, const BlockPlan& bp, bool pass2, cudaStream_t s) 
   a.mid = c.mid;
   a.lscl = pass2 ? c.lsclh : c.lscl;
   a.amax = pass2 ? nullptr : &c.sc->amax_a;
+  if (getenv("TRD_DIAG_NOAMAX")) a.amax = nullptr;           // (diagnostic: results invalid)
   const int64_t pad = bp.n_row_tiles * TC_M;
   if (bp.p > 0 && bp.rk == 8 && bp.rk1 == 8 && bp.rs == 8) {
     const int grid = (int)std::min<int64_t>((pad + 127) / 128, (int64_t)c.num_sm * 16);
@@ -1102,6 +1204,16 @@ void launch_tc_stage(Context& c, const BlockPlan& bp, TcStage& st, cudaStream_t 
   a.row_off = c.row_off; a.col_off = c.col_off;
   a.mask = c.mask; a.rank_prefix = c.rank_prefix; a.values = c.values;
   a.tbits = st.tbits; a.troff = st.troff; a.tcount = st.tbase; a.tvals = st.tvals; a.tidx = st.tidx;
+  // fibre windows: mode 0 is the fastest column digit with a sampled set of >= 16 positions,
+  // I0 <= 128 (a window of five words), and not a partial shard (offsets = global indices)
+  a.fib = 0; a.fib_s0 = 0; a.idx0 = nullptr;
+  if (!bp.explicit_cols && bp.nright > 0 && bp.right[bp.rdig[0]] == 0 && bp.s[0] < c.dims[0] && bp.s[0] >= 16 &&
+      c.dims[0] <= 128 && !(c.cfg.shard_mode == 0 && c.shard_end - c.shard_begin < c.dims[0]) &&
+      !(getenv("TRD_NO_FIB"))) {
+    a.fib = 1;
+    a.fib_s0 = (int)bp.s[0];
+    a.idx0 = c.idx + c.idx_off[0];
+  }
   const int grid = (int)std::min<int64_t>(a.n_tiles, 148 * 16);
   stage_bits_kernel<<<grid, TC_M, 0, s>>>(a);
   cudaMemsetAsync(st.tbase + a.n_tiles, 0, sizeof(uint64_t), s);   // tbase[n_tiles] = total

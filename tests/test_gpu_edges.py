@@ -320,3 +320,32 @@ def test_large_ranks_match_oracle(name, dims, ranks, sketch):
     ctx.sweep(1)
     assert cores_rel_err(ctx.get_cores(), st.cores) <= 1e-4
     ctx.close()
+
+
+# ---------------------------------------------------------------- staging paths (a2)
+@pytest.mark.parametrize("name,dims,sketch", [("C4", [48, 20, 18, 16], [24, 8, 8, 8]),
+                                               ("C5a", [40, 12, 10, 9, 8], [20, 5, 5, 4, 4])])
+def test_fibre_window_staging_equals_per_column_lookups(name, dims, sketch, monkeypatch):
+    """Eq. 14 sketch staging with a sampled mode 0 among the column digits: the fibre-window
+    path (one aligned window per mode-0 fibre and row) stages the same tiles as the per-column
+    lookups (TRD_NO_FIB=1): bit-identical cores after two sweeps, and within 1e-4 of the
+    oracle, dense and packed storage."""
+    _cuda()
+    spec = small_spec(name, dims, sketch)
+    prob = make_problem(spec)
+    src, _ = oracle_source(prob)
+    st, _ = O.run(oracle_config(spec), prob.init, src, 2)
+    for packed in (False, True):
+        outs = []
+        for nofib in ("1", None):
+            if nofib:
+                monkeypatch.setenv("TRD_NO_FIB", nofib)
+            else:
+                monkeypatch.delenv("TRD_NO_FIB", raising=False)
+            ctx = gpu_context(prob, packed=packed)
+            ctx.sweep(2, stats=False)
+            outs.append(ctx.get_cores())
+            ctx.close()
+        for a, b in zip(outs[0], outs[1]):
+            assert np.array_equal(a, b)
+        assert cores_rel_err(outs[1], st.cores) <= 1e-4
