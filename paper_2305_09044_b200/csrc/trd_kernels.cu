@@ -1240,28 +1240,28 @@ __global__ void dt_D_kernel(const float* __restrict__ Zn, int64_t In, int rk, in
 // bits 9..0; the two targets are the order statistics floor((n-1)/2) and floor(n/2).  Counts
 // are integers (atomics in any order give the same histogram); scans run in one thread.
 // ----------------------------------------------------------------------------------------
+// level 0 (|e| concentrates in a few top-11-bit bins): one private histogram per warp in
+// dynamic shared memory (kMadWarps x 2048 counters), added up at the end of the CTA
+constexpr int kMadThreads = 256, kMadWarps = kMadThreads / 32;
 template <int LEVEL>
-__global__ void __launch_bounds__(512) mad_hist_kernel(const uint32_t* __restrict__ eabs,
-                                                       const DevScalars* __restrict__ sc, double* __restrict__ mh) {
+__global__ void __launch_bounds__(kMadThreads) mad_hist_kernel(const uint32_t* __restrict__ eabs,
+                                                               const DevScalars* __restrict__ sc, double* __restrict__ mh) {
   constexpr int NB = LEVEL == 2 ? kMadBins2 : kMadBins0;
-  constexpr int NT = LEVEL == 0 ? 1 : 2;
-  __shared__ unsigned int h[NT * NB];
+  constexpr int NT = LEVEL == 0 ? kMadWarps : 2;
+  extern __shared__ unsigned int h[];                  // [NT][NB]
   for (int i = threadIdx.x; i < NT * NB; i += blockDim.x) h[i] = 0u;
   __syncthreads();
   const unsigned long long n = sc->eabs_fill;
   const uint32_t p0 = sc->mad_pre[0], p1 = sc->mad_pre[1];
-  const int lane = threadIdx.x & 31;
+  unsigned int* hw = h + (LEVEL == 0 ? (threadIdx.x >> 5) * NB : 0);
   for (unsigned long long q = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; q < n;
        q += (unsigned long long)gridDim.x * blockDim.x) {
     const uint32_t b = __ldg(eabs + q);
+    if (b >= 0x80000000u) continue;                      // padding slot (kEabsPad)
     if (LEVEL == 0) {
-      // |e| concentrates in few top-11-bit bins: lanes with the same bin add once (match_any)
-      const uint32_t bin = b >= 0x80000000u ? 0xFFFFFFFFu : (b >> 21);
-      const unsigned peers = __match_any_sync(__activemask(), bin);
-      if (bin != 0xFFFFFFFFu && lane == __ffs(peers) - 1) atomicAdd(&h[bin], (unsigned)__popc(peers));
+      atomicAdd(&hw[b >> 21], 1u);
       continue;
     }
-    if (b >= 0x80000000u) continue;                      // padding slot (kEabsPad)
     if (LEVEL == 1) {
       const uint32_t pf = b >> 21, bin = (b >> 10) & 2047u;
       if (pf == p0) atomicAdd(&h[bin], 1u);
@@ -1274,8 +1274,16 @@ __global__ void __launch_bounds__(512) mad_hist_kernel(const uint32_t* __restric
   }
   __syncthreads();
   double* dst = mh + (LEVEL == 0 ? 0 : LEVEL == 1 ? kMadBins0 : kMadBins0 + 2 * kMadBins1);
-  for (int i = threadIdx.x; i < NT * NB; i += blockDim.x)
-    if (h[i]) atomicAdd(dst + i, (double)h[i]);
+  if (LEVEL == 0) {
+    for (int i = threadIdx.x; i < NB; i += blockDim.x) {
+      unsigned int t = 0;
+      for (int w = 0; w < kMadWarps; ++w) t += h[w * NB + i];
+      if (t) atomicAdd(dst + i, (double)t);
+    }
+  } else {
+    for (int i = threadIdx.x; i < NT * NB; i += blockDim.x)
+      if (h[i]) atomicAdd(dst + i, (double)h[i]);
+  }
 }
 
 template <int LEVEL>
@@ -1773,14 +1781,18 @@ void launch_eabs_advance(Context& c, const TcStage& st, cudaStream_t s) {
 }
 
 void launch_mad_hist(Context& c, int level, cudaStream_t s) {
-  const int grid = c.num_sm * 4;
+  const int grid = c.num_sm * 3;           // (level 0: three 64 KB CTAs per SM)
+  static uint64_t attr = 0;
+  const size_t sm0 = (size_t)kMadWarps * kMadBins0 * 4;
+  if (first_on_device(attr))
+    cudaFuncSetAttribute(mad_hist_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm0);
   if (level == 0) {
     cudaMemsetAsync(c.mhist, 0, kMadHist * sizeof(double), s);
-    mad_hist_kernel<0><<<grid, 512, 0, s>>>(c.eabs, c.sc, c.mhist);
+    mad_hist_kernel<0><<<grid, kMadThreads, sm0, s>>>(c.eabs, c.sc, c.mhist);
   } else if (level == 1) {
-    mad_hist_kernel<1><<<grid, 512, 0, s>>>(c.eabs, c.sc, c.mhist);
+    mad_hist_kernel<1><<<grid, kMadThreads, 2 * kMadBins1 * 4, s>>>(c.eabs, c.sc, c.mhist);
   } else {
-    mad_hist_kernel<2><<<grid, 512, 0, s>>>(c.eabs, c.sc, c.mhist);
+    mad_hist_kernel<2><<<grid, kMadThreads, 2 * kMadBins2 * 4, s>>>(c.eabs, c.sc, c.mhist);
   }
   c.launches++;
 }
