@@ -342,7 +342,9 @@ trd_status block_pass1(Context* c, const BlockPlan& bp) {
     if (!stg.valid) {                       // a2: stage the sketch in tile order
       launch_tc_stage(*c, bp, stg, s);
       stg.valid = stg.invariant;
-      tl_mark(c, s, "stage");
+      static const char* kStageLabel[kMaxN] = {"stage k=0", "stage k=1", "stage k=2", "stage k=3",
+                                               "stage k=4", "stage k=5", "stage k=6", "stage k=7"};
+      tl_mark(c, s, kStageLabel[bp.k]);
     }
   }
   const bool pe = c->prof || c->capturing;

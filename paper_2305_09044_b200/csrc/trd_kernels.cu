@@ -784,6 +784,16 @@ __global__ void phi_kernel(const double* __restrict__ C, int rk, int rk1, double
 // ----------------------------------------------------------------------------------------
 constexpr int kSolveThreads = 1024;
 
+// tr(G) by warp 0: lane l sums G[i][i] for i = l, l + 32, .. in order, then a fixed butterfly
+// (the diagonal is read in parallel; a single-thread loop of dependent global loads cost ~25 us)
+__device__ __forceinline__ void tr_s_warp(const double* __restrict__ G, int n, double* out) {
+  const int lane = threadIdx.x & 31;
+  double t = 0.0;
+  for (int i = lane; i < n; i += 32) t += G[(int64_t)i * n + i];
+  for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+  if (lane == 0) *out = t;
+}
+
 // forward (L Y = B) then backward (L^T X = Y) substitution, in place on the n x n matrix
 // B (row-major, column j = one right-hand side).  8 lanes cooperate on one column.
 __device__ void chol_solve_inplace(const double* L, double* B, int n) {
@@ -827,11 +837,7 @@ solve_kernel(const double* __restrict__ G, int n, double lambda_rel, double* __r
   __shared__ double tr_s;
   __shared__ int fail_s;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-  if (threadIdx.x == 0) {
-    double tr = 0.0;
-    for (int i = 0; i < n; ++i) tr += G[i * n + i];
-    tr_s = tr;
-  }
+  if (threadIdx.x < 32) tr_s_warp(G, n, &tr_s);
   __syncthreads();
   double lam = lambda_rel * tr_s / n;
   int attempt = 0;
@@ -911,11 +917,7 @@ __global__ void __launch_bounds__(1024) gj_solve_kernel(const double* __restrict
   __shared__ double tr_s;
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
   double a[NB][NB];
-  if (threadIdx.x == 0) {
-    double tr = 0.0;
-    for (int i = 0; i < n; ++i) tr += G[i * n + i];
-    tr_s = tr;
-  }
+  if (threadIdx.x < 32) tr_s_warp(G, n, &tr_s);
   __syncthreads();
   double lam = lambda_rel * tr_s / n;
   for (int attempt = 0;; ++attempt) {
@@ -1026,11 +1028,7 @@ __global__ void __launch_bounds__(256) gj2_solve_kernel(const double* __restrict
   const int tid = threadIdx.x, lane = tid & 31;
   const int row = tid >> 1, half = tid & 1;
   const bool act = row < NP;
-  if (tid == 0) {
-    double tr = 0.0;
-    for (int i = 0; i < n; ++i) tr += G[i * n + i];
-    tr_s = tr;
-  }
+  if (tid < 32) tr_s_warp(G, n, &tr_s);
   __syncthreads();
   double lam = lambda_rel * tr_s / n;
   double a[HC];
@@ -1254,15 +1252,11 @@ __global__ void __launch_bounds__(kMadThreads) mad_hist_kernel(const uint32_t* _
   const unsigned long long n = sc->eabs_fill;
   const uint32_t p0 = sc->mad_pre[0], p1 = sc->mad_pre[1];
   unsigned int* hw = h + (LEVEL == 0 ? (threadIdx.x >> 5) * NB : 0);
-  for (unsigned long long q = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; q < n;
-       q += (unsigned long long)gridDim.x * blockDim.x) {
-    const uint32_t b = __ldg(eabs + q);
-    if (b >= 0x80000000u) continue;                      // padding slot (kEabsPad)
+  auto count = [&](uint32_t b) {
+    if (b >= 0x80000000u) return;                        // padding slot (kEabsPad)
     if (LEVEL == 0) {
       atomicAdd(&hw[b >> 21], 1u);
-      continue;
-    }
-    if (LEVEL == 1) {
+    } else if (LEVEL == 1) {
       const uint32_t pf = b >> 21, bin = (b >> 10) & 2047u;
       if (pf == p0) atomicAdd(&h[bin], 1u);
       if (pf == p1) atomicAdd(&h[NB + bin], 1u);
@@ -1271,7 +1265,25 @@ __global__ void __launch_bounds__(kMadThreads) mad_hist_kernel(const uint32_t* _
       if (pf == p0) atomicAdd(&h[bin], 1u);
       if (pf == p1) atomicAdd(&h[NB + bin], 1u);
     }
+  };
+  // 16-byte loads, four in flight per thread (memory-level parallelism for the 3+ GB scans)
+  const unsigned long long n4 = n / 4;
+  const uint4* e4 = reinterpret_cast<const uint4*>(eabs);
+  const unsigned long long step = (unsigned long long)gridDim.x * blockDim.x;
+  unsigned long long q = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x;
+  for (; q + 3 * step < n4; q += 4 * step) {
+    uint4 v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) v[u] = __ldg(e4 + q + u * step);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) { count(v[u].x); count(v[u].y); count(v[u].z); count(v[u].w); }
   }
+  for (; q < n4; q += step) {
+    const uint4 v = __ldg(e4 + q);
+    count(v.x); count(v.y); count(v.z); count(v.w);
+  }
+  for (unsigned long long t = n4 * 4 + blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; t < n; t += step)
+    count(__ldg(eabs + t));
   __syncthreads();
   double* dst = mh + (LEVEL == 0 ? 0 : LEVEL == 1 ? kMadBins0 : kMadBins0 + 2 * kMadBins1);
   if (LEVEL == 0) {
@@ -1286,43 +1298,60 @@ __global__ void __launch_bounds__(kMadThreads) mad_hist_kernel(const uint32_t* _
   }
 }
 
+// The target bins: a block-wide exclusive scan of the (integer) counts, each thread checks its
+// two bins for the one that holds the target rank (one CTA of 1024 threads, bins <= 2048)
+__device__ __forceinline__ void mad_find_bin(const double* __restrict__ h, int nb, long long r, int* bin_out,
+                                             long long* rank_out) {
+  using Scan = cub::BlockScan<long long, 1024>;
+  __shared__ typename Scan::TempStorage tmp;
+  const int t = threadIdx.x;
+  const long long c0 = 2 * t < nb ? (long long)h[2 * t] : 0ll;
+  const long long c1 = 2 * t + 1 < nb ? (long long)h[2 * t + 1] : 0ll;
+  long long ex;
+  Scan(tmp).ExclusiveSum(c0 + c1, ex);
+  if (2 * t < nb && ex <= r && r < ex + c0) { *bin_out = 2 * t; *rank_out = r - ex; }
+  if (2 * t + 1 < nb && ex + c0 <= r && r < ex + c0 + c1) { *bin_out = 2 * t + 1; *rank_out = r - ex - c0; }
+  __syncthreads();
+}
+
 template <int LEVEL>
-__global__ void mad_scan_kernel(const double* __restrict__ mh, DevScalars* sc) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+__global__ void __launch_bounds__(1024) mad_scan_kernel(const double* __restrict__ mh, DevScalars* sc) {
+  __shared__ int bin_s;
+  __shared__ long long rank_s;
+  __shared__ long long n_s;
   if (LEVEL == 0) {
-    double n = 0.0;
-    for (int b = 0; b < kMadBins0; ++b) n += mh[b];
-    sc->mad_n = n;
-    const long long ni = (long long)n;
-    const long long r[2] = {ni > 0 ? (ni - 1) / 2 : 0, ni / 2};
-    for (int t = 0; t < 2; ++t) {
-      long long cum = 0;
-      int b = 0;
-      for (; b < kMadBins0 - 1; ++b) {
-        if (cum + (long long)mh[b] > r[t]) break;
-        cum += (long long)mh[b];
-      }
-      sc->mad_pre[t] = (uint32_t)b;
-      sc->mad_rank[t] = r[t] - cum;
-    }
-    return;
+    // n = total count (block reduction of the level-0 bins)
+    using Red = cub::BlockReduce<long long, 1024>;
+    __shared__ typename Red::TempStorage rt;
+    long long c = 0;
+    for (int b = threadIdx.x; b < kMadBins0; b += blockDim.x) c += (long long)mh[b];
+    const long long n = Red(rt).Sum(c);
+    if (threadIdx.x == 0) { n_s = n; sc->mad_n = (double)n; }
+    __syncthreads();
   }
-  const int NB = LEVEL == 1 ? kMadBins1 : kMadBins2;
-  const double* h0 = mh + (LEVEL == 1 ? kMadBins0 : kMadBins0 + 2 * kMadBins1);
-  float v[2];
+  const int NB = LEVEL == 0 ? kMadBins0 : (LEVEL == 1 ? kMadBins1 : kMadBins2);
+  const double* h0 = mh + (LEVEL == 0 ? 0 : LEVEL == 1 ? kMadBins0 : kMadBins0 + 2 * kMadBins1);
+  float v[2] = {0.f, 0.f};
   for (int t = 0; t < 2; ++t) {
-    const double* h = h0 + t * NB;
-    long long cum = 0;
-    int b = 0;
-    for (; b < NB - 1; ++b) {
-      if (cum + (long long)h[b] > sc->mad_rank[t]) break;
-      cum += (long long)h[b];
+    long long r;
+    if (LEVEL == 0) {
+      const long long ni = n_s;
+      r = t == 0 ? (ni > 0 ? (ni - 1) / 2 : 0) : ni / 2;
+    } else {
+      r = sc->mad_rank[t];
     }
-    sc->mad_rank[t] -= cum;
-    if (LEVEL == 1) sc->mad_pre[t] = (sc->mad_pre[t] << 11) | (uint32_t)b;
-    else v[t] = __uint_as_float((sc->mad_pre[t] << 10) | (uint32_t)b);
+    if (threadIdx.x == 0) { bin_s = NB - 1; rank_s = 0; }
+    __syncthreads();
+    mad_find_bin(h0 + (LEVEL == 0 ? 0 : t * NB), NB, r, &bin_s, &rank_s);
+    if (threadIdx.x == 0) {
+      sc->mad_rank[t] = rank_s;
+      if (LEVEL == 0) sc->mad_pre[t] = (uint32_t)bin_s;
+      else if (LEVEL == 1) sc->mad_pre[t] = (sc->mad_pre[t] << 11) | (uint32_t)bin_s;
+      else v[t] = __uint_as_float((sc->mad_pre[t] << 10) | (uint32_t)bin_s);
+    }
+    __syncthreads();
   }
-  if (LEVEL == 2) sc->mad_med = sc->mad_n > 0.0 ? 0.5 * ((double)v[0] + (double)v[1]) : 0.0;
+  if (LEVEL == 2 && threadIdx.x == 0) sc->mad_med = sc->mad_n > 0.0 ? 0.5 * ((double)v[0] + (double)v[1]) : 0.0;
 }
 
 // pass 1 of a staged block wrote its tile slots (padding included) at eabs_fill + [0, total)
@@ -1462,12 +1491,21 @@ error_kernel(PassArgs a, const float* __restrict__ ref, const uint32_t* __restri
   }
 }
 
+// 256 threads: thread t folds partials t, t + 256, .. (fixed order), then a fixed tree
 __global__ void error_reduce_kernel(const double* __restrict__ part, int n, double* __restrict__ out) {
-  if (threadIdx.x < 6 && blockIdx.x == 0) {
-    double v = 0.0;
-    for (int b = 0; b < n; ++b) v = (threadIdx.x == 5) ? fmax(v, part[b * 6 + threadIdx.x]) : v + part[b * 6 + threadIdx.x];
-    out[threadIdx.x] = v;
+  __shared__ double red[6][256];
+  double v[6] = {0, 0, 0, 0, 0, 0};
+  for (int b = threadIdx.x; b < n; b += blockDim.x)
+    for (int j = 0; j < 6; ++j) v[j] = (j == 5) ? fmax(v[j], part[b * 6 + j]) : v[j] + part[b * 6 + j];
+  for (int j = 0; j < 6; ++j) red[j][threadIdx.x] = v[j];
+  __syncthreads();
+  for (int w = 128; w > 0; w >>= 1) {
+    if (threadIdx.x < w)
+      for (int j = 0; j < 6; ++j)
+        red[j][threadIdx.x] = (j == 5) ? fmax(red[j][threadIdx.x], red[j][threadIdx.x + w]) : red[j][threadIdx.x] + red[j][threadIdx.x + w];
+    __syncthreads();
   }
+  if (threadIdx.x < 6) out[threadIdx.x] = red[threadIdx.x][0];
 }
 
 __global__ void popc_kernel(const uint32_t* __restrict__ mask, int64_t nw, uint32_t* __restrict__ out) {
@@ -1798,9 +1836,9 @@ void launch_mad_hist(Context& c, int level, cudaStream_t s) {
 }
 
 void launch_mad_scan(Context& c, int level, cudaStream_t s) {
-  if (level == 0) mad_scan_kernel<0><<<1, 32, 0, s>>>(c.mhist, c.sc);
-  else if (level == 1) mad_scan_kernel<1><<<1, 32, 0, s>>>(c.mhist, c.sc);
-  else mad_scan_kernel<2><<<1, 32, 0, s>>>(c.mhist, c.sc);
+  if (level == 0) mad_scan_kernel<0><<<1, 1024, 0, s>>>(c.mhist, c.sc);
+  else if (level == 1) mad_scan_kernel<1><<<1, 1024, 0, s>>>(c.mhist, c.sc);
+  else mad_scan_kernel<2><<<1, 1024, 0, s>>>(c.mhist, c.sc);
   c.launches++;
 }
 
@@ -1820,7 +1858,7 @@ void launch_error(Context& c, const float* ref, const uint32_t* eval_bits, doubl
   PassArgs a = make_pass_args(c, bp);
   const int nb = 148 * 4;
   error_kernel<<<nb, 256, 0, s>>>(a, ref, eval_bits, c.dpart);
-  error_reduce_kernel<<<1, 32, 0, s>>>(c.dpart, nb, out6);
+  error_reduce_kernel<<<1, 256, 0, s>>>(c.dpart, nb, out6);
   c.launches += 2;
 }
 

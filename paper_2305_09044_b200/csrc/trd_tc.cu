@@ -759,15 +759,22 @@ __global__ void __launch_bounds__(128) stage_vals_kernel(StageArgs s) {
       // linear positions per column, so its packed values are consecutive.  The columns' row
       // masks come from the staged row masks by a warp bit-matrix transpose (no mask reads)
       const uint32_t cws[2] = {warp_transpose32((uint32_t)bits, lane), warp_transpose32((uint32_t)(bits >> 32), lane)};
-#pragma unroll 1
+      // both columns' rank lookups first (independent loads in flight), then their entries
+      int64_t la[2], lb[2], va[2], vb[2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int64_t co = sco[lane + 32 * h];
+        la[h] = wr.baseA + co;                           // linear positions of lanes 0, b
+        lb[h] = wr.baseB + co;
+        const bool act = co >= 0 && cws[h] != 0u;
+        va[h] = (s.packed && act) ? mask_rank(s, la[h]) : la[h];
+        vb[h] = (s.packed && act && wr.b < 32) ? mask_rank(s, lb[h]) : lb[h];
+      }
+#pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int j = lane + 32 * h;
-        const int64_t co = sco[j];
         uint32_t cw = cws[h];
-        if (co < 0 || !cw) continue;
-        const int64_t la = wr.baseA + co, lb = wr.baseB + co;   // linear positions of lanes 0, b
-        const int64_t va = s.packed ? mask_rank(s, la) : la;
-        const int64_t vb = (s.packed && wr.b < 32) ? mask_rank(s, lb) : lb;
+        if (sco[j] < 0) cw = 0u;
         int qa = 0, qb = 0;
         while (cw) {
           const int r = __ffs(cw) - 1;
@@ -775,8 +782,8 @@ __global__ void __launch_bounds__(128) stage_vals_kernel(StageArgs s) {
           const int rr = warp * 32 + r;                   // row in the tile
           const int pos = soff[rr] + __popcll(sbits[rr] & ((1ull << j) - 1ull));
           int64_t vi;
-          if (r < wr.b) vi = s.packed ? va + qa++ : la + r;
-          else vi = s.packed ? vb + qb++ : lb + (r - wr.b);
+          if (r < wr.b) vi = s.packed ? va[h] + qa++ : la[h] + r;
+          else vi = s.packed ? vb[h] + qb++ : lb[h] + (r - wr.b);
           ov[pos] = __ldg(s.values + vi);
           oi[pos] = (uint16_t)(rr * TC_NT + j);
         }
@@ -1140,9 +1147,21 @@ __global__ void tc_reduce_final_kernel(const double* __restrict__ dpart, int64_t
     }
     return;
   }
+  // statistics: thread t sums the CTA partials t, t + 128, ... (fixed order), then a fixed
+  // tree over the threads (the partials are read in parallel, not by one thread)
+  __shared__ double red[3][128];
+  double v[3] = {0.0, 0.0, 0.0};
+  for (int64_t q = threadIdx.x; q < nparts; q += blockDim.x)
+    for (int j = 0; j < 3; ++j) v[j] += spart[q * 3 + j];
+  for (int j = 0; j < 3; ++j) red[j][threadIdx.x] = v[j];
+  __syncthreads();
+  for (int w = 64; w > 0; w >>= 1) {
+    if (threadIdx.x < w)
+      for (int j = 0; j < 3; ++j) red[j][threadIdx.x] += red[j][threadIdx.x + w];
+    __syncthreads();
+  }
   if (threadIdx.x < 3) {
-    double t = 0.0;
-    for (int64_t q = 0; q < nparts; ++q) t += spart[q * 3 + threadIdx.x];
+    const double t = red[threadIdx.x][0];
     dvec[Ik_tot * R2 + threadIdx.x] = t;
     if (threadIdx.x == 2 && sc && sc->prof_on) sc->prof_nobs[kblk] += t;
   }
@@ -1214,11 +1233,20 @@ void launch_tc_stage(Context& c, const BlockPlan& bp, TcStage& st, cudaStream_t 
     a.fib_s0 = (int)bp.s[0];
     a.idx0 = c.idx + c.idx_off[0];
   }
-  const int grid = (int)std::min<int64_t>(a.n_tiles, 148 * 16);
-  stage_bits_kernel<<<grid, TC_M, 0, s>>>(a);
+  // grids of exactly the resident CTAs (the kernels loop over tiles): no partial last wave
+  static int occ_bits = 0, occ_vals = 0;
+  if (!occ_bits) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_bits, stage_bits_kernel, TC_M, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_vals, stage_vals_kernel, TC_M, 0);
+    occ_bits = std::max(occ_bits, 1);
+    occ_vals = std::max(occ_vals, 1);
+  }
+  const int gb = (int)std::min<int64_t>(a.n_tiles, (int64_t)c.num_sm * occ_bits);
+  const int gv = (int)std::min<int64_t>(a.n_tiles, (int64_t)c.num_sm * occ_vals);
+  stage_bits_kernel<<<gb, TC_M, 0, s>>>(a);
   cudaMemsetAsync(st.tbase + a.n_tiles, 0, sizeof(uint64_t), s);   // tbase[n_tiles] = total
   cub::DeviceScan::ExclusiveSum(st.scan_tmp, st.scan_tmp_bytes, st.tbase, st.tbase, (int)a.n_tiles + 1, s);
-  stage_vals_kernel<<<grid, TC_M, 0, s>>>(a);
+  stage_vals_kernel<<<gv, TC_M, 0, s>>>(a);
   c.launches += 3;
 }
 
