@@ -354,6 +354,17 @@ trd_status block_pass1(Context* c, const BlockPlan& bp) {
   if (pe) prof_pair(c, 1, e0, prof_event(c));
   tl_mark(c, s, "pass 1");
   if (bp.use_tc && c->eabs) launch_eabs_advance(*c, stg, s);   // R21 |e| slots of this block
+  if (getenv("TRD_DEBUG_MAD") && c->eabs && !c->capturing && c->eabs_cap < (1u << 22)) {   // (diagnostic)
+    DevScalars hs;
+    cudaMemcpyAsync(&hs, c->sc, sizeof(hs), cudaMemcpyDeviceToHost, s);
+    std::vector<uint32_t> e(c->eabs_cap);
+    cudaMemcpyAsync(e.data(), c->eabs, c->eabs_cap * 4, cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+    unsigned long long sum = 0;
+    for (size_t i = 0; i < (size_t)hs.eabs_fill && i < e.size(); ++i) sum += e[i];
+    fprintf(stderr, "[trd mad blk %d] use_tc %d fill %llu sum %llu e0 %08x %08x err %s\n", bp.k, bp.use_tc, hs.eabs_fill,
+            sum, e[0], e[1], cudaGetErrorString(cudaGetLastError()));
+  }
   if (bp.use_tc) launch_tc_reduce_d(*c, bp, s);
   else launch_reduce_d(*c, bp, s);
   trd_status st = check_launch(c, "pass 1");
@@ -385,6 +396,16 @@ trd_status block_pass2(Context* c, const BlockPlan& bp) {
   tl_mark(c, s, "pass 2");
   launch_reduce_den(*c, bp, s);
   tl_mark(c, s, "reduce den");
+  if (getenv("TRD_DEBUG_MAD") && !c->capturing) {               // (diagnostic)
+    DevScalars hs;
+    double nd[2];
+    cudaMemcpyAsync(&hs, c->sc, sizeof(hs), cudaMemcpyDeviceToHost, s);
+    cudaMemcpyAsync(nd, c->red_ws, 16, cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+    fprintf(stderr, "[trd blk %d] den %.6g num %.6g lam %.3g h_lam %.3g sigma %.6g amax x %g a %g b %g nobs %.0f\n", bp.k,
+            nd[0], nd[1], hs.lambda, hs.h_lam, hs.sigma, (double)__builtin_bit_cast(float, hs.amax_x),
+            (double)__builtin_bit_cast(float, hs.amax_a), (double)__builtin_bit_cast(float, hs.amax_b), hs.n_obs);
+  }
   trd_status st = check_launch(c, "pass 2");
   if (st) return st;
   return allreduce(c, c->red_ws, 1);
@@ -779,11 +800,22 @@ trd_status trd_init_ex(const trd_config* cfg, const trd_shard* shard, const floa
       sg.scan_tmp_bytes = tc_scan_tmp_bytes(sg.n_tiles);
       if ((st = dalloc(c, &sg.tbits, (size_t)sg.n_tiles * 128)) ||
           (st = dalloc(c, &sg.troff, (size_t)sg.n_tiles * 128)) ||
+          (st = dalloc(c, &sg.tcount, (size_t)sg.n_tiles + 1)) ||
           (st = dalloc(c, &sg.tbase, (size_t)sg.n_tiles + 1)) ||
           (st = dalloc(c, &sg.tvals, (size_t)sg.vcap)) || (st = dalloc(c, &sg.tidx, (size_t)sg.vcap)) ||
           (st = dalloc(c, reinterpret_cast<char**>(&sg.scan_tmp), sg.scan_tmp_bytes + 16)))
         return bail(st);
       max_v = std::max(max_v, sg.vcap);
+      CUDA_TRY(c, cudaMemsetAsync(sg.tcount, 0, ((size_t)sg.n_tiles + 1) * sizeof(uint64_t), c->stream));
+      // layout cache of a sweep-invariant sketch (value indices fit int32): an upload whose mask
+      // equals the staged one only re-gathers the values (e2e restaging)
+      if (sg.invariant && (c->packed || c->n_local < (1LL << 31)) && !getenv("TRD_NO_PERM")) {
+        if ((st = dalloc(c, &sg.perm, (size_t)sg.vcap))) return bail(st);
+        if (!c->stage_mask) {
+          if ((st = dalloc(c, &c->stage_mask, (size_t)c->n_words))) return bail(st);
+          CUDA_TRY(c, cudaMemcpyAsync(c->stage_mask, c->mask, c->n_words * 4, cudaMemcpyDeviceToDevice, c->stream));
+        }
+      }
     }
     if (max_v > 0 && (st = dalloc(c, &c->tw, (size_t)max_v))) return bail(st);
   }
@@ -819,6 +851,7 @@ trd_status trd_init_ex(const trd_config* cfg, const trd_shard* shard, const floa
   DevScalars hs;
   memset(&hs, 0, sizeof(hs));
   hs.sigma = cfg->sigma_mode == TRD_SIGMA_FIXED ? cfg->sigma : (cfg->sigma_mode == TRD_SIGMA_INF ? INFINITY : 1.0);
+  hs.mask_gen = 1;                             // (layout_gen = 0: no staged layout built yet)
   CUDA_TRY(c, cudaMemcpyAsync(c->sc, &hs, sizeof(hs), cudaMemcpyHostToDevice, s));
   CUDA_TRY(c, cudaMemsetAsync(c->Dprev, 0, (size_t)(In * In) * 8, s));
   launch_amax_obs(*c, s);
@@ -892,7 +925,8 @@ static trd_status consume_upload(Context* c) {
   c->mask = c->own_mask;
   if (c->packed) launch_rank_prefix(*c, c->stream);
   launch_amax_obs(*c, c->stream);
-  for (int k = 0; k < c->N; ++k) c->stage[k].valid = false;   // staged sketches are stale
+  if (c->stage_mask) launch_mask_compare(*c, c->stream);      // staged layouts reusable?
+  for (int k = 0; k < c->N; ++k) c->stage[k].valid = false;   // staged values are stale
   return check_launch(c, "upload consume");
 }
 
@@ -939,6 +973,13 @@ static trd_status enqueue_sweep(Context* c) {
     if ((st = check_launch(c, "update"))) return st;
   }
   if (c->eabs && (st = mad_select(c))) return st;         // R21 (histograms allreduced)
+  if (getenv("TRD_DEBUG_MAD") && c->eabs && !c->capturing) {   // (diagnostic)
+    DevScalars hs;
+    cudaMemcpyAsync(&hs, c->sc, sizeof(hs), cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+    fprintf(stderr, "[trd mad] fill %llu cap %zu n %.0f med %.9g pre %u %u rank %lld %lld\n", hs.eabs_fill,
+            c->eabs_cap, hs.mad_n, hs.mad_med, hs.mad_pre[0], hs.mad_pre[1], hs.mad_rank[0], hs.mad_rank[1]);
+  }
   launch_sweep_end(*c, s);
   tl_mark(c, s, "sweep end (D^t, sigma)");
   if (c->cfg.world > 1) {                 // replica consistency of the replicated cores
@@ -1260,7 +1301,7 @@ void trd_destroy(trd_ctx* ctx) {
                   c->denpart, c->numpart, c->dvec, c->G, c->G_last, c->Mop, c->chol_ws,
                   c->chain_ws, c->h, c->Dcur, c->Dprev, c->sc, c->stats, c->red_ws,
                   c->lftHL, c->lfthHL, c->lscl, c->lsclh, c->rgtHL, c->rgtHL2, c->contrib, c->Qloc, c->Gloc, c->mhist,
-                  c->eabs, c->chk, c->chk_acc};
+                  c->eabs, c->chk, c->chk_acc, c->stage_mask};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->tw) cudaFree(c->tw);
@@ -1268,7 +1309,7 @@ void trd_destroy(trd_ctx* ctx) {
   if (getenv("TRD_TC_EXP")) tc_debug_dump();
   for (int k = 0; k < kMaxN; ++k) {
     TcStage& sg = c->stage[k];
-    void* sp[] = {sg.tbits, sg.troff, sg.tbase, sg.tvals, sg.tidx, sg.scan_tmp};
+    void* sp[] = {sg.tbits, sg.troff, sg.tcount, sg.tbase, sg.tvals, sg.tidx, sg.scan_tmp, sg.perm};
     for (void* p : sp)
       if (p) cudaFree(p);
   }

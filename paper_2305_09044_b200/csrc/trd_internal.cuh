@@ -66,6 +66,9 @@ struct DevScalars {
   int not_spd;           // Cholesky failed after retries
   int nonfinite;         // non-finite value detected
   int replica_bad;       // world > 1: a sweep ended with differing replicas
+  int mask_same;         // the last uploaded mask equalled stage_mask
+  int mask_gen;          // generation of the current mask (bumped when an upload changes it)
+  int layout_gen[kMaxN]; // generation of the mask each block's staged layout was built from
   double acc_e2, acc_n;  // sweep accumulators for the RMS sigma rule (R9)
   double stop_e;         // relative change of D^t
   int have_prev_D;
@@ -130,13 +133,15 @@ struct BlockPlan {
 struct TcStage {
   uint64_t* tbits = nullptr;     // [tile][128] observation mask of (row, 64 columns)
   uint16_t* troff = nullptr;     // [tile][128] row offset into the tile's compacted values
-  uint64_t* tbase = nullptr;     // [tile] exclusive prefix of the tile counts
+  uint64_t* tcount = nullptr;    // [tile + 1] padded tile counts (last = 0)
+  uint64_t* tbase = nullptr;     // [tile + 1] exclusive prefix of the tile counts
   float* tvals = nullptr;        // compacted observed values, tile-major, row-major in a tile,
                                  // tile blocks padded to 8 entries
   uint16_t* tidx = nullptr;      // entry list: row * 64 + column per value, 0xFFFF = padding
   void* scan_tmp = nullptr;
   size_t scan_tmp_bytes = 0;
   int64_t n_tiles = 0, vcap = 0;
+  int32_t* perm = nullptr;       // invariant sketches: value index of every staged slot
   bool invariant = false;        // working set identical every sweep (full index sets)
   bool valid = false;            // staged data current
 };
@@ -186,6 +191,7 @@ struct Context {
   cudaEvent_t ev_up_ready[2] = {nullptr, nullptr}, ev_up_free = nullptr;
   int64_t n_values = 0;
   uint32_t* rank_prefix = nullptr;     // packed layout: exclusive popcount prefix per word
+  uint32_t* stage_mask = nullptr;      // the mask the invariant staged layouts were built from
   void* rp_tmp = nullptr;              // its scan's scratch (allocated once)
   size_t rp_tmp_bytes = 0;
 
@@ -294,6 +300,7 @@ void launch_error(Context& c, const float* ref, const uint32_t* eval_bits, doubl
 void launch_rank_prefix(Context& c, cudaStream_t s);
 void launch_count_bits(Context& c, unsigned long long* out, cudaStream_t s);
 void launch_amax_obs(Context& c, cudaStream_t s);   // sc->amax_x of the observed values
+void launch_mask_compare(Context& c, cudaStream_t s); // sc->mask_same; stage_mask <- mask
 void launch_sweep_begin(Context& c, cudaStream_t s);
 
 // ---- tensor-core pass kernels (trd_tc.cu) ---------------------------------------------

@@ -1181,7 +1181,10 @@ __global__ void block_scalars_kernel(const double* __restrict__ dvec, int64_t Ik
   st.sum_e2 += sc->sum_e2;
   st.welsch += sc->welsch;
   if (eta == 0.0) st.skipped |= (1u << k);
-  if (!(eta == eta) || isinf(eta) || !(sc->num == sc->num)) { st.nonfinite = 1; sc->nonfinite = 1; }
+  if (!(eta == eta) || isinf(eta) || !(sc->num == sc->num) || !(sc->den == sc->den) || isinf(sc->den)) {
+    st.nonfinite = 1;
+    sc->nonfinite = 1;
+  }
   sc->acc_e2 += sc->sum_e2;
   sc->acc_n += sc->n_obs;
 }
@@ -1517,13 +1520,11 @@ __global__ void popc_kernel(const uint32_t* __restrict__ mask, int64_t nw, uint3
 // ----------------------------------------------------------------------------------------
 // Launchers
 // ----------------------------------------------------------------------------------------
-// kernel attributes are per device: remember which devices a launcher has configured
+// Kernel attributes are per device, and contexts may be driven from several host threads: the
+// attribute is set before every launch that needs it (a cheap host call; a "done" flag shared
+// between threads let a second thread launch before the first had set it)
 static bool first_on_device(uint64_t& done_mask) {
-  int dev = 0;
-  cudaGetDevice(&dev);
-  const uint64_t bit = 1ull << (dev & 63);
-  if (done_mask & bit) return false;
-  done_mask |= bit;
+  (void)done_mask;
   return true;
 }
 
@@ -1898,6 +1899,33 @@ void launch_amax_obs(Context& c, cudaStream_t s) {
   const int64_t n = c.packed ? c.n_values : c.n_local;
   amax_obs_kernel<<<grid_for(n), 256, 0, s>>>(c.values, c.mask, n, c.packed, c.sc);
   c.launches++;
+}
+
+// mask_same = (mask == stage_mask) over all words (set to 1 before), then stage_mask <- mask
+__global__ void mask_compare_kernel(const uint32_t* __restrict__ m, const uint32_t* __restrict__ ref, int64_t nw,
+                                    int* __restrict__ same) {
+  bool diff = false;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < nw; t += (int64_t)gridDim.x * blockDim.x)
+    diff |= m[t] != ref[t];
+  if (__any_sync(0xffffffffu, diff) && (threadIdx.x & 31) == 0) *same = 0;
+}
+__global__ void mask_copy_kernel(const uint32_t* __restrict__ m, uint32_t* __restrict__ ref, int64_t nw,
+                                 DevScalars* __restrict__ sc) {
+  if (sc->mask_same) return;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < nw; t += (int64_t)gridDim.x * blockDim.x)
+    ref[t] = m[t];
+}
+// a new mask generation (after the copy: every layout built before is stale)
+__global__ void mask_gen_kernel(DevScalars* sc) {
+  if (threadIdx.x == 0 && blockIdx.x == 0 && !sc->mask_same) sc->mask_gen += 1;
+}
+
+void launch_mask_compare(Context& c, cudaStream_t s) {
+  cudaMemsetAsync(&c.sc->mask_same, 1, sizeof(int), s);          // nonzero: same (until a difference)
+  mask_compare_kernel<<<grid_for(c.n_words), 256, 0, s>>>(c.mask, c.stage_mask, c.n_words, &c.sc->mask_same);
+  mask_copy_kernel<<<grid_for(c.n_words), 256, 0, s>>>(c.mask, c.stage_mask, c.n_words, c.sc);
+  mask_gen_kernel<<<1, 32, 0, s>>>(c.sc);
+  c.launches += 3;
 }
 
 void launch_rank_prefix(Context& c, cudaStream_t s) {

@@ -510,7 +510,12 @@ struct StageArgs {
   const float* values;
   uint64_t* tbits;        // [tile][128]
   uint16_t* troff;        // [tile][128]
-  uint64_t* tcount;       // [tile]  (counts, then exclusive prefix)
+  uint64_t* tcount;       // [tile]  padded counts (stage_bits)
+  uint64_t* tbase;        // [tile + 1] their exclusive prefix (the scan; tile block starts)
+  const int* gen_cur;     // sweep-invariant sketch: the current mask generation, and
+  int* gen_layout;        //   the one this block's staged layout was built from (equal: only the
+                          //   values are re-gathered); nullptr otherwise
+  int32_t* perm;          // sweep-invariant sketch: value index of every staged slot (-1 padding)
   float* tvals;           // compacted values (tile blocks padded to 8 entries)
   uint16_t* tidx;         // entry list: (row in tile) * 64 + column, 0xFFFF = padding
   // fibre windows (sampled mode 0 as the fastest column digit, 16 <= s0, I0 <= 128): columns
@@ -634,6 +639,7 @@ __device__ __forceinline__ uint32_t warp_col_bits(const StageArgs& s, const Warp
 }
 
 __global__ void __launch_bounds__(128) stage_bits_kernel(StageArgs s) {
+  if (s.gen_cur && *s.gen_layout == *s.gen_cur) return;   // layout current (same mask): nothing to do
   __shared__ int64_t sco[TC_NT];
   __shared__ uint32_t sstart[2];
   __shared__ int wsum[4];
@@ -725,7 +731,13 @@ __global__ void __launch_bounds__(128) stage_bits_kernel(StageArgs s) {
 // the tile block is assembled in shared memory (scattered entry positions) and written out
 // coalesced; tiles with more than SV_OUT entries write to global memory directly
 constexpr int SV_OUT = 1024;
+// the staged word of value index vi: the value, or (perm mode) the index itself as fp32 bits
+__device__ __forceinline__ float stage_word(const StageArgs& s, int64_t vi) {
+  return s.perm ? __int_as_float((int)vi) : __ldg(s.values + vi);
+}
+
 __global__ void __launch_bounds__(128) stage_vals_kernel(StageArgs s) {
+  if (s.gen_cur && *s.gen_layout == *s.gen_cur) return;   // layout current: gather_vals_kernel re-reads
   __shared__ int64_t sco[TC_NT];
   __shared__ uint32_t sstart[2];
   __shared__ uint64_t sbits[TC_M];
@@ -738,8 +750,8 @@ __global__ void __launch_bounds__(128) stage_vals_kernel(StageArgs s) {
     const int64_t row = rt * TC_M + tid;
     const uint64_t bits = s.tbits[tile * TC_M + tid];
     const int roff = s.troff[tile * TC_M + tid];
-    const int64_t tb = (int64_t)s.tcount[tile];          // tile block start (after the scan)
-    const int nt = (int)((int64_t)s.tcount[tile + 1] - tb);   // padded entry count of the tile
+    const int64_t tb = (int64_t)s.tbase[tile];           // tile block start (after the scan)
+    const int nt = (int)((int64_t)s.tbase[tile + 1] - tb);    // padded entry count of the tile
     const bool in_smem = nt <= SV_OUT;
     float* ov = in_smem ? sov : s.tvals + tb;            // tile-relative output positions
     uint16_t* oi = in_smem ? soi : s.tidx + tb;
@@ -784,7 +796,7 @@ __global__ void __launch_bounds__(128) stage_vals_kernel(StageArgs s) {
           int64_t vi;
           if (r < wr.b) vi = s.packed ? va[h] + qa++ : la[h] + r;
           else vi = s.packed ? vb[h] + qb++ : lb[h] + (r - wr.b);
-          ov[pos] = __ldg(s.values + vi);
+          ov[pos] = stage_word(s, vi);
           oi[pos] = (uint16_t)(rr * TC_NT + j);
         }
       }
@@ -824,7 +836,7 @@ __global__ void __launch_bounds__(128) stage_vals_kernel(StageArgs s) {
               vi = base + p;
             }
             oidx[q] = (uint16_t)(tid * TC_NT + j + u);
-            out[q++] = __ldg(s.values + vi);
+            out[q++] = stage_word(s, vi);
           }
         }
         j += nj;
@@ -849,7 +861,7 @@ __global__ void __launch_bounds__(128) stage_vals_kernel(StageArgs s) {
           vi = (int64_t)cp + __popc(cwd & ((1u << (lin & 31)) - 1u));
         }
         oidx[q] = (uint16_t)(tid * TC_NT + j);
-        out[q++] = __ldg(s.values + vi);
+        out[q++] = stage_word(s, vi);
       }
     } else if (bits) {
       // row-wise over the column runs: a run's observed values are consecutive
@@ -872,7 +884,7 @@ __global__ void __launch_bounds__(128) stage_vals_kernel(StageArgs s) {
             const int jj = __ffsll((long long)b) - 1;
             b &= b - 1;
             oidx[q] = (uint16_t)(tid * TC_NT + j0 + jj);
-            out[q++] = __ldg(s.values + v0 + u);
+            out[q++] = stage_word(s, v0 + u);
           }
         } else {
           uint64_t b = rb;
@@ -880,7 +892,7 @@ __global__ void __launch_bounds__(128) stage_vals_kernel(StageArgs s) {
             const int jj = __ffsll((long long)b) - 1;
             b &= b - 1;
             oidx[q] = (uint16_t)(tid * TC_NT + j0 + jj);
-            out[q++] = __ldg(s.values + lin0 + jj);
+            out[q++] = stage_word(s, lin0 + jj);
           }
         }
       }
@@ -894,6 +906,20 @@ __global__ void __launch_bounds__(128) stage_vals_kernel(StageArgs s) {
     }
     __syncthreads();
   }
+}
+
+__global__ void layout_gen_kernel(const int* __restrict__ cur, int* __restrict__ layout) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) *layout = *cur;
+}
+
+// Sweep-invariant sketches: the staged values from the staged value indices (perm), so that a
+// new upload with an unchanged mask re-gathers the values without rebuilding the layout
+__global__ void __launch_bounds__(256) gather_vals_kernel(const int32_t* __restrict__ perm, const uint16_t* __restrict__ tidx,
+                                                          const float* __restrict__ values,
+                                                          const uint64_t* __restrict__ total, float* __restrict__ tvals) {
+  const int64_t n = (int64_t)*total;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    tvals[i] = tidx[i] == 0xFFFFu ? 0.f : __ldg(values + perm[i]);
 }
 
 // ---------------------------------------------------------------------------------------
@@ -1222,7 +1248,15 @@ void launch_tc_stage(Context& c, const BlockPlan& bp, TcStage& st, cudaStream_t 
   a.packed = c.packed;
   a.row_off = c.row_off; a.col_off = c.col_off;
   a.mask = c.mask; a.rank_prefix = c.rank_prefix; a.values = c.values;
-  a.tbits = st.tbits; a.troff = st.troff; a.tcount = st.tbase; a.tvals = st.tvals; a.tidx = st.tidx;
+  a.tbits = st.tbits; a.troff = st.troff; a.tcount = st.tcount; a.tbase = st.tbase; a.tvals = st.tvals;
+  a.tidx = st.tidx;
+  // sweep-invariant sketch with a layout cache: stage the value indices (perm), then gather; both
+  // layout kernels exit at once when the uploaded mask equals the one the layout was built from
+  const bool cached = st.perm != nullptr;
+  a.gen_cur = cached ? &c.sc->mask_gen : nullptr;
+  a.gen_layout = cached ? &c.sc->layout_gen[bp.k] : nullptr;
+  a.perm = cached ? st.perm : nullptr;
+  if (cached) a.tvals = reinterpret_cast<float*>(st.perm);
   // fibre windows: mode 0 is the fastest column digit with a sampled set of >= 16 positions,
   // I0 <= 128 (a window of five words), and not a partial shard (offsets = global indices)
   a.fib = 0; a.fib_s0 = 0; a.idx0 = nullptr;
@@ -1244,10 +1278,16 @@ void launch_tc_stage(Context& c, const BlockPlan& bp, TcStage& st, cudaStream_t 
   const int gb = (int)std::min<int64_t>(a.n_tiles, (int64_t)c.num_sm * occ_bits);
   const int gv = (int)std::min<int64_t>(a.n_tiles, (int64_t)c.num_sm * occ_vals);
   stage_bits_kernel<<<gb, TC_M, 0, s>>>(a);
-  cudaMemsetAsync(st.tbase + a.n_tiles, 0, sizeof(uint64_t), s);   // tbase[n_tiles] = total
-  cub::DeviceScan::ExclusiveSum(st.scan_tmp, st.scan_tmp_bytes, st.tbase, st.tbase, (int)a.n_tiles + 1, s);
+  // tbase = exclusive prefix of tcount (tcount[n_tiles] = 0: tbase[n_tiles] = total); out of
+  // place, so a skipped stage_bits leaves the same prefix
+  cub::DeviceScan::ExclusiveSum(st.scan_tmp, st.scan_tmp_bytes, st.tcount, st.tbase, (int)a.n_tiles + 1, s);
   stage_vals_kernel<<<gv, TC_M, 0, s>>>(a);
   c.launches += 3;
+  if (cached) {
+    layout_gen_kernel<<<1, 32, 0, s>>>(&c.sc->mask_gen, &c.sc->layout_gen[bp.k]);
+    gather_vals_kernel<<<c.num_sm * 8, 256, 0, s>>>(st.perm, st.tidx, c.values, st.tbase + a.n_tiles, st.tvals);
+    c.launches += 2;
+  }
 }
 
 size_t tc_scan_tmp_bytes(int64_t n_tiles) {

@@ -349,3 +349,54 @@ def test_fibre_window_staging_equals_per_column_lookups(name, dims, sketch, monk
         for a, b in zip(outs[0], outs[1]):
             assert np.array_equal(a, b)
         assert cores_rel_err(outs[1], st.cores) <= 1e-4
+
+
+# ---------------------------------------------------------------- upload layout cache (e2e)
+@pytest.mark.parametrize("packed", [False, True])
+def test_upload_with_changed_mask_restages_the_layout(packed):
+    """Sweep-invariant sketches keep their staged layout across uploads whose mask is unchanged
+    (only the values are re-gathered); an upload with a different mask must rebuild it.  After
+    uploads with (same mask, new values) and then (new mask, new values) the cores equal, bit
+    for bit, those of fresh contexts created on each data set."""
+    _cuda()
+    from paper_2305_09044_b200 import TRD
+    spec = small_spec("C5b", [12, 9, 8, 7, 6])
+    prob = make_problem(spec, keep_mask_bool=True)
+    over = dict(sigma_mode=O.SIGMA_FIXED, sigma=0.8)
+    n = spec.numel
+    mb = prob.mask_bool.clone()
+    # a second mask with the same number of observed entries: the first 64 entries' bits rotated
+    # (packed storage needs an unchanged count)
+    mb2 = mb.clone()
+    mb2[:64] = torch.roll(mb[:64], 7)
+    if not packed:
+        mb2[100:400] = ~mb2[100:400]
+    X1 = prob.X
+    X2 = prob.X * 0.75 + 0.1
+    datasets = [(X2, mb), (X2 * 1.5 - 0.2, mb2)]
+
+    def host_arrays(X, m):
+        vals = X[m] if packed else X
+        return vals.contiguous().cpu().pin_memory(), pack_bits(m).cpu().pin_memory()
+
+    v0, w0 = host_arrays(X1, mb)
+    a = TRD(spec.dims, spec.ranks, v0, w0, prob.init, packed=packed, host=True, sketch=spec.sketch,
+            seed=spec.sampler_seed, **over)
+    a.sweep(1, stats=False)
+    got = []
+    for X, m in datasets:
+        v, w = host_arrays(X, m)
+        a.set_cores(prob.init)
+        a.upload(v, w)
+        a.sweep(1, stats=False)
+        got.append(a.get_cores())
+    a.close()
+    for (X, m), cores in zip(datasets, got):
+        v, w = host_arrays(X, m)
+        b = TRD(spec.dims, spec.ranks, v.cuda(), w.cuda(), prob.init, packed=packed, sketch=spec.sketch,
+                seed=spec.sampler_seed, **over)
+        b.sweep(1, stats=False)
+        ref = b.get_cores()
+        b.close()
+        for x, y in zip(cores, ref):
+            assert np.array_equal(x, y)
