@@ -354,17 +354,6 @@ trd_status block_pass1(Context* c, const BlockPlan& bp) {
   if (pe) prof_pair(c, 1, e0, prof_event(c));
   tl_mark(c, s, "pass 1");
   if (bp.use_tc && c->eabs) launch_eabs_advance(*c, stg, s);   // R21 |e| slots of this block
-  if (getenv("TRD_DEBUG_MAD") && c->eabs && !c->capturing && c->eabs_cap < (1u << 22)) {   // (diagnostic)
-    DevScalars hs;
-    cudaMemcpyAsync(&hs, c->sc, sizeof(hs), cudaMemcpyDeviceToHost, s);
-    std::vector<uint32_t> e(c->eabs_cap);
-    cudaMemcpyAsync(e.data(), c->eabs, c->eabs_cap * 4, cudaMemcpyDeviceToHost, s);
-    cudaStreamSynchronize(s);
-    unsigned long long sum = 0;
-    for (size_t i = 0; i < (size_t)hs.eabs_fill && i < e.size(); ++i) sum += e[i];
-    fprintf(stderr, "[trd mad blk %d] use_tc %d fill %llu sum %llu e0 %08x %08x err %s\n", bp.k, bp.use_tc, hs.eabs_fill,
-            sum, e[0], e[1], cudaGetErrorString(cudaGetLastError()));
-  }
   if (bp.use_tc) launch_tc_reduce_d(*c, bp, s);
   else launch_reduce_d(*c, bp, s);
   trd_status st = check_launch(c, "pass 1");
@@ -396,16 +385,6 @@ trd_status block_pass2(Context* c, const BlockPlan& bp) {
   tl_mark(c, s, "pass 2");
   launch_reduce_den(*c, bp, s);
   tl_mark(c, s, "reduce den");
-  if (getenv("TRD_DEBUG_MAD") && !c->capturing) {               // (diagnostic)
-    DevScalars hs;
-    double nd[2];
-    cudaMemcpyAsync(&hs, c->sc, sizeof(hs), cudaMemcpyDeviceToHost, s);
-    cudaMemcpyAsync(nd, c->red_ws, 16, cudaMemcpyDeviceToHost, s);
-    cudaStreamSynchronize(s);
-    fprintf(stderr, "[trd blk %d] den %.6g num %.6g lam %.3g h_lam %.3g sigma %.6g amax x %g a %g b %g nobs %.0f\n", bp.k,
-            nd[0], nd[1], hs.lambda, hs.h_lam, hs.sigma, (double)__builtin_bit_cast(float, hs.amax_x),
-            (double)__builtin_bit_cast(float, hs.amax_a), (double)__builtin_bit_cast(float, hs.amax_b), hs.n_obs);
-  }
   trd_status st = check_launch(c, "pass 2");
   if (st) return st;
   return allreduce(c, c->red_ws, 1);
@@ -973,13 +952,6 @@ static trd_status enqueue_sweep(Context* c) {
     if ((st = check_launch(c, "update"))) return st;
   }
   if (c->eabs && (st = mad_select(c))) return st;         // R21 (histograms allreduced)
-  if (getenv("TRD_DEBUG_MAD") && c->eabs && !c->capturing) {   // (diagnostic)
-    DevScalars hs;
-    cudaMemcpyAsync(&hs, c->sc, sizeof(hs), cudaMemcpyDeviceToHost, s);
-    cudaStreamSynchronize(s);
-    fprintf(stderr, "[trd mad] fill %llu cap %zu n %.0f med %.9g pre %u %u rank %lld %lld\n", hs.eabs_fill,
-            c->eabs_cap, hs.mad_n, hs.mad_med, hs.mad_pre[0], hs.mad_pre[1], hs.mad_rank[0], hs.mad_rank[1]);
-  }
   launch_sweep_end(*c, s);
   tl_mark(c, s, "sweep end (D^t, sigma)");
   if (c->cfg.world > 1) {                 // replica consistency of the replicated cores
