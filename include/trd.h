@@ -234,6 +234,25 @@ TRD_API trd_status trd_error(trd_ctx* ctx, const float* ref_dev, const uint32_t*
 TRD_API trd_status trd_get_cores(trd_ctx* ctx, float* const* cores_host);
 TRD_API trd_status trd_set_cores(trd_ctx* ctx, const float* const* cores_host);
 
+/* Iteration state of Alg. 1 beyond the cores, for an exact resume (checkpoint /
+ * resume): the kernel width sigma the next sweep uses (the sigma rules of R9 / R21 update
+ * it at sweep end), the sweep counter t that selects the next sweep's RStS draw (Alg. 1 l.3-4,
+ * P:267-268; reading R11), and D^{t-1} of the stop metric (Alg. 1 l.12-13; reading
+ * R15), an I_{N-1} x I_{N-1} float64 matrix (row-major) that exists once a sweep has run.  A
+ * context created from saved cores (trd_init / trd_set_cores) and given the saved state with
+ * trd_set_state continues bit for bit as the saving context would have. */
+typedef struct {
+  double sigma;                     /* kernel width of the next sweep                         */
+  int32_t sweep;                    /* sweep counter t of the next sweep                      */
+  int32_t have_prev_D;              /* 1: prev_D holds D^{t-1}; 0: the next stop_e is NaN      */
+  int64_t prev_D_size;              /* I_{N-1}^2 (set by trd_get_state; checked by trd_set_state) */
+} trd_state;
+/* prev_D_host: host double[I_{N-1}^2] or NULL (get: not copied; set: only valid with
+ * have_prev_D == 0).  sigma must be > 0 (any value when sigma_mode == TRD_SIGMA_INF), sweep
+ * >= 0.  Both synchronise the stream. */
+TRD_API trd_status trd_get_state(trd_ctx* ctx, trd_state* out, double* prev_D_host);
+TRD_API trd_status trd_set_state(trd_ctx* ctx, const trd_state* st, const double* prev_D_host);
+
 /* Diagnostic probe of block k at the current cores without updating them (parity tests):
  * runs a1-a10 of the block exactly as trd_sweep would at sweep index `sweep` and copies
  * d (I_k x R_k^2, row-major, column a + r_k b), G (R_k^2 x R_k^2), h (like d) and

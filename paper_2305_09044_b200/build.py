@@ -6,6 +6,9 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libtrd.so")
+# checked build (-DTRD_CHECKED=1): device invariant checks, mbarrier watchdog, schedule fuzzing
+# (tests/test_gpu_checked.py loads it in a subprocess via TRD_LIB_PATH)
+CHECKED_LIB = os.path.join(HERE, "libtrd_checked.so")
 SOURCES = ["trd_kernels.cu", "trd_tc.cu", "trd_api.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
@@ -45,6 +48,31 @@ def build(force=False, verbose=False, out=None, defines=()):
     for o in objs:
         os.remove(o)
     return lib
+
+
+def build_all(force=False):
+    """The product library and the checked library, built concurrently."""
+    import threading
+    errs = []
+
+    def run(kw):
+        try:
+            build(**kw)
+        except Exception as e:   # re-raised below
+            errs.append(e)
+
+    need_checked = force or not os.path.exists(CHECKED_LIB) or \
+        os.path.getmtime(CHECKED_LIB) < max(os.path.getmtime(os.path.join(CSRC, f)) for f in os.listdir(CSRC))
+    ts = [threading.Thread(target=run, args=(dict(force=force),))]
+    if need_checked:
+        ts.append(threading.Thread(target=run, args=(dict(out=CHECKED_LIB, defines=("TRD_CHECKED=1",)),)))
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    if errs:
+        raise errs[0]
+    return LIB, CHECKED_LIB
 
 
 if __name__ == "__main__":

@@ -12,6 +12,18 @@
 #include <vector>
 
 #include "trd_internal.cuh"
+#include <nvtx3/nvToolsExt.h>   // header-only NVTX v3: ranges cost a pointer test without a tool
+
+// NVTX ranges on the host side of the API (nsys / ncu --nvtx): one per call, per sweep and per
+// block stage, so a profiler timeline shows which block and pass each enqueued kernel belongs to
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
+static const char* const kNvtxBlock[] = {"trd block 0", "trd block 1", "trd block 2", "trd block 3",
+                                         "trd block 4", "trd block 5", "trd block 6", "trd block 7"};
 
 using namespace trd;
 
@@ -64,6 +76,26 @@ trd_status fail(Context* c, trd_status st, const char* fmt, ...) {
     if (st == TRD_ERR_CUDA || st == TRD_ERR_NCCL) c->sticky = st;
   }
   return st;
+}
+
+// checked build (trd_internal.cuh): collect the device check records of both kernel
+// translation units and re-arm the schedule fuzzing (TRD_JITTER_NS)
+bool check_both(DevCheck* out, unsigned int jitter_ns, cudaStream_t s) {
+  DevCheck a = {}, b = {};
+  const bool fa = tc_check_collect(&a, jitter_ns, s);
+  const bool fb = kern_check_collect(&b, jitter_ns, s);
+  *out = fa ? a : b;
+  if (fa && fb) out->count += b.count;
+  return fa || fb;
+}
+static trd_status device_checks(Context* c) {
+  if (!TRD_CHECKED) return TRD_OK;
+  const char* e = getenv("TRD_JITTER_NS");
+  DevCheck d;
+  if (check_both(&d, e ? (unsigned int)atoi(e) : 0u, c->stream))
+    return fail(c, TRD_ERR_STATE, "device check %u failed (block %u thread %u; %u failures)", d.code, d.block,
+                d.thread, d.count);
+  return TRD_OK;
 }
 
 #define CUDA_TRY(ctx, expr)                                                                   \
@@ -342,6 +374,10 @@ trd_status block_pass1(Context* c, const BlockPlan& bp) {
     if (!stg.valid) {                       // a2: stage the sketch in tile order
       launch_tc_stage(*c, bp, stg, s);
       stg.valid = stg.invariant;
+      // checked build only: TRD_CHECK_INJECT=entry corrupts the first staged entry id of this
+      // block (an id outside the tile), which the pass kernels must report (tests/test_gpu_checked.py)
+      if (TRD_CHECKED && getenv("TRD_CHECK_INJECT") && !strcmp(getenv("TRD_CHECK_INJECT"), "entry"))
+        CUDA_TRY(c, cudaMemsetAsync(stg.tidx, 0xFE, 2, s));
       static const char* kStageLabel[kMaxN] = {"stage k=0", "stage k=1", "stage k=2", "stage k=3",
                                                "stage k=4", "stage k=5", "stage k=6", "stage k=7"};
       tl_mark(c, s, kStageLabel[bp.k]);
@@ -467,7 +503,8 @@ void host_to_dev_core(const Context& c, int k, const float* src, std::vector<flo
 extern "C" {
 
 const char* trd_version(void) {
-  return "libtrd 0.2 (sm_100a: persistent tcgen05 pass kernels, CTA pairs; fp64 FGMC / filtered solve)";
+  return TRD_CHECKED ? "libtrd 0.3 checked (device invariant checks, mbarrier watchdog, schedule fuzzing)"
+                     : "libtrd 0.3 (sm_100a: persistent tcgen05 pass kernels, CTA pairs; fp64 FGMC / filtered solve)";
 }
 
 trd_status trd_nccl_unique_id(void* out128) {
@@ -558,6 +595,7 @@ trd_status trd_init(const trd_config* cfg, const trd_shard* shard, const float* 
 trd_status trd_init_ex(const trd_config* cfg, const trd_shard* shard, const float* const* init_cores,
                        void* stream, const trd_exchange* ex, trd_ctx** out) {
   if (!out) return TRD_ERR_INVALID_ARG;
+  NvtxRange nr("trd_init");
   *out = nullptr;
   if (!cfg || !shard || !init_cores) return TRD_ERR_INVALID_ARG;
   const int N = cfg->order;
@@ -853,12 +891,14 @@ trd_status trd_init_ex(const trd_config* cfg, const trd_shard* shard, const floa
     if ((st = sigma0_pass(c))) return bail(st);
   }
   CUDA_TRY(c, cudaStreamSynchronize(s));
+  if ((st = device_checks(c))) return bail(st);
   *out = reinterpret_cast<trd_ctx*>(c);
   return TRD_OK;
 }
 
 trd_status trd_upload(trd_ctx* ctx, const float* values_host, const uint32_t* mask_host) {
   Context* c = reinterpret_cast<Context*>(ctx);
+  NvtxRange nr("trd_upload");
   if (!c || !values_host || !mask_host) return TRD_ERR_INVALID_ARG;
   if (c->sticky) return c->sticky;
   if (!c->own_values || !c->own_mask) return fail(c, TRD_ERR_STATE, "shard is not host-resident");
@@ -941,6 +981,7 @@ static trd_status enqueue_sweep(Context* c) {
   launch_sweep_begin(*c, s);
   for (int k = 0; k < c->N; ++k) {
     const BlockPlan& bp = c->plan[k];
+    NvtxRange nr(kNvtxBlock[k]);
     if ((st = block_pass1(c, bp))) return st;
     if ((st = block_pass2(c, bp))) return st;
     if (k == c->N - 1)
@@ -951,7 +992,10 @@ static trd_status enqueue_sweep(Context* c) {
     tl_mark(c, s, "Q refresh");
     if ((st = check_launch(c, "update"))) return st;
   }
-  if (c->eabs && (st = mad_select(c))) return st;         // R21 (histograms allreduced)
+  if (c->eabs) {
+    NvtxRange nr("trd mad select");
+    if ((st = mad_select(c))) return st;                   // R21 (histograms allreduced)
+  }
   launch_sweep_end(*c, s);
   tl_mark(c, s, "sweep end (D^t, sigma)");
   if (c->cfg.world > 1) {                 // replica consistency of the replicated cores
@@ -1046,9 +1090,13 @@ trd_status trd_sweep(trd_ctx* ctx, int32_t n_sweeps, trd_sweep_stats* stats) {
   if (!c || n_sweeps < 0) return TRD_ERR_INVALID_ARG;
   if (c->sticky) return c->sticky;
   if (n_sweeps == 0) return TRD_OK;
+  NvtxRange nr("trd_sweep");
   trd_status st = ensure_stats(c, n_sweeps);
   if (st) return st;
-  if ((st = consume_upload(c))) return st;
+  {
+    NvtxRange nu("trd consume upload");
+    if ((st = consume_upload(c))) return st;
+  }
   cudaStream_t s = c->stream;
   CUDA_TRY(c, cudaMemsetAsync(&c->sc->slot_next, 0, sizeof(int), s));
   std::vector<cudaEvent_t> ev;
@@ -1057,7 +1105,9 @@ trd_status trd_sweep(trd_ctx* ctx, int32_t n_sweeps, trd_sweep_stats* stats) {
     for (auto& e : ev) CUDA_TRY(c, cudaEventCreate(&e));
     CUDA_TRY(c, cudaEventRecord(ev[0], s));
   }
+  if (TRD_CHECKED && (st = device_checks(c))) return st;     // (re-arms the jitter)
   for (int t = 0; t < n_sweeps; ++t) {
+    NvtxRange ns("trd sweep");
     if (graph_usable(c)) {
       SweepGraph& g = c->graphs[c->up_active];
       if (!g.exec || g.stats_ptr != c->stats) {
@@ -1069,6 +1119,7 @@ trd_status trd_sweep(trd_ctx* ctx, int32_t n_sweeps, trd_sweep_stats* stats) {
     }
     if (stats) CUDA_TRY(c, cudaEventRecord(ev[(size_t)t + 1], s));
   }
+  if (TRD_CHECKED && (st = device_checks(c))) return st;
   if (!stats) return TRD_OK;
   std::vector<DevStats> hs((size_t)n_sweeps);
   CUDA_TRY(c, cudaMemcpyAsync(hs.data(), c->stats, sizeof(DevStats) * n_sweeps, cudaMemcpyDeviceToHost, s));
@@ -1124,6 +1175,7 @@ trd_status trd_block_probe(trd_ctx* ctx, int32_t sweep, int32_t k, double* d_hos
   if (h_host) CUDA_TRY(c, cudaMemcpyAsync(h_host, c->h, (size_t)(Ik * bp.R2) * 8, cudaMemcpyDeviceToHost, s));
   CUDA_TRY(c, cudaMemcpyAsync(&c->sc->sweep, &saved, 4, cudaMemcpyHostToDevice, s));
   CUDA_TRY(c, cudaStreamSynchronize(s));
+  if (TRD_CHECKED && (st = device_checks(c))) return st;
   if (d_host) memcpy(d_host, dv.data(), (size_t)(Ik * bp.R2) * 8);
   if (stats5_host) {
     stats5_host[0] = dv[(size_t)(Ik * bp.R2)];
@@ -1147,6 +1199,7 @@ trd_status trd_reconstruct(trd_ctx* ctx, const int64_t* lin_idx_dev, int64_t n, 
 trd_status trd_error(trd_ctx* ctx, const float* ref_dev, const uint32_t* eval_bits, double peak,
                      trd_error_stats* out) {
   Context* c = reinterpret_cast<Context*>(ctx);
+  NvtxRange nr("trd_error");
   if (!c || !ref_dev || !out || !(peak >= 0.0)) return TRD_ERR_INVALID_ARG;
   if (peak == 0.0) peak = 1.0;                // data rescaled to [0, 1]
   if (c->sticky) return c->sticky;
@@ -1215,6 +1268,41 @@ trd_status trd_set_cores(trd_ctx* ctx, const float* const* cores_host) {
   for (int k = 0; k < c->N; ++k) launch_q(*c, k, c->stream);
   CUDA_TRY(c, cudaStreamSynchronize(c->stream));
   return check_launch(c, "set_cores");
+}
+
+trd_status trd_get_state(trd_ctx* ctx, trd_state* out, double* prev_D_host) {
+  Context* c = reinterpret_cast<Context*>(ctx);
+  if (!c || !out) return TRD_ERR_INVALID_ARG;
+  if (c->sticky) return c->sticky;
+  const int64_t In = c->dims[c->N - 1];
+  DevScalars hs;
+  CUDA_TRY(c, cudaMemcpyAsync(&hs, c->sc, sizeof(hs), cudaMemcpyDeviceToHost, c->stream));
+  if (prev_D_host)
+    CUDA_TRY(c, cudaMemcpyAsync(prev_D_host, c->Dprev, (size_t)(In * In) * 8, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  out->sigma = hs.sigma;
+  out->sweep = hs.sweep;
+  out->have_prev_D = hs.have_prev_D;
+  out->prev_D_size = In * In;
+  return TRD_OK;
+}
+
+trd_status trd_set_state(trd_ctx* ctx, const trd_state* st, const double* prev_D_host) {
+  Context* c = reinterpret_cast<Context*>(ctx);
+  if (!c || !st) return TRD_ERR_INVALID_ARG;
+  if (c->sticky) return c->sticky;
+  const int64_t In = c->dims[c->N - 1];
+  if (st->sweep < 0 || (st->have_prev_D != 0 && st->have_prev_D != 1)) return TRD_ERR_INVALID_ARG;
+  if (c->cfg.sigma_mode != TRD_SIGMA_INF && !(st->sigma > 0.0 && std::isfinite(st->sigma))) return TRD_ERR_INVALID_ARG;
+  if (st->have_prev_D && (!prev_D_host || st->prev_D_size != In * In)) return TRD_ERR_INVALID_ARG;
+  // the fields live in DevScalars: write them in place on the context stream
+  CUDA_TRY(c, cudaMemcpyAsync(&c->sc->sigma, &st->sigma, 8, cudaMemcpyHostToDevice, c->stream));
+  CUDA_TRY(c, cudaMemcpyAsync(&c->sc->sweep, &st->sweep, 4, cudaMemcpyHostToDevice, c->stream));
+  CUDA_TRY(c, cudaMemcpyAsync(&c->sc->have_prev_D, &st->have_prev_D, 4, cudaMemcpyHostToDevice, c->stream));
+  if (st->have_prev_D)
+    CUDA_TRY(c, cudaMemcpyAsync(c->Dprev, prev_D_host, (size_t)(In * In) * 8, cudaMemcpyHostToDevice, c->stream));
+  CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  return TRD_OK;
 }
 
 void trd_destroy(trd_ctx* ctx) {

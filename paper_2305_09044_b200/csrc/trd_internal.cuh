@@ -34,6 +34,61 @@ struct DevStats {
 // statistics.  Histogram regions of c->mhist: level 0 [2048] | level 1 [2][2048] | level 2 [2][1024].
 constexpr uint32_t kEabsPad = 0xFFFFFFFFu;
 
+// ---- checked build (-DTRD_CHECKED=1 -> libtrd_checked.so) -------------
+// compute-sanitizer is not available on the GPU pool, so the checked library carries its own:
+// device-side invariant checks (bounds of every staged-slot, entry and shared-memory index the
+// data decides), an mbarrier watchdog (a wait that has not completed after ~2^34 cycles records
+// a hang and gives up, so a broken pipeline ends instead of hanging the GPU) and schedule
+// fuzzing (TRD_JITTER_NS: a pseudo-random __nanosleep after every pipeline wait, which must not
+// change any result bit).  A failed check is recorded (first code, block, thread, count) and
+// trd_sweep / trd_block_probe report it as TRD_ERR_STATE; the faulty access is skipped.  In the
+// product library TRD_CHECKED is 0 and all of it compiles away.
+#ifndef TRD_CHECKED
+#define TRD_CHECKED 0
+#endif
+enum : unsigned int {
+  kChkHang = 1,        // mbarrier wait watchdog expired
+  kChkEntry = 2,       // staged entry id outside the 128 x 64 tile
+  kChkStageCap = 3,    // a tile's staged slots beyond the stage capacity
+  kChkSmemVals = 4,    // smem-staged tile with more entries than the stage holds
+  kChkSampler = 5,     // RStS index outside [0, I_m) or a set not strictly ascending
+  kChkStageWrite = 6,  // staging kernel slot index beyond the capacity
+  kChkTileBase = 7     // tile value blocks not monotone
+};
+struct DevCheck {
+  unsigned int code, block, thread, count;
+  unsigned int jitter_ns;
+};
+// (one instance per translation unit: trd_kernels.cu and trd_tc.cu collect their own)
+static __device__ DevCheck g_check;
+#if TRD_CHECKED
+static __device__ __noinline__ void trd_check_fail(unsigned int code) {
+  if (atomicCAS(&g_check.code, 0u, code) == 0u) {
+    g_check.block = blockIdx.x;
+    g_check.thread = threadIdx.x;
+  }
+  atomicAdd(&g_check.count, 1u);
+}
+#endif
+#define TRD_CHECK(cond, code) \
+  do { if (TRD_CHECKED && !(cond)) { TRD_CHECK_FAIL(code); } } while (0)
+#if TRD_CHECKED
+#define TRD_CHECK_FAIL(code) trd_check_fail(code)
+#else
+#define TRD_CHECK_FAIL(code) do { } while (0)
+#endif
+// schedule fuzzing after a pipeline wait (checked build with TRD_JITTER_NS > 0)
+__device__ __forceinline__ void trd_jitter() {
+#if TRD_CHECKED
+  const unsigned int j = *(volatile unsigned int*)&g_check.jitter_ns;
+  if (j) {
+    unsigned int x = (unsigned int)clock() * 0x9E3779B1u ^ (threadIdx.x * 0x85EBCA77u) ^ (blockIdx.x * 0xC2B2AE3Du);
+    x ^= x >> 15;
+    __nanosleep(x % j);
+  }
+#endif
+}
+
 // Power-of-two scale exponent E of an fp16 hi / lo operand with max |.| = amax: amax 2^E lies
 // in [2^14, 2^15), so every element is below the fp16 maximum (65504) and elements down to
 // 2^-15 of the maximum keep a normal lo part (22 significant bits).  Scaling by 2^E is exact.
@@ -312,5 +367,10 @@ void launch_tc_reduce_d(Context& c, const BlockPlan& bp, cudaStream_t s);
 void launch_tc_stage(Context& c, const BlockPlan& bp, TcStage& st, cudaStream_t s);
 size_t tc_scan_tmp_bytes(int64_t n_tiles);
 void tc_debug_dump();   // TRD_TC_EXP diagnostics
+
+// checked build: read and clear the device check records of both translation units (the
+// first failure of either), and set the schedule-fuzzing delay; false if none failed
+bool tc_check_collect(DevCheck* out, unsigned int jitter_ns, cudaStream_t s);
+bool kern_check_collect(DevCheck* out, unsigned int jitter_ns, cudaStream_t s);
 
 }  // namespace trd

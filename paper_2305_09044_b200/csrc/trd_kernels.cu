@@ -106,6 +106,7 @@ sampler_kernel(SamplerArgs sa, const DevScalars* __restrict__ sc, int32_t* __res
       n_out += put_tot;
     }
     n_local = compact ? n_out : s;
+    TRD_CHECK(compact || n_out == s_draw, kChkSampler);
     for (int64_t q = n_local + tid; q < s; q += blockDim.x) out[q] = (int32_t)sa.shard_begin;   // padding
   } else {
     // radix select of the key of rank s_draw - 1
@@ -156,12 +157,15 @@ sampler_kernel(SamplerArgs sa, const DevScalars* __restrict__ sc, int32_t* __res
       n_out += put_tot;
     }
     n_local = compact ? n_out : s;
+    TRD_CHECK(compact || n_out == s_draw, kChkSampler);     // exactly s_draw selected
     for (int64_t q = n_local + tid; q < s; q += blockDim.x) out[q] = (int32_t)sa.shard_begin;   // padding
   }
   __syncthreads();
   const int64_t cnt = s >= I ? I : s;
   for (int64_t q = tid; q < cnt; q += blockDim.x) {
     int64_t g = out[q];
+    // checked build: a real entry lies in [0, I) and the set is strictly ascending
+    TRD_CHECK(q >= n_local || (g >= 0 && g < I && (q == 0 || g > (int64_t)out[q - 1])), kChkSampler);
     int64_t loc = g;
     if (m == sa.shard_mode) loc = (g >= sa.shard_begin && g < sa.shard_end) ? g - sa.shard_begin : -1;
     if (q >= n_local) loc = -1;                                       // padding of a compacted list
@@ -1523,6 +1527,16 @@ __global__ void popc_kernel(const uint32_t* __restrict__ mask, int64_t nw, uint3
 // Kernel attributes are per device, and contexts may be driven from several host threads: the
 // attribute is set before every launch that needs it (a cheap host call; a "done" flag shared
 // between threads let a second thread launch before the first had set it)
+bool kern_check_collect(DevCheck* out, unsigned int jitter_ns, cudaStream_t s) {
+  DevCheck h = {}, z = {};
+  z.jitter_ns = jitter_ns;
+  cudaMemcpyFromSymbolAsync(&h, g_check, sizeof(h), 0, cudaMemcpyDeviceToHost, s);
+  cudaMemcpyToSymbolAsync(g_check, &z, sizeof(z), 0, cudaMemcpyHostToDevice, s);
+  cudaStreamSynchronize(s);
+  *out = h;
+  return h.code != 0;
+}
+
 static bool first_on_device(uint64_t& done_mask) {
   (void)done_mask;
   return true;

@@ -61,10 +61,22 @@ __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
 __device__ __forceinline__ void mbar_wait_spin(uint64_t* bar, uint32_t phase) {
   const uint32_t addr = smem_u32(bar);
   uint32_t ok = 0;
+#if TRD_CHECKED
+  uint32_t spins = 0;
+  long long t0 = 0;
+#endif
   do {
     asm volatile("{\n\t.reg .pred p;\n\tmbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
                  "selp.u32 %0, 1, 0, p;\n\t}" : "=r"(ok) : "r"(addr), "r"(phase) : "memory");
+#if TRD_CHECKED
+    if (!ok && (++spins & 4095u) == 0u) {   // watchdog (checked build)
+      const long long now = clock64();
+      if (spins == 4096u) t0 = now;
+      else if (now - t0 > (1ll << 34)) { trd_check_fail(kChkHang); break; }
+    }
+#endif
   } while (!ok);
+  trd_jitter();
 }
 // try_wait with an explicit suspend-time hint (ns): the thread sleeps until the phase
 // completes or the hint elapses, instead of re-polling (keeps issue slots free for the MMA warp)
@@ -90,14 +102,20 @@ __device__ __noinline__ void mbar_hang_report(uint32_t addr, uint32_t phase) {
 __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t phase) {
   const uint32_t addr = smem_u32(bar);
   uint32_t ok = 0;
-#if TRD_DEBUG_HANG
+#if TRD_DEBUG_HANG || TRD_CHECKED
   uint32_t spins = 0;
   long long t0 = 0;
 #endif
   do {
     asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
                  "selp.u32 %0, 1, 0, p;\n\t}" : "=r"(ok) : "r"(addr), "r"(phase), "r"(TRD_SLEEP_NS) : "memory");
-#if TRD_DEBUG_HANG
+#if TRD_CHECKED
+    if (!ok && (++spins & 255u) == 0u) {    // watchdog (checked build)
+      const long long now = clock64();
+      if (spins == 256u) t0 = now;
+      else if (now - t0 > (1ll << 34)) { trd_check_fail(kChkHang); break; }
+    }
+#elif TRD_DEBUG_HANG
     if (!ok && g_debug_hang && (++spins & 255u) == 0u) {
       const long long now = clock64();
       if (spins == 256u) t0 = now;
@@ -105,6 +123,7 @@ __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t phase) {
     }
 #endif
   } while (!ok);
+  trd_jitter();
 }
 #ifndef TRD_MBAR_SPIN
 #define TRD_MBAR_SPIN 0
@@ -115,7 +134,7 @@ __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t phase) {
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
   const uint32_t addr = smem_u32(bar);
   uint32_t ok = 0;
-#if TRD_DEBUG_HANG
+#if TRD_DEBUG_HANG || TRD_CHECKED
   uint32_t spins = 0;
   long long t0 = 0;
 #endif
@@ -127,7 +146,13 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
     asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
                  "selp.u32 %0, 1, 0, p;\n\t}" : "=r"(ok) : "r"(addr), "r"(phase) : "memory");
 #endif
-#if TRD_DEBUG_HANG
+#if TRD_CHECKED
+    if (!ok && (++spins & 4095u) == 0u) {   // watchdog (checked build)
+      const long long now = clock64();
+      if (spins == 4096u) t0 = now;
+      else if (now - t0 > (1ll << 34)) { trd_check_fail(kChkHang); break; }
+    }
+#elif TRD_DEBUG_HANG
     if (!ok && g_debug_hang && (++spins & 4095u) == 0u) {
       const long long now = clock64();
       if (spins == 4096u) t0 = now;
@@ -135,6 +160,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
     }
 #endif
   } while (!ok);
+  trd_jitter();
 }
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
@@ -518,6 +544,7 @@ struct StageArgs {
   int32_t* perm;          // sweep-invariant sketch: value index of every staged slot (-1 padding)
   float* tvals;           // compacted values (tile blocks padded to 8 entries)
   uint16_t* tidx;         // entry list: (row in tile) * 64 + column, 0xFFFF = padding
+  int64_t vcap;           // capacity of tvals / tidx / perm (checked build)
   // fibre windows (sampled mode 0 as the fastest column digit, 16 <= s0, I0 <= 128): columns
   // f s0 .. f s0 + s0 - 1 lie in one mode-0 fibre at base col_off[f s0] - idx0[0], at the
   // positions idx0[0..s0-1]; 0 = off
@@ -752,6 +779,10 @@ __global__ void __launch_bounds__(128) stage_vals_kernel(StageArgs s) {
     const int roff = s.troff[tile * TC_M + tid];
     const int64_t tb = (int64_t)s.tbase[tile];           // tile block start (after the scan)
     const int nt = (int)((int64_t)s.tbase[tile + 1] - tb);    // padded entry count of the tile
+    if (TRD_CHECKED && !(tb >= 0 && nt >= 0 && tb + nt <= s.vcap)) {   // (block-uniform)
+      if (tid == 0) TRD_CHECK_FAIL(kChkStageWrite);
+      continue;
+    }
     const bool in_smem = nt <= SV_OUT;
     float* ov = in_smem ? sov : s.tvals + tb;            // tile-relative output positions
     uint16_t* oi = in_smem ? soi : s.tidx + tb;
@@ -793,6 +824,7 @@ __global__ void __launch_bounds__(128) stage_vals_kernel(StageArgs s) {
           cw &= cw - 1;
           const int rr = warp * 32 + r;                   // row in the tile
           const int pos = soff[rr] + __popcll(sbits[rr] & ((1ull << j) - 1ull));
+          if (TRD_CHECKED && pos >= nt) { TRD_CHECK_FAIL(kChkStageWrite); continue; }
           int64_t vi;
           if (r < wr.b) vi = s.packed ? va[h] + qa++ : la[h] + r;
           else vi = s.packed ? vb[h] + qb++ : lb[h] + (r - wr.b);
@@ -916,8 +948,13 @@ __global__ void layout_gen_kernel(const int* __restrict__ cur, int* __restrict__
 // new upload with an unchanged mask re-gathers the values without rebuilding the layout
 __global__ void __launch_bounds__(256) gather_vals_kernel(const int32_t* __restrict__ perm, const uint16_t* __restrict__ tidx,
                                                           const float* __restrict__ values,
-                                                          const uint64_t* __restrict__ total, float* __restrict__ tvals) {
-  const int64_t n = (int64_t)*total;
+                                                          const uint64_t* __restrict__ total, float* __restrict__ tvals,
+                                                          int64_t vcap) {
+  int64_t n = (int64_t)*total;
+  if (TRD_CHECKED && n > vcap) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) TRD_CHECK_FAIL(kChkStageWrite);
+    n = vcap;
+  }
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     tvals[i] = tidx[i] == 0xFFFFu ? 0.f : __ldg(values + perm[i]);
 }
@@ -940,6 +977,7 @@ struct TcArgs {
   const uint64_t* tbase;
   const float* tvals;
   const uint16_t* tidx;    // staged entry lists
+  int64_t vcap;            // their capacity (checked build)
   float* tw;               // staged weights (pass 1 writes, pass 2 reads)
   const float* lscl;       // [row] 2^-E of the A rows' scaling (Lft in pass 1, Lft_h in pass 2)
   uint32_t* eabs;          // TRD_SIGMA_MAD: |e| bit patterns (pass 1, R21), else nullptr
@@ -1250,6 +1288,7 @@ void launch_tc_stage(Context& c, const BlockPlan& bp, TcStage& st, cudaStream_t 
   a.mask = c.mask; a.rank_prefix = c.rank_prefix; a.values = c.values;
   a.tbits = st.tbits; a.troff = st.troff; a.tcount = st.tcount; a.tbase = st.tbase; a.tvals = st.tvals;
   a.tidx = st.tidx;
+  a.vcap = st.vcap;
   // sweep-invariant sketch with a layout cache: stage the value indices (perm), then gather; both
   // layout kernels exit at once when the uploaded mask equals the one the layout was built from
   const bool cached = st.perm != nullptr;
@@ -1285,7 +1324,7 @@ void launch_tc_stage(Context& c, const BlockPlan& bp, TcStage& st, cudaStream_t 
   c.launches += 3;
   if (cached) {
     layout_gen_kernel<<<1, 32, 0, s>>>(&c.sc->mask_gen, &c.sc->layout_gen[bp.k]);
-    gather_vals_kernel<<<c.num_sm * 8, 256, 0, s>>>(st.perm, st.tidx, c.values, st.tbase + a.n_tiles, st.tvals);
+    gather_vals_kernel<<<c.num_sm * 8, 256, 0, s>>>(st.perm, st.tidx, c.values, st.tbase + a.n_tiles, st.tvals, st.vcap);
     c.launches += 2;
   }
 }
@@ -1314,6 +1353,7 @@ static TcArgs make_tc_args(const Context& c, const BlockPlan& bp, const TcStage&
   a.exp = ex ? atoi(ex) : 0;
   a.rgtHL = ((!pass2 && !TRD_P1_MERGE) || (pass2 && TRD_EXPERIMENTS && (a.exp & 32))) ? c.rgtHL : c.rgtHL2;
   a.tbits = st.tbits; a.troff = st.troff; a.tbase = st.tbase; a.tvals = st.tvals; a.tidx = st.tidx;
+  a.vcap = st.vcap;
   a.tw = c.tw;
   a.lscl = pass2 ? c.lsclh : c.lscl;
   a.sc = c.sc;
@@ -1382,14 +1422,14 @@ void tc_debug_dump() {
   }
   if (cudaMemcpyFromSymbol(tr, g_trace, sizeof(tr)) == cudaSuccess && tr[0] != 0) {
     fprintf(stderr, "[trd tc trace] pass-1 CTA 0 (cycles rel. to tile 0 GEMM1 start)\n"
-                    "  tile | G1 start wait issue | G2 start wait issue | EPI start skfull sfull dumped ppfree done fenced barred\n");
+                    "  tile | G1 start wait issue | G2 start wait issue | EPI start skfull sfull dumped ppfree cleared done fenced barred\n");
     const long long t0 = tr[0];
     for (int i = 0; i < 48; ++i) {
       const long long* q = tr + i * 16;
       auto f = [&](int k) { return q[k] ? q[k] - t0 : -1; };
-      fprintf(stderr, "  %4d | %7lld %5lld %5lld | %7lld %5lld %5lld | %7lld %5lld %5lld %5lld %5lld %5lld %5lld %5lld\n", i,
+      fprintf(stderr, "  %4d | %7lld %5lld %5lld | %7lld %5lld %5lld | %7lld %5lld %5lld %5lld %5lld %5lld %5lld %5lld %5lld\n", i,
               f(0), q[1] - q[0], q[2] - q[0], f(3), q[4] - q[3], q[5] - q[3], f(6), q[7] - q[6], q[8] - q[6],
-              q[9] - q[6], q[10] - q[6], q[11] - q[6], q[12] - q[6], q[13] - q[6]);
+              q[9] - q[6], q[10] - q[6], q[14] - q[6], q[11] - q[6], q[12] - q[6], q[13] - q[6]);
     }
   }
   unsigned long long v[16];
@@ -1397,6 +1437,16 @@ void tc_debug_dump() {
   const char* nm[6] = {"a_full_wait", "bf_full_wait", "t_free_wait", "issue", "tiles", "total"};
   fprintf(stderr, "[trd tc exp] pass-2 MMA thread cycles summed over CTAs\n");
   for (int i = 0; i < 6; ++i) fprintf(stderr, "  %-14s %.4e\n", nm[i], (double)v[i]);
+}
+
+bool tc_check_collect(DevCheck* out, unsigned int jitter_ns, cudaStream_t s) {
+  DevCheck h = {}, z = {};
+  z.jitter_ns = jitter_ns;
+  cudaMemcpyFromSymbolAsync(&h, g_check, sizeof(h), 0, cudaMemcpyDeviceToHost, s);
+  cudaMemcpyToSymbolAsync(g_check, &z, sizeof(z), 0, cudaMemcpyHostToDevice, s);
+  cudaStreamSynchronize(s);
+  *out = h;
+  return h.code != 0;
 }
 
 bool tc_supported_kp(int KP) { return KP >= 16 && KP <= 128 && KP % 16 == 0; }

@@ -92,6 +92,11 @@ class trd_error_stats(ctypes.Structure):
                 ("n_eval", ctypes.c_int64)]
 
 
+class trd_state(ctypes.Structure):
+    _fields_ = [("sigma", ctypes.c_double), ("sweep", ctypes.c_int32), ("have_prev_D", ctypes.c_int32),
+                ("prev_D_size", ctypes.c_int64)]
+
+
 class trd_profile(ctypes.Structure):
     _fields_ = [("pass1_ms", ctypes.c_double), ("pass2_ms", ctypes.c_double),
                 ("pass1_launches", ctypes.c_int64), ("pass2_launches", ctypes.c_int64),
@@ -124,6 +129,8 @@ def load_library(path: str = LIB_PATH):
         "trd_error": (i32, [P, P, P, d, ctypes.POINTER(trd_error_stats)]),
         "trd_get_cores": (i32, [P, P]),
         "trd_set_cores": (i32, [P, P]),
+        "trd_get_state": (i32, [P, ctypes.POINTER(trd_state), P]),
+        "trd_set_state": (i32, [P, ctypes.POINTER(trd_state), P]),
         "trd_block_probe": (i32, [P, i32, i32, P, P, P, P]),
         "trd_launch_count": (i64, [P]),
         "trd_set_profiling": (i32, [P, i32]),
@@ -311,6 +318,23 @@ class TRD:
         cores = [np.ascontiguousarray(c, dtype=np.float32) for c in cores]
         arr = (ctypes.c_void_p * self.N)(*[c.ctypes.data for c in cores])
         self._check(self.lib.trd_set_cores(self.ctx, arr), "trd_set_cores")
+
+    def get_state(self):
+        """Iteration state beyond the cores (sigma, sweep counter t, D^{t-1}) for an exact resume."""
+        In = self.dims[self.N - 1]
+        prev = np.zeros((In, In))
+        st = trd_state()
+        self._check(self.lib.trd_get_state(self.ctx, ctypes.byref(st), prev.ctypes.data), "trd_get_state")
+        return dict(sigma=st.sigma, sweep=st.sweep, have_prev_D=st.have_prev_D,
+                    prev_D=prev if st.have_prev_D else None)
+
+    def set_state(self, state):
+        In = self.dims[self.N - 1]
+        prev = state.get("prev_D")
+        st = trd_state(float(state["sigma"]), int(state["sweep"]), int(state["have_prev_D"]), In * In)
+        buf = None if prev is None else np.ascontiguousarray(prev, dtype=np.float64)
+        self._check(self.lib.trd_set_state(self.ctx, ctypes.byref(st), None if buf is None else buf.ctypes.data),
+                    "trd_set_state")
 
     def upload(self, values_host, mask_host):
         self._check(self.lib.trd_upload(self.ctx, ctypes.c_void_p(_ptr(values_host)),

@@ -51,6 +51,9 @@ def test_invalid_arguments_rejected_without_gpu():
         cfg.ranks[m] = 99               # rank > TRD_MAX_RANK
     assert lib.trd_init(ctypes.byref(cfg), ctypes.byref(sh), arr, None, ctypes.byref(ctx)) in (1, 2)
     assert lib.trd_sweep(None, 1, None) == 1
+    st = T.trd_state()
+    assert lib.trd_get_state(None, ctypes.byref(st), None) == 1
+    assert lib.trd_set_state(None, ctypes.byref(st), None) == 1
     assert lib.trd_destroy(None) is None
 
 
@@ -60,7 +63,7 @@ def test_ctypes_structs_match_the_c_header(tmp_path):
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     structs = {"trd_config": T.trd_config, "trd_shard": T.trd_shard,
                "trd_sweep_stats": T.trd_sweep_stats}
-    for extra in ("trd_error_stats", "trd_profile"):
+    for extra in ("trd_error_stats", "trd_profile", "trd_state", "trd_exchange"):
         if hasattr(T, extra):
             structs[extra] = getattr(T, extra)
     lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "trd.h"', "int main(void) {"]
