@@ -835,6 +835,7 @@ trd_status trd_init_ex(const trd_config* cfg, const trd_shard* shard, const floa
       }
     }
     if (max_v > 0 && (st = dalloc(c, &c->tw, (size_t)max_v))) return bail(st);
+    if ((st = dalloc(c, &c->ptab, (size_t)(16 * 256 + 16)))) return bail(st);
   }
   // R21: |e| slots of one sweep (every block's staged slots, or its observed entries) or of the
   // sigma_0 pass (all local observed entries)
@@ -1361,7 +1362,7 @@ void trd_destroy(trd_ctx* ctx) {
                   c->denpart, c->numpart, c->dvec, c->G, c->G_last, c->Mop, c->chol_ws,
                   c->chain_ws, c->h, c->Dcur, c->Dprev, c->sc, c->stats, c->red_ws,
                   c->lftHL, c->lfthHL, c->lscl, c->lsclh, c->rgtHL, c->rgtHL2, c->contrib, c->Qloc, c->Gloc, c->mhist,
-                  c->eabs, c->chk, c->chk_acc, c->stage_mask};
+                  c->eabs, c->chk, c->chk_acc, c->stage_mask, c->ptab};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->tw) cudaFree(c->tw);

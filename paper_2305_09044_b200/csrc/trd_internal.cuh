@@ -247,6 +247,7 @@ struct Context {
   int64_t n_values = 0;
   uint32_t* rank_prefix = nullptr;     // packed layout: exclusive popcount prefix per word
   uint32_t* stage_mask = nullptr;      // the mask the invariant staged layouts were built from
+  uint8_t* ptab = nullptr;             // compaction tables of the sampled mode-0 positions (staging)
   void* rp_tmp = nullptr;              // its scan's scratch (allocated once)
   size_t rp_tmp_bytes = 0;
 
@@ -360,6 +361,7 @@ void launch_sweep_begin(Context& c, cudaStream_t s);
 
 // ---- tensor-core pass kernels (trd_tc.cu) ---------------------------------------------
 bool tc_supported_kp(int KP);
+bool stage_uses_pext(const Context& c, const BlockPlan& bp);   // sampler writes c.ptab
 void launch_tc_pack_cols(Context& c, const BlockPlan& bp, cudaStream_t s);
 void launch_tc_lft(Context& c, const BlockPlan& bp, bool pass2, cudaStream_t s);
 void launch_tc_pass(Context& c, const BlockPlan& bp, const TcStage& st, bool pass2, cudaStream_t s);

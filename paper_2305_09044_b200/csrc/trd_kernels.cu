@@ -46,6 +46,9 @@ struct SamplerArgs {
   int shard_local;       // shard mode enumerates [shard_begin, shard_end) (full set)
   int shard_sampled;     // shard mode: this rank's sampled indices, compacted, capacity s[m]
   int64_t s_samp[kMaxN]; // RStS sample sizes (the draw; s[m] may be a smaller capacity)
+  uint8_t* ptab;         // non-null: also write the staging's compaction tables of mode 0's
+                         // sampled positions (byte b of a fibre window, value v -> the sampled
+                         // bits packed at ptab[b * 256 + v]; positions below byte b at ptab[4096 + b])
 };
 
 constexpr int kSamplerThreads = 256;
@@ -161,6 +164,29 @@ sampler_kernel(SamplerArgs sa, const DevScalars* __restrict__ sc, int32_t* __res
     for (int64_t q = n_local + tid; q < s; q += blockDim.x) out[q] = (int32_t)sa.shard_begin;   // padding
   }
   __syncthreads();
+  if (m == 0 && sa.ptab) {                  // (s <= 64, I <= 128: the window bytes b < 16)
+    __shared__ uint32_t pm[16], pb[16];
+    if (tid < 16) {
+      uint32_t msk = 0, below = 0;
+      for (int64_t q = 0; q < s; ++q) {
+        const int p = out[q];
+        if ((p >> 3) == tid) msk |= 1u << (p & 7);
+        else if (p < 8 * tid) ++below;
+      }
+      pm[tid] = msk;
+      pb[tid] = below;
+    }
+    __syncthreads();
+    for (int b = 0; b < 16; ++b) {
+      const uint32_t msk = pm[b];
+      uint32_t r = 0;
+      int qq = 0;
+      for (int t2 = 0; t2 < 8; ++t2)
+        if ((msk >> t2) & 1u) { r |= (((uint32_t)tid >> t2) & 1u) << qq; ++qq; }
+      sa.ptab[b * 256 + tid] = (uint8_t)r;
+    }
+    if (tid < 16) sa.ptab[4096 + tid] = (uint8_t)pb[tid];
+  }
   const int64_t cnt = s >= I ? I : s;
   for (int64_t q = tid; q < cnt; q += blockDim.x) {
     int64_t g = out[q];
@@ -1563,6 +1589,7 @@ void launch_sampler(Context& c, const BlockPlan& bp, cudaStream_t s) {
     sa.lstride[m] = c.lstride[m];
   }
   sa.idx_off[c.N] = c.idx_off[c.N];
+  sa.ptab = stage_uses_pext(c, bp) ? c.ptab : nullptr;
   if (bp.explicit_cols) {
     const int64_t J = bp.ncols;
     row_sampler_kernel<<<grid_for(J + c.dims[bp.k]), 256, 0, s>>>(sa, J, c.sc, c.idx, c.doff);

@@ -551,7 +551,16 @@ struct StageArgs {
   int fib;
   int fib_s0;
   const int32_t* idx0;
+  // row fibres: mode 0 sampled with s0 = 32 positions is the fastest row digit (nL % 32 == 0),
+  // so the 32 rows of a warp are the sampled positions of one mode-0 fibre; 0 = off
+  int rfib;
+  // compaction tables of the sampled mode-0 positions (s0 <= 64; fib_pext): byte b of a fibre
+  // window -> its sampled bits packed (tab[b * 256 + v]); sampled positions below byte b at
+  // tab[4096 + b]; fib_nb = bytes of the window that hold positions (I0 / 8 rounded up)
+  const uint8_t* ptab;
+  int fib_nb;
 };
+constexpr int kPextTab = 16 * 256 + 16;
 
 // ---- fibre windows: the I0 <= 128 observation bits of a mode-0 fibre starting at linear
 // position lin0 as four aligned words (a0: bits 0-31 of the fibre, ...), from five raw words ----
@@ -614,6 +623,40 @@ __device__ __forceinline__ FibWin fib_window(const StageArgs& s, int64_t lin0) {
   return f;
 }
 
+// the sampled bits of a fibre window, packed in sampled order (s0 <= 64): one table lookup per
+// window byte instead of one extraction per sampled position
+__device__ __forceinline__ uint64_t fib_pext(const FibWin& f, const uint8_t* tab, const uint32_t* offw, int nb) {
+  uint64_t r = 0;
+#pragma unroll
+  for (int b = 0; b < 16; ++b) {
+    if (b < nb) {
+      const uint32_t w = b < 4 ? f.a0 : (b < 8 ? f.a1 : (b < 12 ? f.a2 : f.a3));
+      const uint32_t v = (w >> (8 * (b & 3))) & 255u;
+      r |= (uint64_t)tab[b * 256 + v] << ((offw[b >> 2] >> (8 * (b & 3))) & 255u);
+    }
+  }
+  return r;
+}
+// (the tables are written by the sampler of the block, sampler_kernel, trd_kernels.cu)
+// staging of block bp compacts fibre windows by table: a sampled mode 0 (s0 <= 64, I0 <= 128)
+// as the fastest column digit, or (s0 = 32) as the fastest row digit
+bool stage_uses_pext(const Context& c, const BlockPlan& bp) {
+  if (!bp.use_tc || bp.explicit_cols || !c.ptab || getenv("TRD_NO_PEXT")) return false;
+  if (!(bp.s[0] < c.dims[0] && c.dims[0] <= 128 && bp.s[0] <= 64)) return false;
+  if (c.cfg.shard_mode == 0 && c.shard_end - c.shard_begin < c.dims[0]) return false;
+  const bool col = bp.nright > 0 && bp.right[bp.rdig[0]] == 0 && bp.s[0] >= 16;
+  const bool row = bp.k != 0 && bp.nleft > 0 && bp.left[bp.ldig[0]] == 0 && bp.s[0] == 32 && bp.nL % 32 == 0;
+  return col || row;
+}
+// per CTA: the tables into shared memory, the byte offsets into four words
+__device__ __forceinline__ void load_pext(const StageArgs& s, uint8_t* tabS, uint32_t* offw) {
+  for (int i = threadIdx.x; i < kPextTab / 16; i += blockDim.x)
+    reinterpret_cast<uint4*>(tabS)[i] = __ldg(reinterpret_cast<const uint4*>(s.ptab) + i);
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < 4; ++q) offw[q] = reinterpret_cast<const uint32_t*>(tabS + 4096)[q];
+}
+
 // 32 x 32 bit-matrix transpose across a warp: in, lane i holds row i (bit j = element (i, j));
 // out, lane i holds column i (bit j = element (j, i))
 __device__ __forceinline__ uint32_t warp_transpose32(uint32_t x, int lane) {
@@ -670,7 +713,10 @@ __global__ void __launch_bounds__(128) stage_bits_kernel(StageArgs s) {
   __shared__ int64_t sco[TC_NT];
   __shared__ uint32_t sstart[2];
   __shared__ int wsum[4];
+  __shared__ __align__(16) uint8_t tabS[kPextTab];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  uint32_t offw[4] = {0u, 0u, 0u, 0u};
+  if (s.ptab) load_pext(s, tabS, offw);
   for (int64_t tile = blockIdx.x; tile < s.n_tiles; tile += gridDim.x) {
     const int64_t rt = tile / s.n_col_tiles, ct = tile % s.n_col_tiles;
     stage_tile_cols(s, ct, tid, sco, sstart);
@@ -678,7 +724,17 @@ __global__ void __launch_bounds__(128) stage_bits_kernel(StageArgs s) {
     const int64_t ro = row < s.nrows ? s.row_off[row] : -1;
     uint64_t bits = 0;
     WarpRows wr;
-    if (warp_row_segments(ro, lane, wr)) {
+    if (s.rfib) {
+      // row fibres: lane j packs column j's (and j + 32's) sampled bits of the warp's fibre
+      // (one window each), then the transpose gives every row its 64 column bits
+      if (__all_sync(0xffffffffu, ro >= 0)) {
+        const int64_t fb0 = __shfl_sync(0xffffffffu, ro, 0) - s.idx0[0];
+        const int64_t c0 = sco[lane], c1 = sco[lane + 32];
+        const uint32_t w0 = c0 >= 0 ? (uint32_t)fib_pext(fib_window(s, fb0 + c0), tabS, offw, s.fib_nb) : 0u;
+        const uint32_t w1 = c1 >= 0 ? (uint32_t)fib_pext(fib_window(s, fb0 + c1), tabS, offw, s.fib_nb) : 0u;
+        bits = (uint64_t)warp_transpose32(w0, lane) | ((uint64_t)warp_transpose32(w1, lane) << 32);
+      }
+    } else if (warp_row_segments(ro, lane, wr)) {
       // lane j: column j's and column (j + 32)'s bits over the warp's 32 rows, then transpose
       const int64_t c0 = sco[lane], c1 = sco[lane + 32];
       const uint32_t w0 = c0 >= 0 ? warp_col_bits(s, wr, c0) : 0u;
@@ -697,9 +753,14 @@ __global__ void __launch_bounds__(128) stage_bits_kernel(StageArgs s) {
           const int64_t co = sco[j];
           if (co >= 0) {
             const FibWin fw = fib_window(s, ro + co - s.idx0[q0]);
-            for (int u = 0; u < nj; ++u) {
-              const uint32_t p = (uint32_t)s.idx0[q0 + u];
-              bits |= (uint64_t)((fib_word(fw, p >> 5) >> (p & 31)) & 1u) << (j + u);
+            if (s.ptab) {                                    // s0 <= 64: table compaction
+              const uint64_t e = fib_pext(fw, tabS, offw, s.fib_nb) >> q0;
+              bits |= (nj >= 64 ? e : (e & ((1ull << nj) - 1ull))) << j;
+            } else {
+              for (int u = 0; u < nj; ++u) {
+                const uint32_t p = (uint32_t)s.idx0[q0 + u];
+                bits |= (uint64_t)((fib_word(fw, p >> 5) >> (p & 31)) & 1u) << (j + u);
+              }
             }
           }
           j += nj;
@@ -1298,13 +1359,25 @@ void launch_tc_stage(Context& c, const BlockPlan& bp, TcStage& st, cudaStream_t 
   if (cached) a.tvals = reinterpret_cast<float*>(st.perm);
   // fibre windows: mode 0 is the fastest column digit with a sampled set of >= 16 positions,
   // I0 <= 128 (a window of five words), and not a partial shard (offsets = global indices)
-  a.fib = 0; a.fib_s0 = 0; a.idx0 = nullptr;
-  if (!bp.explicit_cols && bp.nright > 0 && bp.right[bp.rdig[0]] == 0 && bp.s[0] < c.dims[0] && bp.s[0] >= 16 &&
-      c.dims[0] <= 128 && !(c.cfg.shard_mode == 0 && c.shard_end - c.shard_begin < c.dims[0]) &&
-      !(getenv("TRD_NO_FIB"))) {
+  a.fib = 0; a.fib_s0 = 0; a.idx0 = nullptr; a.rfib = 0; a.ptab = nullptr; a.fib_nb = 0;
+  const bool mode0_sampled = !bp.explicit_cols && bp.s[0] < c.dims[0] && c.dims[0] <= 128 &&
+                             !(c.cfg.shard_mode == 0 && c.shard_end - c.shard_begin < c.dims[0]);
+  if (mode0_sampled && bp.nright > 0 && bp.right[bp.rdig[0]] == 0 && bp.s[0] >= 16 && !(getenv("TRD_NO_FIB"))) {
     a.fib = 1;
     a.fib_s0 = (int)bp.s[0];
     a.idx0 = c.idx + c.idx_off[0];
+  }
+  // row fibres: mode 0 the fastest row digit (k != 0 enumerates rows j_L fastest), 32 sampled
+  // positions, whole warps of rows per fibre
+  if (mode0_sampled && bp.k != 0 && bp.nleft > 0 && bp.left[bp.ldig[0]] == 0 && bp.s[0] == 32 &&
+      bp.nL % 32 == 0 && bp.rowmode == 0 && !(getenv("TRD_NO_RFIB"))) {
+    a.rfib = 1;
+    a.fib_s0 = 32;
+    a.idx0 = c.idx + c.idx_off[0];
+  }
+  if ((a.fib || a.rfib) && stage_uses_pext(c, bp)) {   // (tables written by the sampler)
+    a.ptab = c.ptab;
+    a.fib_nb = (int)((c.dims[0] + 7) / 8);
   }
   // grids of exactly the resident CTAs (the kernels loop over tiles): no partial last wave
   static int occ_bits = 0, occ_vals = 0;

@@ -141,6 +141,8 @@ def load_library(path: str = LIB_PATH):
         "trd_version": (ctypes.c_char_p, []),
     }
     for name, (res, args) in sig.items():
+        if path != os.path.join(HERE, "libtrd.so") and not hasattr(lib, name):
+            continue        # A/B experiments (TRD_LIB_PATH): an older library may lack newer calls
         f = getattr(lib, name)
         f.restype = res
         f.argtypes = args

@@ -351,6 +351,38 @@ def test_fibre_window_staging_equals_per_column_lookups(name, dims, sketch, monk
         assert cores_rel_err(outs[1], st.cores) <= 1e-4
 
 
+@pytest.mark.parametrize("name,dims,sketch", [("C4", [64, 20, 18, 16], [32, 8, 8, 8]),
+                                               ("C5a", [48, 12, 10, 9, 8], [32, 5, 5, 4, 4])])
+def test_row_fibre_and_table_compaction_staging_are_bitwise(name, dims, sketch, monkeypatch):
+    """Eq. 14 sketch staging with 32 sampled mode-0 positions: the row-fibre path (mode 0 the
+    fastest row digit: the 32 rows of a warp are one fibre, one window per column) and the
+    table compaction of fibre windows stage the same tiles as the per-column lookups: cores
+    after two sweeps bit-identical across (all off | default | tables off), within 1e-4 of the
+    oracle, dense and packed storage."""
+    _cuda()
+    spec = small_spec(name, dims, sketch)
+    prob = make_problem(spec)
+    src, _ = oracle_source(prob)
+    st, _ = O.run(oracle_config(spec), prob.init, src, 2)
+    variants = ({"TRD_NO_FIB": "1", "TRD_NO_RFIB": "1"}, {}, {"TRD_NO_PEXT": "1"})
+    for packed in (False, True):
+        outs = []
+        for env in variants:
+            for key in ("TRD_NO_FIB", "TRD_NO_RFIB", "TRD_NO_PEXT"):
+                if key in env:
+                    monkeypatch.setenv(key, env[key])
+                else:
+                    monkeypatch.delenv(key, raising=False)
+            ctx = gpu_context(prob, packed=packed)
+            ctx.sweep(2, stats=False)
+            outs.append(ctx.get_cores())
+            ctx.close()
+        for o in outs[1:]:
+            for a, b in zip(outs[0], o):
+                assert np.array_equal(a, b)
+        assert cores_rel_err(outs[1], st.cores) <= 1e-4
+
+
 # ---------------------------------------------------------------- upload layout cache (e2e)
 @pytest.mark.parametrize("packed", [False, True])
 def test_upload_with_changed_mask_restages_the_layout(packed):
