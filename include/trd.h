@@ -43,7 +43,7 @@ extern "C" {
 #endif
 
 #define TRD_MAX_ORDER 8
-#define TRD_MAX_RANK 32
+#define TRD_MAX_RANK 128
 
 typedef struct trd_ctx trd_ctx;
 
@@ -73,8 +73,13 @@ typedef struct {
   int32_t order;                    /* N, 3..TRD_MAX_ORDER                                  */
   int64_t dims[TRD_MAX_ORDER];      /* global I_0..I_{N-1}                                  */
   int32_t ranks[TRD_MAX_ORDER];     /* r_0..r_{N-1}, 1..TRD_MAX_RANK, ring r_N = r_0;
-                                       r_k r_{k+1} <= 1024, and every block must have a split
-                                       with r_k r_s <= 256 (else TRD_ERR_SHAPE)               */
+                                       r_k r_{k+1} <= TRD_MAX_RANK^2, and every block must have a
+                                       split with r_k r_s <= 256 (else TRD_ERR_SHAPE).  Blocks
+                                       with R_k^2 = r_k r_{k+1} > 1024 (the paper's [80,80,3,20],
+                                       P:328) take the large-rank path: FGMC products,
+                                       Q refresh and the filtered solve as fp64 cuBLAS /
+                                       cuSOLVER calls (dlopen'ed; TRD_ERR_CUDA if absent), one
+                                       host synchronisation per such block (no CUDA graphs)   */
   int32_t sigma_mode;               /* trd_sigma_mode                                       */
   double sigma;                     /* FIXED: the kernel width; RMS: ignored (sigma_0 from
                                        an initial residual pass); INF: ignored              */

@@ -9,7 +9,7 @@ LIB = os.path.join(HERE, "libtrd.so")
 # checked build (-DTRD_CHECKED=1): device invariant checks, mbarrier watchdog, schedule fuzzing
 # (tests/test_gpu_checked.py loads it in a subprocess via TRD_LIB_PATH)
 CHECKED_LIB = os.path.join(HERE, "libtrd_checked.so")
-SOURCES = ["trd_kernels.cu", "trd_tc.cu", "trd_api.cu"]
+SOURCES = ["trd_kernels.cu", "trd_tc.cu", "trd_big.cu", "trd_api.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden", "--expt-relaxed-constexpr",

@@ -118,6 +118,7 @@ trd_status dalloc(Context* c, T** p, size_t n) {
 }
 
 trd_status check_launch(Context* c, const char* what) {
+  if (c->sticky) return c->sticky;           // (a library call of the large-rank path failed)
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(c, TRD_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
   return TRD_OK;
@@ -261,8 +262,11 @@ void build_plan(const Context& c, int k, const int64_t* s_in, BlockPlan& bp, boo
     bp.tc_jl_chunk = (bp.nL + jc - 1) / jc;
     bp.tc_jc = (bp.nL + bp.tc_jl_chunk - 1) / bp.tc_jl_chunk;
   }
+  // large-rank path (R^2 > kBigR2): the SIMT pass writes one D row per (row, split), so one
+  // warp per row (ws_split = 1)
+  bp.big = bp.R2 > kBigR2 ? 1 : 0;
   // geometry: 8 warps per CTA, one (row, column sub-range) item per warp
-  if (bp.nL >= 8) { bp.jl_per_cta = 8; bp.ws_split = 1; }
+  if (bp.nL >= 8 || bp.big) { bp.jl_per_cta = (int)std::min<int64_t>(8, bp.nL); bp.ws_split = 1; }
   else {
     bp.jl_per_cta = (int)bp.nL;
     int ws = 8 / (int)bp.nL;
@@ -361,6 +365,7 @@ trd_status block_pass1(Context* c, const BlockPlan& bp) {
     launch_solve(*c, bp, side, c->Gloc);
   }
   tl_mark(c, side, "side: solve");
+  if (c->sticky) return c->sticky;
   CUDA_TRY(c, cudaEventRecord(c->ev_join, side));
   launch_plan(*c, bp, s);
   tl_mark(c, s, "plan (offsets, mid, rgt)");
@@ -409,6 +414,7 @@ trd_status block_pass2(Context* c, const BlockPlan& bp) {
   CUDA_TRY(c, cudaStreamWaitEvent(s, c->ev_join, 0));       // M of this block (side stream)
   tl_mark(c, s, "join (wait for the solve)");
   launch_h(*c, bp, s);
+  if (c->sticky) return c->sticky;           // (large-rank path: library call failures)
   tl_mark(c, s, "h = d M");
   if (!bp.use_tc) launch_lft(*c, bp, nullptr, 1, c->lfth, s);
   else launch_tc_lft(*c, bp, true, s);
@@ -461,6 +467,7 @@ trd_status sigma0_pass(Context* c) {
   // reduce the statistics into red_ws[0..2]: reuse reduce_d with R2 = 0 semantics
   BlockPlan tmp = bp;
   tmp.R2 = 0;
+  tmp.big = 0;
   double* saved = c->dvec;
   c->dvec = c->red_ws;
   launch_reduce_d(*c, tmp, s);
@@ -672,12 +679,23 @@ trd_status trd_init_ex(const trd_config* cfg, const trd_shard* shard, const floa
     const int64_t r2 = (int64_t)c->ranks[k] * c->ranks[(k + 1) % N];
     if (r2 > kMaxR2) { delete c; return TRD_ERR_SHAPE; }
     r2max = std::max(r2max, r2);
-    c->rbucket = std::max(c->rbucket, c->ranks[k] <= 16 ? 16 : 32);
+    c->rbucket = std::max(c->rbucket, c->ranks[k] <= 16 ? 16 : c->ranks[k] <= 32 ? 32 : 128);
     // FGMC chain products r_{k+1}^2 x r_m^2 (Eq. 13): the largest intermediate
     for (int m = 0; m < N; ++m)
       chain_max = std::max(chain_max, (int64_t)c->ranks[(k + 1) % N] * c->ranks[(k + 1) % N] * c->ranks[m] * c->ranks[m]);
   }
   c->chain_half = (size_t)chain_max;
+  int64_t r2big = 0, zd_rows = 0;                 // large-rank blocks (trd_big.cu)
+  for (int k = 0; k < N; ++k) {
+    const int64_t r2 = (int64_t)c->ranks[k] * c->ranks[(k + 1) % N];
+    if (r2 > kBigR2) { r2big = std::max(r2big, r2); zd_rows = std::max<int64_t>(zd_rows, c->dims[k]); }
+  }
+  if (r2big > 0) {                                // chain products in either order: <= (max r)^4
+    int64_t rmax = 0;
+    for (int k = 0; k < N; ++k) rmax = std::max<int64_t>(rmax, c->ranks[k]);
+    c->chain_half = std::max(c->chain_half, (size_t)(rmax * rmax * rmax * rmax));
+    c->has_big = 1;
+  }
 
   trd_status st = TRD_OK;
   auto bail = [&](trd_status s2) { trd_destroy(reinterpret_cast<trd_ctx*>(c)); return s2; };
@@ -712,6 +730,9 @@ trd_status trd_init_ex(const trd_config* cfg, const trd_shard* shard, const floa
       max_contrib = std::max(max_contrib, (size_t)bp.tc_nsplit * bp.n_row_tiles * 128 * bp.KP);
       max_sp = std::max(max_sp, (size_t)bp.tc_grid * 3);
       max_dp = std::max(max_dp, (size_t)(bp.tc_jc * c->dims[bp.k] * bp.R2));
+    } else if (bp.big && k < N) {            // SIMT D rows [nsplit][nrows][KP], contracted per jl chunk
+      max_contrib = std::max(max_contrib, (size_t)bp.nsplit * bp.nrows * bp.KP);
+      max_dp = std::max(max_dp, (size_t)(bp.tc_jc * c->dims[bp.k] * bp.R2));
     }
     max_rows = std::max(max_rows, (size_t)bp.nrows);
     max_cols = std::max(max_cols, (size_t)bp.ncols);
@@ -719,7 +740,7 @@ trd_status trd_init_ex(const trd_config* cfg, const trd_shard* shard, const floa
     max_rgt = std::max(max_rgt, (size_t)(bp.ncols * bp.K));
     max_mid = std::max(max_mid, (size_t)(bp.nL * bp.rk1 * bp.rs));
     const size_t Ik = (size_t)c->dims[bp.k];
-    max_dp = std::max(max_dp, Ik * ncta_of(bp) * (size_t)bp.R2);
+    if (!bp.big) max_dp = std::max(max_dp, Ik * ncta_of(bp) * (size_t)bp.R2);
     max_sp = std::max(max_sp, Ik * ncta_of(bp) * 3);
     max_dvec = std::max(max_dvec, Ik * (size_t)bp.R2 + 3);
     max_h = std::max(max_h, Ik * (size_t)bp.R2);
@@ -775,10 +796,11 @@ trd_status trd_init_ex(const trd_config* cfg, const trd_shard* shard, const floa
   if (max_lhl > 0) {
     if ((st = dalloc(c, &c->lftHL, max_lhl)) || (st = dalloc(c, &c->lfthHL, max_lhl)) ||
         (st = dalloc(c, &c->lscl, max_rpad)) || (st = dalloc(c, &c->lsclh, max_rpad)) ||
-        (st = dalloc(c, &c->rgtHL, max_rhl)) || (st = dalloc(c, &c->rgtHL2, max_rhl)) ||
-        (st = dalloc(c, &c->contrib, max_contrib)))
+        (st = dalloc(c, &c->rgtHL, max_rhl)) || (st = dalloc(c, &c->rgtHL2, max_rhl)))
       return bail(st);
   }
+  if (max_contrib > 0 && (st = dalloc(c, &c->contrib, max_contrib))) return bail(st);
+  if (c->has_big && (st = big_init(c, r2big, zd_rows))) return bail(st);
   if ((st = ensure_stats(c, 4))) return bail(st);
   cudaStream_t s = c->stream;
 
@@ -1020,7 +1042,7 @@ static void destroy_graph(SweepGraph& g) {
 static bool graph_usable(const Context* c) {
   const char* ge = getenv("TRD_GRAPH");
   const bool off = (ge && atoi(ge) == 0) || c->tl_on;
-  if (off || c->ex.allreduce) return false;
+  if (off || c->ex.allreduce || c->has_big) return false;   // (large-rank blocks sync the host)
   for (int k = 0; k < c->N; ++k)
     if (c->plan[k].use_tc && c->stage[k].invariant && !c->stage[k].valid) return false;
   return true;
@@ -1337,6 +1359,8 @@ void trd_destroy(trd_ctx* ctx) {
       fprintf(stderr, "  %-28s %9.1f  (x%d)\n", names[j].c_str(), sum[j] / cnt[j], cnt[j]);
     for (auto& t : c->tl) cudaEventDestroy((cudaEvent_t)t.ev);
   }
+  if (c->side) cudaStreamSynchronize(c->side);
+  big_destroy(c);
   for (auto& g : c->graphs) destroy_graph(g);
   if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
   if (c->nccl_comm && g_nccl.comm_destroy) g_nccl.comm_destroy(c->nccl_comm);

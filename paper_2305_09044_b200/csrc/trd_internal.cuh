@@ -14,6 +14,9 @@ namespace trd {
 constexpr int kMaxN = TRD_MAX_ORDER;
 constexpr int kMaxR = TRD_MAX_RANK;
 constexpr int kMaxR2 = kMaxR * kMaxR;
+// blocks with R_k^2 above this take the large-rank path (trd_big.cu): the d contraction by
+// reduce_d_big_kernel, and FGMC / Q refresh / filtered solve as fp64 cuBLAS / cuSOLVER calls
+constexpr int kBigR2 = 1024;
 
 // Per-sweep statistics kept on the device (one record per sweep of a trd_sweep call).
 struct DevStats {
@@ -182,6 +185,7 @@ struct BlockPlan {
   int tc_cl;             // CTAs per cluster of the pass kernels (2: B tiles multicast to a pair)
   int tc_u;              // column tiles per ring unit of the pass kernels (2: N = 128 GEMMs)
   int64_t tc_jc, tc_jl_chunk;   // d reduction: jl chunks
+  int big;               // R2 > kBigR2: large-rank path (SIMT pass 1 writes D rows to contrib)
 };
 
 // Staged working set of one block in tile order (trd_tc.cu "stage sketch", row a2)
@@ -226,7 +230,7 @@ struct Context {
                                        // concurrently with pass 1 (they need only cores != k)
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   int num_sm = 148;                    // SMs of the current device (persistent grids)
-  int rbucket = 16;                    // 16 or 32: >= every rank (register arrays of the plan kernels)
+  int rbucket = 16;                    // 16, 32 or 128: >= every rank (register arrays of the plan kernels)
   size_t chain_half = 0;               // doubles per FGMC chain buffer (chain_ws holds two)
   std::string err;
   trd_status sticky = TRD_OK;
@@ -324,6 +328,19 @@ struct Context {
   bool tl_on = false;
   std::vector<TlMark> tl;
   cudaStream_t cap_stream = nullptr;   // capture stream (the caller's may be the legacy stream)
+
+  // large-rank path (blocks with R_k^2 > kBigR2, trd_big.cu)
+  int has_big = 0;
+  void* blas = nullptr;                // cublasHandle_t
+  void* solver = nullptr;              // cusolverDnHandle_t
+  double* big_A = nullptr;             // A = G + lambda I, then its Cholesky factor (R2 x R2)
+  double* big_gam = nullptr;           // Q refresh: Zd^T Zd (R2 x R2)
+  double* big_zd = nullptr;            // Q refresh: the core in fp64, I_k x R2
+  double* big_work = nullptr;          // potrf workspace
+  int big_lwork = 0;
+  int* big_info = nullptr;             // potrf / potrs status (device)
+  int* big_info_h = nullptr;           // (pinned host copy)
+  const double* big_G = nullptr;       // the Gram the current block's solve factorised
 };
 
 // ---- kernels (trd_kernels.cu) --------------------------------------------------------
@@ -358,6 +375,17 @@ void launch_count_bits(Context& c, unsigned long long* out, cudaStream_t s);
 void launch_amax_obs(Context& c, cudaStream_t s);   // sc->amax_x of the observed values
 void launch_mask_compare(Context& c, cudaStream_t s); // sc->mask_same; stage_mask <- mask
 void launch_sweep_begin(Context& c, cudaStream_t s);
+void launch_phi(Context& c, const BlockPlan& bp, const double* C, double* G, cudaStream_t s);
+
+// ---- large-rank path (trd_big.cu) ------------------------------------------------------
+trd_status big_init(Context* c, int64_t r2big, int64_t zd_rows);   // handles + workspaces
+void big_destroy(Context* c);
+// row-major C (m x n) = A (m x q) B (q x n), fp64 (cuBLAS dgemm)
+trd_status big_dgemm(Context& c, cudaStream_t s, int m, int n, int q, const double* A, const double* B, double* C);
+trd_status big_q(Context& c, int k, cudaStream_t s);                 // Q_k refresh
+trd_status big_gram(Context& c, const BlockPlan& bp, cudaStream_t s, const double* Qsrc, double* Gout);
+trd_status big_factor(Context& c, const BlockPlan& bp, cudaStream_t s, const double* G);   // side stream
+trd_status big_h(Context& c, const BlockPlan& bp, cudaStream_t s);   // host check + retries, h, num
 
 // ---- tensor-core pass kernels (trd_tc.cu) ---------------------------------------------
 bool tc_supported_kp(int KP);
@@ -366,6 +394,9 @@ void launch_tc_pack_cols(Context& c, const BlockPlan& bp, cudaStream_t s);
 void launch_tc_lft(Context& c, const BlockPlan& bp, bool pass2, cudaStream_t s);
 void launch_tc_pass(Context& c, const BlockPlan& bp, const TcStage& st, bool pass2, cudaStream_t s);
 void launch_tc_reduce_d(Context& c, const BlockPlan& bp, cudaStream_t s);
+// d contraction of D rows in contrib ([nsplit][nrows_pad][KP]) for any R2, + final reduction
+void launch_reduce_d_contrib(Context& c, const BlockPlan& bp, int nsplit, int64_t nrows_pad, int64_t nparts,
+                             cudaStream_t s);
 void launch_tc_stage(Context& c, const BlockPlan& bp, TcStage& st, cudaStream_t s);
 size_t tc_scan_tmp_bytes(int64_t n_tiles);
 void tc_debug_dump();   // TRD_TC_EXP diagnostics

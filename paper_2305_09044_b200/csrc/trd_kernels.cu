@@ -482,6 +482,8 @@ struct PassArgs {
   uint32_t* eabs;     // TRD_SIGMA_MAD: |e| bit patterns of pass 1 (R21), else nullptr
   unsigned long long* efill;   // its fill counter (warp-aggregated atomics)
   unsigned long long ecap;
+  float* contrib;     // large-rank path (R2M == 0): D rows [split][row][KP] (ws_split == 1)
+  int KP;
 };
 
 __device__ __forceinline__ float warp_sum_f(float v) {
@@ -534,7 +536,10 @@ pass_kernel(PassArgs a) {
   const double s2 = sigma * sigma;
 
   double st_e2 = 0.0, st_w = 0.0, st_n = 0.0, st_den = 0.0;
-  constexpr int OUTS = R2M / 32;
+  // R2M == 0 (large-rank path, R^2 > kBigR2): the warp's D row (K floats) goes to contrib and
+  // reduce_d_big_kernel contracts it with Mid; the plan has ws_split == 1 (one warp per row)
+  constexpr bool WD = R2M == 0;
+  constexpr int OUTS = WD ? 1 : R2M / 32;
   double outacc[OUTS];
 #pragma unroll
   for (int q = 0; q < OUTS; ++q) outacc[q] = 0.0;
@@ -544,7 +549,11 @@ pass_kernel(PassArgs a) {
     const int sub = item % a.ws_split;
     const int64_t row = a.rowmode == 0 ? jl + a.nL * ik : ik + a.Ik * jl;
     const int64_t ro = a.row_off[row];
-    if (ro < 0) continue;
+    if (ro < 0) {
+      if (WD && !PASS2 && !STATS_ONLY)         // (a row outside the shard: zero D row)
+        for (int q = lane; q < a.K; q += 32) a.contrib[((int64_t)blockIdx.z * a.nrows + row) * a.KP + q] = 0.f;
+      continue;
+    }
     for (int q = lane; q < a.K; q += 32) {
       lftS[warp][q] = a.lft[row * a.K + q];
       if (PASS2) lfhS[warp][q] = a.lfth[row * a.K + q];
@@ -596,7 +605,15 @@ pass_kernel(PassArgs a) {
         }
       }
     }
-    if (!PASS2 && !STATS_ONLY) {
+    if (!PASS2 && !STATS_ONLY && WD) {
+#pragma unroll
+      for (int q = 0; q < KT; ++q) {
+        if (q < a.K) {
+          const float v = warp_sum_f(dacc[q]);
+          if (lane == 0) a.contrib[((int64_t)blockIdx.z * a.nrows + row) * a.KP + q] = v;
+        }
+      }
+    } else if (!PASS2 && !STATS_ONLY) {
       // reduce the per-lane gradient partials of this row over the warp
 #pragma unroll
       for (int q = 0; q < KT; ++q) {
@@ -651,7 +668,7 @@ pass_kernel(PassArgs a) {
     for (int w = 0; w < kPassWarps; ++w) tot += redS[w][RCH + threadIdx.x];
     a.spart[(ik * ncta + cta) * 3 + threadIdx.x] = tot;
   }
-  if (!STATS_ONLY) {
+  if (!STATS_ONLY && !WD) {
     // d partials over the warps in chunks of RCH columns (fixed order)
 #pragma unroll
     for (int c0 = 0; c0 < R2M; c0 += RCH) {
@@ -688,6 +705,8 @@ static PassArgs make_pass_args(const Context& c, const BlockPlan& bp) {
   a.eabs = c.cfg.sigma_mode == TRD_SIGMA_MAD ? c.eabs : nullptr;
   a.efill = &c.sc->eabs_fill;
   a.ecap = (unsigned long long)c.eabs_cap;
+  a.contrib = c.contrib;
+  a.KP = bp.KP;
   return a;
 }
 
@@ -695,8 +714,13 @@ template <bool PASS2, bool STATS_ONLY>
 static void launch_pass_t(Context& c, const BlockPlan& bp, cudaStream_t s) {
   PassArgs a = make_pass_args(c, bp);
   dim3 grid((unsigned)bp.grid_x, (unsigned)(bp.nrows / bp.nL), (unsigned)bp.nsplit);
-  // (K <= 256 and R^2 <= 1024 are checked at trd_init)
-  if (bp.R2 <= 256) {
+  // (K <= 256 is checked at trd_init; R^2 > kBigR2: D rows to contrib, no per-lane d)
+  if (bp.R2 > kBigR2 || PASS2 || STATS_ONLY) {
+    if (bp.K <= 32) pass_kernel<32, 0, PASS2, STATS_ONLY><<<grid, kPassThreads, 0, s>>>(a);
+    else if (bp.K <= 64) pass_kernel<64, 0, PASS2, STATS_ONLY><<<grid, kPassThreads, 0, s>>>(a);
+    else if (bp.K <= 128) pass_kernel<128, 0, PASS2, STATS_ONLY><<<grid, kPassThreads, 0, s>>>(a);
+    else pass_kernel<256, 0, PASS2, STATS_ONLY><<<grid, kPassThreads, 0, s>>>(a);
+  } else if (bp.R2 <= 256) {
     if (bp.K <= 32) pass_kernel<32, 256, PASS2, STATS_ONLY><<<grid, kPassThreads, 0, s>>>(a);
     else if (bp.K <= 64) pass_kernel<64, 256, PASS2, STATS_ONLY><<<grid, kPassThreads, 0, s>>>(a);
     else if (bp.K <= 128) pass_kernel<128, 256, PASS2, STATS_ONLY><<<grid, kPassThreads, 0, s>>>(a);
@@ -1128,8 +1152,8 @@ __global__ void __launch_bounds__(256) gj2_solve_kernel(const double* __restrict
 // num partial per row = <d(i), h(i)>
 __global__ void h_kernel(const double* __restrict__ dvec, const double* __restrict__ M, int R2,
                          double* __restrict__ h, double* __restrict__ numpart, const DevScalars* __restrict__ sc) {
-  __shared__ double drow[kMaxR2];
-  __shared__ double urow[kMaxR2];
+  __shared__ double drow[kBigR2];       // (R^2 <= kBigR2; larger blocks: big_h)
+  __shared__ double urow[kBigR2];
   __shared__ double red[256];
   const int64_t ik = blockIdx.x;
   const double hl = sc->h_lam;
@@ -1475,7 +1499,7 @@ __global__ void recon_kernel(ReconArgs a, const float* __restrict__ Z, const int
 __global__ void __launch_bounds__(256)
 error_kernel(PassArgs a, const float* __restrict__ ref, const uint32_t* __restrict__ evalb,
              double* __restrict__ part) {
-  __shared__ float lftS[8][kMaxR2];
+  __shared__ float lftS[8][256];        // (K <= 256)
   __shared__ double red[8][6];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   double s[6] = {0, 0, 0, 0, 0, 0};
@@ -1606,11 +1630,13 @@ void launch_plan(Context& c, const BlockPlan& bp, cudaStream_t s) {
   c.launches++;
   if (bp.p > 0) {
     if (c.rbucket <= 16) mid_kernel<16><<<grid_for(bp.nL * bp.rk1), 256, 0, s>>>(a, c.idx, c.Z, c.mid);
-    else mid_kernel<32><<<grid_for(bp.nL * bp.rk1), 256, 0, s>>>(a, c.idx, c.Z, c.mid);
+    else if (c.rbucket <= 32) mid_kernel<32><<<grid_for(bp.nL * bp.rk1), 256, 0, s>>>(a, c.idx, c.Z, c.mid);
+    else mid_kernel<128><<<grid_for(bp.nL * bp.rk1), 128, 0, s>>>(a, c.idx, c.Z, c.mid);
     c.launches++;
   }
   if (c.rbucket <= 16) rgt_kernel<16><<<grid_for(bp.ncols * bp.rs), 256, 0, s>>>(a, c.idx, c.Z, c.rgtT, c.sc);
-  else rgt_kernel<32><<<grid_for(bp.ncols * bp.rs), 256, 0, s>>>(a, c.idx, c.Z, c.rgtT, c.sc);
+  else if (c.rbucket <= 32) rgt_kernel<32><<<grid_for(bp.ncols * bp.rs), 256, 0, s>>>(a, c.idx, c.Z, c.rgtT, c.sc);
+  else rgt_kernel<128><<<grid_for(bp.ncols * bp.rs), 128, 0, s>>>(a, c.idx, c.Z, c.rgtT, c.sc);
   c.launches++;
 }
 
@@ -1620,9 +1646,12 @@ void launch_lft(Context& c, const BlockPlan& bp, const float* Zsrc_k, int src_is
   if (c.rbucket <= 16)
     lft_kernel<16><<<grid_for(bp.nrows * bp.rk), 256, 0, s>>>(a, src_is_h ? nullptr : Zsrc_k,
                                                               src_is_h ? c.h : nullptr, c.mid, out);
-  else
+  else if (c.rbucket <= 32)
     lft_kernel<32><<<grid_for(bp.nrows * bp.rk), 256, 0, s>>>(a, src_is_h ? nullptr : Zsrc_k,
                                                               src_is_h ? c.h : nullptr, c.mid, out);
+  else
+    lft_kernel<128><<<grid_for(bp.nrows * bp.rk), 128, 0, s>>>(a, src_is_h ? nullptr : Zsrc_k,
+                                                               src_is_h ? c.h : nullptr, c.mid, out);
   c.launches++;
 }
 
@@ -1638,6 +1667,10 @@ void launch_pass2(Context& c, const BlockPlan& bp, cudaStream_t s) {
 void launch_reduce_d(Context& c, const BlockPlan& bp, cudaStream_t s) {
   const int64_t Ik = bp.nrows / bp.nL, Ik_tot = c.dims[bp.k];
   const int64_t ncta = bp.grid_x * bp.nsplit;
+  if (bp.big && bp.R2 > 0) {           // D rows of the SIMT pass in contrib ([nsplit][nrows][KP])
+    launch_reduce_d_contrib(c, bp, bp.nsplit, bp.nrows, Ik * ncta, s);
+    return;
+  }
   if (bp.R2 > 0 && Ik < Ik_tot) cudaMemsetAsync(c.dvec, 0, (size_t)(Ik_tot * bp.R2) * sizeof(double), s);
   reduce_d_kernel<<<(unsigned)(Ik + 1), 256, 0, s>>>(c.dpart, c.spart, ncta, bp.R2, Ik, c.dvec,
                                                       bp.R2 > 0 ? c.sc : nullptr, bp.k, bp.ik0, Ik_tot);
@@ -1661,6 +1694,10 @@ void launch_reduce_den(Context& c, const BlockPlan& bp, cudaStream_t s) {
 
 void launch_q(Context& c, int k, cudaStream_t s) {
   const int r0 = c.ranks[k], r1 = c.ranks[(k + 1) % c.N];
+  if (r0 * r1 > kBigR2) {                   // large-rank path: Zd^T Zd by dgemm, permuted
+    big_q(c, k, s);                         // (a failure sets the context's sticky status)
+    return;
+  }
   q_kernel<<<grid_for((int64_t)r0 * r0 * r1 * r1 * 32), 256, 0, s>>>(c.Z + c.zoff[k], c.dims[k], r0, r1,
                                                                       c.Q + c.qoff[k]);
   c.launches++;
@@ -1701,12 +1738,22 @@ __global__ void identity_kernel(double* __restrict__ M, int n, DevScalars* __res
 
 // M = I: h = d M = d (the 'gradient descent' ablation arm)
 void launch_identity_op(Context& c, const BlockPlan& bp, cudaStream_t s) {
+  if (bp.big) return;                  // (big_h: h = d)
   identity_kernel<<<grid_for((int64_t)bp.R2 * bp.R2), 256, 0, s>>>(c.Mop, bp.R2, c.sc);
+  c.launches++;
+}
+
+void launch_phi(Context& c, const BlockPlan& bp, const double* C, double* G, cudaStream_t s) {
+  phi_kernel<<<grid_for((int64_t)bp.R2 * bp.R2), 256, 0, s>>>(C, bp.rk, bp.rk1, G);
   c.launches++;
 }
 
 void launch_gram(Context& c, const BlockPlan& bp, cudaStream_t s, const double* Qsrc, double* Gout) {
   const int N = c.N, k = bp.k;
+  if (bp.big) {
+    big_gram(c, bp, s, Qsrc, Gout);
+    return;
+  }
   // C = Q_{k+1} Q_{k+2} ... Q_{k-1}
   const double* cur = Qsrc + c.qoff[(k + 1) % N];
   int m_rows = bp.rk1 * bp.rk1;
@@ -1728,6 +1775,10 @@ void launch_gram(Context& c, const BlockPlan& bp, cudaStream_t s, const double* 
 
 void launch_solve(Context& c, const BlockPlan& bp, cudaStream_t s, const double* G) {
   const int n = bp.R2;
+  if (bp.big) {                        // Cholesky of G + lambda I (cuSOLVER); h in big_h
+    big_factor(c, bp, s, G);
+    return;
+  }
   if (n <= 128 && !(getenv("TRD_SOLVE") && atoi(getenv("TRD_SOLVE")) == 1)) {
     const int np = (n + 15) / 16 * 16;
     switch (np) {
@@ -1772,6 +1823,10 @@ void launch_solve(Context& c, const BlockPlan& bp, cudaStream_t s, const double*
 }
 
 void launch_h(Context& c, const BlockPlan& bp, cudaStream_t s) {
+  if (bp.big) {
+    big_h(c, bp, s);
+    return;
+  }
   const int64_t Ik = c.dims[bp.k];                     // h of every i_k (replicated update)
   h_kernel<<<(unsigned)Ik, 256, 0, s>>>(c.dvec, c.Mop, bp.R2, c.h, c.numpart, c.sc);
   c.launches++;
@@ -1890,7 +1945,8 @@ void launch_reconstruct(Context& c, const int64_t* lin, int64_t n, float* out, c
   for (int m = 0; m < c.N; ++m) a.dims[m] = c.dims[m];
   for (int m = 0; m <= c.N; ++m) { a.ranks[m] = c.ranks[m % c.N]; a.zoff[m] = c.zoff[m]; }
   if (c.rbucket <= 16) recon_kernel<16><<<grid_for(n), 256, 0, s>>>(a, c.Z, lin, n, out);
-  else recon_kernel<32><<<grid_for(n), 256, 0, s>>>(a, c.Z, lin, n, out);
+  else if (c.rbucket <= 32) recon_kernel<32><<<grid_for(n), 256, 0, s>>>(a, c.Z, lin, n, out);
+  else recon_kernel<128><<<grid_for(n), 128, 0, s>>>(a, c.Z, lin, n, out);
   c.launches++;
 }
 

@@ -1258,6 +1258,39 @@ __global__ void __launch_bounds__(128) tc_reduce_d_rb_kernel(const float* __rest
   }
 }
 
+// Large-rank stage 1 (R^2 > kBigR2, any KP; D rows of the tcgen05 or the SIMT pass 1): thread
+// per output o = a + r_k b of d(i_k), grid (I_k, JC, ceil(R^2 / 256)); for each jl of the chunk
+// (ascending) u = sum_c Mid(jl)[b][c] sum_split D(split, row)[a + r_k c] in fp32, added to an
+// fp64 sum -- the same contraction as tc_reduce_d_kernel without the shared-memory staging
+// (Eq. 9/15).
+__global__ void __launch_bounds__(256) reduce_d_big_kernel(
+    const float* __restrict__ contrib, const float* __restrict__ mid, int nsplit, int64_t nrows_pad, int64_t nL,
+    int64_t Ik, int rowmode, int KP, int R2, int rk, int rk1, int rs, int p, int64_t jl_chunk,
+    double* __restrict__ dpart) {
+  const int64_t ik = blockIdx.x, jc = blockIdx.y;
+  const int o = blockIdx.z * blockDim.x + threadIdx.x;
+  if (o >= R2) return;
+  const int aa = o % rk, bq = o / rk;
+  const int64_t j0 = jc * jl_chunk, j1 = min(nL, j0 + jl_chunk);
+  double s = 0.0;
+  for (int64_t jl = j0; jl < j1; ++jl) {
+    const int64_t row = rowmode == 0 ? jl + nL * ik : ik + Ik * jl;
+    float u = 0.f;
+    if (p == 0) {
+      for (int sp = 0; sp < nsplit; ++sp) u += __ldg(contrib + ((int64_t)sp * nrows_pad + row) * KP + o);
+    } else {
+      const float* M = mid + (jl * rk1 + bq) * rs;
+      for (int c = 0; c < rs; ++c) {
+        float dsum = 0.f;
+        for (int sp = 0; sp < nsplit; ++sp) dsum += __ldg(contrib + ((int64_t)sp * nrows_pad + row) * KP + aa + rk * c);
+        u = fmaf(__ldg(M + c), dsum, u);
+      }
+    }
+    s += (double)u;
+  }
+  dpart[(jc * Ik + ik) * R2 + o] = s;
+}
+
 // stage 2: dvec = [d | sum_e2 | welsch | n] from the chunk partials and the per-CTA statistics
 __global__ void tc_reduce_final_kernel(const double* __restrict__ dpart, int64_t JC, int64_t Ik, int R2,
                                        const double* __restrict__ spart, int64_t nparts,
@@ -1543,8 +1576,24 @@ void launch_tc_pass(Context& c, const BlockPlan& bp, const TcStage& st, bool pas
   }
 }
 
+void launch_reduce_d_contrib(Context& c, const BlockPlan& bp, int nsplit, int64_t nrows_pad, int64_t nparts,
+                             cudaStream_t s) {
+  const int64_t Ik = bp.nrows / bp.nL;
+  if (Ik < c.dims[bp.k]) cudaMemsetAsync(c.dvec, 0, (size_t)(c.dims[bp.k] * bp.R2) * sizeof(double), s);
+  reduce_d_big_kernel<<<dim3((unsigned)Ik, (unsigned)bp.tc_jc, (unsigned)((bp.R2 + 255) / 256)), 256, 0, s>>>(
+      c.contrib, c.mid, nsplit, nrows_pad, bp.nL, Ik, bp.rowmode, bp.KP, bp.R2, bp.rk, bp.rk1, bp.rs, bp.p,
+      bp.tc_jl_chunk, c.dpart);
+  tc_reduce_final_kernel<<<(unsigned)(Ik + 1), 128, 0, s>>>(c.dpart, bp.tc_jc, Ik, bp.R2, c.spart, nparts,
+                                                            c.dvec, c.sc, bp.k, bp.ik0, c.dims[bp.k]);
+  c.launches += 2;
+}
+
 void launch_tc_reduce_d(Context& c, const BlockPlan& bp, cudaStream_t s) {
   const int64_t Ik = bp.nrows / bp.nL;
+  if (bp.R2 > kBigR2) {
+    launch_reduce_d_contrib(c, bp, bp.tc_nsplit, bp.n_row_tiles * TC_M, bp.tc_grid1, s);
+    return;
+  }
   if (Ik < c.dims[bp.k]) cudaMemsetAsync(c.dvec, 0, (size_t)(c.dims[bp.k] * bp.R2) * sizeof(double), s);
   if (bp.p > 0 && bp.rk == 8 && bp.rk1 == 8 && bp.rs == 8 && bp.KP == 64) {
     tc_reduce_d_rb_kernel<8, 8, 8><<<dim3((unsigned)Ik, (unsigned)bp.tc_jc), 128, 0, s>>>(

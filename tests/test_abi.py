@@ -48,7 +48,7 @@ def test_invalid_arguments_rejected_without_gpu():
     cfg.order = 3
     for m in range(3):
         cfg.dims[m] = 4
-        cfg.ranks[m] = 99               # rank > TRD_MAX_RANK
+        cfg.ranks[m] = 129              # rank > TRD_MAX_RANK (128)
     assert lib.trd_init(ctypes.byref(cfg), ctypes.byref(sh), arr, None, ctypes.byref(ctx)) in (1, 2)
     assert lib.trd_sweep(None, 1, None) == 1
     st = T.trd_state()

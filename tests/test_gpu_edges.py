@@ -289,11 +289,16 @@ def test_graph_replay_equals_eager_sweeps(name, dims, sketch, monkeypatch):
 @pytest.mark.parametrize("name,dims,ranks,sketch", [
     ("C2", [256, 256, 3], [20, 20, 3], None),            # the paper's image ranks
     ("C3", [40, 36, 3, 16], [12, 12, 3, 8], [24, 20, 0, 10]),
+    # the paper's video ranks: R^2 = 6400 / 240 / 60 / 1600, i.e. the large-rank
+    # path (R^2 > 1024: cuBLAS / cuSOLVER fp64 Gram, Q and solve; SIMT pass 1 with K = 240
+    # writing D rows; tensor-core block 3 with K = 60 and the large-rank d contraction)
+    ("C3", [24, 48, 3, 48], [80, 80, 3, 20], [0, 24, 0, 24]),
 ])
 def test_large_ranks_match_oracle(name, dims, ranks, sketch):
     """The large-rank regime: R_k^2 = 400 / 144 blocks (Cholesky solve,
-    generic Lft pack from global memory), tensor-core splits with K = r_k r_s <= 128; block
-    quantities row by row and the cores after one sweep."""
+    generic Lft pack from global memory), tensor-core splits with K = r_k r_s <= 128, and the
+    paper's [80, 80, 3, 20] (R_k^2 up to 6400); block quantities row by row and the cores
+    after one sweep."""
     _cuda()
     spec = small_spec(name, dims, sketch)
     spec.ranks = list(ranks)
