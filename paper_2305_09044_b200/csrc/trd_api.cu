@@ -179,6 +179,28 @@ void build_plan(const Context& c, int k, const int64_t* s_in, BlockPlan& bp, boo
     int64_t ncols = 1;
     for (int q = p + 1; q <= N - 1; ++q) ncols *= bp.s[(k + q) % N];
     double cost = want_tc ? plan_cost_tc(K, ncols) : plan_cost(K, ncols);
+    if (c.rbucket > 32) {
+      // ranks > 32: K > 128 runs the SIMT pass (~8x the tensor-core cost per position), and
+      // the chain products of the plan kernels (per column / left index / row, not shared
+      // between them) can exceed the passes: add their FMAs per working-set position
+      const int64_t KP = (K + 15) / 16 * 16;
+      if (!(want_tc && KP <= 128)) cost = 8.0 * plan_cost(K, ncols);
+      int64_t nL = 1;
+      double f_mid = 0.0, f_rgt = 0.0;
+      for (int q = 1; q <= p; ++q) {
+        const int m = (k + q) % N;
+        nL *= bp.s[m];
+        f_mid += (double)c.ranks[m] * c.ranks[(m + 1) % N];
+      }
+      for (int q = p + 1; q <= N - 1; ++q) {
+        const int m = (k + q) % N;
+        f_rgt += (double)c.ranks[m] * c.ranks[(m + 1) % N];
+      }
+      const double rows = (double)bp.s[k] * nL;
+      const double chain = (double)ncols * rs * f_rgt + (double)nL * c.ranks[(k + 1) % N] * f_mid +
+                           (p > 0 ? rows * c.ranks[k] * c.ranks[(k + 1) % N] * rs : 0.0);
+      cost += chain / std::max(1.0, rows * (double)ncols);
+    }
     if (K > 256) cost += 1e200;            // the pass kernels need K = r_k r_s <= 256
     if (cost < best - 1e-12) { best = cost; best_p = p; }
   }

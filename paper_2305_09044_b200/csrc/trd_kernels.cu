@@ -335,6 +335,18 @@ __global__ void offsets_kernel(PlanArgs a, const int64_t* __restrict__ doff,
 // (16 or 32, >= every rank of the context: register arrays of compile-time size)
 template <int RM>
 __device__ __forceinline__ void vecmat(float* v, const float* __restrict__ Zs, int rin, int rout) {
+  if (RM > 32) {                     // large-rank bucket: runtime loop bounds (the arrays live in
+    float nv[RM];                    // local memory; a fully unrolled predicated RM-loop would
+    for (int c = 0; c < rout; ++c) nv[c] = 0.f;   // issue RM FMAs per input for any r_out)
+    for (int a = 0; a < rin; ++a) {
+      const float va = v[a];
+      const float* row = Zs + a * rout;
+      for (int c = 0; c < rout; ++c) nv[c] = fmaf(va, __ldg(row + c), nv[c]);
+    }
+    for (int c = 0; c < rout; ++c) v[c] = nv[c];
+    for (int c = rout; c < RM; ++c) v[c] = 0.f;
+    return;
+  }
   float nv[RM];
 #pragma unroll
   for (int c = 0; c < RM; ++c) nv[c] = 0.f;
@@ -1750,7 +1762,7 @@ void launch_phi(Context& c, const BlockPlan& bp, const double* C, double* G, cud
 
 void launch_gram(Context& c, const BlockPlan& bp, cudaStream_t s, const double* Qsrc, double* Gout) {
   const int N = c.N, k = bp.k;
-  if (bp.big) {
+  if (c.has_big) {                     // (cuBLAS loaded: every chain by dgemm, cheaper order)
     big_gram(c, bp, s, Qsrc, Gout);
     return;
   }

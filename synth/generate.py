@@ -67,6 +67,11 @@ CONFIGS = {
                        [32] * 5, 2, 20, 1005, 2005, 3005),
     "C5b": ProblemSpec("C5b", [80] * 5, [8] * 5, 0.05, 0.10, "uniform", 10.0, 0.0, "unit",
                        [0] * 5, 2, 20, 1005, 2005, 3005),
+    # C6 (not a BASELINE config): the paper's own video completion workload
+    # -- 1920 x 1080 x 3 x 50 rescaled to [0, 1], 30 % observed, 20 % salt & pepper,
+    # TR ranks [80, 80, 3, 20], J = prod_{m != k} s_m = 3e4 for blocks 0 and 1 (s = 200, 200, 3, 50)
+    "C6": ProblemSpec("C6", [1920, 1080, 3, 50], [80, 80, 3, 20], 0.3, 0.20, "saltpepper", 0.0, 0.0,
+                      "minmax", [200, 200, 3, 50], 2, 20, 1006, 2006, 3006),
 }
 
 
