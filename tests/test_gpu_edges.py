@@ -327,6 +327,48 @@ def test_large_ranks_match_oracle(name, dims, ranks, sketch):
     ctx.close()
 
 
+def _paper_rank_spec():
+    spec = small_spec("C3", [24, 48, 3, 48], [0, 24, 0, 24])
+    spec.ranks = [80, 80, 3, 20]
+    return spec
+
+
+@pytest.mark.parametrize("over", [dict(sigma_mode=O.SIGMA_MAD), dict(scaling=O.SCALING_NONE),
+                                  dict(scaling=O.SCALING_LOCAL)])
+def test_paper_ranks_variants_match_oracle(over):
+    """The large-rank path under the method's variants: the robust sigma rule R21 (the SIMT
+    pass's |e| stores feed the exact select), the 'gradient descent' arm (h = d without a
+    solve) and the 'local scaled term' arm (Gram of the sampled slices, cuSOLVER solve) --
+    cores after one sweep vs the oracle."""
+    _cuda()
+    spec = _paper_rank_spec()
+    prob = make_problem(spec)
+    src, _ = oracle_source(prob)
+    st, _ = O.run(oracle_config(spec, **over), prob.init, src, 1)
+    ctx = gpu_context(prob, packed=True, **over)
+    ctx.sweep(1)
+    assert cores_rel_err(ctx.get_cores(), st.cores) <= 1e-4
+    ctx.close()
+
+
+def test_paper_ranks_final_error_matches_oracle():
+    """North-star bar on the paper's ranks: relative reconstruction error after 4 sweeps
+    within 1e-3 of the oracle's, and trd_error equal to the oracle formula."""
+    _cuda()
+    spec = _paper_rank_spec()
+    prob = make_problem(spec)
+    src, Xc = oracle_source(prob)
+    st, _ = O.run(oracle_config(spec), prob.init, src, 4)
+    e_or = O.relative_error(st.cores, Xc)
+    ctx = gpu_context(prob, packed=True)
+    ctx.sweep(4, stats=False)
+    gerr = ctx.error(prob.X_clean.cuda())
+    e_gpu_or = O.relative_error(ctx.get_cores(), Xc)
+    assert abs(gerr["rel_err_all"] - e_gpu_or) <= 1e-5
+    assert abs(e_gpu_or - e_or) <= 1e-3, (e_gpu_or, e_or)
+    ctx.close()
+
+
 # ---------------------------------------------------------------- staging paths (a2)
 @pytest.mark.parametrize("name,dims,sketch", [("C4", [48, 20, 18, 16], [24, 8, 8, 8]),
                                                ("C5a", [40, 12, 10, 9, 8], [20, 5, 5, 4, 4])])

@@ -134,6 +134,27 @@ def test_world2_exchange_matches_oracle_and_replicas_agree(name, dims, sketch, s
         c.close()
 
 
+def test_world2_exchange_with_paper_ranks():
+    """World 2 on the large-rank path (ranks [80, 80, 3, 20]): per-rank SIMT passes
+    writing D rows, the exchange of the 6400-column d, identical cuSOLVER / cuBLAS solves on
+    both replicas (bitwise equal cores), cores vs the oracle."""
+    _cuda()
+    spec = small_spec("C3", [24, 48, 3, 48], [0, 24, 0, 24])
+    spec.ranks = [80, 80, 3, 20]
+    prob = make_problem(spec, keep_mask_bool=True)
+    src, _ = oracle_source(prob)
+    st, _ = O.run(oracle_config(spec), prob.init, src, 1)
+    ctxs, outs, errs, _ = _run_world2(spec, prob, 1)
+    assert errs == [None, None], errs
+    c0, c1 = ctxs[0].get_cores(), ctxs[1].get_cores()
+    for a, b in zip(c0, c1):
+        assert np.array_equal(a, b)
+    assert outs[0][0]["replica_mismatch"] == 0
+    assert cores_rel_err(c0, st.cores) <= 1e-4
+    for c in ctxs:
+        c.close()
+
+
 def test_world2_replica_divergence_is_detected():
     """A rank whose exchange result differs (here: its d scaled by 1 + 1e-3) ends the sweep with
     cores that differ from its peer's: the per-sweep checksum comparison flags it and
