@@ -725,7 +725,7 @@ trd_status trd_init_ex(const trd_config* cfg, const trd_shard* shard, const floa
   // ---- plans and workspace sizes ----
   size_t max_rows = 0, max_cols = 0, max_lft = 0, max_rgt = 0, max_mid = 0, max_dp = 0, max_sp = 0;
   size_t max_dvec = 0, max_h = 0, idx_total = 0;
-  size_t max_lhl = 0, max_rhl = 0, max_contrib = 0, max_rpad = 0;
+  size_t max_lhl = 0, max_rhl = 0, max_contrib = 0, max_rpad = 0, max_rgtc = 0;
   int64_t full_s[kMaxN];
   for (int m = 0; m < N; ++m) full_s[m] = 0;
   {
@@ -738,6 +738,24 @@ trd_status trd_init_ex(const trd_config* cfg, const trd_shard* shard, const floa
     else build_plan(*c, 0, full_s, bp, false);
     if (bp.use_tc && !tc_supported_kp(bp.KP)) bp.use_tc = 0;
     if (bp.K > 256) return bail(fail(c, TRD_ERR_SHAPE, "block %d: no split with r_k r_s <= 256", k));
+    bp.rows = 0;
+    if (!bp.use_tc && bp.K > 128) {          // warp-per-row SIMT passes (simt_rows_kernel)
+      bp.rows = 1;
+      int64_t ns = ((int64_t)c->num_sm * 64 + bp.nrows - 1) / std::max<int64_t>(1, bp.nrows);
+      ns = std::max<int64_t>(1, std::min<int64_t>(ns, std::max<int64_t>(1, bp.ncols / 64)));
+      int64_t per = (bp.ncols + ns - 1) / ns;
+      per = (per + 31) / 32 * 32;
+      bp.rows_per = per;
+      bp.rows_nsplit = (int)((bp.ncols + per - 1) / per);
+      const int64_t items = bp.nrows * bp.rows_nsplit;
+      bp.rows_grid = (int)std::max<int64_t>(1, std::min<int64_t>((items + 7) / 8, (int64_t)c->num_sm * 8));
+      max_rgtc = std::max(max_rgtc, (size_t)(bp.ncols * bp.KP));
+      max_sp = std::max(max_sp, (size_t)bp.rows_grid * 3);
+      if (k < N) {
+        max_contrib = std::max(max_contrib, (size_t)bp.rows_nsplit * bp.nrows * bp.KP);
+        max_dp = std::max(max_dp, (size_t)(bp.tc_jc * c->dims[bp.k] * bp.R2));
+      }
+    }
     if (bp.use_tc) {
       TcStage& st = c->stage[k];
       st.n_tiles = bp.n_row_tiles * bp.n_col_tiles;
@@ -752,7 +770,7 @@ trd_status trd_init_ex(const trd_config* cfg, const trd_shard* shard, const floa
       max_contrib = std::max(max_contrib, (size_t)bp.tc_nsplit * bp.n_row_tiles * 128 * bp.KP);
       max_sp = std::max(max_sp, (size_t)bp.tc_grid * 3);
       max_dp = std::max(max_dp, (size_t)(bp.tc_jc * c->dims[bp.k] * bp.R2));
-    } else if (bp.big && k < N) {            // SIMT D rows [nsplit][nrows][KP], contracted per jl chunk
+    } else if (bp.big && !bp.rows && k < N) {   // SIMT D rows [nsplit][nrows][KP], contracted per jl chunk
       max_contrib = std::max(max_contrib, (size_t)bp.nsplit * bp.nrows * bp.KP);
       max_dp = std::max(max_dp, (size_t)(bp.tc_jc * c->dims[bp.k] * bp.R2));
     }
@@ -762,8 +780,8 @@ trd_status trd_init_ex(const trd_config* cfg, const trd_shard* shard, const floa
     max_rgt = std::max(max_rgt, (size_t)(bp.ncols * bp.K));
     max_mid = std::max(max_mid, (size_t)(bp.nL * bp.rk1 * bp.rs));
     const size_t Ik = (size_t)c->dims[bp.k];
-    if (!bp.big) max_dp = std::max(max_dp, Ik * ncta_of(bp) * (size_t)bp.R2);
-    max_sp = std::max(max_sp, Ik * ncta_of(bp) * 3);
+    if (!bp.big && !bp.rows) max_dp = std::max(max_dp, Ik * ncta_of(bp) * (size_t)bp.R2);
+    if (!bp.rows) max_sp = std::max(max_sp, Ik * ncta_of(bp) * 3);
     max_dvec = std::max(max_dvec, Ik * (size_t)bp.R2 + 3);
     max_h = std::max(max_h, Ik * (size_t)bp.R2);
   }
@@ -822,6 +840,7 @@ trd_status trd_init_ex(const trd_config* cfg, const trd_shard* shard, const floa
       return bail(st);
   }
   if (max_contrib > 0 && (st = dalloc(c, &c->contrib, max_contrib))) return bail(st);
+  if (max_rgtc > 0 && (st = dalloc(c, &c->rgtC, max_rgtc))) return bail(st);
   if (c->has_big && (st = big_init(c, r2big, zd_rows))) return bail(st);
   if ((st = ensure_stats(c, 4))) return bail(st);
   cudaStream_t s = c->stream;
@@ -1411,7 +1430,7 @@ void trd_destroy(trd_ctx* ctx) {
                   c->denpart, c->numpart, c->dvec, c->G, c->G_last, c->Mop, c->chol_ws,
                   c->chain_ws, c->h, c->Dcur, c->Dprev, c->sc, c->stats, c->red_ws,
                   c->lftHL, c->lfthHL, c->lscl, c->lsclh, c->rgtHL, c->rgtHL2, c->contrib, c->Qloc, c->Gloc, c->mhist,
-                  c->eabs, c->chk, c->chk_acc, c->stage_mask, c->ptab};
+                  c->eabs, c->chk, c->chk_acc, c->stage_mask, c->ptab, c->rgtC};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (c->tw) cudaFree(c->tw);

@@ -186,6 +186,9 @@ struct BlockPlan {
   int tc_u;              // column tiles per ring unit of the pass kernels (2: N = 128 GEMMs)
   int64_t tc_jc, tc_jl_chunk;   // d reduction: jl chunks
   int big;               // R2 > kBigR2: large-rank path (SIMT pass 1 writes D rows to contrib)
+  int rows;              // SIMT plan with K > 128: warp-per-row passes (simt_rows_kernel)
+  int rows_nsplit, rows_grid;   //   column splits per row, CTAs (8 warps each)
+  int64_t rows_per;             //   columns per split (multiple of 32)
 };
 
 // Staged working set of one block in tile order (trd_tc.cu "stage sketch", row a2)
@@ -278,6 +281,7 @@ struct Context {
   float* lft = nullptr;                // Lft rows: [row][K]
   float* lfth = nullptr;               // Lft of the scaled gradient (pass 2)
   float* rgtT = nullptr;               // Rgt: [K][ncols]
+  float* rgtC = nullptr;               // Rgt column-major [col][KP] (warp-per-row SIMT passes)
   // tensor-core operands: fp16 hi/lo core-matrix tiles, and per-row gradient contributions
   int want_tc = 1;                     // TRD_PASS=simt disables the tcgen05 pass kernels
   __half* lftHL = nullptr;             // [row][hi KP | lo KP] (A operand, loaded into TMEM)

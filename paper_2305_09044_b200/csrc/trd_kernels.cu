@@ -373,10 +373,20 @@ __global__ void mid_kernel(PlanArgs a, const int32_t* __restrict__ idx, const fl
     int64_t dq[kMaxN];
     left_digits(a, jl, dq);
     float v[RM];
+    int rin = a.rk1, q0 = 0;
+    if (RM > 32 && a.nleft > 0) {            // large ranks: e_b Z(i) is row b of the first slice
+      const int m = a.left[0];
+      const int rout = a.rank_of[m + 1];
+      const float* zr = Z + a.zoff[m] + (int64_t)idx[a.offL[0] + dq[0]] * a.rank_of[m] * rout + (int64_t)b * rout;
+      for (int c = 0; c < rout; ++c) v[c] = __ldg(zr + c);
+      for (int c = rout; c < RM; ++c) v[c] = 0.f;
+      rin = rout;
+      q0 = 1;
+    } else {
 #pragma unroll
-    for (int c = 0; c < RM; ++c) v[c] = (c == b) ? 1.f : 0.f;
-    int rin = a.rk1;
-    for (int q = 0; q < a.nleft; ++q) {
+      for (int c = 0; c < RM; ++c) v[c] = (c == b) ? 1.f : 0.f;
+    }
+    for (int q = q0; q < a.nleft; ++q) {
       int m = a.left[q];
       int64_t i = idx[a.offL[q] + dq[q]];
       int rout = a.rank_of[m + 1];
@@ -416,10 +426,20 @@ __global__ void rgt_kernel(PlanArgs a, const int32_t* __restrict__ idx, const fl
     int64_t dq[kMaxN];
     right_digits(a, col, dq);
     float v[RM];
+    int rin = a.rs, q0 = 0;
+    if (RM > 32 && a.nright > 0) {           // large ranks: e_cc Z(i) is row cc of the first slice
+      const int m = a.right[0];
+      const int rout = a.rank_of[m + 1];
+      const float* zr = Z + a.zoff[m] + (int64_t)idx[a.offR[0] + dq[0]] * a.rank_of[m] * rout + (int64_t)cc * rout;
+      for (int c = 0; c < rout; ++c) v[c] = __ldg(zr + c);
+      for (int c = rout; c < RM; ++c) v[c] = 0.f;
+      rin = rout;
+      q0 = 1;
+    } else {
 #pragma unroll
-    for (int c = 0; c < RM; ++c) v[c] = (c == cc) ? 1.f : 0.f;
-    int rin = a.rs;
-    for (int q = 0; q < a.nright; ++q) {
+      for (int c = 0; c < RM; ++c) v[c] = (c == cc) ? 1.f : 0.f;
+    }
+    for (int q = q0; q < a.nright; ++q) {
       int m = a.right[q];
       int64_t i = idx[a.offR[q] + dq[q]];
       int rout = a.rank_of[m + 1];
@@ -701,6 +721,160 @@ pass_kernel(PassArgs a) {
   }
 }
 
+// ----------------------------------------------------------------------------------------
+// SIMT passes for 128 < K <= 256 (no tensor-core kernel; the large-rank regime, e.g. the
+// paper's [80, 80, 3, 20] with K = r_k r_s = 240).  Warp per (GEMM row, column split); lane l
+// owns the inner indices kappa = l + 32 m (m < 8) of Lft(row) and of the D row in registers.
+// Columns are scanned 32 at a time (lane = column: mask bit and value), and the warp
+// walks the observed ones: the entry's Rgt column (stored column-major, rgtC[col][kappa]:
+// one coalesced 128-B load per m) gives s = <Lft, Rgt> by a fixed butterfly over the lanes,
+// then e, w, c = w e (Eq. 7, 9; Thm 1) and D += c Rgt on the lanes' own kappa -- no per-lane
+// K-long accumulators (the column-per-lane pass_kernel needs 256 registers at K = 256 and
+// spills), and unobserved positions cost nothing.  Pass 1 writes the D row to contrib
+// ([split][row][KP], contracted by reduce_d_big_kernel); pass 2 recomputes w from the cores'
+// residual and sums den += w t^2 with t = <Lft_h, Rgt> (Eq. 12 / 18).
+// ----------------------------------------------------------------------------------------
+struct RowsArgs {
+  int64_t nrows, ncols, per;     // columns per split
+  int K, KP, nsplit;
+  int sigma_inf, packed;
+  const int64_t* row_off;
+  const int64_t* col_off;
+  const float* lft;              // [row][K]
+  const float* lfth;             // [row][K] (pass 2)
+  const float* rgtC;             // [col][KP]
+  const float* values;
+  const uint32_t* mask;
+  const uint32_t* rank_prefix;
+  const DevScalars* sc;
+  float* contrib;                // [split][row][KP]
+  double* spart;                 // [cta][3]
+  double* denpart;               // [cta]
+  uint32_t* eabs;                // R21 |e| slots (pass 1), else nullptr
+  unsigned long long* efill;
+  unsigned long long ecap;
+};
+
+__global__ void rgt_colmajor_kernel(const float* __restrict__ rgtT, int64_t ncols, int K, int KP,
+                                    float* __restrict__ rgtC) {
+  const int64_t tot = ncols * KP;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tot; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t col = t / KP;
+    const int q = (int)(t - col * KP);
+    rgtC[t] = q < K ? rgtT[(int64_t)q * ncols + col] : 0.f;
+  }
+}
+
+template <bool PASS2, bool STATS_ONLY>
+__global__ void __launch_bounds__(256) simt_rows_kernel(RowsArgs a) {
+  constexpr int M = 8;                       // kappa slots per lane (K <= 256)
+  __shared__ double red[8][3];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const double sigma = a.sc->sigma;
+  const float inv2s2 = a.sigma_inf ? 0.f : (float)(0.5 / (sigma * sigma));
+  const double s2 = sigma * sigma;
+  double st0 = 0.0, st1 = 0.0, st2 = 0.0;    // pass 1: sum e^2, welsch, n; pass 2: den
+  const int64_t items = a.nrows * a.nsplit;
+  for (int64_t it = (int64_t)blockIdx.x * 8 + warp; it < items; it += (int64_t)gridDim.x * 8) {
+    const int64_t row = it / a.nsplit;
+    const int split = (int)(it - row * a.nsplit);
+    const int64_t ro = a.row_off[row];
+    float* drow = a.contrib + ((int64_t)split * a.nrows + row) * a.KP;
+    if (ro < 0) {                            // (a row outside the shard)
+      if (!PASS2 && !STATS_ONLY)
+        for (int q = lane; q < a.K; q += 32) drow[q] = 0.f;
+      continue;
+    }
+    float lf[M], lh[M], D[M];
+#pragma unroll
+    for (int m = 0; m < M; ++m) {
+      const int q = lane + 32 * m;
+      lf[m] = q < a.K ? __ldg(a.lft + row * a.K + q) : 0.f;
+      lh[m] = (PASS2 && q < a.K) ? __ldg(a.lfth + row * a.K + q) : 0.f;
+      D[m] = 0.f;
+    }
+    const int64_t cb = (int64_t)split * a.per, ce = min(a.ncols, cb + a.per);
+    for (int64_t c0 = cb; c0 < ce; c0 += 32) {
+      const int64_t col = c0 + lane;
+      float x = 0.f;
+      bool obs = false;
+      if (col < ce) {
+        const int64_t co = a.col_off[col];
+        if (co >= 0) {
+          const int64_t lin = ro + co;
+          const uint32_t word = __ldg(a.mask + (lin >> 5));
+          const uint32_t bit = (uint32_t)(lin & 31);
+          if ((word >> bit) & 1u) {
+            int64_t vi = lin;
+            if (a.packed) vi = (int64_t)__ldg(a.rank_prefix + (lin >> 5)) + __popc(word & ((1u << bit) - 1u));
+            x = __ldg(a.values + vi);
+            obs = true;
+          }
+        }
+      }
+      unsigned bal = __ballot_sync(0xffffffffu, obs);
+      if (!bal) continue;
+      unsigned long long ebase = 0ull;
+      if (!PASS2 && a.eabs) {                // R21: |e| of the observed entries, any order
+        if (lane == 0) ebase = atomicAdd(a.efill, (unsigned long long)__popc(bal));
+        ebase = __shfl_sync(0xffffffffu, ebase, 0);
+      }
+      int qe = 0;
+      while (bal) {
+        const int j = __ffs(bal) - 1;
+        bal &= bal - 1;
+        const float xj = __shfl_sync(0xffffffffu, x, j);
+        const float* R = a.rgtC + (c0 + j) * a.KP;
+        float r[M];
+        float sp = 0.f, tp = 0.f;
+#pragma unroll
+        for (int m = 0; m < M; ++m) {
+          const int q = lane + 32 * m;
+          r[m] = q < a.KP ? __ldg(R + q) : 0.f;
+          sp = fmaf(lf[m], r[m], sp);
+          if (PASS2) tp = fmaf(lh[m], r[m], tp);
+        }
+        const float s = warp_sum_f(sp);
+        const float e = xj - s;
+        const float w = a.sigma_inf ? 1.f : expf(-e * e * inv2s2);
+        if (PASS2) {
+          const float t = warp_sum_f(tp);
+          if (lane == 0) st0 += (double)w * (double)t * (double)t;
+        } else {
+          if (lane == 0) {
+            st0 += (double)e * (double)e;
+            st1 += s2 * (1.0 - (double)w);
+            st2 += 1.0;
+            if (a.eabs && ebase + qe < a.ecap) a.eabs[ebase + qe] = __float_as_uint(fabsf(e));
+          }
+          ++qe;
+          if (!STATS_ONLY) {
+            const float cv = w * e;
+#pragma unroll
+            for (int m = 0; m < M; ++m) D[m] = fmaf(cv, r[m], D[m]);
+          }
+        }
+      }
+    }
+    if (!PASS2 && !STATS_ONLY) {
+#pragma unroll
+      for (int m = 0; m < M; ++m) {
+        const int q = lane + 32 * m;
+        if (q < a.K) drow[q] = D[m];
+      }
+    }
+  }
+  // CTA partials in a fixed order (lane 0 of each warp holds the warp's sums)
+  if (lane == 0) { red[warp][0] = st0; red[warp][1] = st1; red[warp][2] = st2; }
+  __syncthreads();
+  if (threadIdx.x < (PASS2 ? 1 : 3)) {
+    double t = 0.0;
+    for (int w = 0; w < 8; ++w) t += red[w][threadIdx.x];
+    if (PASS2) a.denpart[blockIdx.x] = t;
+    else a.spart[(int64_t)blockIdx.x * 3 + threadIdx.x] = t;
+  }
+}
+
 static PassArgs make_pass_args(const Context& c, const BlockPlan& bp) {
   PassArgs a;
   a.nL = bp.nL; a.nrows = bp.nrows; a.ncols = bp.ncols;
@@ -722,8 +896,72 @@ static PassArgs make_pass_args(const Context& c, const BlockPlan& bp) {
   return a;
 }
 
+// Lft rows of a warp-per-row SIMT block with p > 0 (K > 128; the large-rank regime):
+// Lft(ik, jl)[a + r_k c] = sum_b X(ik)[a][b] Mid(jl)[b][c] for a chunk of 32 left indices jl
+// of one i_k per CTA, X(ik) (r_k x r_{k+1}, padded rows) and the Mid chunk staged in shared
+// memory; X is the core slice (pass 1) or the folded scaled gradient h (pass 2).  Same fp32
+// fmaf order over b as lft_kernel.
+constexpr int kLftJ = 32;
+__global__ void __launch_bounds__(256) lft_rows_kernel(PlanArgs a, const float* __restrict__ Zk, const double* __restrict__ h,
+                                                       const float* __restrict__ mid, float* __restrict__ lft) {
+  extern __shared__ float lsm[];
+  const int rk = a.rk, rk1 = a.rk1, rs = a.rs, K = a.K, XS = rk1 + 1;
+  float* Xs = lsm;                             // [rk][rk1 + 1]
+  float* Ms = lsm + rk * XS;                   // [kLftJ][rk1][rs]
+  const int64_t Ik = a.Ik;
+  const int64_t ik = blockIdx.x;
+  const int64_t jl0 = (int64_t)blockIdx.y * kLftJ;
+  const int nj = (int)min((int64_t)kLftJ, a.nL - jl0);
+  for (int t = threadIdx.x; t < rk * rk1; t += blockDim.x) {
+    const int aa = t / rk1, b = t - aa * rk1;
+    Xs[aa * XS + b] = h ? (float)h[(a.ik0 + ik) * rk * rk1 + aa + rk * b] : __ldg(Zk + (a.ik0 + ik) * rk * rk1 + t);
+  }
+  const int MS = rk1 * rs;
+  for (int t = threadIdx.x; t < nj * MS; t += blockDim.x) Ms[t] = __ldg(mid + jl0 * MS + t);
+  __syncthreads();
+  for (int t = threadIdx.x; t < nj * K; t += blockDim.x) {
+    const int jj = t / K, kap = t - jj * K;
+    const int aa = kap % rk, cc = kap / rk;
+    const float* xr = Xs + aa * XS;
+    const float* mc = Ms + jj * MS + cc;
+    float v = 0.f;
+    for (int b = 0; b < rk1; ++b) v = fmaf(xr[b], mc[b * rs], v);
+    const int64_t jl = jl0 + jj;
+    const int64_t row = a.rowmode == 0 ? jl + a.nL * ik : ik + Ik * jl;
+    lft[row * K + kap] = v;
+  }
+}
+
+template <bool PASS2, bool STATS_ONLY>
+static void launch_rows_t(Context& c, const BlockPlan& bp, cudaStream_t s) {
+  RowsArgs a;
+  a.nrows = bp.nrows; a.ncols = bp.ncols; a.per = bp.rows_per;
+  a.K = bp.K; a.KP = bp.KP; a.nsplit = bp.rows_nsplit;
+  a.sigma_inf = c.cfg.sigma_mode == TRD_SIGMA_INF;
+  a.packed = c.packed;
+  a.row_off = c.row_off; a.col_off = c.col_off;
+  a.lft = c.lft; a.lfth = c.lfth; a.rgtC = c.rgtC;
+  a.values = c.values; a.mask = c.mask; a.rank_prefix = c.rank_prefix;
+  a.sc = c.sc;
+  a.contrib = c.contrib; a.spart = c.spart; a.denpart = c.denpart;
+  a.eabs = (!PASS2 && c.cfg.sigma_mode == TRD_SIGMA_MAD) ? c.eabs : nullptr;
+  a.efill = &c.sc->eabs_fill;
+  a.ecap = (unsigned long long)c.eabs_cap;
+  if (!PASS2) {                              // Rgt column-major (pass 2 reuses it)
+    const int g = (int)std::max<int64_t>(1, std::min<int64_t>((bp.ncols * bp.KP + 255) / 256, 148 * 16));
+    rgt_colmajor_kernel<<<g, 256, 0, s>>>(c.rgtT, bp.ncols, bp.K, bp.KP, c.rgtC);
+    c.launches++;
+  }
+  simt_rows_kernel<PASS2, STATS_ONLY><<<bp.rows_grid, 256, 0, s>>>(a);
+  c.launches++;
+}
+
 template <bool PASS2, bool STATS_ONLY>
 static void launch_pass_t(Context& c, const BlockPlan& bp, cudaStream_t s) {
+  if (bp.rows) {                             // 128 < K <= 256: warp-per-row SIMT passes
+    launch_rows_t<PASS2, STATS_ONLY>(c, bp, s);
+    return;
+  }
   PassArgs a = make_pass_args(c, bp);
   dim3 grid((unsigned)bp.grid_x, (unsigned)(bp.nrows / bp.nL), (unsigned)bp.nsplit);
   // (K <= 256 is checked at trd_init; R^2 > kBigR2: D rows to contrib, no per-lane d)
@@ -1276,7 +1514,7 @@ __global__ void dt_T_kernel(const float* __restrict__ Zn, int64_t In, int rk, in
                             const double* __restrict__ G, double* __restrict__ T) {
   const int R2 = rk * rk1;
   const int64_t i = blockIdx.x;
-  for (int o = threadIdx.x; o < R2; o += blockDim.x) {
+  for (int o = blockIdx.y * blockDim.x + threadIdx.x; o < R2; o += gridDim.y * blockDim.x) {
     double acc = 0.0;
     for (int q = 0; q < R2; ++q) {
       const int aa = q % rk, b = q / rk;
@@ -1655,6 +1893,16 @@ void launch_plan(Context& c, const BlockPlan& bp, cudaStream_t s) {
 void launch_lft(Context& c, const BlockPlan& bp, const float* Zsrc_k, int src_is_h, float* out,
                 cudaStream_t s) {
   PlanArgs a = make_plan_args(c, bp);
+  if (bp.rows && bp.p > 0) {
+    const size_t smem = (size_t)(bp.rk * (bp.rk1 + 1) + kLftJ * bp.rk1 * bp.rs) * sizeof(float);
+    if (smem <= 200 * 1024) {
+      cudaFuncSetAttribute(lft_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      const dim3 grid((unsigned)(bp.nrows / bp.nL), (unsigned)((bp.nL + kLftJ - 1) / kLftJ));
+      lft_rows_kernel<<<grid, 256, smem, s>>>(a, src_is_h ? nullptr : Zsrc_k, src_is_h ? c.h : nullptr, c.mid, out);
+      c.launches++;
+      return;
+    }
+  }
   if (c.rbucket <= 16)
     lft_kernel<16><<<grid_for(bp.nrows * bp.rk), 256, 0, s>>>(a, src_is_h ? nullptr : Zsrc_k,
                                                               src_is_h ? c.h : nullptr, c.mid, out);
@@ -1679,6 +1927,10 @@ void launch_pass2(Context& c, const BlockPlan& bp, cudaStream_t s) {
 void launch_reduce_d(Context& c, const BlockPlan& bp, cudaStream_t s) {
   const int64_t Ik = bp.nrows / bp.nL, Ik_tot = c.dims[bp.k];
   const int64_t ncta = bp.grid_x * bp.nsplit;
+  if (bp.rows) {                       // warp-per-row SIMT pass: D rows in contrib, per-CTA stats
+    launch_reduce_d_contrib(c, bp, bp.rows_nsplit, bp.nrows, bp.rows_grid, s);
+    return;
+  }
   if (bp.big && bp.R2 > 0) {           // D rows of the SIMT pass in contrib ([nsplit][nrows][KP])
     launch_reduce_d_contrib(c, bp, bp.nsplit, bp.nrows, Ik * ncta, s);
     return;
@@ -1699,7 +1951,7 @@ void launch_block_stats(Context& c, const BlockPlan& bp, cudaStream_t s) {
 void launch_reduce_den(Context& c, const BlockPlan& bp, cudaStream_t s) {
   const int64_t Ik = bp.nrows / bp.nL;                 // plan rows (pass-2 partials)
   const int64_t ncta = bp.grid_x * bp.nsplit;
-  const int64_t nden = bp.use_tc ? (int64_t)bp.tc_grid : Ik * ncta;
+  const int64_t nden = bp.use_tc ? (int64_t)bp.tc_grid : bp.rows ? (int64_t)bp.rows_grid : Ik * ncta;
   reduce_den_kernel<<<1, 256, 0, s>>>(c.denpart, nden, c.numpart, c.dims[bp.k], c.red_ws);
   c.launches++;
 }
@@ -1907,7 +2159,8 @@ void launch_sweep_end(Context& c, cudaStream_t s) {
   const int rk = c.ranks[n], rk1 = c.ranks[0];
   const int64_t In = c.dims[n];
   double* T = c.chain_ws;     // In x R2 (<= chain_ws capacity, checked at init)
-  dt_T_kernel<<<(unsigned)In, 128, 0, s>>>(c.Z + c.zoff[n], In, rk, rk1, c.G_last, T);
+  dt_T_kernel<<<dim3((unsigned)In, (unsigned)((rk * rk1 + 127) / 128)), 128, 0, s>>>(c.Z + c.zoff[n], In, rk, rk1,
+                                                                                      c.G_last, T);
   dt_D_kernel<<<grid_for(In * In), 256, 0, s>>>(c.Z + c.zoff[n], In, rk, rk1, T, c.Dcur);
   sweep_end_kernel<<<1, 1024, 0, s>>>(c.Dcur, c.Dprev, In * In, c.sc, c.stats,
                                       c.cfg.sigma_mode, c.cfg.sigma_theta, c.cfg.sigma_min);

@@ -394,6 +394,63 @@ __global__ void __launch_bounds__(256) tc_lft_pack_hw_kernel(LftArgs a, int pass
   }
 }
 
+// Large ranks (r_{k+1} >= 32, p > 0: the paper's [80, 80, 3, 20]): CTA per (i_k, 32 left
+// indices jl); X(i_k) (r_k x r_{k+1}, padded rows) and the 32 Mid(jl) staged in shared memory,
+// the 32 x K Lft rows computed into shared memory (fmaf over b ascending, as the half-warp
+// kernel), then warp per row: max |Lft|, the power-of-two scale, fp16 hi / lo stores.  CTA
+// (0, 0) also writes the padding rows [nrows, nrows_pad).
+constexpr int kPackJ = 32;
+__global__ void __launch_bounds__(256) tc_lft_pack_tile_kernel(LftArgs a, int pass2, int64_t nrows_pad,
+                                                               __half* __restrict__ dst) {
+  extern __shared__ float psm[];
+  const int rk = a.rk, rk1 = a.rk1, rs = a.rs, K = a.K, KP = a.KP, XS = rk1 + 1, MS = rk1 * rs, LS = K + 1;
+  float* Xs = psm;                              // [rk][rk1 + 1]
+  float* Ms = Xs + rk * XS;                     // [kPackJ][rk1][rs]
+  float* Ls = Ms + kPackJ * MS;                 // [kPackJ][K + 1]
+  const int64_t ik = blockIdx.x, jl0 = (int64_t)blockIdx.y * kPackJ;
+  const int nj = (int)min((int64_t)kPackJ, a.nL - jl0);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t xb = (a.ik0 + ik) * rk * rk1;
+  for (int t = tid; t < rk * rk1; t += blockDim.x) {
+    const int aa = t / rk1, b = t - aa * rk1;
+    Xs[aa * XS + b] = pass2 ? (float)__ldg(a.hk + xb + aa + rk * b) : __ldg(a.zk + xb + t);
+  }
+  for (int t = tid; t < nj * MS; t += blockDim.x) Ms[t] = __ldg(a.mid + jl0 * MS + t);
+  __syncthreads();
+  for (int t = tid; t < nj * K; t += blockDim.x) {
+    const int jj = t / K, kap = t - jj * K;
+    const int aa = kap % rk, cc = kap / rk;
+    const float* xr = Xs + aa * XS;
+    const float* mc = Ms + jj * MS + cc;
+    float x = 0.f;
+    for (int b = 0; b < rk1; ++b) x = fmaf(xr[b], mc[b * rs], x);
+    Ls[jj * LS + kap] = x;
+  }
+  __syncthreads();
+  float wmax = 0.f;
+  for (int jj = warp; jj < nj; jj += 8) {
+    const int64_t jl = jl0 + jj;
+    const int64_t row = a.rowmode == 0 ? jl + a.nL * ik : ik + a.Ik * jl;
+    float amax = 0.f;
+    for (int q = lane; q < K; q += 32) amax = fmaxf(amax, fabsf(Ls[jj * LS + q]));
+    for (int o = 16; o > 0; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+    const int E = tc_scale_exp(amax);
+    if (lane == 0) a.lscl[row] = ldexpf(1.f, -E);
+    wmax = fmaxf(wmax, amax);
+    for (int q = lane; q < KP; q += 32) {
+      const float x = q < K ? ldexpf(Ls[jj * LS + q], E) : 0.f;
+      const __half hh = __float2half_rn(x);
+      dst[row * 2 * KP + q] = hh;
+      dst[row * 2 * KP + KP + q] = __float2half_rn(x - __half2float(hh));
+    }
+  }
+  if (a.amax && lane == 0) amax_update(a.amax, wmax);
+  if (blockIdx.x == 0 && blockIdx.y == 0) {     // padding rows: zero operand, scale 1
+    for (int64_t t = a.nrows * 2 * KP + tid; t < nrows_pad * 2 * KP; t += blockDim.x) dst[t] = __float2half_rn(0.f);
+    for (int64_t r = a.nrows + tid; r < nrows_pad; r += blockDim.x) a.lscl[r] = 1.f;
+  }
+}
+
 // Register-blocked variant for compile-time ranks (RK = r_k, RK1 = r_{k+1}, RS = r_s, p > 0):
 // one thread per row holds X(i_k) (RK x RK1) and Mid(j_L) (RK1 x RS) and produces the whole
 // row, Lft[a + RK c] = sum_b X[a][b] Mid[b][c] (fmaf over b ascending, as lft_kernel).
@@ -1291,6 +1348,63 @@ __global__ void __launch_bounds__(256) reduce_d_big_kernel(
   dpart[(jc * Ik + ik) * R2 + o] = s;
 }
 
+// The same contraction with the D rows (summed over the splits) and Mid rows of RB left
+// indices staged in shared memory, 1024 threads, NO outputs per thread (o = tid + 1024 i).
+// Per output and jl: u = sum_c Mid[b][c] D[a + r_k c] in fp32 (c ascending), added to an fp64
+// sum in jl order -- bitwise the arithmetic of reduce_d_big_kernel.
+template <int NO>
+__global__ void __launch_bounds__(1024) reduce_d_big_smem_kernel(
+    const float* __restrict__ contrib, const float* __restrict__ mid, int nsplit, int64_t nrows_pad, int64_t nL,
+    int64_t Ik, int rowmode, int KP, int K, int R2, int rk, int rk1, int rs, int p, int64_t jl_chunk, int RB,
+    double* __restrict__ dpart) {
+  extern __shared__ float bsm[];
+  const int MS = rk1 * rs;
+  float* Dt = bsm;                       // [RB][K]
+  float* Mt = bsm + RB * K;              // [RB][MS]
+  const int64_t ik = blockIdx.x, jc = blockIdx.y;
+  const int tid = threadIdx.x;
+  const int64_t j0 = jc * jl_chunk, j1 = min(nL, j0 + jl_chunk);
+  double acc[NO];
+  int aa[NO], bq[NO];
+#pragma unroll
+  for (int i = 0; i < NO; ++i) { acc[i] = 0.0; const int o = tid + 1024 * i; aa[i] = o % rk; bq[i] = o / rk; }
+  for (int64_t jb = j0; jb < j1; jb += RB) {
+    const int nr = (int)min((int64_t)RB, j1 - jb);
+    for (int t = tid; t < nr * K; t += blockDim.x) {
+      const int rr = t / K, q = t - rr * K;
+      const int64_t jl = jb + rr;
+      const int64_t row = rowmode == 0 ? jl + nL * ik : ik + Ik * jl;
+      float v = 0.f;
+      for (int sp = 0; sp < nsplit; ++sp) v += __ldg(contrib + ((int64_t)sp * nrows_pad + row) * KP + q);
+      Dt[t] = v;
+    }
+    if (p > 0)
+      for (int t = tid; t < nr * MS; t += blockDim.x) Mt[t] = __ldg(mid + jb * MS + t);
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < NO; ++i) {
+      if (tid + 1024 * i >= R2) break;
+      for (int rr = 0; rr < nr; ++rr) {
+        float u = 0.f;
+        if (p == 0) {
+          u = Dt[rr * K + tid + 1024 * i];
+        } else {
+          const float* M = Mt + rr * MS + bq[i] * rs;
+          const float* D = Dt + rr * K + aa[i];
+          for (int c = 0; c < rs; ++c) u = fmaf(M[c], D[rk * c], u);
+        }
+        acc[i] += (double)u;
+      }
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < NO; ++i) {
+    const int o = tid + 1024 * i;
+    if (o < R2) dpart[(jc * Ik + ik) * R2 + o] = acc[i];
+  }
+}
+
 // stage 2: dvec = [d | sum_e2 | welsch | n] from the chunk partials and the per-CTA statistics
 __global__ void tc_reduce_final_kernel(const double* __restrict__ dpart, int64_t JC, int64_t Ik, int R2,
                                        const double* __restrict__ spart, int64_t nparts,
@@ -1349,6 +1463,16 @@ void launch_tc_lft(Context& c, const BlockPlan& bp, bool pass2, cudaStream_t s) 
     tc_lft_pack_rb_kernel<8, 8, 8><<<grid, 128, 0, s>>>(a, pass2 ? 1 : 0, pad, pass2 ? c.lfthHL : c.lftHL);
     c.launches++;
     return;
+  }
+  if (c.rbucket > 32 && bp.p > 0 && bp.rk1 >= 32) {
+    const size_t smem = (size_t)(bp.rk * (bp.rk1 + 1) + kPackJ * bp.rk1 * bp.rs + kPackJ * (bp.K + 1)) * sizeof(float);
+    if (smem <= 200 * 1024) {
+      cudaFuncSetAttribute(tc_lft_pack_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      const dim3 grid((unsigned)a.Ik, (unsigned)((bp.nL + kPackJ - 1) / kPackJ));
+      tc_lft_pack_tile_kernel<<<grid, 256, smem, s>>>(a, pass2 ? 1 : 0, pad, pass2 ? c.lfthHL : c.lftHL);
+      c.launches++;
+      return;
+    }
   }
   if (getenv("TRD_LFT_TILE") == nullptr) {        // half-warp per row (TRD_LFT_TILE: the tile kernel, A/B)
     const int grid = (int)std::min<int64_t>((pad * 16 + 255) / 256, (int64_t)c.num_sm * 16);
@@ -1579,10 +1703,34 @@ void launch_tc_pass(Context& c, const BlockPlan& bp, const TcStage& st, bool pas
 void launch_reduce_d_contrib(Context& c, const BlockPlan& bp, int nsplit, int64_t nrows_pad, int64_t nparts,
                              cudaStream_t s) {
   const int64_t Ik = bp.nrows / bp.nL;
+  if (bp.R2 == 0) {                          // statistics only (the sigma_0 pass)
+    tc_reduce_final_kernel<<<1, 128, 0, s>>>(c.dpart, 0, 0, 0, c.spart, nparts, c.dvec, nullptr, bp.k, 0, 0);
+    c.launches++;
+    return;
+  }
   if (Ik < c.dims[bp.k]) cudaMemsetAsync(c.dvec, 0, (size_t)(c.dims[bp.k] * bp.R2) * sizeof(double), s);
-  reduce_d_big_kernel<<<dim3((unsigned)Ik, (unsigned)bp.tc_jc, (unsigned)((bp.R2 + 255) / 256)), 256, 0, s>>>(
-      c.contrib, c.mid, nsplit, nrows_pad, bp.nL, Ik, bp.rowmode, bp.KP, bp.R2, bp.rk, bp.rk1, bp.rs, bp.p,
-      bp.tc_jl_chunk, c.dpart);
+  const int no = (bp.R2 + 1023) / 1024;
+  const int RB = 16;
+  const size_t smem = (size_t)RB * (bp.K + bp.rk1 * bp.rs) * sizeof(float);
+  if (no <= 16 && smem <= 200 * 1024 && !getenv("TRD_RD_PLAIN")) {
+#define RD_BIG(NO_)                                                                                            \
+  do {                                                                                                       \
+    cudaFuncSetAttribute(reduce_d_big_smem_kernel<NO_>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+    reduce_d_big_smem_kernel<NO_><<<dim3((unsigned)Ik, (unsigned)bp.tc_jc), 1024, smem, s>>>(                    \
+        c.contrib, c.mid, nsplit, nrows_pad, bp.nL, Ik, bp.rowmode, bp.KP, bp.K, bp.R2, bp.rk, bp.rk1, bp.rs, bp.p, \
+        bp.tc_jl_chunk, RB, c.dpart);                                                                        \
+  } while (0)
+    if (no <= 1) RD_BIG(1);
+    else if (no <= 2) RD_BIG(2);
+    else if (no <= 4) RD_BIG(4);
+    else if (no <= 8) RD_BIG(8);
+    else RD_BIG(16);
+#undef RD_BIG
+  } else {
+    reduce_d_big_kernel<<<dim3((unsigned)Ik, (unsigned)bp.tc_jc, (unsigned)((bp.R2 + 255) / 256)), 256, 0, s>>>(
+        c.contrib, c.mid, nsplit, nrows_pad, bp.nL, Ik, bp.rowmode, bp.KP, bp.R2, bp.rk, bp.rk1, bp.rs, bp.p,
+        bp.tc_jl_chunk, c.dpart);
+  }
   tc_reduce_final_kernel<<<(unsigned)(Ik + 1), 128, 0, s>>>(c.dpart, bp.tc_jc, Ik, bp.R2, c.spart, nparts,
                                                             c.dvec, c.sc, bp.k, bp.ik0, c.dims[bp.k]);
   c.launches += 2;
