@@ -356,6 +356,8 @@ def run_mine(args):
         except Exception:
             traffic = None
     kname = {"pass1": "tc_pass1_kernel", "pass2": "tc_pass2_kernel"}[dom]
+    if max(a * b for i, a in enumerate(spec.ranks) for j, b in enumerate(spec.ranks) if i != j) > 128:
+        kname += " / simt_rows_kernel (blocks with K = r_k r_s > 128)"   # e.g. C6, ranks [80,80,3,20]
     roof = {"bound": "alu", "kernel": f"{dom} ({kname}, libtrd)", "achieved": achieved,
             "peak": p_fp32, "unit": "TFLOP/s", "frac": achieved / p_fp32, "traffic": traffic,
             "peak_source": fp32_src,

@@ -366,6 +366,17 @@ def test_paper_ranks_final_error_matches_oracle():
     e_gpu_or = O.relative_error(ctx.get_cores(), Xc)
     assert abs(gerr["rel_err_all"] - e_gpu_or) <= 1e-5
     assert abs(e_gpu_or - e_or) <= 1e-3, (e_gpu_or, e_or)
+    # trd_reconstruct (Def. 1) with rank-80 chain products, vs the oracle trace
+    cores = [c.astype(np.float64) for c in ctx.get_cores()]
+    n = int(np.prod(spec.dims))
+    lin = torch.randint(0, n, (200,), generator=torch.Generator().manual_seed(2))
+    out = ctx.reconstruct(lin.cuda()).cpu().numpy()
+    for t, l in enumerate(lin.tolist()):
+        idx, rem = [], l
+        for I in spec.dims:
+            idx.append(rem % I)
+            rem //= I
+        assert abs(out[t] - O.tr_entry(cores, idx)) <= 1e-5 * max(1.0, abs(out[t]))
     ctx.close()
 
 
