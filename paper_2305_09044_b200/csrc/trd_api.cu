@@ -712,6 +712,10 @@ trd_status trd_init_ex(const trd_config* cfg, const trd_shard* shard, const floa
     const int64_t r2 = (int64_t)c->ranks[k] * c->ranks[(k + 1) % N];
     if (r2 > kBigR2) { r2big = std::max(r2big, r2); zd_rows = std::max<int64_t>(zd_rows, c->dims[k]); }
   }
+  if (r2big > 0)                                  // (cuSOLVER loaded: every R2 > 128 solve uses it;
+    for (int k = 0; k < N; ++k)                   //  the one-CTA Cholesky takes ~13 ms at R2 = 240)
+      if ((int64_t)c->ranks[k] * c->ranks[(k + 1) % N] > 128)
+        zd_rows = std::max<int64_t>(zd_rows, c->dims[k]);
   if (r2big > 0) {                                // chain products in either order: <= (max r)^4
     int64_t rmax = 0;
     for (int k = 0; k < N; ++k) rmax = std::max<int64_t>(rmax, c->ranks[k]);
@@ -738,6 +742,7 @@ trd_status trd_init_ex(const trd_config* cfg, const trd_shard* shard, const floa
     else build_plan(*c, 0, full_s, bp, false);
     if (bp.use_tc && !tc_supported_kp(bp.KP)) bp.use_tc = 0;
     if (bp.K > 256) return bail(fail(c, TRD_ERR_SHAPE, "block %d: no split with r_k r_s <= 256", k));
+    bp.lib_solve = (bp.big || (c->has_big && bp.R2 > 128)) ? 1 : 0;
     bp.rows = 0;
     if (!bp.use_tc && bp.K > 128) {          // warp-per-row SIMT passes (simt_rows_kernel)
       bp.rows = 1;

@@ -186,6 +186,8 @@ struct BlockPlan {
   int tc_u;              // column tiles per ring unit of the pass kernels (2: N = 128 GEMMs)
   int64_t tc_jc, tc_jl_chunk;   // d reduction: jl chunks
   int big;               // R2 > kBigR2: large-rank path (SIMT pass 1 writes D rows to contrib)
+  int lib_solve;         // filtered solve by cuSOLVER (big blocks, and R2 > 128 blocks of a
+                         // context that loads it): big_factor / big_h instead of solve_kernel
   int rows;              // SIMT plan with K > 128: warp-per-row passes (simt_rows_kernel)
   int rows_nsplit, rows_grid;   //   column splits per row, CTAs (8 warps each)
   int64_t rows_per;             //   columns per split (multiple of 32)

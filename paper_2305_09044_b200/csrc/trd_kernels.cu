@@ -2002,7 +2002,7 @@ __global__ void identity_kernel(double* __restrict__ M, int n, DevScalars* __res
 
 // M = I: h = d M = d (the 'gradient descent' ablation arm)
 void launch_identity_op(Context& c, const BlockPlan& bp, cudaStream_t s) {
-  if (bp.big) return;                  // (big_h: h = d)
+  if (bp.lib_solve) return;            // (big_h: h = d)
   identity_kernel<<<grid_for((int64_t)bp.R2 * bp.R2), 256, 0, s>>>(c.Mop, bp.R2, c.sc);
   c.launches++;
 }
@@ -2039,7 +2039,7 @@ void launch_gram(Context& c, const BlockPlan& bp, cudaStream_t s, const double* 
 
 void launch_solve(Context& c, const BlockPlan& bp, cudaStream_t s, const double* G) {
   const int n = bp.R2;
-  if (bp.big) {                        // Cholesky of G + lambda I (cuSOLVER); h in big_h
+  if (bp.lib_solve) {                  // Cholesky of G + lambda I (cuSOLVER); h in big_h
     big_factor(c, bp, s, G);
     return;
   }
@@ -2087,7 +2087,7 @@ void launch_solve(Context& c, const BlockPlan& bp, cudaStream_t s, const double*
 }
 
 void launch_h(Context& c, const BlockPlan& bp, cudaStream_t s) {
-  if (bp.big) {
+  if (bp.lib_solve) {
     big_h(c, bp, s);
     return;
   }
