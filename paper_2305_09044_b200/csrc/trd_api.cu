@@ -360,14 +360,58 @@ void tl_mark(Context* c, cudaStream_t s, const char* label) {
   c->tl.push_back({label, (void*)e, (s == c->side || strncmp(label, "side", 4) == 0) ? 1 : 0});
 }
 
-// a1-a6 + a7 (pass 1 and the d/stat exchange) of block k
-trd_status block_pass1(Context* c, const BlockPlan& bp) {
+// index / offset buffers of block k (k < 0 or no pipeline: the context's default buffers)
+void select_bufs(Context* c, int k) {
+  if (!c->pipe) return;
+  const bool d = k < 0;
+  c->idx = d ? c->idx_d : c->idx_b[k];
+  c->doff = d ? c->doff_d : c->doff_b[k];
+  c->row_off = d ? c->row_off_d : c->row_off_b[k];
+  c->col_off = d ? c->col_off_d : c->col_off_b[k];
+  c->ptab = d ? c->ptab_d : c->ptab_b[k];
+}
+
+// block k takes part in the staging pipeline: a sampled (sweep-varying) tensor-core sketch
+static bool pipelined(const Context* c, int k) {
+  return c->pipe && k >= 0 && k < c->N && c->plan[k].use_tc && !c->stage[k].invariant && !c->plan[k].explicit_cols &&
+         c->stage[k].n_tiles >= c->pipe_min_tiles;
+}
+
+// Enqueue part `part` of block k's staging on the staging stream after `after` (an event of the
+// main stream): part 0 = everything, 1 = sampler, offsets, masks and tile prefix, 2 = values.
+// Records ev_samp[k] once the index sets and offsets exist and ev_staged[k] after the values.
+// The index sets depend only on (seed, k, t), the staging only on them and the data: none of it
+// reads the cores that blocks < k are still updating (Alg. 1 l.4-5).
+static trd_status prestage(Context* c, int k, cudaEvent_t after, int part, int cur_block) {
+  const BlockPlan& bp = c->plan[k];
+  cudaStream_t t = c->stg;
+  CUDA_TRY(c, cudaStreamWaitEvent(t, after, 0));
+  select_bufs(c, k);
+  if (part != 2) {
+    launch_sampler(*c, bp, t);
+    launch_offsets(*c, bp, t, false);
+    CUDA_TRY(c, cudaEventRecord(c->ev_samp[k], t));
+  }
+  launch_tc_stage(*c, bp, c->stage[k], t, part);
+  if (part != 1) CUDA_TRY(c, cudaEventRecord(c->ev_staged[k], t));
+  select_bufs(c, cur_block);
+  return check_launch(c, "prestage");
+}
+
+// inside enqueue_sweep: the staging of block k + 1 is enqueued ahead (block 0 stages in line)
+static bool pre_next(const Context* c, int k) { return c->in_sweep && pipelined(c, k + 1); }
+
+// a1-a6 + a7 (pass 1 and the d/stat exchange) of block k.  pre: the sampler, offsets and staging
+// of this block were enqueued ahead on the staging stream (enqueue_sweep)
+trd_status block_pass1(Context* c, const BlockPlan& bp, bool pre) {
   cudaStream_t s = c->stream;
+  select_bufs(c, bp.k);
   // a8 + a9 (FGMC Gram, filtered operator M) depend only on the cores != k: run them on the
   // side stream, overlapping the sampler / staging / pass 1 (which leaves one SM free)
   // (the sampler first: the local-scaled-term arm builds its Gram from the sampled slices)
   tl_mark(c, s, "block start");
-  launch_sampler(*c, bp, s);
+  if (pre) CUDA_TRY(c, cudaStreamWaitEvent(s, c->ev_samp[bp.k], 0));
+  else launch_sampler(*c, bp, s);
   tl_mark(c, s, "sampler");
   // (TRD_NO_SIDE=1, diagnostic: the Gram and the solve in line on the main stream)
   const bool inl = getenv("TRD_NO_SIDE") && atoi(getenv("TRD_NO_SIDE")) != 0;
@@ -389,7 +433,7 @@ trd_status block_pass1(Context* c, const BlockPlan& bp) {
   tl_mark(c, side, "side: solve");
   if (c->sticky) return c->sticky;
   CUDA_TRY(c, cudaEventRecord(c->ev_join, side));
-  launch_plan(*c, bp, s);
+  launch_plan(*c, bp, s, !pre);
   tl_mark(c, s, "plan (offsets, mid, rgt)");
   if (!bp.use_tc) launch_lft(*c, bp, c->Z + c->zoff[bp.k], 0, c->lft, s);
   TcStage& stg = c->stage[bp.k];
@@ -398,7 +442,9 @@ trd_status block_pass1(Context* c, const BlockPlan& bp) {
     tl_mark(c, s, "lft pack 1");
     launch_tc_pack_cols(*c, bp, s);
     tl_mark(c, s, "pack cols");
-    if (!stg.valid) {                       // a2: stage the sketch in tile order
+    if (pre) {
+      CUDA_TRY(c, cudaStreamWaitEvent(s, c->ev_staged[bp.k], 0));
+    } else if (!stg.valid) {                // a2: stage the sketch in tile order
       launch_tc_stage(*c, bp, stg, s);
       stg.valid = stg.invariant;
       // checked build only: TRD_CHECK_INJECT=entry corrupts the first staged entry id of this
@@ -416,6 +462,11 @@ trd_status block_pass1(Context* c, const BlockPlan& bp) {
   else launch_pass1(*c, bp, 0, s);
   if (pe) prof_pair(c, 1, e0, prof_event(c));
   tl_mark(c, s, "pass 1");
+  if (pre_next(c, bp.k) && c->pipe != 2) {   // the next block's staging, behind this pass 1
+    CUDA_TRY(c, cudaEventRecord(c->ev_p1[bp.k], s));    // (pipe 1: all of it, 3: up to the prefix)
+    trd_status sp = prestage(c, bp.k + 1, c->ev_p1[bp.k], c->pipe == 1 ? 0 : 1, bp.k);
+    if (sp) return sp;
+  }
   if (bp.use_tc && c->eabs) launch_eabs_advance(*c, stg, s);   // R21 |e| slots of this block
   if (bp.use_tc) launch_tc_reduce_d(*c, bp, s);
   else launch_reduce_d(*c, bp, s);
@@ -447,6 +498,11 @@ trd_status block_pass2(Context* c, const BlockPlan& bp) {
   else launch_pass2(*c, bp, s);
   if (pe) prof_pair(c, 2, e0, prof_event(c));
   tl_mark(c, s, "pass 2");
+  if (pre_next(c, bp.k) && c->pipe >= 2) {   // (pipe 2: all of it, 3: the values)
+    CUDA_TRY(c, cudaEventRecord(c->ev_p2[bp.k], s));
+    trd_status sp = prestage(c, bp.k + 1, c->ev_p2[bp.k], c->pipe == 2 ? 0 : 2, bp.k);
+    if (sp) return sp;
+  }
   launch_reduce_den(*c, bp, s);
   tl_mark(c, s, "reduce den");
   trd_status st = check_launch(c, "pass 2");
@@ -479,6 +535,7 @@ trd_status ensure_stats(Context* c, int n) {
 }
 
 trd_status sigma0_pass(Context* c) {
+  select_bufs(c, -1);
   const BlockPlan& bp = c->full_plan;
   cudaStream_t s = c->stream;
   if (c->eabs) CUDA_TRY(c, cudaMemsetAsync(&c->sc->eabs_fill, 0, sizeof(unsigned long long), s));
@@ -905,6 +962,38 @@ trd_status trd_init_ex(const trd_config* cfg, const trd_shard* shard, const floa
     if (max_v > 0 && (st = dalloc(c, &c->tw, (size_t)max_v))) return bail(st);
     if ((st = dalloc(c, &c->ptab, (size_t)(16 * 256 + 16)))) return bail(st);
   }
+  // ---- pipelined staging of the sampled tensor-core blocks (TRD_PIPE=0 disables) ----
+  {
+    const char* pe = getenv("TRD_PIPE");
+    const int mode = pe ? atoi(pe) : kPipeDefault;
+    c->pipe_min_tiles = pe ? 0 : kPipeMinTiles;     // (an explicit TRD_PIPE pipelines every sampled block)
+    bool any = false;
+    for (int k = 0; k < N; ++k)
+      if (c->plan[k].use_tc && !c->stage[k].invariant && !c->plan[k].explicit_cols &&
+          c->stage[k].n_tiles >= c->pipe_min_tiles)
+        any = true;
+    if (mode > 0 && mode <= 3 && any) {
+      c->idx_d = c->idx; c->doff_d = c->doff; c->row_off_d = c->row_off; c->col_off_d = c->col_off;
+      c->ptab_d = c->ptab;
+      if (cudaStreamCreateWithFlags(&c->stg, cudaStreamNonBlocking) != cudaSuccess ||
+          cudaEventCreateWithFlags(&c->ev_stg_fork, cudaEventDisableTiming) != cudaSuccess)
+        return bail(TRD_ERR_CUDA);
+      for (int k = 0; k < N; ++k) {
+        if (cudaEventCreateWithFlags(&c->ev_p1[k], cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&c->ev_p2[k], cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&c->ev_samp[k], cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&c->ev_staged[k], cudaEventDisableTiming) != cudaSuccess)
+          return bail(TRD_ERR_CUDA);
+        const BlockPlan& bp = c->plan[k];
+        if ((st = dalloc(c, &c->idx_b[k], idx_total)) || (st = dalloc(c, &c->doff_b[k], idx_total)) ||
+            (st = dalloc(c, &c->row_off_b[k], (size_t)std::max<int64_t>(1, bp.nrows))) ||
+            (st = dalloc(c, &c->col_off_b[k], (size_t)std::max<int64_t>(1, bp.ncols))) ||
+            (st = dalloc(c, &c->ptab_b[k], (size_t)(16 * 256 + 16))))
+          return bail(st);
+      }
+      c->pipe = mode;
+    }
+  }
   // R21: |e| slots of one sweep (every block's staged slots, or its observed entries) or of the
   // sigma_0 pass (all local observed entries)
   if (cfg->sigma_mode == TRD_SIGMA_MAD) {
@@ -1028,6 +1117,7 @@ trd_status trd_sketch(trd_ctx* ctx, int32_t sweep, int32_t k, int32_t* idx_dev, 
   CUDA_TRY(c, cudaMemcpyAsync(&saved, &c->sc->sweep, 4, cudaMemcpyDeviceToHost, c->stream));
   CUDA_TRY(c, cudaStreamSynchronize(c->stream));
   CUDA_TRY(c, cudaMemcpyAsync(&c->sc->sweep, &sweep, 4, cudaMemcpyHostToDevice, c->stream));
+  select_bufs(c, -1);
   launch_sampler(*c, bp, c->stream);
   trd_status st = check_launch(c, "sampler");
   if (st) return st;
@@ -1048,10 +1138,15 @@ static trd_status enqueue_sweep(Context* c) {
   cudaStream_t s = c->stream;
   trd_status st;
   launch_sweep_begin(*c, s);
+  struct InSweep {                       // (prestaging of block k + 1 only inside a sweep)
+    Context* c;
+    explicit InSweep(Context* cc) : c(cc) { c->in_sweep = 1; }
+    ~InSweep() { c->in_sweep = 0; select_bufs(c, -1); }
+  } in_sweep(c);
   for (int k = 0; k < c->N; ++k) {
     const BlockPlan& bp = c->plan[k];
     NvtxRange nr(kNvtxBlock[k]);
-    if ((st = block_pass1(c, bp))) return st;
+    if ((st = block_pass1(c, bp, k > 0 && pipelined(c, k)))) return st;
     if ((st = block_pass2(c, bp))) return st;
     if (k == c->N - 1)
       CUDA_TRY(c, cudaMemcpyAsync(c->G_last, c->G, (size_t)bp.R2 * bp.R2 * 8, cudaMemcpyDeviceToDevice, s));
@@ -1236,8 +1331,9 @@ trd_status trd_block_probe(trd_ctx* ctx, int32_t sweep, int32_t k, double* d_hos
   if (c->eabs) CUDA_TRY(c, cudaMemsetAsync(&c->sc->eabs_fill, 0, sizeof(unsigned long long), s));
   CUDA_TRY(c, cudaMemsetAsync(&c->sc->slot, 0, sizeof(int), s));
   trd_status st;
-  if ((st = block_pass1(c, bp))) return st;
+  if ((st = block_pass1(c, bp, false))) return st;
   if ((st = block_pass2(c, bp))) return st;
+  select_bufs(c, -1);
   const int64_t Ik = c->dims[k];
   std::vector<double> dv((size_t)(Ik * bp.R2 + 3));
   double nd[2];
@@ -1278,6 +1374,7 @@ trd_status trd_error(trd_ctx* ctx, const float* ref_dev, const uint32_t* eval_bi
   if (trd_status su = consume_upload(c)) return su;
   const BlockPlan& bp = c->full_plan;
   cudaStream_t s = c->stream;
+  select_bufs(c, -1);
   launch_sampler(*c, bp, s);
   launch_plan(*c, bp, s);
   launch_lft(*c, bp, c->Z + c->zoff[bp.k], 0, c->lft, s);
@@ -1430,6 +1527,17 @@ void trd_destroy(trd_ctx* ctx) {
   }
   if (c->ev_fork) cudaEventDestroy(c->ev_fork);
   if (c->ev_join) cudaEventDestroy(c->ev_join);
+  if (c->stg) { cudaStreamSynchronize(c->stg); cudaStreamDestroy(c->stg); }
+  if (c->ev_stg_fork) cudaEventDestroy(c->ev_stg_fork);
+  for (int k = 0; k < kMaxN; ++k) {
+    cudaEvent_t ev[] = {c->ev_p1[k], c->ev_p2[k], c->ev_samp[k], c->ev_staged[k]};
+    for (cudaEvent_t e : ev)
+      if (e) cudaEventDestroy(e);
+    void* bp[] = {c->idx_b[k], c->doff_b[k], c->row_off_b[k], c->col_off_b[k], c->ptab_b[k]};
+    for (void* p : bp)
+      if (p) cudaFree(p);
+  }
+  if (c->pipe) select_bufs(c, -1);         // (the current pointers may be a block's buffers)
   void* ptrs[] = {c->own_values, c->own_mask, c->rank_prefix, c->Z, c->Q, c->idx, c->doff,
                   c->row_off, c->col_off, c->mid, c->lft, c->lfth, c->rgtT, c->dpart, c->spart,
                   c->denpart, c->numpart, c->dvec, c->G, c->G_last, c->Mop, c->chol_ws,

@@ -12,6 +12,11 @@
 namespace trd {
 
 constexpr int kMaxN = TRD_MAX_ORDER;
+// default mode of the pipelined staging of sampled blocks (Context::pipe; TRD_PIPE overrides) and
+// the smallest staged tile count of a pipelined block (smaller stagings are cheaper in line:
+// measured C4 0.87 ms/sweep in line vs 0.93 pipelined, C5a 2.24 vs 2.15)
+constexpr int kPipeDefault = 3;
+constexpr int64_t kPipeMinTiles = 2048;
 constexpr int kMaxR = TRD_MAX_RANK;
 constexpr int kMaxR2 = kMaxR * kMaxR;
 // blocks with R_k^2 above this take the large-rank path (trd_big.cu): the d contraction by
@@ -279,6 +284,29 @@ struct Context {
   int64_t idx_off[kMaxN + 1];
   int64_t* row_off = nullptr;          // per GEMM row
   int64_t* col_off = nullptr;          // per GEMM col
+  // Pipelined staging of sampled blocks (RStS): block k+1's sampler, offsets
+  // and tile staging depend only on (seed, k+1, t) and the data, not on the cores, so they run
+  // on `stg` while block k finishes.  Each block then owns its index / offset buffers; the
+  // pointers above are the current block's (select_bufs), `*_d` the defaults (sigma_0, trd_error,
+  // trd_sketch, contexts without the pipeline).
+  int in_sweep = 0;                    // enqueue_sweep is running (prestaging allowed)
+  int64_t pipe_min_tiles = 0;          // blocks staging fewer tiles stay in line
+  int pipe = 0;                        // 0 off, 1 prestage after pass 1 of the previous block,
+                                       // 2 after its pass 2, 3 split (sampler + bits after pass 1,
+                                       // values after pass 2)
+  cudaStream_t stg = nullptr;
+  cudaEvent_t ev_stg_fork = nullptr, ev_p1[kMaxN] = {}, ev_p2[kMaxN] = {}, ev_samp[kMaxN] = {},
+              ev_staged[kMaxN] = {};
+  int32_t* idx_b[kMaxN] = {};
+  int64_t* doff_b[kMaxN] = {};
+  int64_t* row_off_b[kMaxN] = {};
+  int64_t* col_off_b[kMaxN] = {};
+  uint8_t* ptab_b[kMaxN] = {};
+  int32_t* idx_d = nullptr;
+  int64_t* doff_d = nullptr;
+  int64_t* row_off_d = nullptr;
+  int64_t* col_off_d = nullptr;
+  uint8_t* ptab_d = nullptr;
   float* mid = nullptr;                // Mid(j_L): r_{k+1} x r_s
   float* lft = nullptr;                // Lft rows: [row][K]
   float* lfth = nullptr;               // Lft of the scaled gradient (pass 2)
@@ -351,7 +379,11 @@ struct Context {
 
 // ---- kernels (trd_kernels.cu) --------------------------------------------------------
 void launch_sampler(Context& c, const BlockPlan& bp, cudaStream_t s);
-void launch_plan(Context& c, const BlockPlan& bp, cudaStream_t s);
+// offsets = false: the row / column data offsets were computed ahead (pipelined staging, launch_offsets);
+// only the operand-scale maxima are reset
+void launch_plan(Context& c, const BlockPlan& bp, cudaStream_t s, bool offsets = true);
+// row / column data offsets of block bp (reset_amax: also zero the operand-scale maxima of the block)
+void launch_offsets(Context& c, const BlockPlan& bp, cudaStream_t s, bool reset_amax);
 void launch_lft(Context& c, const BlockPlan& bp, const float* Zsrc_k, int src_is_h, float* out,
                 cudaStream_t s);
 void launch_pass1(Context& c, const BlockPlan& bp, int stats_only, cudaStream_t s);
@@ -403,7 +435,8 @@ void launch_tc_reduce_d(Context& c, const BlockPlan& bp, cudaStream_t s);
 // d contraction of D rows in contrib ([nsplit][nrows_pad][KP]) for any R2, + final reduction
 void launch_reduce_d_contrib(Context& c, const BlockPlan& bp, int nsplit, int64_t nrows_pad, int64_t nparts,
                              cudaStream_t s);
-void launch_tc_stage(Context& c, const BlockPlan& bp, TcStage& st, cudaStream_t s);
+// phase 0: the whole staging; 1: masks, row offsets and tile prefix (stage_bits + scan); 2: the values
+void launch_tc_stage(Context& c, const BlockPlan& bp, TcStage& st, cudaStream_t s, int phase = 0);
 size_t tc_scan_tmp_bytes(int64_t n_tiles);
 void tc_debug_dump();   // TRD_TC_EXP diagnostics
 

@@ -299,7 +299,8 @@ __device__ __forceinline__ void right_digits(const PlanArgs& a, int64_t col, int
 __global__ void offsets_kernel(PlanArgs a, const int64_t* __restrict__ doff,
                                int64_t* __restrict__ row_off, int64_t* __restrict__ col_off,
                                DevScalars* __restrict__ sc) {
-  if (blockIdx.x == 0 && threadIdx.x == 0) { sc->amax_a = 0u; sc->amax_b = 0u; }   // (operand scaling)
+  // (operand scaling; sc = nullptr when the offsets run ahead on the staging stream)
+  if (sc && blockIdx.x == 0 && threadIdx.x == 0) { sc->amax_a = 0u; sc->amax_b = 0u; }
   const int64_t tot = a.nrows + a.ncols;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tot;
        t += (int64_t)gridDim.x * blockDim.x) {
@@ -1397,6 +1398,128 @@ __global__ void __launch_bounds__(256) gj2_solve_kernel(const double* __restrict
   if (tid == 0) { sc->lambda = lam; sc->h_lam = lam; }
 }
 
+// Register Gauss-Jordan inverse, 2-D distribution (the default a9 solve for R^2 <= 128): the same
+// in-place elimination as gj2_solve_kernel (X = A^-1, A = G + lambda I, no pivoting: A is SPD, a
+// non-positive pivot triggers the R23 retry), but every thread of the CTA holds an NU x NV block
+// of A (rows ty*NU + u, columns tx*NV + v; 8 warps x 32 lanes) so that one step costs NU*NV
+// independent DFMAs per thread instead of NP/2, the k loop is not unrolled (the round-1 / gj2
+// kernels unrolled it over NP steps: instruction-cache bound, ~120-190 us at R^2 = 100), and only
+// the n real pivots are eliminated (the identity padding never changes).  Step k: generic update
+// a_ij -= (a_ik / p) a_kj over the whole block, then row k (a_kj / p, owner warp) and column k
+// (-a_ik / p, owner lane; a_kk = 1 / p) are fixed up, and the owners publish row k+1 / column
+// k+1 to double-buffered shared vectors; one barrier per step.
+template <int NU, int NV>
+__global__ void __launch_bounds__(256) gj3_solve_kernel(const double* __restrict__ G, int n, double lambda_rel,
+                                                        double* __restrict__ Xout, DevScalars* __restrict__ sc) {
+  constexpr int NP = 8 * NU, NC = 32 * NV;
+  static_assert(NU % 2 == 0 && NC >= NP, "row pairs, columns cover the padded matrix");
+  __shared__ __align__(16) double rowb[2][NC];
+  __shared__ __align__(16) double colb[2][NP];
+  __shared__ int fail_s;
+  __shared__ double tr_s;
+  const int tid = threadIdx.x, tx = tid & 31, ty = tid >> 5;
+  const int i0 = ty * NU, j0 = tx * NV;
+  if (tid < 32) tr_s_warp(G, n, &tr_s);
+  __syncthreads();
+  double lam = lambda_rel * tr_s / n;
+  double a[NU][NV];
+  for (int attempt = 0;; ++attempt) {
+#pragma unroll
+    for (int u = 0; u < NU; ++u)
+#pragma unroll
+      for (int v = 0; v < NV; ++v) {
+        const int i = i0 + u, j = j0 + v;
+        a[u][v] = (i < n && j < n) ? G[i * n + j] + (i == j ? lam : 0.0) : (i == j ? 1.0 : 0.0);
+        if (i == 0) rowb[0][j] = a[u][v];
+        if (j == 0) colb[0][i] = a[u][v];
+      }
+    if (tid == 0) fail_s = 0;
+    __syncthreads();
+    for (int k = 0; k < n; ++k) {
+      const int b = k & 1;
+      const double p = rowb[b][k];
+      if (!(p > 0.0)) {                      // (uniform: every thread reads the same pivot)
+        if (tid == 0) fail_s = 1;
+        break;
+      }
+      const double ip = 1.0 / p;
+      double rj[NV], f[NU];
+      if (NV % 2 == 0) {
+#pragma unroll
+        for (int v = 0; v < NV; v += 2) {
+          const double2 t = *reinterpret_cast<const double2*>(&rowb[b][j0 + v]);
+          rj[v] = t.x;
+          rj[v + 1] = t.y;
+        }
+      } else {
+#pragma unroll
+        for (int v = 0; v < NV; ++v) rj[v] = rowb[b][j0 + v];
+      }
+#pragma unroll
+      for (int u = 0; u < NU; u += 2) {
+        const double2 t = *reinterpret_cast<const double2*>(&colb[b][i0 + u]);
+        f[u] = t.x * ip;
+        f[u + 1] = t.y * ip;
+      }
+#pragma unroll
+      for (int u = 0; u < NU; ++u)
+#pragma unroll
+        for (int v = 0; v < NV; ++v) a[u][v] = fma(-f[u], rj[v], a[u][v]);
+      if (ty == k / NU) {                    // row k: a_kj / p (warp-uniform)
+#pragma unroll
+        for (int u = 0; u < NU; ++u)
+          if (i0 + u == k) {
+#pragma unroll
+            for (int v = 0; v < NV; ++v) a[u][v] = rj[v] * ip;
+          }
+      }
+      if (tx == k / NV) {                    // column k: -a_ik / p, a_kk = 1 / p
+#pragma unroll
+        for (int v = 0; v < NV; ++v)
+          if (j0 + v == k) {
+#pragma unroll
+            for (int u = 0; u < NU; ++u) a[u][v] = (i0 + u == k) ? ip : -f[u];
+          }
+      }
+      const int k1 = k + 1;
+      if (ty == k1 / NU) {                   // publish row k + 1
+#pragma unroll
+        for (int u = 0; u < NU; ++u)
+          if (i0 + u == k1) {
+#pragma unroll
+            for (int v = 0; v < NV; ++v) rowb[b ^ 1][j0 + v] = a[u][v];
+          }
+      }
+      if (tx == k1 / NV) {                   // publish column k + 1
+#pragma unroll
+        for (int v = 0; v < NV; ++v)
+          if (j0 + v == k1) {
+#pragma unroll
+            for (int u = 0; u < NU; ++u) colb[b ^ 1][i0 + u] = a[u][v];
+          }
+      }
+      __syncthreads();
+    }
+    __syncthreads();
+    if (!fail_s || attempt >= 3) break;
+    lam = lam > 0.0 ? 10.0 * lam : ldexp(tr_s / n, -40);   // R23 retry rule
+    __syncthreads();
+  }
+  if (fail_s) {
+    if (tid == 0) { sc->not_spd = 1; sc->lambda = lam; sc->h_lam = 0.0; }
+    for (int t = tid; t < n * n; t += blockDim.x) Xout[t] = 0.0;
+    return;
+  }
+#pragma unroll
+  for (int u = 0; u < NU; ++u)
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      const int i = i0 + u, j = j0 + v;
+      if (i < n && j < n) Xout[i * n + j] = a[u][v];
+    }
+  if (tid == 0) { sc->lambda = lam; sc->h_lam = lam; }
+}
+
 // h = d M (row-wise) with M = Mop - h_lam Mop^2 (h_lam = lambda when Mop = (G + lambda I)^-1 from
 // gj2_solve_kernel, 0 when Mop is M itself), computed as u = d Mop, h = u - h_lam u Mop;
 // num partial per row = <d(i), h(i)>
@@ -1874,10 +1997,21 @@ void launch_sampler(Context& c, const BlockPlan& bp, cudaStream_t s) {
   c.launches++;
 }
 
-void launch_plan(Context& c, const BlockPlan& bp, cudaStream_t s) {
+void launch_offsets(Context& c, const BlockPlan& bp, cudaStream_t s, bool reset_amax) {
   PlanArgs a = make_plan_args(c, bp);
-  offsets_kernel<<<grid_for(bp.nrows + bp.ncols), 256, 0, s>>>(a, c.doff, c.row_off, c.col_off, c.sc);
+  offsets_kernel<<<grid_for(bp.nrows + bp.ncols), 256, 0, s>>>(a, c.doff, c.row_off, c.col_off,
+                                                              reset_amax ? c.sc : nullptr);
   c.launches++;
+}
+
+void launch_plan(Context& c, const BlockPlan& bp, cudaStream_t s, bool offsets) {
+  PlanArgs a = make_plan_args(c, bp);
+  if (offsets) {
+    launch_offsets(c, bp, s, true);
+  } else {
+    static_assert(offsetof(DevScalars, amax_b) == offsetof(DevScalars, amax_a) + 4, "adjacent maxima");
+    cudaMemsetAsync(&c.sc->amax_a, 0, 2 * sizeof(unsigned int), s);
+  }
   if (bp.p > 0) {
     if (c.rbucket <= 16) mid_kernel<16><<<grid_for(bp.nL * bp.rk1), 256, 0, s>>>(a, c.idx, c.Z, c.mid);
     else if (c.rbucket <= 32) mid_kernel<32><<<grid_for(bp.nL * bp.rk1), 256, 0, s>>>(a, c.idx, c.Z, c.mid);
@@ -2043,7 +2177,23 @@ void launch_solve(Context& c, const BlockPlan& bp, cudaStream_t s, const double*
     big_factor(c, bp, s, G);
     return;
   }
-  if (n <= 128 && !(getenv("TRD_SOLVE") && atoi(getenv("TRD_SOLVE")) == 1)) {
+  const int solve_sel = getenv("TRD_SOLVE") ? atoi(getenv("TRD_SOLVE")) : 0;
+  if (n <= 128 && solve_sel == 0) {    // 2-D register Gauss-Jordan (NU x NV blocks per thread)
+    const int np = (n + 15) / 16 * 16;
+    switch (np) {
+      case 16: gj3_solve_kernel<2, 1><<<1, 256, 0, s>>>(G, n, c.cfg.lambda_rel, c.Mop, c.sc); break;
+      case 32: gj3_solve_kernel<4, 1><<<1, 256, 0, s>>>(G, n, c.cfg.lambda_rel, c.Mop, c.sc); break;
+      case 48: gj3_solve_kernel<6, 2><<<1, 256, 0, s>>>(G, n, c.cfg.lambda_rel, c.Mop, c.sc); break;
+      case 64: gj3_solve_kernel<8, 2><<<1, 256, 0, s>>>(G, n, c.cfg.lambda_rel, c.Mop, c.sc); break;
+      case 80: gj3_solve_kernel<10, 3><<<1, 256, 0, s>>>(G, n, c.cfg.lambda_rel, c.Mop, c.sc); break;
+      case 96: gj3_solve_kernel<12, 3><<<1, 256, 0, s>>>(G, n, c.cfg.lambda_rel, c.Mop, c.sc); break;
+      case 112: gj3_solve_kernel<14, 4><<<1, 256, 0, s>>>(G, n, c.cfg.lambda_rel, c.Mop, c.sc); break;
+      default: gj3_solve_kernel<16, 4><<<1, 256, 0, s>>>(G, n, c.cfg.lambda_rel, c.Mop, c.sc); break;
+    }
+    c.launches++;
+    return;
+  }
+  if (n <= 128 && solve_sel == 2) {    // (A/B: the one-dimensional register kernel)
     const int np = (n + 15) / 16 * 16;
     switch (np) {
       case 16: gj2_solve_kernel<16><<<1, 256, 0, s>>>(G, n, c.cfg.lambda_rel, c.Mop, c.sc); break;

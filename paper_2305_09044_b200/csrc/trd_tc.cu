@@ -1496,7 +1496,7 @@ void launch_tc_pack_cols(Context& c, const BlockPlan& bp, cudaStream_t s) {
 }
 
 // Stage sketch for block bp into the staging buffers st (bits, offsets, prefix, values)
-void launch_tc_stage(Context& c, const BlockPlan& bp, TcStage& st, cudaStream_t s) {
+void launch_tc_stage(Context& c, const BlockPlan& bp, TcStage& st, cudaStream_t s, int phase) {
   StageArgs a;
   a.nrows = bp.nrows; a.ncols = bp.ncols; a.n_col_tiles = bp.n_col_tiles;
   a.n_tiles = bp.n_row_tiles * bp.n_col_tiles;
@@ -1546,12 +1546,16 @@ void launch_tc_stage(Context& c, const BlockPlan& bp, TcStage& st, cudaStream_t 
   }
   const int gb = (int)std::min<int64_t>(a.n_tiles, (int64_t)c.num_sm * occ_bits);
   const int gv = (int)std::min<int64_t>(a.n_tiles, (int64_t)c.num_sm * occ_vals);
-  stage_bits_kernel<<<gb, TC_M, 0, s>>>(a);
-  // tbase = exclusive prefix of tcount (tcount[n_tiles] = 0: tbase[n_tiles] = total); out of
-  // place, so a skipped stage_bits leaves the same prefix
-  cub::DeviceScan::ExclusiveSum(st.scan_tmp, st.scan_tmp_bytes, st.tcount, st.tbase, (int)a.n_tiles + 1, s);
+  if (phase != 2) {
+    stage_bits_kernel<<<gb, TC_M, 0, s>>>(a);
+    // tbase = exclusive prefix of tcount (tcount[n_tiles] = 0: tbase[n_tiles] = total); out of
+    // place, so a skipped stage_bits leaves the same prefix
+    cub::DeviceScan::ExclusiveSum(st.scan_tmp, st.scan_tmp_bytes, st.tcount, st.tbase, (int)a.n_tiles + 1, s);
+    c.launches += 2;
+  }
+  if (phase == 1) return;
   stage_vals_kernel<<<gv, TC_M, 0, s>>>(a);
-  c.launches += 3;
+  c.launches += 1;
   if (cached) {
     layout_gen_kernel<<<1, 32, 0, s>>>(&c.sc->mask_gen, &c.sc->layout_gen[bp.k]);
     gather_vals_kernel<<<c.num_sm * 8, 256, 0, s>>>(st.perm, st.tidx, c.values, st.tbase + a.n_tiles, st.tvals, st.vcap);

@@ -285,6 +285,34 @@ def test_graph_replay_equals_eager_sweeps(name, dims, sketch, monkeypatch):
     assert pb["pass1_ms"] > 0.0 and pb["pass2_ms"] > 0.0
 
 
+# ---------------------------------------------------------------- pipelined staging (RStS)
+@pytest.mark.parametrize("name,dims,sketch", [("C4", [16, 16, 16, 16], [8, 8, 8, 8]),
+                                               ("C5a", [16, 12, 10, 9, 8], [8, 6, 5, 4, 4])])
+def test_pipelined_staging_equals_in_line_staging(name, dims, sketch, monkeypatch):
+    """Block k+1's sampler, offsets and tile staging enqueued ahead on the staging stream
+    (TRD_PIPE = 1: behind block k's pass 1; 2: behind its pass 2; 3: split) give the cores,
+    records and sigma of in-line staging (TRD_PIPE = 0) bit for bit, eagerly and replayed from
+    CUDA graphs (Alg. 1 l.4-5: the index sets depend only on (seed, k, t))."""
+    _cuda()
+    spec = small_spec(name, dims, sketch)
+    prob = make_problem(spec)
+    ref = None
+    for pipe in ("0", "1", "2", "3"):
+        for graph in ("0", "1"):
+            monkeypatch.setenv("TRD_PIPE", pipe)
+            monkeypatch.setenv("TRD_GRAPH", graph)
+            ctx = gpu_context(prob, packed=True, sigma_mode=O.SIGMA_MAD)
+            recs = ctx.sweep(3)
+            got = (ctx.get_cores(), [(r["sigma"], r["eta"], r["n_obs"]) for r in recs])
+            ctx.close()
+            if ref is None:
+                ref = got
+                continue
+            for x, y in zip(ref[0], got[0]):
+                assert np.array_equal(x, y), (pipe, graph)
+            assert ref[1] == got[1], (pipe, graph)
+
+
 # ---------------------------------------------------------------- large ranks (SURVEY 8f rank 3)
 @pytest.mark.parametrize("name,dims,ranks,sketch", [
     ("C2", [256, 256, 3], [20, 20, 3], None),            # the paper's image ranks (P:362)
