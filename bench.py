@@ -38,6 +38,9 @@ def parse():
     ap.add_argument("--config", default="C5b")
     ap.add_argument("--impl", default="mine", choices=["mine", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
+    # (measurement only, not a bench line of a BASELINE config: the config's observed fraction
+    #  replaced, e.g. for the dense-tile vs per-entry SIMT crossover in density)
+    ap.add_argument("--observed", type=float, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget-s", type=float, default=10.0)
     # variants of the method (defaults: the config's sigma rule, the paper's scaled gradient)
@@ -229,6 +232,9 @@ def run_mine(args):
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     spec = CONFIGS[args.config]
+    if args.observed is not None:
+        import dataclasses
+        spec = dataclasses.replace(spec, observed=args.observed, name=f"{spec.name}@rho={args.observed:g}")
     N = spec.order
     prob = make_workload(spec, "cuda")
     (b, e), vals, words, Ml = local_shard(prob, rank, world)

@@ -789,9 +789,13 @@ trd_status trd_init_ex(const trd_config* cfg, const trd_shard* shard, const floa
   size_t max_lhl = 0, max_rhl = 0, max_contrib = 0, max_rpad = 0, max_rgtc = 0;
   int64_t full_s[kMaxN];
   for (int m = 0; m < N; ++m) full_s[m] = 0;
+  bool rows_forced = false;
   {
     const char* pe = getenv("TRD_PASS");
-    c->want_tc = !(pe && strcmp(pe, "simt") == 0);
+    c->want_tc = !(pe && (strcmp(pe, "simt") == 0 || strcmp(pe, "rows") == 0));
+    // (TRD_PASS=rows, measurement: every block through the warp-per-row SIMT passes, which touch
+    //  the observed entries only -- the per-entry SIMT cost of DESIGN.md sec. 7)
+    rows_forced = pe && strcmp(pe, "rows") == 0;
   }
   for (int k = 0; k <= N; ++k) {
     BlockPlan& bp = (k < N) ? c->plan[k] : c->full_plan;
@@ -801,7 +805,7 @@ trd_status trd_init_ex(const trd_config* cfg, const trd_shard* shard, const floa
     if (bp.K > 256) return bail(fail(c, TRD_ERR_SHAPE, "block %d: no split with r_k r_s <= 256", k));
     bp.lib_solve = (bp.big || (c->has_big && bp.R2 > 128)) ? 1 : 0;
     bp.rows = 0;
-    if (!bp.use_tc && bp.K > 128) {          // warp-per-row SIMT passes (simt_rows_kernel)
+    if (!bp.use_tc && (bp.K > 128 || (rows_forced && k < N))) {   // warp-per-row SIMT passes (simt_rows_kernel)
       bp.rows = 1;
       int64_t ns = ((int64_t)c->num_sm * 64 + bp.nrows - 1) / std::max<int64_t>(1, bp.nrows);
       ns = std::max<int64_t>(1, std::min<int64_t>(ns, std::max<int64_t>(1, bp.ncols / 64)));
