@@ -398,6 +398,10 @@ static trd_status prestage(Context* c, int k, cudaEvent_t after, int part, int c
   return check_launch(c, "prestage");
 }
 
+// inside enqueue_sweep with world 1: den reduction, block scalars and update as one launch
+// (launch_block_tail; TRD_NO_FUSE=1 keeps the separate kernels)
+static bool fuse_tail(const Context* c) { return c->in_sweep && c->cfg.world <= 1 && c->fuse; }
+
 // inside enqueue_sweep: the staging of block k + 1 is enqueued ahead (block 0 stages in line)
 static bool pre_next(const Context* c, int k) { return c->in_sweep && pipelined(c, k + 1); }
 
@@ -476,7 +480,7 @@ trd_status block_pass1(Context* c, const BlockPlan& bp, bool pre) {
   tl_mark(c, s, "reduce d");
   st = allreduce(c, c->dvec, (size_t)(Ik * bp.R2 + 3));
   if (st) return st;
-  launch_block_stats(*c, bp, s);
+  if (!fuse_tail(c)) launch_block_stats(*c, bp, s);
   tl_mark(c, s, "exchange + stats");
   return TRD_OK;
 }
@@ -503,7 +507,7 @@ trd_status block_pass2(Context* c, const BlockPlan& bp) {
     trd_status sp = prestage(c, bp.k + 1, c->ev_p2[bp.k], c->pipe == 2 ? 0 : 2, bp.k);
     if (sp) return sp;
   }
-  launch_reduce_den(*c, bp, s);
+  if (!fuse_tail(c)) launch_reduce_den(*c, bp, s);
   tl_mark(c, s, "reduce den");
   trd_status st = check_launch(c, "pass 2");
   if (st) return st;
@@ -718,6 +722,7 @@ trd_status trd_init_ex(const trd_config* cfg, const trd_shard* shard, const floa
   c->cfg = *cfg;
   c->cfg.nccl_unique_id = nullptr;
   c->tl_on = getenv("TRD_TIMELINE") && atoi(getenv("TRD_TIMELINE")) != 0;
+  c->fuse = !(getenv("TRD_NO_FUSE") && atoi(getenv("TRD_NO_FUSE")) != 0);
   if (ex && cfg->world > 1) c->ex = *ex;
   c->N = N;
   c->stream = (cudaStream_t)stream;
@@ -1154,7 +1159,8 @@ static trd_status enqueue_sweep(Context* c) {
     if ((st = block_pass2(c, bp))) return st;
     if (k == c->N - 1)
       CUDA_TRY(c, cudaMemcpyAsync(c->G_last, c->G, (size_t)bp.R2 * bp.R2 * 8, cudaMemcpyDeviceToDevice, s));
-    launch_update(*c, bp, s);
+    if (fuse_tail(c)) launch_block_tail(*c, bp, s);
+    else launch_update(*c, bp, s);
     tl_mark(c, s, "step + update");
     launch_q(*c, k, s);
     tl_mark(c, s, "Q refresh");

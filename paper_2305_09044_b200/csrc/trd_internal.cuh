@@ -290,6 +290,7 @@ struct Context {
   // pointers above are the current block's (select_bufs), `*_d` the defaults (sigma_0, trd_error,
   // trd_sketch, contexts without the pipeline).
   int in_sweep = 0;                    // enqueue_sweep is running (prestaging allowed)
+  int fuse = 1;                        // world 1: fused block tail (TRD_NO_FUSE=1: separate kernels)
   int64_t pipe_min_tiles = 0;          // blocks staging fewer tiles stay in line
   int pipe = 0;                        // 0 off, 1 prestage after pass 1 of the previous block,
                                        // 2 after its pass 2, 3 split (sampler + bits after pass 1,
@@ -398,6 +399,8 @@ void launch_h(Context& c, const BlockPlan& bp, cudaStream_t s);
 void launch_pass2(Context& c, const BlockPlan& bp, cudaStream_t s);
 void launch_reduce_den(Context& c, const BlockPlan& bp, cudaStream_t s);
 void launch_update(Context& c, const BlockPlan& bp, cudaStream_t s);
+// world 1: reduce_den + the block scalars (both phases) + the update in one single-CTA launch
+void launch_block_tail(Context& c, const BlockPlan& bp, cudaStream_t s);
 void launch_sweep_end(Context& c, cudaStream_t s);
 void launch_core_checksum(Context& c, cudaStream_t s);   // -> c.chk (world > 1)
 void launch_replica_check(Context& c, cudaStream_t s);

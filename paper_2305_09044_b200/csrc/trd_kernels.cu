@@ -1616,6 +1616,71 @@ __global__ void block_scalars_kernel(const double* __restrict__ dvec, int64_t Ik
   sc->acc_n += sc->n_obs;
 }
 
+// World 1 (no den exchange between them): reduce_den_kernel, block_scalars_kernel (both phases)
+// and update2_kernel as one launch.  Every CTA forms the den / num sums in the same fixed order
+// (256 partial sums, then thread 0 / 1 in thread order) and the same eta, so the grid needs no
+// second launch; CTA 0 writes [den, num] and the block record (thread 0), and the CTAs update
+// their share of Z_k <- Z_k + eta fold(h) (Eq. 11/17 with Eq. 12's eta, reading R2).  Bitwise
+// the results of the separate kernels.
+__global__ void __launch_bounds__(256) block_tail_kernel(const double* __restrict__ denpart, int64_t nden,
+                                                         const double* __restrict__ numpart, int64_t nnum,
+                                                         double* __restrict__ numden, const double* __restrict__ dvec,
+                                                         int64_t Ik, int R2, DevScalars* sc, DevStats* stats, int k,
+                                                         double step, float* __restrict__ Zk,
+                                                         const double* __restrict__ h, int rk, int rk1) {
+  __shared__ double acc[2][256];
+  __shared__ double nd_s[2];
+  const int t = threadIdx.x;
+  double a0 = 0.0, a1 = 0.0;
+  for (int64_t i = t; i < nden; i += 256) a0 += denpart[i];
+  for (int64_t i = t; i < nnum; i += 256) a1 += numpart[i];
+  acc[0][t] = a0;
+  acc[1][t] = a1;
+  __syncthreads();
+  if (t < 2) {
+    double tot = 0.0;
+    for (int j = 0; j < 256; ++j) tot += acc[t][j];
+    nd_s[t] = tot;
+    if (blockIdx.x == 0) numden[t] = tot;   // [den, num]
+  }
+  __syncthreads();
+  const double den = nd_s[0], num = nd_s[1];
+  const double eta = step > 0.0 ? step : ((num > 0.0 && den > 0.0) ? num / den : 0.0);   // = block_eta
+  if (blockIdx.x == 0 && t == 0) {
+    sc->sum_e2 = dvec[Ik * R2 + 0];
+    sc->welsch = dvec[Ik * R2 + 1];
+    sc->n_obs = dvec[Ik * R2 + 2];
+    sc->den = den;
+    sc->num = num;
+    sc->eta = eta;
+    DevStats& st = stats[sc->slot];
+    st.eta[k] = eta;
+    st.num[k] = num;
+    st.den[k] = den;
+    st.nnz[k] = (long long)sc->n_obs;
+    st.n_obs += (long long)sc->n_obs;
+    st.sum_e2 += sc->sum_e2;
+    st.welsch += sc->welsch;
+    if (eta == 0.0) st.skipped |= (1u << k);
+    if (!(eta == eta) || isinf(eta) || !(num == num) || !(den == den) || isinf(den)) {
+      st.nonfinite = 1;
+      sc->nonfinite = 1;
+    }
+    sc->acc_e2 += sc->sum_e2;
+    sc->acc_n += sc->n_obs;
+  }
+  if (eta == 0.0) return;
+  const int64_t tot = Ik * rk * rk1;
+  for (int64_t q = blockIdx.x * 256 + t; q < tot; q += (int64_t)gridDim.x * 256) {
+    const int b = (int)(q % rk1);
+    const int64_t ia = q / rk1;
+    const int aa = (int)(ia % rk);
+    const int64_t i = ia / rk;
+    const double v = (double)Zk[q] + eta * h[i * rk * rk1 + aa + rk * b];
+    Zk[q] = (float)v;
+  }
+}
+
 // the sweep's record slot comes from device memory (sc->slot_next, reset by trd_sweep), so a
 // captured sweep replays into successive records
 __global__ void sweep_begin_kernel(DevScalars* sc, DevStats* stats) {
@@ -2243,6 +2308,17 @@ void launch_h(Context& c, const BlockPlan& bp, cudaStream_t s) {
   }
   const int64_t Ik = c.dims[bp.k];                     // h of every i_k (replicated update)
   h_kernel<<<(unsigned)Ik, 256, 0, s>>>(c.dvec, c.Mop, bp.R2, c.h, c.numpart, c.sc);
+  c.launches++;
+}
+
+void launch_block_tail(Context& c, const BlockPlan& bp, cudaStream_t s) {
+  const int64_t Ik = c.dims[bp.k];
+  const int64_t ncta = bp.grid_x * bp.nsplit;
+  const int64_t nden = bp.use_tc ? (int64_t)bp.tc_grid : bp.rows ? (int64_t)bp.rows_grid : (bp.nrows / bp.nL) * ncta;
+  const int64_t tot = Ik * bp.rk * bp.rk1;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((tot + 255) / 256, (int64_t)c.num_sm));
+  block_tail_kernel<<<grid, 256, 0, s>>>(c.denpart, nden, c.numpart, Ik, c.red_ws, c.dvec, Ik, bp.R2, c.sc, c.stats, bp.k,
+                                       c.cfg.step, c.Z + c.zoff[bp.k], c.h, bp.rk, bp.rk1);
   c.launches++;
 }
 

@@ -313,6 +313,30 @@ def test_pipelined_staging_equals_in_line_staging(name, dims, sketch, monkeypatc
             assert ref[1] == got[1], (pipe, graph)
 
 
+@pytest.mark.parametrize("name,dims,sketch", [("C4", [16, 16, 16, 16], [8, 8, 8, 8]),
+                                               ("C5b", [12, 9, 8, 7, 6], None)])
+def test_fused_block_tail_equals_separate_kernels(name, dims, sketch, monkeypatch):
+    """World 1: the den / num reduction, the block scalars and the update (Eq. 11-12 / 17-18,
+    P:164-170) as one launch give the cores and records of the separate kernels (TRD_NO_FUSE=1)
+    bit for bit, with three fewer launches per block."""
+    _cuda()
+    spec = small_spec(name, dims, sketch)
+    prob = make_problem(spec)
+    out = []
+    for off in ("1", "0"):
+        monkeypatch.setenv("TRD_NO_FUSE", off)
+        ctx = gpu_context(prob, packed=True)
+        l0 = ctx.launch_count
+        recs = ctx.sweep(3)
+        out.append((ctx.get_cores(), [(r["sigma"], r["eta"], r["num"], r["den"], r["n_obs"]) for r in recs],
+                    ctx.launch_count - l0))
+        ctx.close()
+    for x, y in zip(out[0][0], out[1][0]):
+        assert np.array_equal(x, y)
+    assert out[0][1] == out[1][1]
+    assert out[0][2] - out[1][2] == 3 * 3 * len(dims)
+
+
 # ---------------------------------------------------------------- large ranks (SURVEY 8f rank 3)
 @pytest.mark.parametrize("name,dims,ranks,sketch", [
     ("C2", [256, 256, 3], [20, 20, 3], None),            # the paper's image ranks (P:362)
