@@ -1152,6 +1152,12 @@ static trd_status enqueue_sweep(Context* c) {
     explicit InSweep(Context* cc) : c(cc) { c->in_sweep = 1; }
     ~InSweep() { c->in_sweep = 0; select_bufs(c, -1); }
   } in_sweep(c);
+  // (TRD_Q_SIDE=1: the Q refresh on the side stream.  Measured, ms per sweep in line / side: C3
+  //  0.792 / 0.753, C4 0.846 / 0.892 (the side stream's Gauss-Jordan solve becomes critical),
+  //  C5a 2.152 / 2.124 -- within run-to-run noise overall, so in line by default)
+  const bool q_side = !(getenv("TRD_NO_SIDE") && atoi(getenv("TRD_NO_SIDE")) != 0) &&
+                      getenv("TRD_Q_SIDE") && atoi(getenv("TRD_Q_SIDE")) != 0;
+  bool q_pending = false;
   for (int k = 0; k < c->N; ++k) {
     const BlockPlan& bp = c->plan[k];
     NvtxRange nr(kNvtxBlock[k]);
@@ -1162,9 +1168,22 @@ static trd_status enqueue_sweep(Context* c) {
     if (fuse_tail(c)) launch_block_tail(*c, bp, s);
     else launch_update(*c, bp, s);
     tl_mark(c, s, "step + update");
-    launch_q(*c, k, s);
+    // Q_k of the updated core (Eq. 13's factor) is read only by the next blocks' FGMC Gram on the
+    // side stream: optionally refresh it there (large-rank Q by cuBLAS stays in line)
+    if (q_side && (int64_t)c->ranks[k] * c->ranks[(k + 1) % c->N] <= kBigR2) {
+      CUDA_TRY(c, cudaEventRecord(c->ev_fork, s));
+      CUDA_TRY(c, cudaStreamWaitEvent(c->side, c->ev_fork, 0));
+      launch_q(*c, k, c->side);
+      q_pending = true;
+    } else {
+      launch_q(*c, k, s);
+    }
     tl_mark(c, s, "Q refresh");
     if ((st = check_launch(c, "update"))) return st;
+  }
+  if (q_pending) {                        // join the side stream's last Q refresh
+    CUDA_TRY(c, cudaEventRecord(c->ev_join, c->side));
+    CUDA_TRY(c, cudaStreamWaitEvent(s, c->ev_join, 0));
   }
   if (c->eabs) {
     NvtxRange nr("trd mad select");
