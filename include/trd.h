@@ -276,7 +276,9 @@ typedef struct {
   double pass1_ms, pass2_ms;        /* summed device time of the pass kernels               */
   int64_t pass1_launches, pass2_launches;
   double pass1_entries, pass2_entries;    /* observed entries processed (sum over launches) */
-  double pass1_flops, pass2_flops;        /* algorithmic flops, SURVEY 8(d) per-entry count  */
+  double pass1_flops, pass2_flops;        /* algorithmic flops, SURVEY 8(d) per-entry count
+                                             (4K + 8 / 2K + 4, K = r_k r_s <= R^2 the per-entry
+                                             contraction length of the block's split)         */
   double pass1_bytes, pass2_bytes;        /* algorithmic bytes, SURVEY 8(d) per-entry count  */
   double pass1_mma_flops, pass2_mma_flops;/* dense tensor-core flops the tcgen05 pass kernels
                                              executed (3-term fp16 split, 128 x 64 tiles)     */

@@ -649,14 +649,17 @@ trd_status trd_get_profile(trd_ctx* ctx, trd_profile* out) {
   out->pass2_launches = (int64_t)c->ev_pass2.size();
   DevScalars hs;
   CUDA_TRY(c, cudaMemcpy(&hs, c->sc, sizeof(hs), cudaMemcpyDeviceToHost));
-  // algorithmic counts: pass 1 = recon + gradient (4 R^2 + 8 flops per
-  // observed entry; value 4 B + staged weight 4 B + mask bits), pass 2 = line-search dot
-  // (2 R^2 + 4 flops; weight 4 B + mask bits).  Blocks were visited cyclically, so each
-  // block's launches are n_launch / N.
+  // algorithmic counts: pass 1 = recon + gradient (4 K + 8 flops per observed
+  // entry; value 4 B + staged weight 4 B + mask bits), pass 2 = line-search dot (2 K + 4 flops;
+  // weight 4 B + mask bits), K = the per-entry contraction length of the block's GEMM form,
+  // r_k r_s <= R^2 (= R^2 with equal ranks: every BASELINE config; with unequal ranks the split
+  // needs fewer flops per entry than the full subchain's R^2, and counting R^2 would put the
+  // achieved rate above the FP32 peak).  Blocks were visited cyclically, so each block's launches
+  // are n_launch / N.
   const double per_block = c->ev_pass1.empty() ? 0.0 : (double)c->ev_pass1.size() / c->N;
   for (int k = 0; k < c->N; ++k) {
     const double n = hs.prof_nobs[k];
-    const double R2 = (double)c->plan[k].R2;
+    const double R2 = (double)std::min(c->plan[k].R2, c->plan[k].K);
     const double ws_bits = (double)c->plan[k].nnz_ws / c->cfg.world / 8.0 * per_block;
     out->pass1_entries += n;
     out->pass2_entries += n;
