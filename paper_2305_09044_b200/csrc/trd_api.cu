@@ -27,6 +27,8 @@ static const char* const kNvtxBlock[] = {"trd block 0", "trd block 1", "trd bloc
 
 using namespace trd;
 
+bool trd::g_pdl_on = true;
+
 // ---------------------------------------------------------------------------------------
 // NCCL, loaded lazily (world > 1 only) so a single-GPU context never needs it.
 // ---------------------------------------------------------------------------------------
@@ -726,6 +728,7 @@ trd_status trd_init_ex(const trd_config* cfg, const trd_shard* shard, const floa
   c->cfg.nccl_unique_id = nullptr;
   c->tl_on = getenv("TRD_TIMELINE") && atoi(getenv("TRD_TIMELINE")) != 0;
   c->fuse = !(getenv("TRD_NO_FUSE") && atoi(getenv("TRD_NO_FUSE")) != 0);
+  g_pdl_on = !(getenv("TRD_PDL") && atoi(getenv("TRD_PDL")) == 0);   // (process-wide launch mode)
   if (ex && cfg->world > 1) c->ex = *ex;
   c->N = N;
   c->stream = (cudaStream_t)stream;

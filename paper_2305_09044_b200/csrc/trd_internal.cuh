@@ -113,6 +113,28 @@ __host__ __device__ __forceinline__ int tc_scale_exp(float amax) {
   const int E = 15 - e;
   return E < -100 ? -100 : (E > 100 ? 100 : E);
 }
+// Programmatic dependent launch (PDL) of the per-block chain of small kernels: a kernel launched
+// with launch_pdl may be scheduled while its stream predecessor finishes (its launch latency hides
+// under the predecessor's tail); trd_gdc_wait(), the first statement of every such kernel, returns
+// once the predecessor grid has completed and its memory is visible (a no-op without PDL).
+__device__ __forceinline__ void trd_gdc_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+extern bool g_pdl_on;                // TRD_PDL=0 launches them as ordinary stream-ordered kernels
+template <typename... KArgs, typename... Args>
+inline void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = g_pdl_on ? 1 : 0;
+  cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+#define TRD_PDL(kern, grid, block, smem, stream, ...) ::trd::launch_pdl(kern, dim3(grid), dim3(block), (size_t)(smem), stream, __VA_ARGS__)
+
 constexpr int kMadBins0 = 2048, kMadBins1 = 2048, kMadBins2 = 1024;
 constexpr int kMadHist = kMadBins0 + 2 * kMadBins1 + 2 * kMadBins2;
 

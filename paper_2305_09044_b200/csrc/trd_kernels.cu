@@ -62,6 +62,7 @@ __device__ __forceinline__ unsigned long long sample_key(uint64_t seed, int64_t 
 __global__ void __launch_bounds__(kSamplerThreads)
 sampler_kernel(SamplerArgs sa, const DevScalars* __restrict__ sc, int32_t* __restrict__ idx,
                int64_t* __restrict__ doff) {
+  trd_gdc_wait();   // (PDL: the stream predecessor has completed, memory visible)
   using Scan = cub::BlockScan<long long, kSamplerThreads>;
   __shared__ typename Scan::TempStorage scan_tmp;
   __shared__ unsigned int hist[256];
@@ -299,6 +300,7 @@ __device__ __forceinline__ void right_digits(const PlanArgs& a, int64_t col, int
 __global__ void offsets_kernel(PlanArgs a, const int64_t* __restrict__ doff,
                                int64_t* __restrict__ row_off, int64_t* __restrict__ col_off,
                                DevScalars* __restrict__ sc) {
+  trd_gdc_wait();   // (PDL: the stream predecessor has completed, memory visible)
   // (operand scaling; sc = nullptr when the offsets run ahead on the staging stream)
   if (sc && blockIdx.x == 0 && threadIdx.x == 0) { sc->amax_a = 0u; sc->amax_b = 0u; }
   const int64_t tot = a.nrows + a.ncols;
@@ -366,6 +368,7 @@ __device__ __forceinline__ void vecmat(float* v, const float* __restrict__ Zs, i
 template <int RM>
 __global__ void mid_kernel(PlanArgs a, const int32_t* __restrict__ idx, const float* __restrict__ Z,
                            float* __restrict__ mid) {
+  trd_gdc_wait();   // (PDL: the stream predecessor has completed, memory visible)
   const int64_t tot = a.nL * a.rk1;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tot;
        t += (int64_t)gridDim.x * blockDim.x) {
@@ -418,6 +421,7 @@ __device__ __forceinline__ void block_amax(float v, unsigned int* dst) {
 template <int RM>
 __global__ void rgt_kernel(PlanArgs a, const int32_t* __restrict__ idx, const float* __restrict__ Z,
                            float* __restrict__ rgtT, DevScalars* __restrict__ sc) {
+  trd_gdc_wait();   // (PDL: the stream predecessor has completed, memory visible)
   float amax = 0.f;
   const int64_t tot = a.ncols * a.rs;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tot;
@@ -1040,6 +1044,7 @@ __global__ void reduce_den_kernel(const double* __restrict__ denpart, int64_t n,
 // one warp per entry of Q_k: lane l sums the slices i = l, l + 32, .. in order, then a fixed
 // butterfly over the lanes (deterministic; Z_k stays in L1 / L2)
 __global__ void q_kernel(const float* __restrict__ Zk, int64_t Ik, int r0, int r1, double* __restrict__ Qk) {
+  trd_gdc_wait();   // (PDL: the stream predecessor has completed, memory visible)
   const int n0 = r0 * r0, n1 = r1 * r1, lane = threadIdx.x & 31;
   const int64_t stride = (int64_t)r0 * r1;
   for (int64_t t = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; t < (int64_t)n0 * n1;
@@ -1525,6 +1530,7 @@ __global__ void __launch_bounds__(256) gj3_solve_kernel(const double* __restrict
 // num partial per row = <d(i), h(i)>
 __global__ void h_kernel(const double* __restrict__ dvec, const double* __restrict__ M, int R2,
                          double* __restrict__ h, double* __restrict__ numpart, const DevScalars* __restrict__ sc) {
+  trd_gdc_wait();   // (PDL: the stream predecessor has completed, memory visible)
   __shared__ double drow[kBigR2];       // (R^2 <= kBigR2; larger blocks: big_h)
   __shared__ double urow[kBigR2];
   __shared__ double red[256];
@@ -1628,6 +1634,7 @@ __global__ void __launch_bounds__(256) block_tail_kernel(const double* __restric
                                                          int64_t Ik, int R2, DevScalars* sc, DevStats* stats, int k,
                                                          double step, float* __restrict__ Zk,
                                                          const double* __restrict__ h, int rk, int rk1) {
+  trd_gdc_wait();   // (PDL: the stream predecessor has completed, memory visible)
   __shared__ double acc[2][256];
   __shared__ double nd_s[2];
   const int t = threadIdx.x;
@@ -2058,13 +2065,13 @@ void launch_sampler(Context& c, const BlockPlan& bp, cudaStream_t s) {
     c.launches++;
     return;
   }
-  sampler_kernel<<<c.N, kSamplerThreads, 0, s>>>(sa, c.sc, c.idx, c.doff);
+  TRD_PDL(sampler_kernel, c.N, kSamplerThreads, 0, s, sa, c.sc, c.idx, c.doff);
   c.launches++;
 }
 
 void launch_offsets(Context& c, const BlockPlan& bp, cudaStream_t s, bool reset_amax) {
   PlanArgs a = make_plan_args(c, bp);
-  offsets_kernel<<<grid_for(bp.nrows + bp.ncols), 256, 0, s>>>(a, c.doff, c.row_off, c.col_off,
+  TRD_PDL(offsets_kernel, grid_for(bp.nrows + bp.ncols), 256, 0, s, a, c.doff, c.row_off, c.col_off,
                                                               reset_amax ? c.sc : nullptr);
   c.launches++;
 }
@@ -2078,14 +2085,14 @@ void launch_plan(Context& c, const BlockPlan& bp, cudaStream_t s, bool offsets) 
     cudaMemsetAsync(&c.sc->amax_a, 0, 2 * sizeof(unsigned int), s);
   }
   if (bp.p > 0) {
-    if (c.rbucket <= 16) mid_kernel<16><<<grid_for(bp.nL * bp.rk1), 256, 0, s>>>(a, c.idx, c.Z, c.mid);
-    else if (c.rbucket <= 32) mid_kernel<32><<<grid_for(bp.nL * bp.rk1), 256, 0, s>>>(a, c.idx, c.Z, c.mid);
-    else mid_kernel<128><<<grid_for(bp.nL * bp.rk1), 128, 0, s>>>(a, c.idx, c.Z, c.mid);
+    if (c.rbucket <= 16) TRD_PDL(mid_kernel<16>, grid_for(bp.nL * bp.rk1), 256, 0, s, a, c.idx, c.Z, c.mid);
+    else if (c.rbucket <= 32) TRD_PDL(mid_kernel<32>, grid_for(bp.nL * bp.rk1), 256, 0, s, a, c.idx, c.Z, c.mid);
+    else TRD_PDL(mid_kernel<128>, grid_for(bp.nL * bp.rk1), 128, 0, s, a, c.idx, c.Z, c.mid);
     c.launches++;
   }
-  if (c.rbucket <= 16) rgt_kernel<16><<<grid_for(bp.ncols * bp.rs), 256, 0, s>>>(a, c.idx, c.Z, c.rgtT, c.sc);
-  else if (c.rbucket <= 32) rgt_kernel<32><<<grid_for(bp.ncols * bp.rs), 256, 0, s>>>(a, c.idx, c.Z, c.rgtT, c.sc);
-  else rgt_kernel<128><<<grid_for(bp.ncols * bp.rs), 128, 0, s>>>(a, c.idx, c.Z, c.rgtT, c.sc);
+  if (c.rbucket <= 16) TRD_PDL(rgt_kernel<16>, grid_for(bp.ncols * bp.rs), 256, 0, s, a, c.idx, c.Z, c.rgtT, c.sc);
+  else if (c.rbucket <= 32) TRD_PDL(rgt_kernel<32>, grid_for(bp.ncols * bp.rs), 256, 0, s, a, c.idx, c.Z, c.rgtT, c.sc);
+  else TRD_PDL(rgt_kernel<128>, grid_for(bp.ncols * bp.rs), 128, 0, s, a, c.idx, c.Z, c.rgtT, c.sc);
   c.launches++;
 }
 
@@ -2161,7 +2168,7 @@ void launch_q(Context& c, int k, cudaStream_t s) {
     big_q(c, k, s);                         // (a failure sets the context's sticky status)
     return;
   }
-  q_kernel<<<grid_for((int64_t)r0 * r0 * r1 * r1 * 32), 256, 0, s>>>(c.Z + c.zoff[k], c.dims[k], r0, r1,
+  TRD_PDL(q_kernel, grid_for((int64_t)r0 * r0 * r1 * r1 * 32), 256, 0, s, c.Z + c.zoff[k], c.dims[k], r0, r1,
                                                                       c.Q + c.qoff[k]);
   c.launches++;
 }
@@ -2307,7 +2314,7 @@ void launch_h(Context& c, const BlockPlan& bp, cudaStream_t s) {
     return;
   }
   const int64_t Ik = c.dims[bp.k];                     // h of every i_k (replicated update)
-  h_kernel<<<(unsigned)Ik, 256, 0, s>>>(c.dvec, c.Mop, bp.R2, c.h, c.numpart, c.sc);
+  TRD_PDL(h_kernel, (unsigned)Ik, 256, 0, s, c.dvec, c.Mop, bp.R2, c.h, c.numpart, c.sc);
   c.launches++;
 }
 
@@ -2317,7 +2324,7 @@ void launch_block_tail(Context& c, const BlockPlan& bp, cudaStream_t s) {
   const int64_t nden = bp.use_tc ? (int64_t)bp.tc_grid : bp.rows ? (int64_t)bp.rows_grid : (bp.nrows / bp.nL) * ncta;
   const int64_t tot = Ik * bp.rk * bp.rk1;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((tot + 255) / 256, (int64_t)c.num_sm));
-  block_tail_kernel<<<grid, 256, 0, s>>>(c.denpart, nden, c.numpart, Ik, c.red_ws, c.dvec, Ik, bp.R2, c.sc, c.stats, bp.k,
+  TRD_PDL(block_tail_kernel, grid, 256, 0, s, c.denpart, nden, c.numpart, Ik, c.red_ws, c.dvec, Ik, bp.R2, c.sc, c.stats, bp.k,
                                        c.cfg.step, c.Z + c.zoff[bp.k], c.h, bp.rk, bp.rk1);
   c.launches++;
 }

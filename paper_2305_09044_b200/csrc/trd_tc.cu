@@ -237,6 +237,7 @@ struct LftArgs {
 // (gmem = 1: ranks too large for the shared-memory stage; X and Mid are read from global memory)
 __global__ void __launch_bounds__(256) tc_lft_pack_kernel(LftArgs a, int pass2, int64_t nrows_pad,
                                                           __half* __restrict__ dst, int gmem) {
+  trd_gdc_wait();   // (PDL: the stream predecessor has completed, memory visible)
   extern __shared__ float lsm[];
   const int XS = a.rk * a.rk1, MS = a.rk1 * a.rs;
   const int XP = XS | 1, MP = MS | 1;                       // odd strides
@@ -335,6 +336,7 @@ __global__ void __launch_bounds__(256) tc_lft_pack_kernel(LftArgs a, int pass2, 
 // lft_kernel (fmaf over b ascending).
 __global__ void __launch_bounds__(256) tc_lft_pack_hw_kernel(LftArgs a, int pass2, int64_t nrows_pad,
                                                              __half* __restrict__ dst) {
+  trd_gdc_wait();   // (PDL: the stream predecessor has completed, memory visible)
   const int lane = threadIdx.x & 31, sub = lane & 15;
   const unsigned hmask = 0xFFFFu << (lane & 16);
   const int XS = a.rk * a.rk1, MS = a.rk1 * a.rs;
@@ -402,6 +404,7 @@ __global__ void __launch_bounds__(256) tc_lft_pack_hw_kernel(LftArgs a, int pass
 constexpr int kPackJ = 32;
 __global__ void __launch_bounds__(256) tc_lft_pack_tile_kernel(LftArgs a, int pass2, int64_t nrows_pad,
                                                                __half* __restrict__ dst) {
+  trd_gdc_wait();   // (PDL: the stream predecessor has completed, memory visible)
   extern __shared__ float psm[];
   const int rk = a.rk, rk1 = a.rk1, rs = a.rs, K = a.K, KP = a.KP, XS = rk1 + 1, MS = rk1 * rs, LS = K + 1;
   float* Xs = psm;                              // [rk][rk1 + 1]
@@ -457,6 +460,7 @@ __global__ void __launch_bounds__(256) tc_lft_pack_tile_kernel(LftArgs a, int pa
 template <int RK, int RK1, int RS>
 __global__ void __launch_bounds__(128, 4) tc_lft_pack_rb_kernel(LftArgs a, int pass2, int64_t nrows_pad,
                                                              __half* __restrict__ dst) {
+  trd_gdc_wait();   // (PDL: the stream predecessor has completed, memory visible)
   constexpr int K = RK * RS;
   constexpr int KP = (K + 15) / 16 * 16;
   constexpr int ROWB = 2 * KP * 2;                 // bytes of one packed row (hi | lo)
@@ -557,6 +561,7 @@ __device__ __forceinline__ int64_t cm_offset(int r, int kap, int HK) {
 __global__ void tc_pack_cols_kernel(const float* __restrict__ rgtT, int64_t ncols, int K, int KP,
                                     int64_t ntiles, __half* __restrict__ dst, __half* __restrict__ dst2,
                                     const DevScalars* __restrict__ sc) {
+  trd_gdc_wait();   // (PDL: the stream predecessor has completed, memory visible)
   const int HK = KP / 8;
   const float sc2 = ldexpf(1.f, tc_scale_exp(__uint_as_float(sc->amax_b)));   // B scaling
   const int64_t tot = ntiles * TC_NT * KP;
@@ -766,6 +771,7 @@ __device__ __forceinline__ uint32_t warp_col_bits(const StageArgs& s, const Warp
 }
 
 __global__ void __launch_bounds__(128) stage_bits_kernel(StageArgs s) {
+  trd_gdc_wait();   // (PDL: the stream predecessor has completed, memory visible)
   if (s.gen_cur && *s.gen_layout == *s.gen_cur) return;   // layout current (same mask): nothing to do
   __shared__ int64_t sco[TC_NT];
   __shared__ uint32_t sstart[2];
@@ -882,6 +888,7 @@ __device__ __forceinline__ float stage_word(const StageArgs& s, int64_t vi) {
 }
 
 __global__ void __launch_bounds__(128) stage_vals_kernel(StageArgs s) {
+  trd_gdc_wait();   // (PDL: the stream predecessor has completed, memory visible)
   if (s.gen_cur && *s.gen_layout == *s.gen_cur) return;   // layout current: gather_vals_kernel re-reads
   __shared__ int64_t sco[TC_NT];
   __shared__ uint32_t sstart[2];
@@ -1197,6 +1204,7 @@ __global__ void __launch_bounds__(1024) tc_reduce_d_kernel(
     const float* __restrict__ contrib, const float* __restrict__ mid, int nsplit, int64_t nrows_pad, int64_t nL,
     int64_t Ik, int rowmode, int KP, int R2, int rk, int rs, int p, int64_t jl_chunk, double* __restrict__ dpart,
     int rd_rows) {
+  trd_gdc_wait();   // (PDL: the stream predecessor has completed, memory visible)
   extern __shared__ float rsm[];
   const int KPp = KP + 4, MS = (R2 / rk) * rs;               // Mid(jl) is r_{k+1} x r_s
   float* Dt = rsm;                                           // [rd_rows][KP + 4] (16-B rows)
@@ -1266,6 +1274,7 @@ __global__ void __launch_bounds__(128) tc_reduce_d_rb_kernel(const float* __rest
                                                              const float* __restrict__ mid, int nsplit,
                                                              int64_t nrows_pad, int64_t nL, int64_t Ik, int rowmode,
                                                              int64_t jl_chunk, double* __restrict__ dpart) {
+  trd_gdc_wait();   // (PDL: the stream predecessor has completed, memory visible)
   constexpr int KP = RK * RS, MS = RK1 * RS, R2 = RK * RK1;
   static_assert(KP % 16 == 0 && MS % 4 == 0, "vector loads");
   __shared__ float red[128][R2 + 1];
@@ -1410,6 +1419,7 @@ __global__ void tc_reduce_final_kernel(const double* __restrict__ dpart, int64_t
                                        const double* __restrict__ spart, int64_t nparts,
                                        double* __restrict__ dvec, DevScalars* sc, int kblk, int64_t ik0,
                                        int64_t Ik_tot) {
+  trd_gdc_wait();   // (PDL: the stream predecessor has completed, memory visible)
   const int64_t ik = blockIdx.x;
   if (ik < Ik) {
     for (int o = threadIdx.x; o < R2; o += blockDim.x) {
@@ -1460,7 +1470,7 @@ void launch_tc_lft(Context& c, const BlockPlan& bp, bool pass2, cudaStream_t s) 
   const int64_t pad = bp.n_row_tiles * TC_M;
   if (bp.p > 0 && bp.rk == 8 && bp.rk1 == 8 && bp.rs == 8) {
     const int grid = (int)std::min<int64_t>((pad + 127) / 128, (int64_t)c.num_sm * 16);
-    tc_lft_pack_rb_kernel<8, 8, 8><<<grid, 128, 0, s>>>(a, pass2 ? 1 : 0, pad, pass2 ? c.lfthHL : c.lftHL);
+    TRD_PDL((tc_lft_pack_rb_kernel<8, 8, 8>), grid, 128, 0, s, a, pass2 ? 1 : 0, pad, pass2 ? c.lfthHL : c.lftHL);
     c.launches++;
     return;
   }
@@ -1469,14 +1479,14 @@ void launch_tc_lft(Context& c, const BlockPlan& bp, bool pass2, cudaStream_t s) 
     if (smem <= 200 * 1024) {
       cudaFuncSetAttribute(tc_lft_pack_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       const dim3 grid((unsigned)a.Ik, (unsigned)((bp.nL + kPackJ - 1) / kPackJ));
-      tc_lft_pack_tile_kernel<<<grid, 256, smem, s>>>(a, pass2 ? 1 : 0, pad, pass2 ? c.lfthHL : c.lftHL);
+      TRD_PDL(tc_lft_pack_tile_kernel, grid, 256, smem, s, a, pass2 ? 1 : 0, pad, pass2 ? c.lfthHL : c.lftHL);
       c.launches++;
       return;
     }
   }
   if (getenv("TRD_LFT_TILE") == nullptr) {        // half-warp per row (TRD_LFT_TILE: the tile kernel, A/B)
     const int grid = (int)std::min<int64_t>((pad * 16 + 255) / 256, (int64_t)c.num_sm * 16);
-    tc_lft_pack_hw_kernel<<<grid, 256, 0, s>>>(a, pass2 ? 1 : 0, pad, pass2 ? c.lfthHL : c.lftHL);
+    TRD_PDL(tc_lft_pack_hw_kernel, grid, 256, 0, s, a, pass2 ? 1 : 0, pad, pass2 ? c.lfthHL : c.lftHL);
     c.launches++;
     return;
   }
@@ -1485,12 +1495,12 @@ void launch_tc_lft(Context& c, const BlockPlan& bp, bool pass2, cudaStream_t s) 
   if (gmem) smem = 0;
   else cudaFuncSetAttribute(tc_lft_pack_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int grid = (int)std::min<int64_t>(bp.n_row_tiles, (int64_t)c.num_sm * 8);
-  tc_lft_pack_kernel<<<grid, 256, smem, s>>>(a, pass2 ? 1 : 0, pad, pass2 ? c.lfthHL : c.lftHL, gmem);
+  TRD_PDL(tc_lft_pack_kernel, grid, 256, smem, s, a, pass2 ? 1 : 0, pad, pass2 ? c.lfthHL : c.lftHL, gmem);
   c.launches++;
 }
 
 void launch_tc_pack_cols(Context& c, const BlockPlan& bp, cudaStream_t s) {
-  tc_pack_cols_kernel<<<tc_grid(bp.n_col_tiles * TC_NT * bp.KP), 256, 0, s>>>(c.rgtT, bp.ncols, bp.K, bp.KP,
+  TRD_PDL(tc_pack_cols_kernel, tc_grid(bp.n_col_tiles * TC_NT * bp.KP), 256, 0, s, c.rgtT, bp.ncols, bp.K, bp.KP,
                                                                                 bp.n_col_tiles, c.rgtHL, c.rgtHL2, c.sc);
   c.launches++;
 }
@@ -1547,14 +1557,14 @@ void launch_tc_stage(Context& c, const BlockPlan& bp, TcStage& st, cudaStream_t 
   const int gb = (int)std::min<int64_t>(a.n_tiles, (int64_t)c.num_sm * occ_bits);
   const int gv = (int)std::min<int64_t>(a.n_tiles, (int64_t)c.num_sm * occ_vals);
   if (phase != 2) {
-    stage_bits_kernel<<<gb, TC_M, 0, s>>>(a);
+    TRD_PDL(stage_bits_kernel, gb, TC_M, 0, s, a);
     // tbase = exclusive prefix of tcount (tcount[n_tiles] = 0: tbase[n_tiles] = total); out of
     // place, so a skipped stage_bits leaves the same prefix
     cub::DeviceScan::ExclusiveSum(st.scan_tmp, st.scan_tmp_bytes, st.tcount, st.tbase, (int)a.n_tiles + 1, s);
     c.launches += 2;
   }
   if (phase == 1) return;
-  stage_vals_kernel<<<gv, TC_M, 0, s>>>(a);
+  TRD_PDL(stage_vals_kernel, gv, TC_M, 0, s, a);
   c.launches += 1;
   if (cached) {
     layout_gen_kernel<<<1, 32, 0, s>>>(&c.sc->mask_gen, &c.sc->layout_gen[bp.k]);
@@ -1708,7 +1718,7 @@ void launch_reduce_d_contrib(Context& c, const BlockPlan& bp, int nsplit, int64_
                              cudaStream_t s) {
   const int64_t Ik = bp.nrows / bp.nL;
   if (bp.R2 == 0) {                          // statistics only (the sigma_0 pass)
-    tc_reduce_final_kernel<<<1, 128, 0, s>>>(c.dpart, 0, 0, 0, c.spart, nparts, c.dvec, nullptr, bp.k, 0, 0);
+    TRD_PDL(tc_reduce_final_kernel, 1, 128, 0, s, c.dpart, 0, 0, 0, c.spart, nparts, c.dvec, nullptr, bp.k, 0, 0);
     c.launches++;
     return;
   }
@@ -1735,7 +1745,7 @@ void launch_reduce_d_contrib(Context& c, const BlockPlan& bp, int nsplit, int64_
         c.contrib, c.mid, nsplit, nrows_pad, bp.nL, Ik, bp.rowmode, bp.KP, bp.R2, bp.rk, bp.rk1, bp.rs, bp.p,
         bp.tc_jl_chunk, c.dpart);
   }
-  tc_reduce_final_kernel<<<(unsigned)(Ik + 1), 128, 0, s>>>(c.dpart, bp.tc_jc, Ik, bp.R2, c.spart, nparts,
+  TRD_PDL(tc_reduce_final_kernel, (unsigned)(Ik + 1), 128, 0, s, c.dpart, bp.tc_jc, Ik, bp.R2, c.spart, nparts,
                                                             c.dvec, c.sc, bp.k, bp.ik0, c.dims[bp.k]);
   c.launches += 2;
 }
@@ -1748,9 +1758,9 @@ void launch_tc_reduce_d(Context& c, const BlockPlan& bp, cudaStream_t s) {
   }
   if (Ik < c.dims[bp.k]) cudaMemsetAsync(c.dvec, 0, (size_t)(c.dims[bp.k] * bp.R2) * sizeof(double), s);
   if (bp.p > 0 && bp.rk == 8 && bp.rk1 == 8 && bp.rs == 8 && bp.KP == 64) {
-    tc_reduce_d_rb_kernel<8, 8, 8><<<dim3((unsigned)Ik, (unsigned)bp.tc_jc), 128, 0, s>>>(
+    TRD_PDL((tc_reduce_d_rb_kernel<8, 8, 8>), dim3((unsigned)Ik, (unsigned)bp.tc_jc), 128, 0, s, 
         c.contrib, c.mid, bp.tc_nsplit, bp.n_row_tiles * TC_M, bp.nL, Ik, bp.rowmode, bp.tc_jl_chunk, c.dpart);
-    tc_reduce_final_kernel<<<(unsigned)(Ik + 1), 128, 0, s>>>(c.dpart, bp.tc_jc, Ik, bp.R2, c.spart, bp.tc_grid1,
+    TRD_PDL(tc_reduce_final_kernel, (unsigned)(Ik + 1), 128, 0, s, c.dpart, bp.tc_jc, Ik, bp.R2, c.spart, bp.tc_grid1,
                                                               c.dvec, c.sc, bp.k, bp.ik0, c.dims[bp.k]);
     c.launches += 2;
     return;
@@ -1760,10 +1770,10 @@ void launch_tc_reduce_d(Context& c, const BlockPlan& bp, cudaStream_t s) {
   const int rd_rows = (int)std::max<size_t>(1, std::min<size_t>(RD_ROWS, (200 * 1024) / per_row));
   const size_t smem = (size_t)rd_rows * per_row;
   cudaFuncSetAttribute(tc_reduce_d_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  tc_reduce_d_kernel<<<dim3((unsigned)Ik, (unsigned)bp.tc_jc), threads, smem, s>>>(
+  TRD_PDL(tc_reduce_d_kernel, dim3((unsigned)Ik, (unsigned)bp.tc_jc), threads, smem, s, 
       c.contrib, c.mid, bp.tc_nsplit, bp.n_row_tiles * TC_M, bp.nL, Ik, bp.rowmode, bp.KP, bp.R2, bp.rk,
       bp.rs, bp.p, bp.tc_jl_chunk, c.dpart, rd_rows);
-  tc_reduce_final_kernel<<<(unsigned)(Ik + 1), 128, 0, s>>>(c.dpart, bp.tc_jc, Ik, bp.R2, c.spart, bp.tc_grid1,
+  TRD_PDL(tc_reduce_final_kernel, (unsigned)(Ik + 1), 128, 0, s, c.dpart, bp.tc_jc, Ik, bp.R2, c.spart, bp.tc_grid1,
                                                             c.dvec, c.sc, bp.k, bp.ik0, c.dims[bp.k]);
   c.launches += 2;
 }
