@@ -459,6 +459,88 @@ __global__ void rgt_kernel(PlanArgs a, const int32_t* __restrict__ idx, const fl
   block_amax(amax, &sc->amax_b);     // (B operand scaling of the tensor-core passes)
 }
 
+// Warp-per-index chain products (ranks <= 32): one warp forms the whole r_first x r_last product
+// Z_{m_0}(i_0) Z_{m_1}(i_1) .. of one column (Rgt) or left index (Mid) in shared memory, lane-parallel
+// over the output entries, instead of one thread per output row walking the chain through register
+// vectors (the thread-per-row kernels above: ~15 us per C4 block for a few MFLOP, latency bound,
+// with one CTA per 32 rows).  Same fp32 arithmetic and order: the first factor is the slice itself
+// (the thread kernels' one-hot start multiplies by exact 0 / 1), every further product is an fmaf
+// sum over the inner index ascending from 0.  Returns the product's column count; A holds it.
+template <int RM>
+__device__ __forceinline__ int warp_chain(const PlanArgs& a, const int32_t* __restrict__ idx, const float* __restrict__ Z,
+                                          const int* modes, const int64_t* offs, const int64_t* dq, int nm, int rows,
+                                          float*& A, float*& Bn, int lane) {
+  int rc;
+  if (nm == 0) {                                   // empty chain: the identity (rows x rows)
+    rc = rows;
+    for (int o = lane; o < rows * rc; o += 32) A[o] = (o / rc == o % rc) ? 1.f : 0.f;
+  } else {
+    const int m = modes[0];
+    rc = a.rank_of[m + 1];
+    const float* zs = Z + a.zoff[m] + (int64_t)idx[offs[0] + dq[0]] * a.rank_of[m] * rc;
+    for (int o = lane; o < rows * rc; o += 32) A[o] = __ldg(zs + o);
+  }
+  __syncwarp();
+  for (int q = 1; q < nm; ++q) {
+    const int m = modes[q];
+    const int rin = rc, rout = a.rank_of[m + 1];
+    const float* zs = Z + a.zoff[m] + (int64_t)idx[offs[q] + dq[q]] * a.rank_of[m] * rout;
+    for (int o = lane; o < rows * rout; o += 32) {
+      const int r = o / rout, c = o - r * rout;
+      float acc = 0.f;
+      for (int b = 0; b < rin; ++b) acc = fmaf(A[r * rin + b], __ldg(zs + b * rout + c), acc);
+      Bn[o] = acc;
+    }
+    __syncwarp();
+    float* t = A; A = Bn; Bn = t;
+    rc = rout;
+  }
+  return rc;
+}
+
+// Rgt(col)[cc][aa] (r_s x r_k) -> RgtT[(aa + r_k cc) ncols + col], warp per column
+template <int RM, int WPC>
+__global__ void __launch_bounds__(32 * WPC) rgt_warp_kernel(PlanArgs a, const int32_t* __restrict__ idx, const float* __restrict__ Z,
+                                                          float* __restrict__ rgtT, DevScalars* __restrict__ sc) {
+  trd_gdc_wait();   // (PDL: the stream predecessor has completed, memory visible)
+  __shared__ float buf[WPC][2][RM * RM];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  float amax = 0.f;
+  for (int64_t col = (int64_t)blockIdx.x * WPC + warp; col < a.ncols; col += (int64_t)gridDim.x * WPC) {
+    int64_t dq[kMaxN];
+    right_digits(a, col, dq);
+    float* A = buf[warp][0];
+    float* Bn = buf[warp][1];
+    const int rc = warp_chain<RM>(a, idx, Z, a.right, a.offR, dq, a.nright, a.rs, A, Bn, lane);
+    for (int o = lane; o < a.rs * rc; o += 32) {
+      const int cc = o / rc, aa = o - cc * rc;
+      const float v = A[o];
+      rgtT[(int64_t)(aa + a.rk * cc) * a.ncols + col] = v;
+      amax = fmaxf(amax, fabsf(v));
+    }
+    __syncwarp();                                  // (the next column reuses the buffers)
+  }
+  block_amax(amax, &sc->amax_b);     // (B operand scaling of the tensor-core passes)
+}
+
+// Mid(jl)[b][c] (r_{k+1} x r_s) -> mid[(jl r_{k+1} + b) r_s + c], warp per left index
+template <int RM, int WPC>
+__global__ void __launch_bounds__(32 * WPC) mid_warp_kernel(PlanArgs a, const int32_t* __restrict__ idx, const float* __restrict__ Z,
+                                                          float* __restrict__ mid) {
+  trd_gdc_wait();   // (PDL: the stream predecessor has completed, memory visible)
+  __shared__ float buf[WPC][2][RM * RM];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int64_t jl = (int64_t)blockIdx.x * WPC + warp; jl < a.nL; jl += (int64_t)gridDim.x * WPC) {
+    int64_t dq[kMaxN];
+    left_digits(a, jl, dq);
+    float* A = buf[warp][0];
+    float* Bn = buf[warp][1];
+    const int rc = warp_chain<RM>(a, idx, Z, a.left, a.offL, dq, a.nleft, a.rk1, A, Bn, lane);
+    for (int o = lane; o < a.rk1 * rc; o += 32) mid[jl * a.rk1 * a.rs + o] = A[o];
+    __syncwarp();
+  }
+}
+
 // Lft(row)[a + r_k c] = (X_k(i_k) Mid(j_L))[a][c] where X_k is the core slice (pass 1) or
 // the folded scaled gradient H(i_k)[a][b] = h[i_k][a + r_k b] (pass 2).  Thread per (row, a).
 template <int RM>
@@ -2078,6 +2160,8 @@ void launch_offsets(Context& c, const BlockPlan& bp, cudaStream_t s, bool reset_
 
 void launch_plan(Context& c, const BlockPlan& bp, cudaStream_t s, bool offsets) {
   PlanArgs a = make_plan_args(c, bp);
+  // warp-per-index chain products (TRD_CHAIN_THREAD=1: the thread-per-row kernels, A/B runs)
+  const bool warp_chains = !(getenv("TRD_CHAIN_THREAD") && atoi(getenv("TRD_CHAIN_THREAD")) != 0);
   if (offsets) {
     launch_offsets(c, bp, s, true);
   } else {
@@ -2085,12 +2169,20 @@ void launch_plan(Context& c, const BlockPlan& bp, cudaStream_t s, bool offsets) 
     cudaMemsetAsync(&c.sc->amax_a, 0, 2 * sizeof(unsigned int), s);
   }
   if (bp.p > 0) {
-    if (c.rbucket <= 16) TRD_PDL(mid_kernel<16>, grid_for(bp.nL * bp.rk1), 256, 0, s, a, c.idx, c.Z, c.mid);
+    if (c.rbucket <= 16 && warp_chains)
+      TRD_PDL((mid_warp_kernel<16, 8>), grid_for(bp.nL * 32), 256, 0, s, a, c.idx, c.Z, c.mid);
+    else if (c.rbucket <= 32 && warp_chains)
+      TRD_PDL((mid_warp_kernel<32, 4>), grid_for(bp.nL * 32, 128), 128, 0, s, a, c.idx, c.Z, c.mid);
+    else if (c.rbucket <= 16) TRD_PDL(mid_kernel<16>, grid_for(bp.nL * bp.rk1), 256, 0, s, a, c.idx, c.Z, c.mid);
     else if (c.rbucket <= 32) TRD_PDL(mid_kernel<32>, grid_for(bp.nL * bp.rk1), 256, 0, s, a, c.idx, c.Z, c.mid);
     else TRD_PDL(mid_kernel<128>, grid_for(bp.nL * bp.rk1), 128, 0, s, a, c.idx, c.Z, c.mid);
     c.launches++;
   }
-  if (c.rbucket <= 16) TRD_PDL(rgt_kernel<16>, grid_for(bp.ncols * bp.rs), 256, 0, s, a, c.idx, c.Z, c.rgtT, c.sc);
+  if (c.rbucket <= 16 && warp_chains)
+    TRD_PDL((rgt_warp_kernel<16, 8>), grid_for(bp.ncols * 32), 256, 0, s, a, c.idx, c.Z, c.rgtT, c.sc);
+  else if (c.rbucket <= 32 && warp_chains)
+    TRD_PDL((rgt_warp_kernel<32, 4>), grid_for(bp.ncols * 32, 128), 128, 0, s, a, c.idx, c.Z, c.rgtT, c.sc);
+  else if (c.rbucket <= 16) TRD_PDL(rgt_kernel<16>, grid_for(bp.ncols * bp.rs), 256, 0, s, a, c.idx, c.Z, c.rgtT, c.sc);
   else if (c.rbucket <= 32) TRD_PDL(rgt_kernel<32>, grid_for(bp.ncols * bp.rs), 256, 0, s, a, c.idx, c.Z, c.rgtT, c.sc);
   else TRD_PDL(rgt_kernel<128>, grid_for(bp.ncols * bp.rs), 128, 0, s, a, c.idx, c.Z, c.rgtT, c.sc);
   c.launches++;
