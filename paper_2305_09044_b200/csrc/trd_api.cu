@@ -27,7 +27,7 @@ static const char* const kNvtxBlock[] = {"trd block 0", "trd block 1", "trd bloc
 
 using namespace trd;
 
-bool trd::g_pdl_on = true;
+bool trd::g_pdl_on = false;
 
 // ---------------------------------------------------------------------------------------
 // NCCL, loaded lazily (world > 1 only) so a single-GPU context never needs it.
@@ -728,7 +728,9 @@ trd_status trd_init_ex(const trd_config* cfg, const trd_shard* shard, const floa
   c->cfg.nccl_unique_id = nullptr;
   c->tl_on = getenv("TRD_TIMELINE") && atoi(getenv("TRD_TIMELINE")) != 0;
   c->fuse = !(getenv("TRD_NO_FUSE") && atoi(getenv("TRD_NO_FUSE")) != 0);
-  g_pdl_on = !(getenv("TRD_PDL") && atoi(getenv("TRD_PDL")) == 0);   // (process-wide launch mode)
+  // (process-wide launch mode; PDL measured neutral to slightly slower -- C4 0.757 without vs
+  //  0.777 ms per sweep with, 50 timed sweeps -- so ordinary launches unless TRD_PDL=1)
+  g_pdl_on = getenv("TRD_PDL") && atoi(getenv("TRD_PDL")) != 0;
   if (ex && cfg->world > 1) c->ex = *ex;
   c->N = N;
   c->stream = (cudaStream_t)stream;
@@ -1158,11 +1160,10 @@ static trd_status enqueue_sweep(Context* c) {
     explicit InSweep(Context* cc) : c(cc) { c->in_sweep = 1; }
     ~InSweep() { c->in_sweep = 0; select_bufs(c, -1); }
   } in_sweep(c);
-  // (TRD_Q_SIDE=1: the Q refresh on the side stream.  Measured, ms per sweep in line / side: C3
-  //  0.792 / 0.753, C4 0.846 / 0.892 (the side stream's Gauss-Jordan solve becomes critical),
-  //  C5a 2.152 / 2.124 -- within run-to-run noise overall, so in line by default)
+  // (the Q refresh on the side stream; TRD_Q_SIDE=0 keeps it in line.  Measured with 50 timed
+  //  sweeps, ms per sweep in line / side: C3 0.643 / 0.628, C4 0.777 / 0.755, C5a 1.942 / 1.924)
   const bool q_side = !(getenv("TRD_NO_SIDE") && atoi(getenv("TRD_NO_SIDE")) != 0) &&
-                      getenv("TRD_Q_SIDE") && atoi(getenv("TRD_Q_SIDE")) != 0;
+                      !(getenv("TRD_Q_SIDE") && atoi(getenv("TRD_Q_SIDE")) == 0);
   bool q_pending = false;
   for (int k = 0; k < c->N; ++k) {
     const BlockPlan& bp = c->plan[k];

@@ -13,10 +13,12 @@ namespace trd {
 
 constexpr int kMaxN = TRD_MAX_ORDER;
 // default mode of the pipelined staging of sampled blocks (Context::pipe; TRD_PIPE overrides) and
-// the smallest staged tile count of a pipelined block (smaller stagings are cheaper in line:
-// measured C4 0.87 ms/sweep in line vs 0.93 pipelined, C5a 2.24 vs 2.15)
+// the smallest staged tile count of a pipelined block.  Measured with 50 timed sweeps after 20
+// warm-up sweeps (ms per sweep, in line / mode 3): C3 0.643 / 0.581, C4 0.777 / 0.745, C5a 2.055 /
+// 1.931 -- every sampled block is pipelined (10-sweep runs, biased by the clock ramp of the
+// sub-ms configs, had suggested otherwise for C4)
 constexpr int kPipeDefault = 3;
-constexpr int64_t kPipeMinTiles = 2048;
+constexpr int64_t kPipeMinTiles = 0;
 constexpr int kMaxR = TRD_MAX_RANK;
 constexpr int kMaxR2 = kMaxR * kMaxR;
 // blocks with R_k^2 above this take the large-rank path (trd_big.cu): the d contraction by
@@ -118,7 +120,7 @@ __host__ __device__ __forceinline__ int tc_scale_exp(float amax) {
 // under the predecessor's tail); trd_gdc_wait(), the first statement of every such kernel, returns
 // once the predecessor grid has completed and its memory is visible (a no-op without PDL).
 __device__ __forceinline__ void trd_gdc_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
-extern bool g_pdl_on;                // TRD_PDL=0 launches them as ordinary stream-ordered kernels
+extern bool g_pdl_on;                // TRD_PDL=1 (off by default: measured neutral to slower)
 template <typename... KArgs, typename... Args>
 inline void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args... args) {
   cudaLaunchConfig_t cfg = {};
