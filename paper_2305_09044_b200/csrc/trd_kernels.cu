@@ -2341,7 +2341,9 @@ void launch_solve(Context& c, const BlockPlan& bp, cudaStream_t s, const double*
     big_factor(c, bp, s, G);
     return;
   }
-  const int solve_sel = getenv("TRD_SOLVE") ? atoi(getenv("TRD_SOLVE")) : 0;
+  // R^2 <= 48: the one-dimensional kernel (two threads per row; measured C3 -- R^2 = 30 / 100 --
+  // 0.624 vs 0.643 ms per sweep with the 2-D kernel throughout); R^2 > 48: the 2-D kernel
+  const int solve_sel = getenv("TRD_SOLVE") ? atoi(getenv("TRD_SOLVE")) : (n <= 48 ? 2 : 0);
   if (n <= 128 && solve_sel == 0) {    // 2-D register Gauss-Jordan (NU x NV blocks per thread)
     const int np = (n + 15) / 16 * 16;
     switch (np) {

@@ -1,8 +1,8 @@
 #!/bin/bash
 # round-2 closing evidence (third session): GPU suite, smoke, default bench + reference arm, every
 # config, C5b launch list, ncu --set full of the pass-1 kernel
-mkdir -p gpurun_out/fin3
-O=gpurun_out/fin3
+mkdir -p gpurun_out/fin4
+O=gpurun_out/fin4
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,memory.total --format=csv > $O/gpu_info.txt 2>&1
 lscpu | grep -E "Model name|^CPU\(s\)" >> $O/gpu_info.txt
 timeout 2400 python -m pytest tests -m gpu -q --timeout 1200 -p no:cacheprovider -rf > $O/gpu_tests.log 2>&1
@@ -11,7 +11,8 @@ timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>
 timeout 900 python bench.py > $O/bench_c5b.log 2>&1; echo "bench rc=$?"
 timeout 900 python bench.py --impl reference > $O/ref_c5b.log 2>&1; echo "ref rc=$?"
 for C in C1 C2 C3 C4 C5a C5b; do
-  timeout 300 python bench.py --config $C --steps 10 --warmup 3 --no-e2e --no-cpu-baseline > $O/cfg_$C.log 2>&1
+  S=50; W=20; [ $C = C5b ] && S=10 && W=3
+  timeout 600 python bench.py --config $C --steps $S --warmup $W --no-e2e --no-cpu-baseline > $O/cfg_$C.log 2>&1
   echo "$C rc=$? $(python scripts/show_bench.py $O/cfg_$C.log 2>/dev/null | head -1 | cut -c1-240)"
 done > $O/all_configs.txt
 timeout 600 python bench.py --config C6 --steps 5 --warmup 2 --no-cpu-baseline > $O/cfg_C6.log 2>&1
