@@ -375,8 +375,9 @@ void select_bufs(Context* c, int k) {
 
 // block k takes part in the staging pipeline: a sampled (sweep-varying) tensor-core sketch
 static bool pipelined(const Context* c, int k) {
-  return c->pipe && k >= 0 && k < c->N && c->plan[k].use_tc && !c->stage[k].invariant && !c->plan[k].explicit_cols &&
-         c->stage[k].n_tiles >= c->pipe_min_tiles;
+  if (!c->pipe || k < 0 || k >= c->N || !c->plan[k].use_tc || c->plan[k].explicit_cols) return false;
+  if (c->stage[k].invariant) return c->pipe_inv && !c->stage[k].valid;
+  return c->stage[k].n_tiles >= c->pipe_min_tiles;
 }
 
 // Enqueue part `part` of block k's staging on the staging stream after `after` (an event of the
@@ -396,6 +397,8 @@ static trd_status prestage(Context* c, int k, cudaEvent_t after, int part, int c
   }
   launch_tc_stage(*c, bp, c->stage[k], t, part);
   if (part != 1) CUDA_TRY(c, cudaEventRecord(c->ev_staged[k], t));
+  if (part != 2) c->prestaged[k] = true;
+  if (part != 1 && c->stage[k].invariant) c->stage[k].valid = true;
   select_bufs(c, cur_block);
   return check_launch(c, "prestage");
 }
@@ -468,9 +471,10 @@ trd_status block_pass1(Context* c, const BlockPlan& bp, bool pre) {
   else launch_pass1(*c, bp, 0, s);
   if (pe) prof_pair(c, 1, e0, prof_event(c));
   tl_mark(c, s, "pass 1");
-  if (pre_next(c, bp.k) && c->pipe != 2) {   // the next block's staging, behind this pass 1
-    CUDA_TRY(c, cudaEventRecord(c->ev_p1[bp.k], s));    // (pipe 1: all of it, 3: up to the prefix)
-    trd_status sp = prestage(c, bp.k + 1, c->ev_p1[bp.k], c->pipe == 1 ? 0 : 1, bp.k);
+  const bool inv_next = bp.k + 1 < c->N && c->stage[bp.k + 1].invariant;
+  if (pre_next(c, bp.k) && (c->pipe != 2 || inv_next)) {   // the next block's staging, behind this pass 1
+    CUDA_TRY(c, cudaEventRecord(c->ev_p1[bp.k], s));    // (pipe 1 or invariant: all of it, 3: up to the prefix)
+    trd_status sp = prestage(c, bp.k + 1, c->ev_p1[bp.k], (c->pipe == 1 || inv_next) ? 0 : 1, bp.k);
     if (sp) return sp;
   }
   if (bp.use_tc && c->eabs) launch_eabs_advance(*c, stg, s);   // R21 |e| slots of this block
@@ -504,7 +508,7 @@ trd_status block_pass2(Context* c, const BlockPlan& bp) {
   else launch_pass2(*c, bp, s);
   if (pe) prof_pair(c, 2, e0, prof_event(c));
   tl_mark(c, s, "pass 2");
-  if (pre_next(c, bp.k) && c->pipe >= 2) {   // (pipe 2: all of it, 3: the values)
+  if (pre_next(c, bp.k) && c->pipe >= 2 && !(bp.k + 1 < c->N && c->stage[bp.k + 1].invariant)) {   // (pipe 2: all of it, 3: the values)
     CUDA_TRY(c, cudaEventRecord(c->ev_p2[bp.k], s));
     trd_status sp = prestage(c, bp.k + 1, c->ev_p2[bp.k], c->pipe == 2 ? 0 : 2, bp.k);
     if (sp) return sp;
@@ -984,10 +988,11 @@ trd_status trd_init_ex(const trd_config* cfg, const trd_shard* shard, const floa
     const char* pe = getenv("TRD_PIPE");
     const int mode = pe ? atoi(pe) : kPipeDefault;
     c->pipe_min_tiles = pe ? 0 : kPipeMinTiles;     // (an explicit TRD_PIPE pipelines every sampled block)
+    c->pipe_inv = getenv("TRD_PIPE_INV") && atoi(getenv("TRD_PIPE_INV")) != 0;
     bool any = false;
     for (int k = 0; k < N; ++k)
-      if (c->plan[k].use_tc && !c->stage[k].invariant && !c->plan[k].explicit_cols &&
-          c->stage[k].n_tiles >= c->pipe_min_tiles)
+      if (c->plan[k].use_tc && !c->plan[k].explicit_cols &&
+          (c->stage[k].invariant ? c->pipe_inv != 0 : c->stage[k].n_tiles >= c->pipe_min_tiles))
         any = true;
     if (mode > 0 && mode <= 3 && any) {
       c->idx_d = c->idx; c->doff_d = c->doff; c->row_off_d = c->row_off; c->col_off_d = c->col_off;
@@ -1158,7 +1163,11 @@ static trd_status enqueue_sweep(Context* c) {
   struct InSweep {                       // (prestaging of block k + 1 only inside a sweep)
     Context* c;
     explicit InSweep(Context* cc) : c(cc) { c->in_sweep = 1; }
-    ~InSweep() { c->in_sweep = 0; select_bufs(c, -1); }
+    ~InSweep() {
+      c->in_sweep = 0;
+      select_bufs(c, -1);
+      for (int k = 0; k < kMaxN; ++k) c->prestaged[k] = false;
+    }
   } in_sweep(c);
   // (the Q refresh on the side stream; TRD_Q_SIDE=0 keeps it in line.  Measured with 50 timed
   //  sweeps, ms per sweep in line / side: C3 0.643 / 0.628, C4 0.777 / 0.755, C5a 1.942 / 1.924)
@@ -1168,7 +1177,9 @@ static trd_status enqueue_sweep(Context* c) {
   for (int k = 0; k < c->N; ++k) {
     const BlockPlan& bp = c->plan[k];
     NvtxRange nr(kNvtxBlock[k]);
-    if ((st = block_pass1(c, bp, k > 0 && pipelined(c, k)))) return st;
+    const bool pre = c->prestaged[k];
+    c->prestaged[k] = false;
+    if ((st = block_pass1(c, bp, pre))) return st;
     if ((st = block_pass2(c, bp))) return st;
     if (k == c->N - 1)
       CUDA_TRY(c, cudaMemcpyAsync(c->G_last, c->G, (size_t)bp.R2 * bp.R2 * 8, cudaMemcpyDeviceToDevice, s));

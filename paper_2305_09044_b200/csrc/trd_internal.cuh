@@ -316,6 +316,10 @@ struct Context {
   int in_sweep = 0;                    // enqueue_sweep is running (prestaging allowed)
   int fuse = 1;                        // world 1: fused block tail (TRD_NO_FUSE=1: separate kernels)
   int64_t pipe_min_tiles = 0;          // blocks staging fewer tiles stay in line
+  int pipe_inv = 0;                    // TRD_PIPE_INV=1: also restage invalidated sweep-invariant
+                                       // blocks (after an upload: the value gather) on `stg`
+                                       // (measured no gain on the C5b e2e path: off by default)
+  bool prestaged[kMaxN] = {};          // block k's staging was enqueued ahead (consumed by its pass 1)
   int pipe = 0;                        // 0 off, 1 prestage after pass 1 of the previous block,
                                        // 2 after its pass 2, 3 split (sampler + bits after pass 1,
                                        // values after pass 2)

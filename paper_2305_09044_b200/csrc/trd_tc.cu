@@ -1568,7 +1568,11 @@ void launch_tc_stage(Context& c, const BlockPlan& bp, TcStage& st, cudaStream_t 
   c.launches += 1;
   if (cached) {
     layout_gen_kernel<<<1, 32, 0, s>>>(&c.sc->mask_gen, &c.sc->layout_gen[bp.k]);
-    gather_vals_kernel<<<c.num_sm * 8, 256, 0, s>>>(st.perm, st.tidx, c.values, st.tbase + a.n_tiles, st.tvals, st.vcap);
+    // (TRD_GATHER_CTAS: CTAs per SM; fewer CTAs on the staging stream, to leave room for the
+    //  concurrent pass kernels, measured slower: C5b e2e 2.35e10 with 1, 2.66e10 with 2, 2.81e10
+    //  with 8 vs 2.83e10 in line)
+    const int gper = getenv("TRD_GATHER_CTAS") ? std::max(1, atoi(getenv("TRD_GATHER_CTAS"))) : 8;
+    gather_vals_kernel<<<c.num_sm * gper, 256, 0, s>>>(st.perm, st.tidx, c.values, st.tbase + a.n_tiles, st.tvals, st.vcap);
     c.launches += 2;
   }
 }
