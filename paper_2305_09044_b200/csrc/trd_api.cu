@@ -1188,7 +1188,10 @@ static trd_status enqueue_sweep(Context* c) {
     tl_mark(c, s, "step + update");
     // Q_k of the updated core (Eq. 13's factor) is read only by the next blocks' FGMC Gram on the
     // side stream: optionally refresh it there (large-rank Q by cuBLAS stays in line)
-    if (q_side && (int64_t)c->ranks[k] * c->ranks[(k + 1) % c->N] <= kBigR2) {
+    // (only when the next block's solve is short, R^2 <= 64: behind a long Gauss-Jordan solve the
+    //  extra side-stream work lands on the critical path -- C4, R^2 = 100: 0.775 ms per sweep with
+    //  every refresh on the side stream vs 0.754 in line)
+    if (q_side && (int64_t)c->ranks[k] * c->ranks[(k + 1) % c->N] <= kBigR2 && c->plan[(k + 1) % c->N].R2 <= 64) {
       CUDA_TRY(c, cudaEventRecord(c->ev_fork, s));
       CUDA_TRY(c, cudaStreamWaitEvent(c->side, c->ev_fork, 0));
       launch_q(*c, k, c->side);

@@ -1495,11 +1495,11 @@ __global__ void __launch_bounds__(256) gj2_solve_kernel(const double* __restrict
 // a_ij -= (a_ik / p) a_kj over the whole block, then row k (a_kj / p, owner warp) and column k
 // (-a_ik / p, owner lane; a_kk = 1 / p) are fixed up, and the owners publish row k+1 / column
 // k+1 to double-buffered shared vectors; one barrier per step.
-template <int NU, int NV>
-__global__ void __launch_bounds__(256) gj3_solve_kernel(const double* __restrict__ G, int n, double lambda_rel,
-                                                        double* __restrict__ Xout, DevScalars* __restrict__ sc) {
-  constexpr int NP = 8 * NU, NC = 32 * NV;
-  static_assert(NU % 2 == 0 && NC >= NP, "row pairs, columns cover the padded matrix");
+template <int NU, int NV, int TY = 8>
+__global__ void __launch_bounds__(32 * TY) gj3_solve_kernel(const double* __restrict__ G, int n, double lambda_rel,
+                                                            double* __restrict__ Xout, DevScalars* __restrict__ sc) {
+  constexpr int NP = TY * NU, NC = 32 * NV;
+  static_assert(NC >= NP, "columns cover the padded matrix");
   __shared__ __align__(16) double rowb[2][NC];
   __shared__ __align__(16) double colb[2][NP];
   __shared__ int fail_s;
@@ -1542,11 +1542,16 @@ __global__ void __launch_bounds__(256) gj3_solve_kernel(const double* __restrict
 #pragma unroll
         for (int v = 0; v < NV; ++v) rj[v] = rowb[b][j0 + v];
       }
+      if (NU % 2 == 0) {
 #pragma unroll
-      for (int u = 0; u < NU; u += 2) {
-        const double2 t = *reinterpret_cast<const double2*>(&colb[b][i0 + u]);
-        f[u] = t.x * ip;
-        f[u + 1] = t.y * ip;
+        for (int u = 0; u < NU; u += 2) {
+          const double2 t = *reinterpret_cast<const double2*>(&colb[b][i0 + u]);
+          f[u] = t.x * ip;
+          f[u + 1] = t.y * ip;
+        }
+      } else {
+#pragma unroll
+        for (int u = 0; u < NU; ++u) f[u] = colb[b][i0 + u] * ip;
       }
 #pragma unroll
       for (int u = 0; u < NU; ++u)
@@ -2344,6 +2349,8 @@ void launch_solve(Context& c, const BlockPlan& bp, cudaStream_t s, const double*
   // R^2 <= 48: the one-dimensional kernel (two threads per row; measured C3 -- R^2 = 30 / 100 --
   // 0.624 vs 0.643 ms per sweep with the 2-D kernel throughout); R^2 > 48: the 2-D kernel
   const int solve_sel = getenv("TRD_SOLVE") ? atoi(getenv("TRD_SOLVE")) : (n <= 48 ? 2 : 0);
+  // (a 32-warp variant, 4 x 4 blocks per thread, measured slower: R^2 = 100 122 vs 103 us, C4
+  //  0.857 vs 0.773 ms per sweep -- barrier and padding cost outweigh the extra latency hiding)
   if (n <= 128 && solve_sel == 0) {    // 2-D register Gauss-Jordan (NU x NV blocks per thread)
     const int np = (n + 15) / 16 * 16;
     switch (np) {
