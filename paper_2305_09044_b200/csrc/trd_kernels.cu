@@ -1612,6 +1612,139 @@ __global__ void __launch_bounds__(32 * TY) gj3_solve_kernel(const double* __rest
   if (tid == 0) { sc->lambda = lam; sc->h_lam = lam; }
 }
 
+// Blocked Gauss-Jordan inverse in shared memory (R^2 in (48, 128]; TRD_SOLVE=3 forces it, 0 the
+// register kernels): the same in-place elimination as gj2 / gj3 with kGjB pivots per step, so the
+// CTA synchronises ~4 times per pivot block instead of once per pivot.  With P the current pivot
+// block (a Schur complement of the SPD A = G + lambda I, so SPD: no pivoting), B its row block, C
+// its column block and D the rest, one step maps [P B; C D] to [P^-1, P^-1 B; -C P^-1, D - C P^-1 B]
+// (kGjB scalar Gauss-Jordan steps at once): warp 0 inverts P in place (scalar Gauss-Jordan, warp
+// synchronous), then the row block, the trailing block (old C, new row block) and the column block.
+// A non-positive pivot triggers the R23 retry.  Row stride LD odd (conflict-free column reads).
+constexpr int kGjB = 16;
+__global__ void __launch_bounds__(256) gjb_solve_kernel(const double* __restrict__ G, int n, double lambda_rel,
+                                                        double* __restrict__ Xout, DevScalars* __restrict__ sc) {
+  trd_gdc_wait();
+  extern __shared__ double gsm_b[];
+  const int LD = n | 1;
+  double* A = gsm_b;                          // [n][LD]
+  __shared__ int fail_s;
+  __shared__ double tr_s;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid < 32) tr_s_warp(G, n, &tr_s);
+  __syncthreads();
+  double lam = lambda_rel * tr_s / n;
+  for (int attempt = 0;; ++attempt) {
+    for (int e = tid; e < n * n; e += blockDim.x) {
+      const int i = e / n, j = e - i * n;
+      A[i * LD + j] = G[e] + (i == j ? lam : 0.0);
+    }
+    if (tid == 0) fail_s = 0;
+    __syncthreads();
+    for (int K = 0; K < n; K += kGjB) {
+      const int bs = min(kGjB, n - K);
+      // (1) P <- P^-1, warp 0, scalar in-place Gauss-Jordan (lane owns up to 8 of the bs x bs)
+      if (warp == 0) {
+        for (int kk = 0; kk < bs; ++kk) {
+          const double piv = A[(K + kk) * LD + K + kk];
+          const bool bad = !(piv > 0.0);
+          if (bad) { if (lane == 0) fail_s = 1; }
+          const double ip = bad ? 0.0 : 1.0 / piv;
+          double nv[8];
+#pragma unroll
+          for (int t = 0; t < 8; ++t) {
+            const int e = lane + 32 * t;
+            nv[t] = 0.0;
+            if (e < bs * bs) {
+              const int r = e / bs, c = e - r * bs;
+              const double prk = A[(K + r) * LD + K + kk], pkc = A[(K + kk) * LD + K + c], prc = A[(K + r) * LD + K + c];
+              nv[t] = (r == kk && c == kk) ? ip : (r == kk) ? pkc * ip : (c == kk) ? -prk * ip : fma(-prk * ip, pkc, prc);
+            }
+          }
+          __syncwarp();
+#pragma unroll
+          for (int t = 0; t < 8; ++t) {
+            const int e = lane + 32 * t;
+            if (e < bs * bs) {
+              const int r = e / bs, c = e - r * bs;
+              A[(K + r) * LD + K + c] = nv[t];
+            }
+          }
+          __syncwarp();
+        }
+      }
+      __syncthreads();
+      if (fail_s) break;
+      // (2) row block B <- P^-1 B  (rows K..K+bs, columns outside the block)
+      const int nc = n - bs;                   // columns outside the block
+      {
+        constexpr int NT = (kGjB * 128 + 255) / 256;   // outputs per thread (blockDim 256)
+        double nv[NT];
+#pragma unroll
+        for (int t = 0; t < NT; ++t) {
+          const int e = tid + 256 * t;
+          nv[t] = 0.0;
+          if (e < bs * nc) {
+            const int r = e / nc, jj = e - r * nc, j = jj < K ? jj : jj + bs;
+            double acc = 0.0;
+            for (int q = 0; q < bs; ++q) acc = fma(A[(K + r) * LD + K + q], A[(K + q) * LD + j], acc);
+            nv[t] = acc;
+          }
+        }
+        __syncthreads();
+#pragma unroll
+        for (int t = 0; t < NT; ++t) {
+          const int e = tid + 256 * t;
+          if (e < bs * nc) {
+            const int r = e / nc, jj = e - r * nc, j = jj < K ? jj : jj + bs;
+            A[(K + r) * LD + j] = nv[t];
+          }
+        }
+      }
+      __syncthreads();
+      // (3) trailing D <- D - C (P^-1 B)   (old column block C, new row block)
+      for (int e = tid; e < nc * nc; e += blockDim.x) {
+        const int ii = e / nc, jj = e - ii * nc;
+        const int i = ii < K ? ii : ii + bs, j = jj < K ? jj : jj + bs;
+        double acc = A[i * LD + j];
+        for (int q = 0; q < bs; ++q) acc = fma(-A[i * LD + K + q], A[(K + q) * LD + j], acc);
+        A[i * LD + j] = acc;
+      }
+      __syncthreads();
+      // (4) column block C <- -C P^-1   (thread per row outside the block)
+      for (int ii = tid; ii < nc; ii += blockDim.x) {
+        const int i = ii < K ? ii : ii + bs;
+        double cr[kGjB];
+#pragma unroll
+        for (int q = 0; q < kGjB; ++q) cr[q] = q < bs ? A[i * LD + K + q] : 0.0;
+#pragma unroll
+        for (int c = 0; c < kGjB; ++c) {
+          if (c >= bs) break;
+          double acc = 0.0;
+#pragma unroll
+          for (int q = 0; q < kGjB; ++q)
+            if (q < bs) acc = fma(cr[q], A[(K + q) * LD + K + c], acc);
+          A[i * LD + K + c] = -acc;
+        }
+      }
+      __syncthreads();
+    }
+    __syncthreads();
+    if (!fail_s || attempt >= 3) break;
+    lam = lam > 0.0 ? 10.0 * lam : ldexp(tr_s / n, -40);   // R23 retry rule
+    __syncthreads();
+  }
+  if (fail_s) {
+    if (tid == 0) { sc->not_spd = 1; sc->lambda = lam; sc->h_lam = 0.0; }
+    for (int t = tid; t < n * n; t += blockDim.x) Xout[t] = 0.0;
+    return;
+  }
+  for (int e = tid; e < n * n; e += blockDim.x) {
+    const int i = e / n, j = e - i * n;
+    Xout[e] = A[i * LD + j];
+  }
+  if (tid == 0) { sc->lambda = lam; sc->h_lam = lam; }
+}
+
 // h = d M (row-wise) with M = Mop - h_lam Mop^2 (h_lam = lambda when Mop = (G + lambda I)^-1 from
 // gj2_solve_kernel, 0 when Mop is M itself), computed as u = d Mop, h = u - h_lam u Mop;
 // num partial per row = <d(i), h(i)>
@@ -2347,8 +2480,18 @@ void launch_solve(Context& c, const BlockPlan& bp, cudaStream_t s, const double*
     return;
   }
   // R^2 <= 48: the one-dimensional kernel (two threads per row; measured C3 -- R^2 = 30 / 100 --
-  // 0.624 vs 0.643 ms per sweep with the 2-D kernel throughout); R^2 > 48: the 2-D kernel
+  // 0.624 vs 0.643 ms per sweep with the 2-D kernel throughout); R^2 > 48: the 2-D register kernel
+  // (TRD_SOLVE=3: the blocked shared-memory kernel, measured slower: R^2 = 100 294 vs 103 us)
   const int solve_sel = getenv("TRD_SOLVE") ? atoi(getenv("TRD_SOLVE")) : (n <= 48 ? 2 : 0);
+  if (n <= 128 && solve_sel == 3) {
+    const int smem = (int)((size_t)n * (n | 1) * sizeof(double));
+    static uint64_t gjb_attr = 0;
+    if (first_on_device(gjb_attr))
+      cudaFuncSetAttribute(gjb_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 128 * 129 * 8);
+    gjb_solve_kernel<<<1, 256, smem, s>>>(G, n, c.cfg.lambda_rel, c.Mop, c.sc);
+    c.launches++;
+    return;
+  }
   // (a 32-warp variant, 4 x 4 blocks per thread, measured slower: R^2 = 100 122 vs 103 us, C4
   //  0.857 vs 0.773 ms per sweep -- barrier and padding cost outweigh the extra latency hiding)
   if (n <= 128 && solve_sel == 0) {    // 2-D register Gauss-Jordan (NU x NV blocks per thread)
