@@ -337,6 +337,35 @@ def test_fused_block_tail_equals_separate_kernels(name, dims, sketch, monkeypatc
     assert out[0][2] - out[1][2] == 3 * 3 * len(dims)
 
 
+@pytest.mark.parametrize("name,dims,ranks,sketch", [("C4", [16, 16, 16, 16], None, [8, 8, 8, 8]),
+                                                     ("C5a", [12, 10, 9, 8, 8], None, [6, 5, 5, 4, 4]),
+                                                     ("C3", [24, 20, 3, 10], [10, 10, 3, 10], [12, 10, 0, 5])])
+def test_solve_variants_agree(name, dims, ranks, sketch, monkeypatch):
+    """The filtered solve (Eq. 10/16; readings R5, R23) by the 2-D register Gauss-Jordan
+    (TRD_SOLVE=0), the one-dimensional one (2), the blocked shared-memory one (3) and the default
+    size-based choice: the same X = (G + lambda I)^-1 up to fp64 rounding, so the cores after one
+    sweep (stored in fp32) agree to 1e-6 and each is within 1e-4 of the oracle."""
+    _cuda()
+    over = {} if ranks is None else {"ranks": ranks}
+    spec = small_spec(name, dims, sketch, **over)
+    prob = make_problem(spec)
+    src, _ = oracle_source(prob)
+    st, _ = O.run(oracle_config(spec), prob.init, src, 1)
+    outs = []
+    for sel in (None, "0", "2", "3"):
+        if sel is None:
+            monkeypatch.delenv("TRD_SOLVE", raising=False)
+        else:
+            monkeypatch.setenv("TRD_SOLVE", sel)
+        ctx = gpu_context(prob, packed=True)
+        ctx.sweep(1)
+        outs.append(ctx.get_cores())
+        ctx.close()
+    for o in outs:
+        assert cores_rel_err(o, st.cores) <= 1e-4
+        assert cores_rel_err(o, outs[0]) <= 1e-6
+
+
 # ---------------------------------------------------------------- large ranks (SURVEY 8f rank 3)
 @pytest.mark.parametrize("name,dims,ranks,sketch", [
     ("C2", [256, 256, 3], [20, 20, 3], None),            # the paper's image ranks (P:362)
@@ -494,13 +523,15 @@ def test_row_fibre_and_table_compaction_staging_are_bitwise(name, dims, sketch, 
 
 
 # ---------------------------------------------------------------- upload layout cache (e2e)
-@pytest.mark.parametrize("packed", [False, True])
-def test_upload_with_changed_mask_restages_the_layout(packed):
+@pytest.mark.parametrize("packed,pipe_inv", [(False, "0"), (True, "0"), (True, "1")])
+def test_upload_with_changed_mask_restages_the_layout(packed, pipe_inv, monkeypatch):
     """Sweep-invariant sketches keep their staged layout across uploads whose mask is unchanged
     (only the values are re-gathered); an upload with a different mask must rebuild it.  After
     uploads with (same mask, new values) and then (new mask, new values) the cores equal, bit
-    for bit, those of fresh contexts created on each data set."""
+    for bit, those of fresh contexts created on each data set -- also when the restaging of
+    blocks 1.. runs ahead on the staging stream (TRD_PIPE_INV=1)."""
     _cuda()
+    monkeypatch.setenv("TRD_PIPE_INV", pipe_inv)
     from paper_2305_09044_b200 import TRD
     spec = small_spec("C5b", [12, 9, 8, 7, 6])
     prob = make_problem(spec, keep_mask_bool=True)
