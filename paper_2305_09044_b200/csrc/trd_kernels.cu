@@ -1612,6 +1612,131 @@ __global__ void __launch_bounds__(32 * TY) gj3_solve_kernel(const double* __rest
   if (tid == 0) { sc->lambda = lam; sc->h_lam = lam; }
 }
 
+// Register Gauss-Jordan inverse with owner-resolved steps (TRD_SOLVE=4): the same elimination,
+// block distribution and arithmetic as gj3_solve_kernel (identical results on the n x n part: the
+// padding rows / columns are identity and never touch it), but the pivot loop runs over chunks of
+// NU pivots with the NU steps of a chunk unrolled, and NU % NV == 0.  Pivot k = kc NU + uu then
+// lives in register row uu of warp kc and register column uu % NV of lane kc NU / NV + uu / NV --
+// compile-time register indices -- so the row / column fix-ups and the publication of row /
+// column k + 1 are a few predicated moves instead of per-element compare-and-select chains over
+// the whole NU x NV block (SASS of gj3<14, 4>: ~560 instructions per step, 75 of them fp64).
+template <int NU, int NV, int TY = 8>
+__global__ void __launch_bounds__(32 * TY) gj4_solve_kernel(const double* __restrict__ G, int n, double lambda_rel,
+                                                            double* __restrict__ Xout, DevScalars* __restrict__ sc) {
+  constexpr int NP = TY * NU, NC = 32 * NV;
+  static_assert(NC >= NP, "columns cover the padded matrix");
+  static_assert(NU % NV == 0, "a pivot chunk maps onto whole lane column groups");
+  __shared__ __align__(16) double rowb[2][NC];
+  __shared__ __align__(16) double colb[2][NP];
+  __shared__ int fail_s;
+  __shared__ double tr_s;
+  const int tid = threadIdx.x, tx = tid & 31, ty = tid >> 5;
+  const int i0 = ty * NU, j0 = tx * NV;
+  if (tid < 32) tr_s_warp(G, n, &tr_s);
+  __syncthreads();
+  double lam = lambda_rel * tr_s / n;
+  double a[NU][NV];
+  for (int attempt = 0;; ++attempt) {
+#pragma unroll
+    for (int u = 0; u < NU; ++u)
+#pragma unroll
+      for (int v = 0; v < NV; ++v) {
+        const int i = i0 + u, j = j0 + v;
+        a[u][v] = (i < n && j < n) ? G[i * n + j] + (i == j ? lam : 0.0) : (i == j ? 1.0 : 0.0);
+        if (i == 0) rowb[0][j] = a[u][v];
+        if (j == 0) colb[0][i] = a[u][v];
+      }
+    if (tid == 0) fail_s = 0;
+    __syncthreads();
+    bool stop = false;
+    for (int kc = 0; kc < TY && !stop; ++kc) {
+#pragma unroll
+      for (int uu = 0; uu < NU; ++uu) {
+        const int k = kc * NU + uu;
+        if (k >= n) { stop = true; break; }
+        const int b = k & 1;
+        const double p = rowb[b][k];
+        if (!(p > 0.0)) {                    // (uniform: every thread reads the same pivot)
+          if (tid == 0) fail_s = 1;
+          stop = true;
+          break;
+        }
+        const double ip = 1.0 / p;
+        double rj[NV], f[NU];
+        if (NV % 2 == 0) {
+#pragma unroll
+          for (int v = 0; v < NV; v += 2) {
+            const double2 t = *reinterpret_cast<const double2*>(&rowb[b][j0 + v]);
+            rj[v] = t.x;
+            rj[v + 1] = t.y;
+          }
+        } else {
+#pragma unroll
+          for (int v = 0; v < NV; ++v) rj[v] = rowb[b][j0 + v];
+        }
+        if (NU % 2 == 0) {
+#pragma unroll
+          for (int u = 0; u < NU; u += 2) {
+            const double2 t = *reinterpret_cast<const double2*>(&colb[b][i0 + u]);
+            f[u] = t.x * ip;
+            f[u + 1] = t.y * ip;
+          }
+        } else {
+#pragma unroll
+          for (int u = 0; u < NU; ++u) f[u] = colb[b][i0 + u] * ip;
+        }
+#pragma unroll
+        for (int u = 0; u < NU; ++u)
+#pragma unroll
+          for (int v = 0; v < NV; ++v) a[u][v] = fma(-f[u], rj[v], a[u][v]);
+        if (ty == kc) {                      // row k = register row uu of warp kc: a_kj / p
+#pragma unroll
+          for (int v = 0; v < NV; ++v) a[uu][v] = rj[v] * ip;
+        }
+        const int vk = uu % NV;              // column k = register column vk of one lane
+        if (tx == kc * (NU / NV) + uu / NV) {
+#pragma unroll
+          for (int u = 0; u < NU; ++u) a[u][vk] = -f[u];
+          if (ty == kc) a[uu][vk] = ip;      // a_kk = 1 / p
+        }
+        const int bn = b ^ 1;                // publish row k + 1 and column k + 1
+        if (uu + 1 < NU) {
+          if (ty == kc) {
+#pragma unroll
+            for (int v = 0; v < NV; ++v) rowb[bn][j0 + v] = a[(uu + 1) % NU][v];
+          }
+        } else if (ty == kc + 1) {
+#pragma unroll
+          for (int v = 0; v < NV; ++v) rowb[bn][j0 + v] = a[0][v];
+        }
+        const int vk1 = (uu + 1) % NV;
+        if (tx == kc * (NU / NV) + (uu + 1) / NV) {
+#pragma unroll
+          for (int u = 0; u < NU; ++u) colb[bn][i0 + u] = a[u][vk1];
+        }
+        __syncthreads();
+      }
+    }
+    __syncthreads();
+    if (!fail_s || attempt >= 3) break;
+    lam = lam > 0.0 ? 10.0 * lam : ldexp(tr_s / n, -40);   // R23 retry rule
+    __syncthreads();
+  }
+  if (fail_s) {
+    if (tid == 0) { sc->not_spd = 1; sc->lambda = lam; sc->h_lam = 0.0; }
+    for (int t = tid; t < n * n; t += blockDim.x) Xout[t] = 0.0;
+    return;
+  }
+#pragma unroll
+  for (int u = 0; u < NU; ++u)
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      const int i = i0 + u, j = j0 + v;
+      if (i < n && j < n) Xout[i * n + j] = a[u][v];
+    }
+  if (tid == 0) { sc->lambda = lam; sc->h_lam = lam; }
+}
+
 // Blocked Gauss-Jordan inverse in shared memory (R^2 in (48, 128]; TRD_SOLVE=3 forces it, 0 the
 // register kernels): the same in-place elimination as gj2 / gj3 with kGjB pivots per step, so the
 // CTA synchronises ~4 times per pivot block instead of once per pivot.  With P the current pivot
@@ -2479,10 +2604,11 @@ void launch_solve(Context& c, const BlockPlan& bp, cudaStream_t s, const double*
     big_factor(c, bp, s, G);
     return;
   }
-  // R^2 <= 48: the one-dimensional kernel (two threads per row; measured C3 -- R^2 = 30 / 100 --
-  // 0.624 vs 0.643 ms per sweep with the 2-D kernel throughout); R^2 > 48: the 2-D register kernel
-  // (TRD_SOLVE=3: the blocked shared-memory kernel, measured slower: R^2 = 100 294 vs 103 us)
-  const int solve_sel = getenv("TRD_SOLVE") ? atoi(getenv("TRD_SOLVE")) : (n <= 48 ? 2 : 0);
+  // Default: the chunked owner-resolved register kernel for every R^2 <= 128 (R^2 = 100: 71 vs
+  // 103 us per launch for gj3; 50-sweep lines C4 0.752 -> 0.648, C3 0.583 -> 0.520, C5a 1.941 ->
+  // 1.927 ms per sweep against the previous default of gj2 for R^2 <= 48 and gj3 above).
+  // TRD_SOLVE=0 / 2 / 3: gj3 / the one-dimensional gj2 / the blocked shared-memory kernel (A/B).
+  const int solve_sel = getenv("TRD_SOLVE") ? atoi(getenv("TRD_SOLVE")) : 4;
   if (n <= 128 && solve_sel == 3) {
     const int smem = (int)((size_t)n * (n | 1) * sizeof(double));
     static uint64_t gjb_attr = 0;
@@ -2505,6 +2631,20 @@ void launch_solve(Context& c, const BlockPlan& bp, cudaStream_t s, const double*
       case 96: gj3_solve_kernel<12, 3><<<1, 256, 0, s>>>(G, n, c.cfg.lambda_rel, c.Mop, c.sc); break;
       case 112: gj3_solve_kernel<14, 4><<<1, 256, 0, s>>>(G, n, c.cfg.lambda_rel, c.Mop, c.sc); break;
       default: gj3_solve_kernel<16, 4><<<1, 256, 0, s>>>(G, n, c.cfg.lambda_rel, c.Mop, c.sc); break;
+    }
+    c.launches++;
+    return;
+  }
+  if (n <= 128 && solve_sel == 4) {    // owner-resolved chunked steps (NU % NV == 0)
+    const int np = (n + 15) / 16 * 16;
+    switch (np) {
+      case 16: gj4_solve_kernel<2, 1><<<1, 256, 0, s>>>(G, n, c.cfg.lambda_rel, c.Mop, c.sc); break;
+      case 32: gj4_solve_kernel<4, 1><<<1, 256, 0, s>>>(G, n, c.cfg.lambda_rel, c.Mop, c.sc); break;
+      case 48: gj4_solve_kernel<6, 2><<<1, 256, 0, s>>>(G, n, c.cfg.lambda_rel, c.Mop, c.sc); break;
+      case 64: gj4_solve_kernel<8, 2><<<1, 256, 0, s>>>(G, n, c.cfg.lambda_rel, c.Mop, c.sc); break;
+      case 80:
+      case 96: gj4_solve_kernel<12, 3><<<1, 256, 0, s>>>(G, n, c.cfg.lambda_rel, c.Mop, c.sc); break;
+      default: gj4_solve_kernel<16, 4><<<1, 256, 0, s>>>(G, n, c.cfg.lambda_rel, c.Mop, c.sc); break;
     }
     c.launches++;
     return;
