@@ -2619,6 +2619,19 @@ static void launch_gj4(int np, const double* G, int n, double lam, double* Mop, 
   }
 }
 
+// 16 warps (512 threads, half the block per thread): TRD_SOLVE=6
+static void launch_gj4_w16(int np, const double* G, int n, double lam, double* Mop, DevScalars* sc, cudaStream_t s) {
+  switch (np) {
+    case 16:
+    case 32: gj4_solve_kernel<2, 1, false, 16><<<1, 512, 0, s>>>(G, n, lam, Mop, sc); break;
+    case 48:
+    case 64: gj4_solve_kernel<4, 2, false, 16><<<1, 512, 0, s>>>(G, n, lam, Mop, sc); break;
+    case 80:
+    case 96: gj4_solve_kernel<6, 3, false, 16><<<1, 512, 0, s>>>(G, n, lam, Mop, sc); break;
+    default: gj4_solve_kernel<8, 4, false, 16><<<1, 512, 0, s>>>(G, n, lam, Mop, sc); break;
+  }
+}
+
 void launch_solve(Context& c, const BlockPlan& bp, cudaStream_t s, const double* G) {
   const int n = bp.R2;
   if (bp.lib_solve) {                  // Cholesky of G + lambda I (cuSOLVER); h in big_h
@@ -2628,8 +2641,10 @@ void launch_solve(Context& c, const BlockPlan& bp, cudaStream_t s, const double*
   // Default: the chunked owner-resolved register kernel for every R^2 <= 128 (R^2 = 100: 71 vs
   // 103 us per launch for gj3; 50-sweep lines C4 0.752 -> 0.648, C3 0.583 -> 0.520, C5a 1.941 ->
   // 1.927 ms per sweep against the previous default of gj2 for R^2 <= 48 and gj3 above).
+  // 16 warps for R^2 > 96 (R^2 = 100: 67.4 vs 71.2 us per launch, C4 0.648 -> 0.627 ms per sweep;
+  // C3 unchanged), 8 warps below.
   // TRD_SOLVE=0 / 2 / 3: gj3 / the one-dimensional gj2 / the blocked shared-memory kernel (A/B).
-  const int solve_sel = getenv("TRD_SOLVE") ? atoi(getenv("TRD_SOLVE")) : 4;
+  const int solve_sel = getenv("TRD_SOLVE") ? atoi(getenv("TRD_SOLVE")) : (n > 96 ? 6 : 4);
   if (n <= 128 && solve_sel == 3) {
     const int smem = (int)((size_t)n * (n | 1) * sizeof(double));
     static uint64_t gjb_attr = 0;
@@ -2656,8 +2671,13 @@ void launch_solve(Context& c, const BlockPlan& bp, cudaStream_t s, const double*
     c.launches++;
     return;
   }
-  if (n <= 128 && (solve_sel == 4 || solve_sel == 5)) {   // owner-resolved chunked steps (NU % NV == 0)
+  if (n <= 128 && (solve_sel == 4 || solve_sel == 5 || solve_sel == 6)) {   // owner-resolved chunked steps
     const int np = (n + 15) / 16 * 16;
+    if (solve_sel == 6) {
+      launch_gj4_w16(np, G, n, c.cfg.lambda_rel, c.Mop, c.sc, s);
+      c.launches++;
+      return;
+    }
     // (TRD_SOLVE=5: the next pivot's reciprocal published ahead by its owner -- measured slower,
     //  R^2 = 100 79.6 vs 71.5 us, C4 0.670 vs 0.652 ms per sweep: the division was not the chain)
     if (solve_sel == 5) launch_gj4<true>(np, G, n, c.cfg.lambda_rel, c.Mop, c.sc, s);

@@ -343,9 +343,9 @@ def test_fused_block_tail_equals_separate_kernels(name, dims, sketch, monkeypatc
 def test_solve_variants_agree(name, dims, ranks, sketch, monkeypatch):
     """The filtered solve (Eq. 10/16; readings R5, R23) by the 2-D register Gauss-Jordan
     (TRD_SOLVE=0), the one-dimensional one (2), the blocked shared-memory one (3), the chunked
-    owner-resolved one (4; 5 with the pivot reciprocal published ahead) and the default size-based choice: the same X = (G + lambda I)^-1 up to
+    owner-resolved one (4; 5 with the pivot reciprocal published ahead; 6 on 16 warps) and the default size-based choice: the same X = (G + lambda I)^-1 up to
     fp64 rounding, so the cores after one sweep (stored in fp32) agree to 1e-6 and each is within
-    1e-4 of the oracle; 4 performs gj3's arithmetic in the same order, so 0, 4 and 5 agree bitwise."""
+    1e-4 of the oracle; 4 performs gj3's arithmetic in the same order, so 0, 4, 5 and 6 agree bitwise."""
     _cuda()
     over = {} if ranks is None else {"ranks": ranks}
     spec = small_spec(name, dims, sketch, **over)
@@ -353,7 +353,7 @@ def test_solve_variants_agree(name, dims, ranks, sketch, monkeypatch):
     src, _ = oracle_source(prob)
     st, _ = O.run(oracle_config(spec), prob.init, src, 1)
     outs = []
-    sels = (None, "0", "2", "3", "4", "5")
+    sels = (None, "0", "2", "3", "4", "5", "6")
     for sel in sels:
         if sel is None:
             monkeypatch.delenv("TRD_SOLVE", raising=False)
@@ -366,7 +366,7 @@ def test_solve_variants_agree(name, dims, ranks, sketch, monkeypatch):
     for o in outs:
         assert cores_rel_err(o, st.cores) <= 1e-4
         assert cores_rel_err(o, outs[0]) <= 1e-6
-    for sel in ("4", "5"):
+    for sel in ("4", "5", "6"):
         for a, b in zip(outs[sels.index("0")], outs[sels.index(sel)]):
             assert np.array_equal(a, b)
 
