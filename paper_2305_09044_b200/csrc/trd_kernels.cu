@@ -2641,10 +2641,11 @@ void launch_solve(Context& c, const BlockPlan& bp, cudaStream_t s, const double*
   // Default: the chunked owner-resolved register kernel for every R^2 <= 128 (R^2 = 100: 71 vs
   // 103 us per launch for gj3; 50-sweep lines C4 0.752 -> 0.648, C3 0.583 -> 0.520, C5a 1.941 ->
   // 1.927 ms per sweep against the previous default of gj2 for R^2 <= 48 and gj3 above).
-  // 16 warps for R^2 > 96 (R^2 = 100: 67.4 vs 71.2 us per launch, C4 0.648 -> 0.627 ms per sweep;
-  // C3 unchanged), 8 warps below.
-  // TRD_SOLVE=0 / 2 / 3: gj3 / the one-dimensional gj2 / the blocked shared-memory kernel (A/B).
-  const int solve_sel = getenv("TRD_SOLVE") ? atoi(getenv("TRD_SOLVE")) : (n > 96 ? 6 : 4);
+  // On 16 warps (R^2 = 100: 67.4 vs 71.2 us per launch, C4 0.648 -> 0.627 ms per sweep; C1 / C2 /
+  // C3 / C5a within noise of 8 warps, 50-sweep lines).
+  // TRD_SOLVE=0 / 2 / 3 / 4: gj3 / the one-dimensional gj2 / the blocked shared-memory kernel /
+  // gj4 on 8 warps (A/B).
+  const int solve_sel = getenv("TRD_SOLVE") ? atoi(getenv("TRD_SOLVE")) : 6;
   if (n <= 128 && solve_sel == 3) {
     const int smem = (int)((size_t)n * (n | 1) * sizeof(double));
     static uint64_t gjb_attr = 0;
