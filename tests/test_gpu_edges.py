@@ -343,9 +343,10 @@ def test_fused_block_tail_equals_separate_kernels(name, dims, sketch, monkeypatc
 def test_solve_variants_agree(name, dims, ranks, sketch, monkeypatch):
     """The filtered solve (Eq. 10/16; readings R5, R23) by the 2-D register Gauss-Jordan
     (TRD_SOLVE=0), the one-dimensional one (2), the blocked shared-memory one (3), the chunked
-    owner-resolved one (4; 5 with the pivot reciprocal published ahead; 6 on 16 warps) and the default size-based choice: the same X = (G + lambda I)^-1 up to
-    fp64 rounding, so the cores after one sweep (stored in fp32) agree to 1e-6 and each is within
-    1e-4 of the oracle; 4 performs gj3's arithmetic in the same order, so 0, 4, 5 and 6 agree bitwise."""
+    owner-resolved one on 8 warps (4; 5 with the pivot reciprocal published ahead) and on 16 warps
+    (6, the default): the same X = (G + lambda I)^-1 up to fp64 rounding, so the cores after one
+    sweep (stored in fp32) agree to 1e-6 and each is within 1e-4 of the oracle; 4 / 5 / 6 perform
+    gj3's arithmetic in the same order, so 0, 4, 5 and 6 agree bitwise."""
     _cuda()
     over = {} if ranks is None else {"ranks": ranks}
     spec = small_spec(name, dims, sketch, **over)
